@@ -1,0 +1,224 @@
+/*
+ * rn.h — C ABI of librn.so: one synchronous training step of 3D-ResAttNet under
+ * the hybrid (model + data) parallelisation of Akintoye et al., arXiv 2104.05035
+ * ("PAPER.md" below, line numbers as P:<line>), built B200-native (sm_100a).
+ *
+ * Entry points follow the paper's problem statement:
+ *   rn_gabra_place  — GABRA, Algorithm 1 over the 0-1 multiple
+ *                     knapsack model Eqs. 3-8: partition loads p_i,
+ *                     GPU capacities d_j -> placement Z*, profit f(Z*).
+ *   rn_net_units    — layer costing + network partitioning (§3.1.1 P:154-156,
+ *                     conv complexity P:366): unit loads -> partitions p_1..p_n.
+ *   rn_plan         — per-rank program for a placement: partitions on GPUs,
+ *                     activation a^t sent to partition i+1 / gradient g^t sent to
+ *                     partition i-1, data-parallel replicas (§3.2).
+ *   rn_forward / rn_backward / rn_step
+ *                   — one synchronous step: forward + cross-entropy loss,
+ *                     backward by the chain rule, gradient averaging over
+ *                     replicas by ring all-reduce (Eqs. 9-11),
+ *                     SGD update w <- w - gamma*g.
+ *
+ * Conventions (all calls):
+ *  - Every call returns rn_status; it never aborts the process.  On error
+ *    rn_last_error() returns a thread-local message describing the failure.
+ *  - Host pointers (suffix _host / plain arrays) are read or written
+ *    synchronously before the call returns.  Device pointers (suffix _dev) are
+ *    used stream-ordered on the plan's CUDA stream: the caller keeps them alive
+ *    until that stream's work completes.
+ *  - Ownership: the caller owns every buffer it passes, including the device
+ *    workspace bound with rn_plan_bind (allocated by the caller, e.g. torch);
+ *    the library owns the plan, its CUDA graphs, events and NCCL communicators,
+ *    released by rn_plan_destroy.
+ *  - rn_forward/rn_backward/rn_step are collective over all ranks of the plan
+ *    when world > 1: every rank calls them in the same order with the same genes.
+ */
+#ifndef RN_H
+#define RN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RN_OK = 0,
+  RN_ERR_ARG = 1,         /* bad argument (null pointer, size mismatch, out of range)       */
+  RN_ERR_SCHEMA = 2,      /* invalid network description / dims ("schema error")  */
+  RN_ERR_INFEASIBLE = 3,  /* no capacity-respecting placement (Eq. 6) found    */
+  RN_ERR_NUMERIC = 4,     /* non-finite loss                                   */
+  RN_ERR_CUDA = 5,        /* a CUDA runtime/driver call failed (message has the CUDA error)   */
+  RN_ERR_NCCL = 6,        /* an NCCL call failed or libnccl could not be loaded               */
+  RN_ERR_STATE = 7,       /* call out of order (e.g. rn_forward before rn_plan_bind)          */
+  RN_ERR_SIZE = 8         /* buffer too small / instance too large                            */
+} rn_status;
+
+/* Arithmetic type of the activation path (reading X19 in DESIGN.md):
+ *  RN_F32  — fp32 storage and fp32 SIMT arithmetic everywhere (no TF32); parity 1e-4.
+ *  RN_BF16 — bf16 activations and conv operands, fp32 accumulation (tcgen05/TMEM),
+ *            fp32 BN statistics, master weights, gradients, all-reduce; parity 2e-2. */
+enum { RN_F32 = 0, RN_BF16 = 1 };
+
+/* ------------------------------------------------------------------------- */
+/* GABRA placement (§3.1.2).                                                  */
+/* ------------------------------------------------------------------------- */
+
+/* GA parameters.  Only p_cross = 0.8 comes from the paper; the rest are
+ * SPEC S:119 defaults and the bounded-retry/early-stop readings G15/G18/G19. */
+typedef struct {
+  int32_t pop_size;          /* population P (default 50; G8)                        */
+  int32_t t_max;             /* generations (default 500)                      */
+  double p_cross;            /* crossover probability (0.8)                    */
+  double p_mut;              /* inversion-mutation probability (0.1; G12)             */
+  uint64_t seed;             /* xoshiro256** seed via splitmix64 (G20)                */
+  int32_t dup_retries;       /* bounded "ignore W and go to" retries (20; G15)        */
+  int32_t init_attempts;     /* random draws per initial chromosome (64; G19)         */
+  int32_t require_all_used;  /* 1: "each GPU runs at least one partition" (G7) */
+  int32_t early_stop_at_ub;  /* 1: stop when f(Z*) == sum_i max_j c_ij (G18)   */
+} rn_ga_params;
+
+/* Fill *gp with the defaults above (seed 7). */
+void rn_ga_default(rn_ga_params *gp);
+
+/* rn_gabra_place — Algorithm 1 as pinned in DESIGN.md "GABRA".
+ *  n, loads[n]   : partition loads p_i >= 0 (int64 MACs per sample; reading G3)
+ *  m, caps[m]    : GPU capacities d_j > 0 (same unit)
+ *  gp            : GA parameters (NULL = rn_ga_default)
+ *  genes_out[n]  : 0-based GPU index of each partition in Z*            (written)
+ *  profit_out    : f(Z*) = sum_i p_i / d_{genes_i}, left-to-right double (written; may be NULL)
+ *  gpu_load_out[m]: per-GPU load sum_{i: genes_i=j} p_i                  (written; may be NULL)
+ * Errors: RN_ERR_ARG (n<1, m<1, pop_size<2, null loads/caps/genes_out, caps<=0,
+ * loads<0), RN_ERR_INFEASIBLE (no feasible initial chromosome within
+ * init_attempts draws + repair).  Deterministic: bit-identical to the oracle. */
+rn_status rn_gabra_place(int32_t n, const int64_t *loads, int32_t m, const int64_t *caps,
+                         const rn_ga_params *gp, int32_t *genes_out, double *profit_out,
+                         int64_t *gpu_load_out);
+
+/* ------------------------------------------------------------------------- */
+/* Network description, costing and partitioning (§3.1.1).            */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+  int32_t depth;          /* 0 = tiny (1 block + 1 attention module), 18, 34 (Table 2) */
+  int32_t base_width;     /* channels of the stem / stage 1 (8 tiny, 64 r18/r34; reading X2) */
+  int32_t in_d, in_h, in_w;/* input volume (91x109x91 MNI grid; reading X1); 1 input channel  */
+  int32_t n_classes;      /* must be 2 (binary tasks)                                  */
+  double alpha;           /* heavy-unit threshold alpha * mean (reading G1; default 1.0)      */
+  int64_t max_merge_load; /* cap on merged light partitions (0 = none)                        */
+} rn_net_desc;
+
+#define RN_MAX_UNITS 64
+
+/* rn_net_units — unit costs (a1) and contiguous partitions (a2).
+ *  n_units          : number of top-level units (stem, residual blocks, attention modules, head)
+ *  unit_loads[64]   : per-sample MACs per unit (conv: Co*Ci*T*H*W*k^3)
+ *  n_parts          : number of partitions n
+ *  part_first_unit[65]: partition i covers units [first[i], first[i+1])
+ *  part_loads[64]   : p_i
+ * Any output pointer may be NULL.  Errors: RN_ERR_SCHEMA. */
+rn_status rn_net_units(const rn_net_desc *net, int32_t *n_units, int64_t *unit_loads,
+                       int32_t *n_parts, int32_t *part_first_unit, int64_t *part_loads);
+
+/* Parameter layout in the canonical order used by rn_set/get_params/grads:
+ * units in forward order; conv W[Cout][Cin][kd][kh][kw]; BN gamma, beta; mask
+ * conv2 bias; FC W[2][C], b[2].
+ *  rn_net_param_count: total scalars and number of tensors.
+ *  rn_net_param_info : tensor idx -> ndim, shape[5], kind (0 conv,1 bn_gamma,
+ *                      2 bn_beta, 3 fc_w, 4 bias), unit index, name (NUL-terminated). */
+rn_status rn_net_param_count(const rn_net_desc *net, int64_t *n_params, int32_t *n_tensors,
+                             int32_t *n_bn_channels);
+rn_status rn_net_param_info(const rn_net_desc *net, int32_t idx, int32_t *ndim, int64_t *shape5,
+                            int32_t *kind, int32_t *unit, char *name, int32_t name_cap);
+
+/* ------------------------------------------------------------------------- */
+/* Training step.                                                              */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+  int32_t rank, world;      /* this process / all processes (one per GPU)                   */
+  int32_t n_stages;         /* GPUs per pipeline group S (1 = pure data parallel)           */
+  const int32_t *genes;     /* [n_parts] partition -> stage index in [0, S) (rn_gabra_place);
+                               NULL allowed when n_stages == 1                               */
+  int32_t micro_batches;    /* M_b micro-batches per replica step (reading X18; >= 1)       */
+  uint8_t nccl_id[128];     /* ncclUniqueId from rn_nccl_unique_id on rank 0, broadcast by
+                               the caller; ignored when world == 1                            */
+} rn_dist_desc;
+
+typedef struct rn_plan_s *rn_plan_t;
+
+/* rn_nccl_unique_id — ncclGetUniqueId (libnccl.so.2 loaded at run time). */
+rn_status rn_nccl_unique_id(uint8_t out[128]);
+
+/* rn_plan — build the per-rank program.  Replica r = rank / S owns samples
+ * [r*b, (r+1)*b) of the global batch (P:366 equal sharding), stage s = rank % S
+ * runs the partitions whose gene == s.  local_batch b must be divisible by
+ * micro_batches.  cuda_stream: a cudaStream_t (NULL = legacy default stream).
+ *  *workspace_bytes : device bytes the caller must bind with rn_plan_bind.
+ * Errors: RN_ERR_ARG, RN_ERR_SCHEMA, RN_ERR_NCCL (communicator init). */
+rn_status rn_plan(const rn_net_desc *net, const rn_dist_desc *dist, int32_t local_batch,
+                  int32_t dtype, void *cuda_stream, rn_plan_t *out, size_t *workspace_bytes);
+
+/* rn_plan_bind — give the plan its device workspace (>= *workspace_bytes,
+ * 256-byte aligned, caller-owned, e.g. a torch uint8 tensor).  Must precede
+ * every compute call.  Errors: RN_ERR_SIZE, RN_ERR_ARG. */
+rn_status rn_plan_bind(rn_plan_t plan, void *dev_workspace, size_t bytes);
+
+/* Parameters in canonical order (float32 host arrays of n_params scalars).
+ * rn_set_params also resets BN running statistics (mean 0, var 1).
+ * rn_get_grads returns the gradient of the last rn_backward (after rn_step:
+ * the replica-averaged gradient G of Eq. 11); entries of partitions not placed on
+ * this rank are 0.  Errors: RN_ERR_SIZE (count != n_params), RN_ERR_STATE. */
+rn_status rn_set_params(rn_plan_t plan, const float *host, int64_t count);
+rn_status rn_get_params(rn_plan_t plan, float *host, int64_t count);
+rn_status rn_get_grads(rn_plan_t plan, float *host, int64_t count);
+/* BN running statistics, BN layers in canonical order, channels concatenated
+ * (count = n_bn_channels from rn_net_param_count). */
+rn_status rn_get_bn_running(rn_plan_t plan, float *mean_host, float *var_host, int64_t count);
+
+/* rn_forward — forward pass of this replica's local batch.
+ *  x_dev : float32 [b][D][H][W] input volumes (device), y_dev: int32 [b] labels in {0,1}
+ *          (only read on the stages that need them: stage of the first / last partition)
+ *  loss_host: if non-NULL, synchronises the stream and writes the replica's mean
+ *          cross-entropy (mean over its micro-batches, P:486 / Eq. 9).  Ranks that
+ *          do not hold the head receive it from the head stage.
+ * Micro-batches run forward in order (GPipe-style; backward in rn_backward).
+ * Errors: RN_ERR_STATE (unbound), RN_ERR_CUDA, RN_ERR_NCCL, RN_ERR_NUMERIC (non-finite loss). */
+rn_status rn_forward(rn_plan_t plan, const void *x_dev, const int32_t *y_dev, float *loss_host);
+
+/* rn_backward — backward pass of every micro-batch; writes this rank's
+ * gradients (already scaled by 1/(m*M_b) so that the replica sum is Eq. 11's G). */
+rn_status rn_backward(rn_plan_t plan);
+
+/* rn_step — all-reduce (sum) of the local partitions' gradients over the
+ * stage's data-parallel group (ring/NVLS all-reduce), then SGD
+ * w <- w - lr*G on fp32 master weights and refresh of the bf16 copies. */
+rn_status rn_step(rn_plan_t plan, float lr);
+
+/* rn_train_step_host — end-to-end convenience: copies x_host/y_host (pageable or
+ * pinned host memory) to the device, runs forward, backward and step, and reads
+ * the loss back.  Same semantics as the three calls above. */
+rn_status rn_train_step_host(rn_plan_t plan, const float *x_host, const int32_t *y_host, float lr,
+                             float *loss_host);
+
+/* Introspection for tests/bench: number of GPU kernels launched by this plan so
+ * far, and the plan's conv-kernel time accounting. */
+int64_t rn_kernel_launches(rn_plan_t plan);
+
+/* rn_set_option — runtime switches:
+ *  "graphs"        : 1 capture forward/backward/step in CUDA graphs (default 1)
+ *  "tc_conv"       : 1 use tcgen05 conv kernels in RN_BF16 (default 1)
+ *  "time_kernels"  : 1 record CUDA events around the dominant conv launches      */
+rn_status rn_set_option(rn_plan_t plan, const char *key, int64_t value);
+
+/* rn_query — named float64 statistics (e.g. "conv_ms", "conv_flops") collected
+ * when time_kernels is on; reset by rn_set_option("time_kernels", 1). */
+rn_status rn_query(rn_plan_t plan, const char *key, double *value);
+
+void rn_plan_destroy(rn_plan_t plan);
+const char *rn_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RN_H */

@@ -1,0 +1,291 @@
+// abi.cpp — extern "C" entry points of librn.so (include/rn.h).  Argument
+// validation, exception -> rn_status conversion, thread-local error message.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "../../include/rn.h"
+#include "comm.h"
+#include "error.h"
+#include "net.h"
+#include "plan.h"
+
+namespace rn {
+rn_status gabra_place(int32_t n, const int64_t *loads, int32_t m, const int64_t *caps, const rn_ga_params &gp,
+                      int32_t *genes_out, double *profit_out, int64_t *gpu_load_out);
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(); }
+rn_status set_error(rn_status s, const std::string &msg) {
+  g_err = msg;
+  return s;
+}
+}  // namespace rn
+
+struct rn_plan_s {
+  rn::Plan *p;
+};
+
+using namespace rn;
+
+#define GUARD_BEGIN try {
+#define GUARD_END                                               \
+  }                                                             \
+  catch (const rn::Error &e) {                                  \
+    return set_error(e.status, e.what());                       \
+  }                                                             \
+  catch (const std::invalid_argument &e) {                      \
+    return set_error(RN_ERR_SCHEMA, e.what());                  \
+  }                                                             \
+  catch (const std::bad_alloc &) {                              \
+    return set_error(RN_ERR_SIZE, "host allocation failed");    \
+  }                                                             \
+  catch (const std::exception &e) {                             \
+    return set_error(RN_ERR_STATE, e.what());                   \
+  }
+
+extern "C" {
+
+void rn_ga_default(rn_ga_params *gp) {
+  if (!gp) return;
+  gp->pop_size = 50;
+  gp->t_max = 500;
+  gp->p_cross = 0.8;
+  gp->p_mut = 0.1;
+  gp->seed = 7;
+  gp->dup_retries = 20;
+  gp->init_attempts = 64;
+  gp->require_all_used = 0;
+  gp->early_stop_at_ub = 1;
+}
+
+rn_status rn_gabra_place(int32_t n, const int64_t *loads, int32_t m, const int64_t *caps, const rn_ga_params *gp,
+                         int32_t *genes_out, double *profit_out, int64_t *gpu_load_out) {
+  GUARD_BEGIN
+  if (n < 1 || m < 1 || !loads || !caps || !genes_out) return set_error(RN_ERR_ARG, "rn_gabra_place: bad arguments");
+  for (int i = 0; i < n; ++i)
+    if (loads[i] < 0) return set_error(RN_ERR_ARG, "rn_gabra_place: negative load");
+  for (int j = 0; j < m; ++j)
+    if (caps[j] <= 0) return set_error(RN_ERR_ARG, "rn_gabra_place: capacity must be > 0");
+  rn_ga_params d;
+  rn_ga_default(&d);
+  const rn_ga_params &g = gp ? *gp : d;
+  if (g.pop_size < 2 || g.t_max < 0 || g.dup_retries < 1 || g.init_attempts < 1 || g.p_cross < 0 || g.p_cross > 1 ||
+      g.p_mut < 0 || g.p_mut > 1)
+    return set_error(RN_ERR_ARG, "rn_gabra_place: bad GA parameters");
+  return gabra_place(n, loads, m, caps, g, genes_out, profit_out, gpu_load_out);
+  GUARD_END
+}
+
+rn_status rn_net_units(const rn_net_desc *net, int32_t *n_units, int64_t *unit_loads, int32_t *n_parts,
+                       int32_t *part_first_unit, int64_t *part_loads) {
+  GUARD_BEGIN
+  if (!net) return set_error(RN_ERR_ARG, "null net");
+  NetModel m = build_net(*net);
+  if (n_units) *n_units = (int32_t)m.units.size();
+  if (unit_loads)
+    for (size_t i = 0; i < m.units.size(); ++i) unit_loads[i] = m.unit_costs[i];
+  if (n_parts) *n_parts = (int32_t)m.part_loads.size();
+  if (part_first_unit)
+    for (size_t i = 0; i < m.part_first.size(); ++i) part_first_unit[i] = m.part_first[i];
+  if (part_loads)
+    for (size_t i = 0; i < m.part_loads.size(); ++i) part_loads[i] = m.part_loads[i];
+  return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_net_param_count(const rn_net_desc *net, int64_t *n_params, int32_t *n_tensors, int32_t *n_bn_channels) {
+  GUARD_BEGIN
+  if (!net) return set_error(RN_ERR_ARG, "null net");
+  NetModel m = build_net(*net);
+  if (n_params) *n_params = m.n_params;
+  if (n_tensors) *n_tensors = (int32_t)m.params.size();
+  if (n_bn_channels) *n_bn_channels = (int32_t)m.n_bn_channels;
+  return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_net_param_info(const rn_net_desc *net, int32_t idx, int32_t *ndim, int64_t *shape5, int32_t *kind,
+                            int32_t *unit, char *name, int32_t name_cap) {
+  GUARD_BEGIN
+  if (!net) return set_error(RN_ERR_ARG, "null net");
+  NetModel m = build_net(*net);
+  if (idx < 0 || idx >= (int)m.params.size()) return set_error(RN_ERR_ARG, "param index out of range");
+  const ParamTensor &t = m.params[idx];
+  if (ndim) *ndim = t.ndim;
+  if (shape5)
+    for (int i = 0; i < 5; ++i) shape5[i] = t.shape[i];
+  if (kind) *kind = t.kind;
+  if (unit) *unit = t.unit;
+  if (name && name_cap > 0) {
+    strncpy(name, t.name.c_str(), name_cap - 1);
+    name[name_cap - 1] = 0;
+  }
+  return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_nccl_unique_id(uint8_t out[128]) {
+  GUARD_BEGIN
+  if (!out) return set_error(RN_ERR_ARG, "null out");
+  nccl_unique_id(out);
+  return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_plan(const rn_net_desc *net, const rn_dist_desc *dist, int32_t local_batch, int32_t dtype,
+                  void *cuda_stream, rn_plan_t *out, size_t *workspace_bytes) {
+  GUARD_BEGIN
+  if (!net || !out || !workspace_bytes) return set_error(RN_ERR_ARG, "rn_plan: null argument");
+  if (dtype != RN_F32 && dtype != RN_BF16) return set_error(RN_ERR_ARG, "rn_plan: dtype must be RN_F32 or RN_BF16");
+  rn_dist_desc d;
+  memset(&d, 0, sizeof d);
+  d.world = 1;
+  d.n_stages = 1;
+  d.micro_batches = 1;
+  if (dist) d = *dist;
+  Plan *p = new Plan(*net, d, local_batch, dtype, (cudaStream_t)cuda_stream);
+  *out = new rn_plan_s{p};
+  *workspace_bytes = p->ws_bytes;
+  return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_plan_bind(rn_plan_t plan, void *dev, size_t bytes) {
+  GUARD_BEGIN
+  if (!plan || !dev) return set_error(RN_ERR_ARG, "rn_plan_bind: null argument");
+  plan->p->bind(dev, bytes);
+  return RN_OK;
+  GUARD_END
+}
+
+#define NEED_BOUND(plan)                                                            \
+  if (!plan) return set_error(RN_ERR_ARG, "null plan");                             \
+  if (!plan->p->base) return set_error(RN_ERR_STATE, "plan has no workspace bound");
+
+rn_status rn_set_params(rn_plan_t plan, const float *host, int64_t count) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  if (!host) return set_error(RN_ERR_ARG, "null host");
+  if (count != plan->p->net.n_params) return set_error(RN_ERR_SIZE, "count != n_params");
+  plan->p->set_params(host);
+  return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_get_params(rn_plan_t plan, float *host, int64_t count) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  if (!host) return set_error(RN_ERR_ARG, "null host");
+  if (count != plan->p->net.n_params) return set_error(RN_ERR_SIZE, "count != n_params");
+  plan->p->get_flat(plan->p->off_master, host);
+  return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_get_grads(rn_plan_t plan, float *host, int64_t count) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  if (!host) return set_error(RN_ERR_ARG, "null host");
+  if (count != plan->p->net.n_params) return set_error(RN_ERR_SIZE, "count != n_params");
+  plan->p->get_flat(plan->p->off_grad, host);
+  return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_get_bn_running(rn_plan_t plan, float *mean_host, float *var_host, int64_t count) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  Plan *p = plan->p;
+  if (count != p->net.n_bn_channels) return set_error(RN_ERR_SIZE, "count != n_bn_channels");
+  CUDA_CHECK(cudaStreamSynchronize(p->stream));
+  if (mean_host) CUDA_CHECK(cudaMemcpy(mean_host, p->P(p->off_run_mean), 4 * count, cudaMemcpyDeviceToHost));
+  if (var_host) CUDA_CHECK(cudaMemcpy(var_host, p->P(p->off_run_var), 4 * count, cudaMemcpyDeviceToHost));
+  return RN_OK;
+  GUARD_END
+}
+
+static rn_status finish_loss(Plan *p, float *loss_host) {
+  if (!loss_host) return RN_OK;
+  float l = p->read_loss();
+  *loss_host = l;
+  if (!std::isfinite(l)) return set_error(RN_ERR_NUMERIC, "non-finite loss");
+  return RN_OK;
+}
+
+rn_status rn_forward(rn_plan_t plan, const void *x_dev, const int32_t *y_dev, float *loss_host) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  Plan *p = plan->p;
+  if (!p->params_set) return set_error(RN_ERR_STATE, "rn_set_params must precede rn_forward");
+  p->stage_inputs((const float *)x_dev, y_dev, false);
+  p->forward((const float *)p->P(p->off_x), (const int32_t *)p->P(p->off_y));
+  return finish_loss(p, loss_host);
+  GUARD_END
+}
+
+rn_status rn_backward(rn_plan_t plan) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  Plan *p = plan->p;
+  if (!p->fwd_done) return set_error(RN_ERR_STATE, "rn_backward before rn_forward");
+  p->backward((const float *)p->P(p->off_x));
+  p->fwd_done = false;
+  return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_step(rn_plan_t plan, float lr) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  plan->p->step(lr);
+  return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_train_step_host(rn_plan_t plan, const float *x_host, const int32_t *y_host, float lr, float *loss_host) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  Plan *p = plan->p;
+  if (!p->params_set) return set_error(RN_ERR_STATE, "rn_set_params must precede a step");
+  p->stage_inputs(x_host, y_host, true);
+  p->forward((const float *)p->P(p->off_x), (const int32_t *)p->P(p->off_y));
+  p->backward((const float *)p->P(p->off_x));
+  p->step(lr);
+  return finish_loss(p, loss_host);
+  GUARD_END
+}
+
+int64_t rn_kernel_launches(rn_plan_t) { return rn::launch_count(); }
+
+rn_status rn_set_option(rn_plan_t plan, const char *key, int64_t value) {
+  GUARD_BEGIN
+  if (!plan || !key) return set_error(RN_ERR_ARG, "null argument");
+  return plan->p->set_option(key, value);
+  GUARD_END
+}
+
+rn_status rn_query(rn_plan_t plan, const char *key, double *value) {
+  GUARD_BEGIN
+  if (!plan || !key || !value) return set_error(RN_ERR_ARG, "null argument");
+  return plan->p->query(key, value);
+  GUARD_END
+}
+
+void rn_plan_destroy(rn_plan_t plan) {
+  if (!plan) return;
+  try {
+    delete plan->p;
+  } catch (...) {
+  }
+  delete plan;
+}
+
+const char *rn_last_error(void) { return rn::g_err.c_str(); }
+
+}  // extern "C"

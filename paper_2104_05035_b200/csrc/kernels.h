@@ -1,0 +1,99 @@
+// kernels.h — host launchers for the sm_100a kernels of the 3D-ResAttNet step.
+// Plain pointers; layouts: activations NDHWC (channels fastest) of element type
+// T = float (RN_F32) or __nv_bfloat16 (RN_BF16); conv weights [Cout][tap][Cin]
+// (tap = (kd*k + kh)*k + kw); BN statistics / gradients fp32.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace rn {
+
+enum DType { DT_F32 = 0, DT_BF16 = 1 };
+inline size_t dt_size(DType t) { return t == DT_F32 ? 4 : 2; }
+
+struct ConvGeom {
+  int N;
+  int Di, Hi, Wi, Ci;
+  int Do, Ho, Wo, Co;
+  int k, s, p;
+  __host__ __device__ int64_t in_vox() const { return (int64_t)N * Di * Hi * Wi; }
+  __host__ __device__ int64_t out_vox() const { return (int64_t)N * Do * Ho * Wo; }
+  __host__ __device__ int taps() const { return k * k * k; }
+};
+
+// ---------------- convolution (SIMT implicit GEMM, fp32 accumulate) ----------------
+// y[vo][co] = sum_{tap,ci} x[vi(vo,tap)][ci] * w[co][tap][ci] (+ bias[co])
+void conv_fprop_simt(DType dt, const ConvGeom &g, const void *x, const void *w, const float *bias, void *y,
+                     cudaStream_t st);
+// dx[vi][ci] (=|+=) sum_{tap,co} dy[vo(vi,tap)][co] * w[co][tap][ci]  (+ res[vi][ci]*(mask[vi][ci]>0))
+void conv_dgrad_simt(DType dt, const ConvGeom &g, const void *dy, const void *w, void *dx, bool accumulate,
+                     const void *res, const void *res_mask, cudaStream_t st);
+// dw[co][tap][ci] += sum_vo dy[vo][co] * x[vi(vo,tap)][ci]; x_is_f32: input is fp32 (stem)
+size_t conv_wgrad_ws_floats(const ConvGeom &g);
+void conv_wgrad_simt(DType dt, bool x_is_f32, const ConvGeom &g, const void *x, const void *dy, float *dw,
+                     float *ws, cudaStream_t st);
+// stem: Ci = 1, x fp32 [N][D][H][W], w fp32 [Co][27]
+void stem_conv_fprop(DType dt, const ConvGeom &g, const float *x, const float *w, void *y, cudaStream_t st);
+
+// ---------------- BatchNorm (train mode), ReLU, residual ----------------
+int chan_reduce_blocks(int64_t V, int C);
+// partial[blk][2][C] = (sum (x-K), sum (x-K)^2), K[c] = x[0][c]
+void bn_stats(DType dt, const void *x, int64_t V, int C, float *partial, int nblk, cudaStream_t st);
+// mean/invstd/scale/shift per channel; running stats momentum update (unbiased var)
+void bn_finalize(DType dt, const void *x, const float *partial, int nblk, int64_t V, int C, const float *gamma,
+                 const float *beta, float *mean, float *invstd, float *scale, float *shift, float *run_mean,
+                 float *run_var, float momentum, float eps, cudaStream_t st);
+// y = act(x*scale + shift + R), R = 0 | res | res*rscale + rshift ; act = relu if relu
+void bn_apply(DType dt, const void *x, int64_t V, int C, const float *scale, const float *shift, const void *res,
+              const float *rscale, const float *rshift, bool relu, void *y, cudaStream_t st);
+enum MaskMode { MASK_NONE = 0, MASK_TENSOR = 1, MASK_RECOMPUTE = 2 };
+// partial[blk][2][C] = (sum dy', sum dy'*xhat), dy' = dy * mask
+void bn_bwd_reduce(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,
+                   const float *scale, const float *shift, const float *mean, const float *invstd, float *partial,
+                   int nblk, cudaStream_t st);
+// dgamma += S2, dbeta += S1; coef[0..C) = A, [C..2C) = B, [2C..3C) = Cc with dx = A dy' + B x + Cc
+void bn_bwd_finalize(const float *partial, int nblk, int64_t V, int C, const float *gamma, const float *mean,
+                     const float *invstd, float *dgamma, float *dbeta, float *coef, cudaStream_t st);
+void bn_bwd_apply(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,
+                  const float *scale, const float *shift, const float *coef, void *dx, cudaStream_t st);
+
+// ---------------- pooling / upsampling / attention ----------------
+// y = maxpool3(act(x*scale+shift)) (scale == nullptr: identity, no act); argmax uint8 (0..26)
+void maxpool_fwd(DType dt, const void *x, int N, int D, int H, int W, int C, const float *scale, const float *shift,
+                 bool relu, void *y, uint8_t *argmax, int Do, int Ho, int Wo, cudaStream_t st);
+void maxpool_bwd(DType dt, const void *dy, const uint8_t *argmax, int N, int D, int H, int W, int C, int Do, int Ho,
+                 int Wo, void *dx, bool accumulate, cudaStream_t st);
+struct UpTables {  // device pointers
+  const int *fw_idx[3];    // [out][2] (i0, i1)
+  const float *fw_w[3];    // [out][2] (1-lambda, lambda)
+  const int *bw_start[3];  // [in+1]
+  const int *bw_o[3];      // [nnz]
+  const float *bw_w[3];    // [nnz]
+};
+void upsample_fwd(DType dt, const void *x, int N, int Di, int Hi, int Wi, int C, void *y, int Do, int Ho, int Wo,
+                  const UpTables &t, cudaStream_t st);
+void upsample_bwd(DType dt, const void *dy, int N, int Di, int Hi, int Wi, int C, void *dx, int Do, int Ho, int Wo,
+                  const UpTables &t, cudaStream_t st);
+// out = (1 + sigmoid(m)) * T
+void att_fwd(DType dt, const void *m, const void *T, int64_t V, int C, void *out, cudaStream_t st);
+// dT = dout*(1+s), dm = dout*T*s*(1-s); partial[blk][2][C] = (sum dm, 0)
+void att_bwd(DType dt, const void *dout, const void *m, const void *T, int64_t V, int C, void *dT, void *dm,
+             float *partial, int nblk, cudaStream_t st);
+// out[c] += sum_blk partial[blk][0][c]
+void chan_sum_finalize(const float *partial, int nblk, int C, float *out, cudaStream_t st);
+
+// ---------------- head: GAP + FC + softmax cross-entropy ----------------
+void head_fwd(DType dt, const void *x, int N, int V, int C, const float *W, const float *b, const int32_t *y,
+              float dz_scale, float loss_scale, float *g, float *dz, float *loss_acc, cudaStream_t st);
+void head_bwd(DType dt, const float *dz, const float *g, const float *W, int N, int V, int C, float *dW, float *db,
+              void *dx, cudaStream_t st);
+
+// ---------------- optimizer ----------------
+void sgd_update(float *w, const float *g, int64_t n, float lr, cudaStream_t st);
+// wf[co][tap][ci] = w, wd[ci][taps-1-tap][co] = w  (either may be null)
+void repack_conv(DType dt, const float *w, int Co, int taps, int Ci, void *wf, void *wd, cudaStream_t st);
+void check_finite(const float *v, int n, int *flag, cudaStream_t st);
+
+}  // namespace rn

@@ -1,0 +1,645 @@
+// plan.cpp — the per-rank executor of one synchronous hybrid-parallel training
+// step of 3D-ResAttNet (§3.1.1, §3.2, §4.3.1).
+//
+// A plan owns: the network model (net.cpp), the placement of partitions on the
+// stages of a pipeline group (genes from GABRA), the workspace layout inside
+// the caller-provided device buffer, and the NCCL communicators.  Forward runs
+// every micro-batch through the local units in ascending order, receiving a
+// partition's input activation from the stage of the previous partition and
+// sending its output to the next; backward runs the chain rule in
+// reverse with the gradient of each partition input passed to partition i-1;
+// the step all-reduces the local partitions' gradients over the stage's
+// data-parallel group and applies SGD.
+#include "plan.h"
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "error.h"
+
+namespace rn {
+
+static const float BN_EPS = 1e-5f;       // reading X8
+static const float BN_MOMENTUM = 0.1f;   // reading X8
+
+size_t Plan::alloc(size_t bytes) {
+  size_t off = (ws_bytes + 255) & ~(size_t)255;
+  ws_bytes = off + ((bytes + 255) & ~(size_t)255);
+  return off;
+}
+
+void Plan::make_bn(BNL &b, int gamma_idx, int C, int64_t V) {
+  b.gamma_idx = gamma_idx;
+  b.C = C;
+  b.V = V;
+  b.run_off = bn_run_off[gamma_idx];
+  b.stat_off.resize(Mb);
+  for (int k = 0; k < Mb; ++k) b.stat_off[k] = alloc(4 * sizeof(float) * C);
+}
+
+void Plan::make_conv(ConvL &c, int w_idx, int Ci, int Co, int k, int s, int p, Dims in, Dims out) {
+  c.w_idx = w_idx;
+  c.g.N = mb;
+  c.g.Di = in.d; c.g.Hi = in.h; c.g.Wi = in.w; c.g.Ci = Ci;
+  c.g.Do = out.d; c.g.Ho = out.h; c.g.Wo = out.w; c.g.Co = Co;
+  c.g.k = k; c.g.s = s; c.g.p = p;
+  size_t wsf = conv_wgrad_ws_floats(c.g);
+  if (wsf > wgrad_ws_floats) wgrad_ws_floats = wsf;
+}
+
+size_t Plan::act_bytes(int C, Dims d) const { return (size_t)mb * d.vol() * C * dt_size(dt); }
+
+std::vector<size_t> Plan::per_mb(size_t bytes) {
+  std::vector<size_t> v(Mb);
+  for (int k = 0; k < Mb; ++k) v[k] = alloc(bytes);
+  return v;
+}
+
+void Plan::make_block(BlockL &b, int pidx, int cin, int cout, int stride, Dims in) {
+  b.cin = cin;
+  b.cout = cout;
+  b.in = in;
+  b.out = conv_out(in, 3, stride, 1);
+  b.proj = (stride != 1 || cin != cout);
+  const int64_t V = (int64_t)mb * b.out.vol();
+  make_conv(b.c1, pidx + 0, cin, cout, 3, stride, 1, in, b.out);
+  make_bn(b.b1, pidx + 1, cout, V);
+  make_conv(b.c2, pidx + 3, cout, cout, 3, 1, 1, b.out, b.out);
+  make_bn(b.b2, pidx + 4, cout, V);
+  if (b.proj) {
+    make_conv(b.cp, pidx + 6, cin, cout, 1, stride, 0, in, b.out);
+    make_bn(b.bp, pidx + 7, cout, V);
+  }
+  const size_t ab = act_bytes(cout, b.out);
+  b.h1 = per_mb(ab);
+  b.a1 = per_mb(ab);
+  b.h2 = per_mb(ab);
+  if (b.proj) b.hp = per_mb(ab);
+  b.out_ = per_mb(ab);
+  b.dh2 = alloc(ab);
+  b.da1 = alloc(ab);
+  b.dh1 = alloc(ab);
+  if (b.proj) b.dhp = alloc(ab);
+}
+
+int Plan::block_param_count(int cin, int cout, int stride) const {
+  return (stride != 1 || cin != cout) ? 9 : 6;
+}
+
+// ---------------------------------------------------------------------------
+Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int dtype, cudaStream_t st)
+    : net(build_net(nd)), stream(st) {
+  dt = dtype == RN_BF16 ? DT_BF16 : DT_F32;
+  rank = dd.rank;
+  world = dd.world;
+  S = dd.n_stages;
+  Mb = dd.micro_batches;
+  b = local_batch;
+  if (world < 1 || rank < 0 || rank >= world) throw Error(RN_ERR_ARG, "bad rank/world");
+  if (S < 1 || world % S != 0) throw Error(RN_ERR_ARG, "world must be a multiple of n_stages");
+  if (Mb < 1 || b < 1 || b % Mb != 0) throw Error(RN_ERR_ARG, "local_batch must be a positive multiple of micro_batches");
+  mb = b / Mb;
+  if (mb > 64) throw Error(RN_ERR_ARG, "micro-batch larger than 64");
+  replicas = world / S;
+  stage = rank % S;
+  replica = rank / S;
+  const int nparts = (int)net.part_loads.size();
+  genes.assign(nparts, 0);
+  if (S > 1) {
+    if (!dd.genes) throw Error(RN_ERR_ARG, "genes required when n_stages > 1");
+    for (int i = 0; i < nparts; ++i) {
+      genes[i] = dd.genes[i];
+      if (genes[i] < 0 || genes[i] >= S) throw Error(RN_ERR_ARG, "gene out of range");
+    }
+  }
+  const int nu = (int)net.units.size();
+  unit_stage.assign(nu, 0);
+  for (int p = 0; p < nparts; ++p)
+    for (int u = net.part_first[p]; u < net.part_first[p + 1]; ++u) unit_stage[u] = genes[p];
+  local.assign(nu, 0);
+  for (int u = 0; u < nu; ++u) local[u] = unit_stage[u] == stage;
+
+  // --- parameters (full model on every rank; only local ranges are used) ---
+  const int np = (int)net.params.size();
+  bn_run_off.assign(np, 0);
+  {
+    int64_t c = 0;
+    for (int i = 0; i < np; ++i)
+      if (net.params[i].kind == P_BN_GAMMA) {
+        bn_run_off[i] = c;
+        c += net.params[i].numel;
+      }
+  }
+  off_master = alloc(sizeof(float) * net.n_params);
+  off_grad = alloc(sizeof(float) * net.n_params);
+  off_run_mean = alloc(sizeof(float) * net.n_bn_channels);
+  off_run_var = alloc(sizeof(float) * net.n_bn_channels);
+  shadow_f.assign(np, 0);
+  shadow_d.assign(np, 0);
+  for (int i = 0; i < np; ++i) {
+    const ParamTensor &t = net.params[i];
+    if (t.kind != P_CONV || !local[t.unit]) continue;
+    if (dt == DT_BF16) {
+      shadow_f[i] = alloc(2 * t.numel);
+      shadow_d[i] = alloc(2 * t.numel);
+    }
+  }
+  off_loss = alloc(64);
+  off_flag = alloc(64);
+  off_x = alloc(sizeof(float) * (size_t)b * net.units[0].in.vol());
+  off_y = alloc(sizeof(int32_t) * (size_t)b);
+
+  // --- units ---
+  units.resize(nu);
+  for (int ui = 0; ui < nu; ++ui) {
+    const Unit &u = net.units[ui];
+    UnitL &L = units[ui];
+    L.kind = u.kind;
+    if (!local[ui]) continue;
+    const int p0 = net.unit_param_begin[ui];
+    if (u.kind == U_STEM) {
+      make_conv(L.stem_conv, p0, 1, u.cout, 3, u.stride, 1, u.in, u.conv);
+      make_bn(L.stem_bn, p0 + 1, u.cout, (int64_t)mb * u.conv.vol());
+      L.stem_h = per_mb(act_bytes(u.cout, u.conv));
+      L.out = per_mb(act_bytes(u.cout, u.out));
+      if (u.pool) L.am = per_mb((size_t)mb * u.out.vol() * u.cout);
+      L.tmp0 = alloc(act_bytes(u.cout, u.conv));
+      L.tmp1 = alloc(act_bytes(u.cout, u.conv));
+    } else if (u.kind == U_BLOCK) {
+      make_block(L.blk, p0, u.cin, u.cout, u.stride, u.in);
+      L.out = L.blk.out_;
+    } else if (u.kind == U_ATT) {
+      const int C = u.cout;
+      make_block(L.trunk, p0, C, C, 1, u.in);
+      const int p1 = p0 + 6;
+      make_block(L.mask, p1, C, C, 1, u.mask);
+      const int p2 = p1 + 6;
+      const int64_t V = (int64_t)mb * u.in.vol();
+      make_conv(L.mc1, p2, C, C, 1, 1, 0, u.in, u.in);
+      make_bn(L.mbn, p2 + 1, C, V);
+      make_conv(L.mc2, p2 + 3, C, C, 1, 1, 0, u.in, u.in);
+      L.bias_idx = p2 + 4;
+      const size_t ab = act_bytes(C, u.in), am_ = act_bytes(C, u.mask);
+      L.u0 = per_mb(am_);
+      L.am = per_mb((size_t)mb * u.mask.vol() * C);
+      L.up = per_mb(ab);
+      L.mh = per_mb(ab);
+      L.r = per_mb(ab);
+      L.m = per_mb(ab);
+      L.out = per_mb(ab);
+      L.dT = alloc(ab);
+      L.dm = alloc(ab);
+      L.dr = alloc(ab);
+      L.dmh = alloc(ab);
+      L.dup = alloc(ab);
+      L.dum = alloc(am_);
+      L.du0 = alloc(am_);
+      // trilinear tables (reading X11), mask dims -> unit dims
+      build_up_tables(L, u.mask, u.in);
+    } else {
+      L.g = per_mb(sizeof(float) * mb * u.cin);
+      L.dz = per_mb(sizeof(float) * mb * 2);
+    }
+  }
+  // gradient-of-output buffers and cut buffers
+  for (int ui = 0; ui < nu; ++ui) {
+    const Unit &u = net.units[ui];
+    UnitL &L = units[ui];
+    if (!local[ui]) continue;
+    if (u.kind != U_HEAD) L.dout = alloc(act_bytes(u.cout, u.out));
+    if (ui > 0 && !local[ui - 1]) {
+      // input comes from another stage: receive buffers (saved per micro-batch)
+      const Unit &pu = net.units[ui - 1];
+      L.recv_in = per_mb(act_bytes(pu.cout, pu.out));
+      L.send_dx = alloc(act_bytes(pu.cout, pu.out));
+    }
+  }
+  // scratch
+  nblk_max = 2 * 148;
+  off_partial = alloc(sizeof(float) * nblk_max * 2 * 512);
+  off_coef = alloc(sizeof(float) * 3 * 512 * 2);
+  off_wgrad_ws = alloc(sizeof(float) * (wgrad_ws_floats ? wgrad_ws_floats : 1));
+
+  // --- communicators ---
+  if (world > 1) {
+    world_comm = nccl_init(dd.nccl_id, world, rank);
+    pipe_comm = nccl_split(world_comm, replica, stage);
+    dp_comm = nccl_split(world_comm, stage, replica);
+  }
+}
+
+Plan::~Plan() {
+  for (auto &kv : up_dev) cudaFree(kv);
+  nccl_destroy(dp_comm);
+  nccl_destroy(pipe_comm);
+  nccl_destroy(world_comm);
+}
+
+void Plan::build_up_tables(UnitL &L, Dims in, Dims out) {
+  // 1-D linear maps per dim: src = max((o+1/2)*in/out - 1/2, 0), i0 = floor(src),
+  // i1 = min(i0+1, in-1), weights (1-lambda, lambda); adjoint as CSR per input index.
+  int ins[3] = {in.d, in.h, in.w}, outs[3] = {out.d, out.h, out.w};
+  for (int a = 0; a < 3; ++a) {
+    const int ni = ins[a], no = outs[a];
+    std::vector<int> fidx(2 * no);
+    std::vector<float> fw(2 * no);
+    std::vector<std::vector<std::pair<int, double>>> adj(ni);
+    const double scale = (double)ni / (double)no;
+    for (int o = 0; o < no; ++o) {
+      double src = ((double)o + 0.5) * scale - 0.5;
+      if (src < 0) src = 0;
+      int i0 = (int)std::floor(src);
+      if (i0 > ni - 1) i0 = ni - 1;
+      int i1 = i0 + 1 < ni ? i0 + 1 : ni - 1;
+      double lam = src - i0;
+      fidx[2 * o] = i0;
+      fidx[2 * o + 1] = i1;
+      fw[2 * o] = (float)(1.0 - lam);
+      fw[2 * o + 1] = (float)lam;
+      if (i0 == i1) {
+        adj[i0].push_back({o, 1.0});
+      } else {
+        adj[i0].push_back({o, 1.0 - lam});
+        adj[i1].push_back({o, lam});
+      }
+    }
+    std::vector<int> start(ni + 1, 0), bo;
+    std::vector<float> bw;
+    for (int i = 0; i < ni; ++i) {
+      start[i] = (int)bo.size();
+      for (auto &pr : adj[i]) {
+        bo.push_back(pr.first);
+        bw.push_back((float)pr.second);
+      }
+    }
+    start[ni] = (int)bo.size();
+    auto up = [&](const void *h, size_t bytes) -> void * {
+      void *d = nullptr;
+      CUDA_CHECK(cudaMalloc(&d, bytes ? bytes : 4));
+      if (bytes) CUDA_CHECK(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice));
+      up_dev.push_back(d);
+      return d;
+    };
+    L.tab.fw_idx[a] = (const int *)up(fidx.data(), fidx.size() * 4);
+    L.tab.fw_w[a] = (const float *)up(fw.data(), fw.size() * 4);
+    L.tab.bw_start[a] = (const int *)up(start.data(), start.size() * 4);
+    L.tab.bw_o[a] = (const int *)up(bo.data(), bo.size() * 4);
+    L.tab.bw_w[a] = (const float *)up(bw.data(), bw.size() * 4);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+float *Plan::master(int idx) { return (float *)P(off_master) + net.params[idx].canon_off; }
+float *Plan::grad(int idx) { return (float *)P(off_grad) + net.params[idx].canon_off; }
+const void *Plan::wfwd(int idx) { return dt == DT_F32 ? (const void *)master(idx) : P(shadow_f[idx]); }
+
+void Plan::conv_fwd(const ConvL &c, const void *x, void *y, const float *bias) {
+  conv_fprop_simt(dt, c.g, x, wfwd(c.w_idx), bias, y, stream);
+}
+void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumulate, const void *res,
+                         const void *res_mask) {
+  conv_dgrad_simt(dt, c.g, dy, wfwd(c.w_idx), dx, accumulate, res, res_mask, stream);
+}
+void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32) {
+  conv_wgrad_simt(dt, x_f32, c.g, x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), stream);
+}
+
+float *Plan::bn_stat(const BNL &b, int k, int which) { return (float *)P(b.stat_off[k]) + which * b.C; }
+
+void Plan::bn_forward_stats(const BNL &b, int k, const void *h) {
+  const int nblk = chan_reduce_blocks(b.V, b.C);
+  float *part = (float *)P(off_partial);
+  bn_stats(dt, h, b.V, b.C, part, nblk, stream);
+  bn_finalize(dt, h, part, nblk, b.V, b.C, master(b.gamma_idx), master(b.gamma_idx + 1), bn_stat(b, k, 0),
+              bn_stat(b, k, 1), bn_stat(b, k, 2), bn_stat(b, k, 3), (float *)P(off_run_mean) + b.run_off,
+              (float *)P(off_run_var) + b.run_off, BN_MOMENTUM, BN_EPS, stream);
+}
+
+// dx = BN-backward of dy' = dy * mask ; coef scratch slot `slot`
+void Plan::bn_backward(const BNL &b, int k, const void *dy, const void *h, int mask_mode, const void *mask_t,
+                       void *dx, int slot) {
+  const int nblk = chan_reduce_blocks(b.V, b.C);
+  float *part = (float *)P(off_partial);
+  float *coef = (float *)P(off_coef) + slot * 3 * 512;
+  bn_bwd_reduce(dt, dy, h, b.V, b.C, mask_mode, mask_t, bn_stat(b, k, 2), bn_stat(b, k, 3), bn_stat(b, k, 0),
+                bn_stat(b, k, 1), part, nblk, stream);
+  bn_bwd_finalize(part, nblk, b.V, b.C, master(b.gamma_idx), bn_stat(b, k, 0), bn_stat(b, k, 1),
+                  grad(b.gamma_idx), grad(b.gamma_idx + 1), coef, stream);
+  bn_bwd_apply(dt, dy, h, b.V, b.C, mask_mode, mask_t, bn_stat(b, k, 2), bn_stat(b, k, 3), coef, dx, stream);
+}
+
+// ---------------------------------------------------------------------------
+// residual network layer (two Conv blocks + skip)
+// ---------------------------------------------------------------------------
+void Plan::block_fwd(BlockL &B, int k, const void *x) {
+  conv_fwd(B.c1, x, P(B.h1[k]));
+  bn_forward_stats(B.b1, k, P(B.h1[k]));
+  const int64_t V = B.b1.V;
+  bn_apply(dt, P(B.h1[k]), V, B.cout, bn_stat(B.b1, k, 2), bn_stat(B.b1, k, 3), nullptr, nullptr, nullptr, true,
+           P(B.a1[k]), stream);
+  conv_fwd(B.c2, P(B.a1[k]), P(B.h2[k]));
+  bn_forward_stats(B.b2, k, P(B.h2[k]));
+  if (B.proj) {
+    conv_fwd(B.cp, x, P(B.hp[k]));
+    bn_forward_stats(B.bp, k, P(B.hp[k]));
+    bn_apply(dt, P(B.h2[k]), V, B.cout, bn_stat(B.b2, k, 2), bn_stat(B.b2, k, 3), P(B.hp[k]), bn_stat(B.bp, k, 2),
+             bn_stat(B.bp, k, 3), true, P(B.out_[k]), stream);
+  } else {
+    bn_apply(dt, P(B.h2[k]), V, B.cout, bn_stat(B.b2, k, 2), bn_stat(B.b2, k, 3), x, nullptr, nullptr, true,
+             P(B.out_[k]), stream);
+  }
+}
+
+void Plan::block_bwd(BlockL &B, int k, const void *x, const void *dout, void *dx, bool accumulate) {
+  const void *out = P(B.out_[k]);
+  bn_backward(B.b2, k, dout, P(B.h2[k]), MASK_TENSOR, out, P(B.dh2), 0);
+  if (B.proj) bn_backward(B.bp, k, dout, P(B.hp[k]), MASK_TENSOR, out, P(B.dhp), 1);
+  conv_bwd_weight(B.c2, P(B.a1[k]), P(B.dh2), false);
+  conv_bwd_data(B.c2, P(B.dh2), P(B.da1), false, nullptr, nullptr);
+  bn_backward(B.b1, k, P(B.da1), P(B.h1[k]), MASK_TENSOR, P(B.a1[k]), P(B.dh1), 0);
+  conv_bwd_weight(B.c1, x, P(B.dh1), false);
+  if (dx) {
+    if (B.proj) {
+      conv_bwd_data(B.c1, P(B.dh1), dx, accumulate, nullptr, nullptr);
+      conv_bwd_data(B.cp, P(B.dhp), dx, true, nullptr, nullptr);
+    } else {
+      // identity skip: dx (+)= dgrad(dh1) + dout * (out > 0)
+      conv_bwd_data(B.c1, P(B.dh1), dx, accumulate, dout, out);
+    }
+  }
+  if (B.proj) conv_bwd_weight(B.cp, x, P(B.dhp), false);
+}
+
+// ---------------------------------------------------------------------------
+// units
+// ---------------------------------------------------------------------------
+const void *Plan::unit_input(int ui, int k, const float *x_in) {
+  if (ui == 0) return x_in + (int64_t)k * mb * net.units[0].in.vol();
+  if (!local[ui - 1]) return P(units[ui].recv_in[k]);
+  return P(units[ui - 1].out[k]);
+}
+
+void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
+  const Unit &u = net.units[ui];
+  UnitL &L = units[ui];
+  const void *x = unit_input(ui, k, x_in);
+  if (u.kind == U_STEM) {
+    stem_conv_fprop(dt, L.stem_conv.g, (const float *)x, master(L.stem_conv.w_idx), P(L.stem_h[k]), stream);
+    bn_forward_stats(L.stem_bn, k, P(L.stem_h[k]));
+    if (u.pool) {
+      maxpool_fwd(dt, P(L.stem_h[k]), mb, u.conv.d, u.conv.h, u.conv.w, u.cout, bn_stat(L.stem_bn, k, 2),
+                  bn_stat(L.stem_bn, k, 3), true, P(L.out[k]), (uint8_t *)P(L.am[k]), u.out.d, u.out.h, u.out.w,
+                  stream);
+    } else {
+      bn_apply(dt, P(L.stem_h[k]), L.stem_bn.V, u.cout, bn_stat(L.stem_bn, k, 2), bn_stat(L.stem_bn, k, 3), nullptr,
+               nullptr, nullptr, true, P(L.out[k]), stream);
+    }
+  } else if (u.kind == U_BLOCK) {
+    block_fwd(L.blk, k, x);
+  } else if (u.kind == U_ATT) {
+    const int C = u.cout;
+    const int64_t V = (int64_t)mb * u.in.vol();
+    block_fwd(L.trunk, k, x);
+    maxpool_fwd(dt, x, mb, u.in.d, u.in.h, u.in.w, C, nullptr, nullptr, false, P(L.u0[k]), (uint8_t *)P(L.am[k]),
+                u.mask.d, u.mask.h, u.mask.w, stream);
+    block_fwd(L.mask, k, P(L.u0[k]));
+    upsample_fwd(dt, P(L.mask.out_[k]), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.up[k]), u.in.d, u.in.h, u.in.w,
+                 L.tab, stream);
+    conv_fwd(L.mc1, P(L.up[k]), P(L.mh[k]));
+    bn_forward_stats(L.mbn, k, P(L.mh[k]));
+    bn_apply(dt, P(L.mh[k]), V, C, bn_stat(L.mbn, k, 2), bn_stat(L.mbn, k, 3), nullptr, nullptr, nullptr, true,
+             P(L.r[k]), stream);
+    conv_fwd(L.mc2, P(L.r[k]), P(L.m[k]), master(L.bias_idx));
+    att_fwd(dt, P(L.m[k]), P(L.trunk.out_[k]), V, C, P(L.out[k]), stream);
+  } else {
+    const float dz_scale = 1.0f / (float)(mb * Mb * replicas);
+    head_fwd(dt, x, mb, (int)u.in.vol(), u.cin, master(net.unit_param_begin[ui]),
+             master(net.unit_param_begin[ui] + 1), y + (int64_t)k * mb, dz_scale, 1.0f / (float)Mb,
+             (float *)P(L.g[k]), (float *)P(L.dz[k]), (float *)P(off_loss), stream);
+  }
+}
+
+// dx target for unit ui's backward: previous unit's dout (local) or the send buffer
+void *Plan::unit_dx_target(int ui) {
+  if (ui == 0) return nullptr;
+  if (!local[ui - 1]) return P(units[ui].send_dx);
+  return P(units[ui - 1].dout);
+}
+
+void Plan::unit_bwd(int ui, int k, const float *x_in) {
+  const Unit &u = net.units[ui];
+  UnitL &L = units[ui];
+  const void *x = unit_input(ui, k, x_in);
+  void *dx = unit_dx_target(ui);
+  if (u.kind == U_STEM) {
+    const void *dy;
+    int mode;
+    const void *mt = nullptr;
+    if (u.pool) {
+      maxpool_bwd(dt, P(L.dout), (const uint8_t *)P(L.am[k]), mb, u.conv.d, u.conv.h, u.conv.w, u.cout, u.out.d,
+                  u.out.h, u.out.w, P(L.tmp0), false, stream);
+      dy = P(L.tmp0);
+      mode = MASK_RECOMPUTE;
+    } else {
+      dy = P(L.dout);
+      mode = MASK_TENSOR;
+      mt = P(L.out[k]);
+    }
+    bn_backward(L.stem_bn, k, dy, P(L.stem_h[k]), mode, mt, P(L.tmp1), 0);
+    conv_bwd_weight(L.stem_conv, x, P(L.tmp1), true);
+  } else if (u.kind == U_BLOCK) {
+    block_bwd(L.blk, k, x, P(L.dout), dx, false);
+  } else if (u.kind == U_ATT) {
+    const int C = u.cout;
+    const int64_t V = (int64_t)mb * u.in.vol();
+    const int nblk = chan_reduce_blocks(V, C);
+    float *part = (float *)P(off_partial);
+    att_bwd(dt, P(L.dout), P(L.m[k]), P(L.trunk.out_[k]), V, C, P(L.dT), P(L.dm), part, nblk, stream);
+    chan_sum_finalize(part, nblk, C, grad(L.bias_idx), stream);
+    conv_bwd_weight(L.mc2, P(L.r[k]), P(L.dm), false);
+    conv_bwd_data(L.mc2, P(L.dm), P(L.dr), false, nullptr, nullptr);
+    bn_backward(L.mbn, k, P(L.dr), P(L.mh[k]), MASK_TENSOR, P(L.r[k]), P(L.dmh), 0);
+    conv_bwd_weight(L.mc1, P(L.up[k]), P(L.dmh), false);
+    conv_bwd_data(L.mc1, P(L.dmh), P(L.dup), false, nullptr, nullptr);
+    upsample_bwd(dt, P(L.dup), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.dum), u.in.d, u.in.h, u.in.w, L.tab, stream);
+    block_bwd(L.mask, k, P(L.u0[k]), P(L.dum), P(L.du0), false);
+    maxpool_bwd(dt, P(L.du0), (const uint8_t *)P(L.am[k]), mb, u.in.d, u.in.h, u.in.w, C, u.mask.d, u.mask.h,
+                u.mask.w, dx, false, stream);
+    block_bwd(L.trunk, k, x, P(L.dT), dx, true);
+  } else {
+    const int p0 = net.unit_param_begin[ui];
+    head_bwd(dt, (const float *)P(L.dz[k]), (const float *)P(L.g[k]), master(p0), mb, (int)u.in.vol(), u.cin,
+             grad(p0), grad(p0 + 1), dx, stream);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// step phases
+// ---------------------------------------------------------------------------
+void Plan::forward(const float *x_in, const int32_t *y) {
+  CUDA_CHECK(cudaMemsetAsync(P(off_loss), 0, sizeof(float), stream));
+  const int nu = (int)net.units.size();
+  for (int k = 0; k < Mb; ++k) {
+    for (int ui = 0; ui < nu; ++ui) {
+      if (!local[ui]) continue;
+      if (ui > 0 && !local[ui - 1]) {
+        const Unit &pu = net.units[ui - 1];
+        nccl_recv_bytes(pipe_comm, P(units[ui].recv_in[k]), act_bytes(pu.cout, pu.out), unit_stage[ui - 1], stream);
+      }
+      unit_fwd(ui, k, x_in, y);
+      if (ui + 1 < nu && !local[ui + 1]) {
+        const Unit &u = net.units[ui];
+        nccl_send_bytes(pipe_comm, P(units[ui].out[k]), act_bytes(u.cout, u.out), unit_stage[ui + 1], stream);
+      }
+    }
+  }
+  if (S > 1) nccl_bcast_f32(pipe_comm, (float *)P(off_loss), 1, unit_stage[nu - 1], stream);
+  fwd_done = true;
+}
+
+void Plan::backward(const float *x_in) {
+  CUDA_CHECK(cudaMemsetAsync(P(off_grad), 0, sizeof(float) * net.n_params, stream));
+  const int nu = (int)net.units.size();
+  for (int k = 0; k < Mb; ++k) {
+    for (int ui = nu - 1; ui >= 0; --ui) {
+      if (!local[ui]) continue;
+      if (ui + 1 < nu && !local[ui + 1]) {
+        const Unit &u = net.units[ui];
+        nccl_recv_bytes(pipe_comm, P(units[ui].dout), act_bytes(u.cout, u.out), unit_stage[ui + 1], stream);
+      }
+      unit_bwd(ui, k, x_in);
+      if (ui > 0 && !local[ui - 1]) {
+        const Unit &pu = net.units[ui - 1];
+        nccl_send_bytes(pipe_comm, P(units[ui].send_dx), act_bytes(pu.cout, pu.out), unit_stage[ui - 1], stream);
+      }
+    }
+  }
+}
+
+// contiguous parameter ranges (in the flat buffer) of the local units
+std::vector<std::pair<int64_t, int64_t>> Plan::local_ranges() const {
+  std::vector<std::pair<int64_t, int64_t>> r;
+  const int nu = (int)net.units.size();
+  for (int ui = 0; ui < nu; ++ui) {
+    if (!local[ui]) continue;
+    const int a = net.unit_param_begin[ui], e = net.unit_param_end[ui];
+    if (a == e) continue;
+    int64_t s = net.params[a].canon_off;
+    int64_t t = net.params[e - 1].canon_off + net.params[e - 1].numel;
+    if (!r.empty() && r.back().second == s)
+      r.back().second = t;
+    else
+      r.push_back({s, t});
+  }
+  return r;
+}
+
+void Plan::step(float lr) {
+  auto ranges = local_ranges();
+  if (replicas > 1)
+    for (auto &rg : ranges)
+      nccl_allreduce_sum_f32(dp_comm, (float *)P(off_grad) + rg.first, (size_t)(rg.second - rg.first), stream);
+  for (auto &rg : ranges)
+    sgd_update((float *)P(off_master) + rg.first, (const float *)P(off_grad) + rg.first, rg.second - rg.first, lr,
+               stream);
+  refresh_shadows();
+}
+
+void Plan::refresh_shadows() {
+  if (dt != DT_BF16) return;
+  for (int i = 0; i < (int)net.params.size(); ++i) {
+    const ParamTensor &t = net.params[i];
+    if (t.kind != P_CONV || !local[t.unit]) continue;
+    const int taps = (int)(t.shape[2] * t.shape[3] * t.shape[4]);
+    repack_conv(dt, master(i), (int)t.shape[0], taps, (int)t.shape[1], P(shadow_f[i]), P(shadow_d[i]), stream);
+  }
+}
+
+void Plan::bind(void *dev, size_t bytes) {
+  if (bytes < ws_bytes) throw Error(RN_ERR_SIZE, "workspace smaller than required");
+  if (((uintptr_t)dev & 255) != 0) throw Error(RN_ERR_ARG, "workspace must be 256-byte aligned");
+  base = (char *)dev;
+}
+
+// canonical conv W[Co][Ci][kd][kh][kw] <-> internal [Co][tap][Ci]
+void Plan::canon_to_internal(const float *src, std::vector<float> &dst) const {
+  dst.assign(src, src + net.n_params);
+  for (const ParamTensor &t : net.params) {
+    if (t.kind != P_CONV) continue;
+    const int64_t Co = t.shape[0], Ci = t.shape[1], taps = t.shape[2] * t.shape[3] * t.shape[4];
+    const float *s = src + t.canon_off;
+    float *d = dst.data() + t.canon_off;
+    for (int64_t co = 0; co < Co; ++co)
+      for (int64_t ci = 0; ci < Ci; ++ci)
+        for (int64_t tap = 0; tap < taps; ++tap) d[(co * taps + tap) * Ci + ci] = s[(co * Ci + ci) * taps + tap];
+  }
+}
+
+void Plan::internal_to_canon(const float *src, float *dst) const {
+  memcpy(dst, src, sizeof(float) * net.n_params);
+  for (const ParamTensor &t : net.params) {
+    if (t.kind != P_CONV) continue;
+    const int64_t Co = t.shape[0], Ci = t.shape[1], taps = t.shape[2] * t.shape[3] * t.shape[4];
+    const float *s = src + t.canon_off;
+    float *d = dst + t.canon_off;
+    for (int64_t co = 0; co < Co; ++co)
+      for (int64_t ci = 0; ci < Ci; ++ci)
+        for (int64_t tap = 0; tap < taps; ++tap) d[(co * Ci + ci) * taps + tap] = s[(co * taps + tap) * Ci + ci];
+  }
+}
+
+void Plan::set_params(const float *host) {
+  std::vector<float> tmp;
+  canon_to_internal(host, tmp);
+  CUDA_CHECK(cudaMemcpyAsync(P(off_master), tmp.data(), sizeof(float) * net.n_params, cudaMemcpyHostToDevice, stream));
+  std::vector<float> z(net.n_bn_channels, 0.f), o(net.n_bn_channels, 1.f);
+  CUDA_CHECK(cudaMemcpyAsync(P(off_run_mean), z.data(), sizeof(float) * z.size(), cudaMemcpyHostToDevice, stream));
+  CUDA_CHECK(cudaMemcpyAsync(P(off_run_var), o.data(), sizeof(float) * o.size(), cudaMemcpyHostToDevice, stream));
+  CUDA_CHECK(cudaMemsetAsync(P(off_grad), 0, sizeof(float) * net.n_params, stream));
+  refresh_shadows();
+  CUDA_CHECK(cudaStreamSynchronize(stream));
+  params_set = true;
+}
+
+void Plan::get_flat(size_t off, float *host) {
+  std::vector<float> tmp(net.n_params);
+  CUDA_CHECK(cudaStreamSynchronize(stream));
+  CUDA_CHECK(cudaMemcpy(tmp.data(), P(off), sizeof(float) * net.n_params, cudaMemcpyDeviceToHost));
+  internal_to_canon(tmp.data(), host);
+}
+
+// inputs are copied into plan-owned buffers so the step's pointers are fixed
+// (CUDA-graph capturable) and x stays valid for the stem's weight gradient.
+void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
+  const cudaMemcpyKind kind = from_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  if (local[0] && x)
+    CUDA_CHECK(cudaMemcpyAsync(P(off_x), x, sizeof(float) * (size_t)b * net.units[0].in.vol(), kind, stream));
+  if (local[net.units.size() - 1] && y)
+    CUDA_CHECK(cudaMemcpyAsync(P(off_y), y, sizeof(int32_t) * (size_t)b, kind, stream));
+}
+
+rn_status Plan::set_option(const std::string &k, int64_t v) {
+  if (k != "graphs" && k != "tc_conv" && k != "time_kernels") return set_error(RN_ERR_ARG, "unknown option " + k);
+  opts[k] = v;
+  return RN_OK;
+}
+
+rn_status Plan::query(const std::string &k, double *v) {
+  auto it = stats.find(k);
+  if (it == stats.end()) return set_error(RN_ERR_ARG, "unknown statistic " + k);
+  *v = it->second;
+  return RN_OK;
+}
+
+float Plan::read_loss() {
+  float l = 0.f;
+  CUDA_CHECK(cudaMemcpyAsync(&l, P(off_loss), sizeof(float), cudaMemcpyDeviceToHost, stream));
+  CUDA_CHECK(cudaStreamSynchronize(stream));
+  return l;
+}
+
+}  // namespace rn

@@ -1,0 +1,144 @@
+// plan.h — per-rank executor state (see plan.cpp).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/rn.h"
+#include "comm.h"
+#include "kernels.h"
+#include "net.h"
+
+namespace rn {
+
+struct BNL {
+  int gamma_idx = -1;  // param index of gamma (beta = +1)
+  int C = 0;
+  int64_t V = 0;       // voxels per micro-batch
+  int64_t run_off = 0;
+  std::vector<size_t> stat_off;  // per micro-batch: mean, invstd, scale, shift [4][C]
+};
+
+struct ConvL {
+  int w_idx = -1;
+  ConvGeom g{};
+};
+
+struct BlockL {
+  int cin = 0, cout = 0;
+  Dims in, out;
+  bool proj = false;
+  ConvL c1, c2, cp;
+  BNL b1, b2, bp;
+  std::vector<size_t> h1, a1, h2, hp, out_;  // saved per micro-batch
+  size_t dh2 = 0, da1 = 0, dh1 = 0, dhp = 0;  // backward temporaries
+};
+
+struct UnitL {
+  int kind = 0;
+  std::vector<size_t> out;    // unit output per micro-batch
+  size_t dout = 0;            // gradient w.r.t. the unit output
+  std::vector<size_t> recv_in;  // input received from another stage (per micro-batch)
+  size_t send_dx = 0;           // gradient of the input, sent to the previous stage
+  // stem
+  ConvL stem_conv;
+  BNL stem_bn;
+  std::vector<size_t> stem_h, am;
+  size_t tmp0 = 0, tmp1 = 0;
+  // block
+  BlockL blk;
+  // attention
+  BlockL trunk, mask;
+  ConvL mc1, mc2;
+  BNL mbn;
+  int bias_idx = -1;
+  std::vector<size_t> u0, up, mh, r, m;
+  size_t dT = 0, dm = 0, dr = 0, dmh = 0, dup = 0, dum = 0, du0 = 0;
+  UpTables tab{};
+  // head
+  std::vector<size_t> g, dz;
+};
+
+struct Plan {
+  NetModel net;
+  DType dt;
+  cudaStream_t stream;
+  int rank = 0, world = 1, S = 1, Mb = 1, b = 1, mb = 1, replicas = 1, stage = 0, replica = 0;
+  std::vector<int> genes, unit_stage;
+  std::vector<char> local;
+  std::vector<int64_t> bn_run_off;
+  std::vector<size_t> shadow_f, shadow_d;
+  size_t off_master = 0, off_grad = 0, off_run_mean = 0, off_run_var = 0, off_loss = 0, off_flag = 0;
+  size_t off_partial = 0, off_coef = 0, off_wgrad_ws = 0, off_x = 0, off_y = 0;
+  size_t wgrad_ws_floats = 0;
+  int nblk_max = 0;
+  size_t ws_bytes = 0;
+  char *base = nullptr;
+  std::vector<UnitL> units;
+  std::vector<void *> up_dev;
+  NcclComm *world_comm = nullptr, *pipe_comm = nullptr, *dp_comm = nullptr;
+  bool params_set = false, fwd_done = false;
+  const float *last_x = nullptr;
+
+  Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int dtype, cudaStream_t st);
+  ~Plan();
+
+  // workspace
+  size_t alloc(size_t bytes);
+  std::vector<size_t> per_mb(size_t bytes);
+  void *P(size_t off) { return base + off; }
+  size_t act_bytes(int C, Dims d) const;
+  void make_bn(BNL &b, int gamma_idx, int C, int64_t V);
+  void make_conv(ConvL &c, int w_idx, int Ci, int Co, int k, int s, int p, Dims in, Dims out);
+  void make_block(BlockL &b, int pidx, int cin, int cout, int stride, Dims in);
+  int block_param_count(int cin, int cout, int stride) const;
+  void build_up_tables(UnitL &L, Dims in, Dims out);
+
+  // params
+  float *master(int idx);
+  float *grad(int idx);
+  const void *wfwd(int idx);
+  float *bn_stat(const BNL &b, int k, int which);
+
+  // ops
+  void conv_fwd(const ConvL &c, const void *x, void *y, const float *bias = nullptr);
+  void conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumulate, const void *res,
+                     const void *res_mask);
+  void conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32);
+  void bn_forward_stats(const BNL &b, int k, const void *h);
+  void bn_backward(const BNL &b, int k, const void *dy, const void *h, int mask_mode, const void *mask_t, void *dx,
+                   int slot);
+  void block_fwd(BlockL &B, int k, const void *x);
+  void block_bwd(BlockL &B, int k, const void *x, const void *dout, void *dx, bool accumulate);
+  const void *unit_input(int ui, int k, const float *x_in);
+  void *unit_dx_target(int ui);
+  void unit_fwd(int ui, int k, const float *x_in, const int32_t *y);
+  void unit_bwd(int ui, int k, const float *x_in);
+
+  // phases
+  void bind(void *dev, size_t bytes);
+  void stage_inputs(const float *x_dev, const int32_t *y_dev, bool from_host);
+  void forward(const float *x_in, const int32_t *y);
+  void backward(const float *x_in);
+  void step(float lr);
+  void refresh_shadows();
+  std::vector<std::pair<int64_t, int64_t>> local_ranges() const;
+
+  // host I/O
+  void canon_to_internal(const float *src, std::vector<float> &dst) const;
+  void internal_to_canon(const float *src, float *dst) const;
+  void set_params(const float *host);
+  void get_flat(size_t off, float *host);
+  float read_loss();
+  // options / statistics
+  std::map<std::string, int64_t> opts;
+  std::map<std::string, double> stats;
+  rn_status set_option(const std::string &k, int64_t v);
+  rn_status query(const std::string &k, double *v);
+};
+
+}  // namespace rn
