@@ -176,6 +176,13 @@ rn_status rn_get_grads(rn_plan_t plan, float *host, int64_t count);
  * (count = n_bn_channels from rn_net_param_count). */
 rn_status rn_get_bn_running(rn_plan_t plan, float *mean_host, float *var_host, int64_t count);
 
+/* rn_get_activation — copy the output of top-level unit `unit` for micro-batch
+ * `micro_batch` of the last rn_forward to host as float32 NDHWC
+ * [mb][D][H][W][C] (count must equal that size; the head's output is the
+ * logits-free GAP vector [mb][C]).  Only for units placed on this rank.
+ * Errors: RN_ERR_ARG (unit not local / out of range), RN_ERR_SIZE. */
+rn_status rn_get_activation(rn_plan_t plan, int32_t unit, int32_t micro_batch, float *host, int64_t count);
+
 /* rn_forward — forward pass of this replica's local batch.
  *  x_dev : float32 [b][D][H][W] input volumes (device), y_dev: int32 [b] labels in {0,1}
  *          (only read on the stages that need them: stage of the first / last partition)

@@ -300,24 +300,45 @@ class BNState:
         self.var[name] = (1 - BN_MOMENTUM) * self.var[name] + BN_MOMENTUM * cache["var_unbiased"]
 
 
+# Storage rounding (reading X23 (ii)): with Net(..., store="bf16")
+# every value the RN_BF16 GPU path STORES in bf16 (conv outputs, BN-apply
+# outputs, pooled / upsampled / attention tensors, every activation gradient,
+# conv weight copies) is rounded to bf16 (round-to-nearest-even of the fp32
+# value) at that point; the arithmetic stays float64.  store="f64" (default)
+# makes Q and QW the identity, i.e. the plain definition.
+def _bf16_round(a):
+    f = np.asarray(a, dtype=np.float32)
+    b = f.view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    return b.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def _identity(a):
+    return a
+
+
+Q = _identity     # rounding of stored activations / gradients
+QW = _identity    # rounding of the conv weights the kernels read
+
+
 def block_forward(P, pre, x, stride, bns):
     c = {}
     c["x"] = x
-    h1 = conv3d(x, P[pre + ".conv1"], stride, 1)
+    h1 = Q(conv3d(x, QW(P[pre + ".conv1"]), stride, 1))
     y1, c["bn1"] = bn_forward(h1, P[pre + ".bn1.gamma"], P[pre + ".bn1.beta"])
-    a1 = relu(y1)
+    a1 = Q(relu(y1))
     c["a1"] = a1
-    h2 = conv3d(a1, P[pre + ".conv2"], 1, 1)
+    h2 = Q(conv3d(a1, QW(P[pre + ".conv2"]), 1, 1))
     y2, c["bn2"] = bn_forward(h2, P[pre + ".bn2.gamma"], P[pre + ".bn2.beta"])
     if (pre + ".proj") in P.d:
-        hp = conv3d(x, P[pre + ".proj"], stride, 0)
+        hp = Q(conv3d(x, QW(P[pre + ".proj"]), stride, 0))
         skip, c["bnp"] = bn_forward(hp, P[pre + ".projbn.gamma"], P[pre + ".projbn.beta"])
         c["proj"] = True
     else:
         skip = x
         c["proj"] = False
     z = y2 + skip
-    out = relu(z)
+    out = Q(relu(z))
     c["out"] = out
     for k, n in (("bn1", ".bn1"), ("bn2", ".bn2"), ("bnp", ".projbn")):
         if k in c:
@@ -325,19 +346,26 @@ def block_forward(P, pre, x, stride, bns):
     return out, c
 
 
-def block_backward(P, pre, dout, c, stride, G):
+def block_backward(P, pre, dout, c, stride, G, dx_acc=None):
+    """dx_acc: gradient already accumulated into the input (attention: the mask
+    branch); the result is dx_acc + this block's input gradient."""
     dz = dout * (c["out"] > 0)
     dh2, G[pre + ".bn2.gamma"], G[pre + ".bn2.beta"] = bn_backward(dz, c["bn2"], P[pre + ".bn2.gamma"])
-    da1, G[pre + ".conv2"] = conv3d_backward(c["a1"], P[pre + ".conv2"], dh2, 1, 1)
+    dh2 = Q(dh2)
+    da1, G[pre + ".conv2"] = conv3d_backward(c["a1"], QW(P[pre + ".conv2"]), dh2, 1, 1)
+    da1 = Q(da1)
     dy1 = da1 * (c["a1"] > 0)
     dh1, G[pre + ".bn1.gamma"], G[pre + ".bn1.beta"] = bn_backward(dy1, c["bn1"], P[pre + ".bn1.gamma"])
-    dx, G[pre + ".conv1"] = conv3d_backward(c["x"], P[pre + ".conv1"], dh1, stride, 1)
+    dh1 = Q(dh1)
+    dx, G[pre + ".conv1"] = conv3d_backward(c["x"], QW(P[pre + ".conv1"]), dh1, stride, 1)
+    acc = 0.0 if dx_acc is None else dx_acc
     if c["proj"]:
         dhp, G[pre + ".projbn.gamma"], G[pre + ".projbn.beta"] = bn_backward(dz, c["bnp"], P[pre + ".projbn.gamma"])
-        dxp, G[pre + ".proj"] = conv3d_backward(c["x"], P[pre + ".proj"], dhp, stride, 0)
-        dx = dx + dxp
+        dhp = Q(dhp)
+        dxp, G[pre + ".proj"] = conv3d_backward(c["x"], QW(P[pre + ".proj"]), dhp, stride, 0)
+        dx = Q(Q(acc + dx) + dxp)
     else:
-        dx = dx + dz
+        dx = Q(acc + dx + dz)
     return dx
 
 
@@ -346,15 +374,17 @@ def unit_forward(P, ui, u, x, bns):
     c = {}
     if u.kind == "stem":
         c["x"] = x
-        h = conv3d(x, P[pre + ".conv"], u.stride, 1)
+        h = Q(conv3d(x, P[pre + ".conv"], u.stride, 1))      # stem reads fp32 master weights
         y, c["bn"] = bn_forward(h, P[pre + ".bn.gamma"], P[pre + ".bn.beta"])
         bns.append((pre + ".bn", c["bn"]))
         a = relu(y)
         c["a"] = a
         if u.extra["pool"]:
             out, c["am"] = maxpool3(a)
+            out = Q(out)
         else:
-            out = a
+            out = Q(a)
+            c["a"] = out
         return out, c
     if u.kind == "block":
         return block_forward(P, pre, x, u.stride, bns)
@@ -364,17 +394,17 @@ def unit_forward(P, ui, u, x, bns):
         c["x_shape"] = x.shape
         um, c["mask"] = block_forward(P, pre + ".mask", u0, 1, bns)
         c["um_dims"] = um.shape[1:4]
-        up = upsample_trilinear(um, T.shape[1:4])
+        up = Q(upsample_trilinear(um, T.shape[1:4]))
         c["up"] = up
-        h = conv3d(up, P[pre + ".mconv1"], 1, 0)
+        h = Q(conv3d(up, QW(P[pre + ".mconv1"]), 1, 0))
         y, c["mbn"] = bn_forward(h, P[pre + ".mbn.gamma"], P[pre + ".mbn.beta"])
         bns.append((pre + ".mbn", c["mbn"]))
-        r = relu(y)
+        r = Q(relu(y))
         c["r"] = r
-        m = conv3d(r, P[pre + ".mconv2"], 1, 0) + P[pre + ".mconv2.bias"]
+        m = Q(conv3d(r, QW(P[pre + ".mconv2"]), 1, 0) + P[pre + ".mconv2.bias"])
         sg = sigmoid(m)
         c["sg"], c["T"] = sg, T
-        return (1.0 + sg) * T, c
+        return Q((1.0 + sg) * T), c
     if u.kind == "head":
         c["x_shape"] = x.shape
         g = x.mean(axis=(1, 2, 3))                     # GAP
@@ -387,34 +417,38 @@ def unit_forward(P, ui, u, x, bns):
 def unit_backward(P, ui, u, dout, c, G):
     pre = f"u{ui}"
     if u.kind == "stem":
-        da = maxpool3_backward(dout, c["am"], c["a"].shape) if u.extra["pool"] else dout
+        da = Q(maxpool3_backward(dout, c["am"], c["a"].shape)) if u.extra["pool"] else dout
         dy = da * (c["a"] > 0)
         dh, G[pre + ".bn.gamma"], G[pre + ".bn.beta"] = bn_backward(dy, c["bn"], P[pre + ".bn.gamma"])
+        dh = Q(dh)
         _, G[pre + ".conv"] = conv3d_backward(c["x"], P[pre + ".conv"], dh, u.stride, 1, need_dx=False)
         return None
     if u.kind == "block":
         return block_backward(P, pre, dout, c, u.stride, G)
     if u.kind == "att":
         sg, T = c["sg"], c["T"]
-        dT = dout * (1.0 + sg)
+        dT = Q(dout * (1.0 + sg))
         dm = dout * T * sg * (1.0 - sg)
         G[pre + ".mconv2.bias"] = dm.sum(axis=(0, 1, 2, 3))
-        dr, G[pre + ".mconv2"] = conv3d_backward(c["r"], P[pre + ".mconv2"], dm, 1, 0)
+        dm = Q(dm)
+        dr, G[pre + ".mconv2"] = conv3d_backward(c["r"], QW(P[pre + ".mconv2"]), dm, 1, 0)
+        dr = Q(dr)
         dy = dr * (c["r"] > 0)
         dh, G[pre + ".mbn.gamma"], G[pre + ".mbn.beta"] = bn_backward(dy, c["mbn"], P[pre + ".mbn.gamma"])
-        dup, G[pre + ".mconv1"] = conv3d_backward(c["up"], P[pre + ".mconv1"], dh, 1, 0)
-        dum = upsample_trilinear_backward(dup, c["um_dims"])
+        dh = Q(dh)
+        dup, G[pre + ".mconv1"] = conv3d_backward(c["up"], QW(P[pre + ".mconv1"]), dh, 1, 0)
+        dup = Q(dup)
+        dum = Q(upsample_trilinear_backward(dup, c["um_dims"]))
         du0 = block_backward(P, pre + ".mask", dum, c["mask"], 1, G)
-        dx_mask = maxpool3_backward(du0, c["am"], c["x_shape"])
-        dx_trunk = block_backward(P, pre + ".trunk", dT, c["trunk"], 1, G)
-        return dx_trunk + dx_mask
+        dx_mask = Q(maxpool3_backward(du0, c["am"], c["x_shape"]))
+        return block_backward(P, pre + ".trunk", dT, c["trunk"], 1, G, dx_acc=dx_mask)
     if u.kind == "head":
         dz = dout
         G[pre + ".fc.weight"] = dz.T @ c["g"]
         G[pre + ".fc.bias"] = dz.sum(axis=0)
         dg = dz @ P[pre + ".fc.weight"]
         N, D, H, W, C = c["x_shape"]
-        return np.broadcast_to(dg[:, None, None, None, :] / (D * H * W), c["x_shape"]).copy()
+        return Q(np.broadcast_to(dg[:, None, None, None, :] / (D * H * W), c["x_shape"]).copy())
     raise ValueError(u.kind)
 
 
@@ -435,7 +469,9 @@ def softmax_ce(z, y):
 # ----------------------------------------------------------------------------
 
 class Net:
-    def __init__(self, depth: int, base_width: int, in_dims):
+    def __init__(self, depth: int, base_width: int, in_dims, store: str = "f64"):
+        assert store in ("f64", "bf16")
+        self.store = store
         self.depth, self.base_width, self.in_dims = depth, base_width, tuple(in_dims)
         self.units = build_units(depth, base_width, in_dims)
         self.tensors = param_tensors(self.units)
@@ -449,6 +485,14 @@ class Net:
         """One micro-batch: forward with train-mode BN, loss, backward.
         x float [N,D,H,W] (single input channel), y int [N].
         Returns (loss, grads dict scaled by loss_scale)."""
+        global Q, QW
+        Q = QW = (_bf16_round if self.store == "bf16" else _identity)
+        try:
+            return self._forward_backward(P, x, y, loss_scale, bnstate)
+        finally:
+            Q = QW = _identity
+
+    def _forward_backward(self, P, x, y, loss_scale, bnstate):
         h = np.asarray(x, dtype=np.float64)[..., None]
         caches = []
         bns = []

@@ -210,6 +210,33 @@ rn_status rn_get_bn_running(rn_plan_t plan, float *mean_host, float *var_host, i
   GUARD_END
 }
 
+rn_status rn_get_activation(rn_plan_t plan, int32_t unit, int32_t micro_batch, float *host, int64_t count) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  Plan *p = plan->p;
+  if (!host || unit < 0 || unit >= (int)p->net.units.size() || !p->local[unit] || micro_batch < 0 ||
+      micro_batch >= p->Mb)
+    return set_error(RN_ERR_ARG, "rn_get_activation: bad unit / micro-batch");
+  const Unit &u = p->net.units[unit];
+  const bool head = u.kind == U_HEAD;
+  const int64_t n = head ? (int64_t)p->mb * u.cin : (int64_t)p->mb * u.out.vol() * u.cout;
+  if (count != n) return set_error(RN_ERR_SIZE, "rn_get_activation: count mismatch");
+  CUDA_CHECK(cudaStreamSynchronize(p->stream));
+  const void *src = head ? p->P(p->units[unit].g[micro_batch]) : p->P(p->units[unit].out[micro_batch]);
+  if (head || p->dt == DT_F32) {
+    CUDA_CHECK(cudaMemcpy(host, src, 4 * n, cudaMemcpyDeviceToHost));
+  } else {
+    std::vector<uint16_t> tmp(n);
+    CUDA_CHECK(cudaMemcpy(tmp.data(), src, 2 * n, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i) {
+      uint32_t b = (uint32_t)tmp[i] << 16;
+      memcpy(&host[i], &b, 4);
+    }
+  }
+  return RN_OK;
+  GUARD_END
+}
+
 static rn_status finish_loss(Plan *p, float *loss_host) {
   if (!loss_host) return RN_OK;
   float l = p->read_loss();

@@ -297,15 +297,47 @@ float *Plan::master(int idx) { return (float *)P(off_master) + net.params[idx].c
 float *Plan::grad(int idx) { return (float *)P(off_grad) + net.params[idx].canon_off; }
 const void *Plan::wfwd(int idx) { return dt == DT_F32 ? (const void *)master(idx) : P(shadow_f[idx]); }
 
+static double conv_flops(const ConvGeom &g) { return 2.0 * (double)g.out_vox() * g.Co * g.Ci * g.taps(); }
+
+bool Plan::timing() const {
+  auto it = opts.find("time_kernels");
+  return it != opts.end() && it->second != 0;
+}
+
+size_t Plan::tk_begin(int cls, double flops) {
+  if (ev_used == ev_pool.size()) {
+    EvPair e;
+    CUDA_CHECK(cudaEventCreate(&e.a));
+    CUDA_CHECK(cudaEventCreate(&e.b));
+    ev_pool.push_back(e);
+  }
+  EvPair &e = ev_pool[ev_used];
+  e.flops = flops;
+  e.cls = cls;
+  CUDA_CHECK(cudaEventRecord(e.a, stream));
+  return ev_used++;
+}
+
+void Plan::tk_end(size_t i) { CUDA_CHECK(cudaEventRecord(ev_pool[i].b, stream)); }
+
 void Plan::conv_fwd(const ConvL &c, const void *x, void *y, const float *bias) {
+  const bool t = timing();
+  size_t e = t ? tk_begin(0, conv_flops(c.g)) : 0;
   conv_fprop_simt(dt, c.g, x, wfwd(c.w_idx), bias, y, stream);
+  if (t) tk_end(e);
 }
 void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumulate, const void *res,
                          const void *res_mask) {
+  const bool t = timing();
+  size_t e = t ? tk_begin(1, conv_flops(c.g)) : 0;
   conv_dgrad_simt(dt, c.g, dy, wfwd(c.w_idx), dx, accumulate, res, res_mask, stream);
+  if (t) tk_end(e);
 }
 void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32) {
+  const bool t = timing();
+  size_t e = t ? tk_begin(2, conv_flops(c.g)) : 0;
   conv_wgrad_simt(dt, x_f32, c.g, x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), stream);
+  if (t) tk_end(e);
 }
 
 float *Plan::bn_stat(const BNL &b, int k, int which) { return (float *)P(b.stat_off[k]) + which * b.C; }
@@ -625,10 +657,33 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 rn_status Plan::set_option(const std::string &k, int64_t v) {
   if (k != "graphs" && k != "tc_conv" && k != "time_kernels") return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
+  if (k == "time_kernels") ev_used = 0;
   return RN_OK;
 }
 
 rn_status Plan::query(const std::string &k, double *v) {
+  if (k.rfind("conv_", 0) == 0) {
+    // conv_ms / conv_flops / conv_launches, optionally suffixed _fprop/_dgrad/_wgrad
+    CUDA_CHECK(cudaStreamSynchronize(stream));
+    int cls = -1;
+    if (k.find("_fprop") != std::string::npos) cls = 0;
+    if (k.find("_dgrad") != std::string::npos) cls = 1;
+    if (k.find("_wgrad") != std::string::npos) cls = 2;
+    double ms = 0, fl = 0, n = 0;
+    for (size_t i = 0; i < ev_used; ++i) {
+      if (cls >= 0 && ev_pool[i].cls != cls) continue;
+      float e = 0.f;
+      CUDA_CHECK(cudaEventElapsedTime(&e, ev_pool[i].a, ev_pool[i].b));
+      ms += e;
+      fl += ev_pool[i].flops;
+      n += 1;
+    }
+    if (k.rfind("conv_ms", 0) == 0) *v = ms;
+    else if (k.rfind("conv_flops", 0) == 0) *v = fl;
+    else if (k.rfind("conv_launches", 0) == 0) *v = n;
+    else return set_error(RN_ERR_ARG, "unknown statistic " + k);
+    return RN_OK;
+  }
   auto it = stats.find(k);
   if (it == stats.end()) return set_error(RN_ERR_ARG, "unknown statistic " + k);
   *v = it->second;

@@ -139,6 +139,17 @@ struct Plan {
   std::map<std::string, double> stats;
   rn_status set_option(const std::string &k, int64_t v);
   rn_status query(const std::string &k, double *v);
+  // live CUDA-event timing of the convolution launches (option time_kernels)
+  struct EvPair {
+    cudaEvent_t a, b;
+    double flops;
+    int cls;  // 0 fprop, 1 dgrad, 2 wgrad
+  };
+  std::vector<EvPair> ev_pool;
+  size_t ev_used = 0;
+  bool timing() const;
+  size_t tk_begin(int cls, double flops);
+  void tk_end(size_t i);
 };
 
 }  // namespace rn

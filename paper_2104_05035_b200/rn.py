@@ -17,7 +17,7 @@ STATUS = {0: "RN_OK", 1: "RN_ERR_ARG", 2: "RN_ERR_SCHEMA", 3: "RN_ERR_INFEASIBLE
           5: "RN_ERR_CUDA", 6: "RN_ERR_NCCL", 7: "RN_ERR_STATE", 8: "RN_ERR_SIZE"}
 EXPORTS = ["rn_ga_default", "rn_gabra_place", "rn_net_units", "rn_net_param_count", "rn_net_param_info",
            "rn_nccl_unique_id", "rn_plan", "rn_plan_bind", "rn_set_params", "rn_get_params", "rn_get_grads",
-           "rn_get_bn_running", "rn_forward", "rn_backward", "rn_step", "rn_train_step_host",
+           "rn_get_bn_running", "rn_get_activation", "rn_forward", "rn_backward", "rn_step", "rn_train_step_host",
            "rn_kernel_launches", "rn_set_option", "rn_query", "rn_plan_destroy", "rn_last_error"]
 
 
@@ -186,6 +186,13 @@ class Plan:
         _check(lib().rn_get_bn_running(self.h, m.ctypes.data_as(C.POINTER(C.c_float)),
                                        v.ctypes.data_as(C.POINTER(C.c_float)), C.c_int64(self.n_bn)))
         return m, v
+
+    def get_activation(self, unit: int, micro_batch: int, shape) -> np.ndarray:
+        n = int(np.prod(shape))
+        a = np.empty(n, dtype=np.float32)
+        _check(lib().rn_get_activation(self.h, unit, micro_batch, a.ctypes.data_as(C.POINTER(C.c_float)),
+                                       C.c_int64(n)))
+        return a.reshape(shape)
 
     # --- step ---
     def forward(self, x_dev, y_dev, want_loss=True):

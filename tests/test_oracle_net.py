@@ -149,3 +149,24 @@ def test_finite_differences_tiny():
             ok += 1
     assert checked >= 100
     assert ok >= 0.99 * checked
+
+
+def test_bf16_storage_gap():
+    """Evidence for reading X23: rounding the stored activations/gradients to
+    bf16 (what any bf16 tensor-core path does) moves the early-layer gradients of
+    this network far more than 2e-2 from the float64 definition, while the loss
+    moves by < 1e-3.  Hence the bf16 gradient parity is checked against the
+    bf16-storage oracle (tests/test_gpu_parity.py::test_bf16_step)."""
+    net64 = O.Net(0, 8, (16, 16, 16))
+    net16 = O.Net(0, 8, (16, 16, 16), store="bf16")
+    arrays = synthetic.perturb_params(net64.tensors, synthetic.init_params(net64.tensors, seed=0))
+    x, y = synthetic.make_batch(2, 16, 16, 16, seed=1)
+    a = net64.train_step(arrays, x, y, 1e-4)
+    b = net16.train_step(arrays, x, y, 1e-4)
+    assert abs(a["loss"] - b["loss"]) < 1e-3 * a["loss"]
+    gap = np.linalg.norm(a["grad"] - b["grad"]) / np.linalg.norm(a["grad"])
+    assert gap > 2e-2
+    # the rounding itself: bf16 RNE of fp32 (pins the helper against torch's cast)
+    v = np.random.default_rng(0).standard_normal(1000) * 100
+    t = torch.tensor(v, dtype=torch.float32).to(torch.bfloat16).to(torch.float64).numpy()
+    np.testing.assert_array_equal(O._bf16_round(v), t)
