@@ -222,6 +222,20 @@ rn_status rn_set_option(rn_plan_t plan, const char *key, int64_t value);
  * when time_kernels is on; reset by rn_set_option("time_kernels", 1). */
 rn_status rn_query(rn_plan_t plan, const char *key, double *value);
 
+/* rn_op_conv3d — ONE convolution of the step as a stand-alone launch, for the
+ * kernel-level parity tests and micro-benchmarks (same kernels the plan uses).
+ *  op 0 fprop : out[N][Do][Ho][Wo][Co] = sum_{tap,ci} a[N][Di][Hi][Wi][Ci] * b[Co][tap][Ci]
+ *  op 1 dgrad : out[N][Di][Hi][Wi][Ci] = sum_{tap,co} a[N][Do][Ho][Wo][Co] * b[Co][tap][Ci]
+ *  op 2 wgrad : out[Co][tap][Ci] (float32) = sum_{n,vo} b[..vo..][Co] * a[..vi(vo,tap)..][Ci]
+ *               (a = x, b = dy)
+ *  geom[12] = {N, Di, Hi, Wi, Ci, Do, Ho, Wo, Co, k, s, p}; element type of a, b
+ *  (and out for ops 0/1) is dtype; impl 0 = auto (tcgen05 when supported),
+ *  1 = SIMT, 2 = tcgen05 only (RN_ERR_ARG if unsupported).  Device pointers,
+ *  stream-ordered on `stream`; scratch is allocated internally.
+ * Errors: RN_ERR_ARG, RN_ERR_CUDA. */
+rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const void *a_dev, const void *b_dev,
+                       void *out_dev, int32_t impl, void *stream);
+
 void rn_plan_destroy(rn_plan_t plan);
 const char *rn_last_error(void);
 

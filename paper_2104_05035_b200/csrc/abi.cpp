@@ -12,6 +12,8 @@
 #include "error.h"
 #include "net.h"
 #include "plan.h"
+#include "tc_conv.h"
+#include "util.cuh"
 
 namespace rn {
 rn_status gabra_place(int32_t n, const int64_t *loads, int32_t m, const int64_t *caps, const rn_ga_params &gp,
@@ -301,6 +303,49 @@ rn_status rn_query(rn_plan_t plan, const char *key, double *value) {
   GUARD_BEGIN
   if (!plan || !key || !value) return set_error(RN_ERR_ARG, "null argument");
   return plan->p->query(key, value);
+  GUARD_END
+}
+
+rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const void *a_dev, const void *b_dev,
+                       void *out_dev, int32_t impl, void *stream) {
+  GUARD_BEGIN
+  if (!geom || !a_dev || !b_dev || !out_dev || op < 0 || op > 2 || impl < 0 || impl > 2 ||
+      (dtype != RN_F32 && dtype != RN_BF16))
+    return set_error(RN_ERR_ARG, "rn_op_conv3d: bad arguments");
+  ConvGeom g;
+  g.N = geom[0]; g.Di = geom[1]; g.Hi = geom[2]; g.Wi = geom[3]; g.Ci = geom[4];
+  g.Do = geom[5]; g.Ho = geom[6]; g.Wo = geom[7]; g.Co = geom[8]; g.k = geom[9]; g.s = geom[10]; g.p = geom[11];
+  if (g.Do != conv_out(g.Di, g.k, g.s, g.p) || g.Ho != conv_out(g.Hi, g.k, g.s, g.p) ||
+      g.Wo != conv_out(g.Wi, g.k, g.s, g.p) || g.Ci % 8 || g.Co % 8)
+    return set_error(RN_ERR_ARG, "rn_op_conv3d: inconsistent geometry");
+  cudaStream_t st = (cudaStream_t)stream;
+  const DType dt = dtype == RN_BF16 ? DT_BF16 : DT_F32;
+  const bool tc_ok = dt == DT_BF16 && op != 2 && tc_conv_supported(g, op == 1);
+  if (impl == 2 && !tc_ok) return set_error(RN_ERR_ARG, "rn_op_conv3d: tcgen05 kernel does not take this conv");
+  const bool tc = tc_ok && impl != 1;
+  if (op == 0) {
+    if (tc) conv_fprop_tc(g, (const bf16 *)a_dev, (const bf16 *)b_dev, nullptr, (bf16 *)out_dev, st);
+    else conv_fprop_simt(dt, g, a_dev, b_dev, nullptr, out_dev, st);
+  } else if (op == 1) {
+    if (tc) {
+      void *wd = nullptr;
+      const size_t n = (size_t)g.Co * g.taps() * g.Ci;
+      CUDA_CHECK(cudaMallocAsync(&wd, n * 2, st));
+      flip_weights(dt, b_dev, g.Co, g.taps(), g.Ci, wd, st);
+      CUDA_CHECK(cudaMemsetAsync(out_dev, 0, 2 * (size_t)g.in_vox() * g.Ci, st));
+      conv_dgrad_tc(g, (const bf16 *)a_dev, (const bf16 *)wd, (bf16 *)out_dev, true, nullptr, nullptr, st);
+      CUDA_CHECK(cudaFreeAsync(wd, st));
+    } else {
+      conv_dgrad_simt(dt, g, a_dev, b_dev, out_dev, false, nullptr, nullptr, st);
+    }
+  } else {
+    float *ws = nullptr;
+    CUDA_CHECK(cudaMallocAsync((void **)&ws, sizeof(float) * conv_wgrad_ws_floats(g), st));
+    CUDA_CHECK(cudaMemsetAsync(out_dev, 0, sizeof(float) * (size_t)g.Co * g.taps() * g.Ci, st));
+    conv_wgrad_simt(dt, false, g, a_dev, b_dev, (float *)out_dev, ws, st);
+    CUDA_CHECK(cudaFreeAsync(ws, st));
+  }
+  return RN_OK;
   GUARD_END
 }
 

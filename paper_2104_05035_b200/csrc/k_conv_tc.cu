@@ -1,0 +1,492 @@
+// k_conv_tc.cu — 3D convolution as an implicit GEMM on the 5th-generation tensor
+// cores (tcgen05, accumulators in TMEM), operands staged by TMA (PAPER.md:366:
+// the Conv block's 3x3x3 convolution, complexity O(Co*Ci*T*H*W*Kt*Kh*Kw), is
+// where the step's operations are).
+//
+// GEMM view of one launch ("implicit GEMM over taps"):
+//   rows    M = output voxels, tiled by a 3-D/4-D box of 128 voxels (bw x bh x bd x bn)
+//   columns N = output channels, tile BN in {64, 128, 256}
+//   K       = sum over taps t of 64-channel blocks of the A tensor
+//   A[m, (t,c)] = src[view_t](voxel(m) + offset_t)[c]   (TMA 5-D box, OOB -> 0)
+//   B[n, (t,c)] = W[n][kcoord_t + c]                      (TMA 2-D box)
+// fprop: src = x, W = W[co][tap][ci];  dgrad (stride 1): src = dy, W = flipped
+// W^T[ci][tap'][co];  dgrad stride 2: one launch per output parity class, each
+// with its subset of taps and a strided output view;  stride-2 fprop: the A
+// views are the 8 parity sub-lattices of x.
+//
+// Kernel: persistent, one CTA per SM, warp-specialised: warp 0 TMA producer,
+// warp 1 MMA issuer (one elected lane, tcgen05.mma M=128, N=BN, K=16), warps
+// 2-5 epilogue (tcgen05.ld 32x32b -> fp32 registers -> bias / accumulate /
+// masked residual -> bf16 stores).  STAGES-deep smem ring (mbarriers), 2 TMEM
+// accumulators so the epilogue of tile i overlaps the main loop of tile i+1.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "error.h"
+#include "kernels.h"
+#include "tc_conv.h"
+#include "tc_ptx.cuh"
+#include "util.cuh"
+
+namespace rn {
+
+namespace {
+
+constexpr int TC_THREADS = 192;
+
+struct __align__(64) TcParams {
+  CUtensorMap a_map[8];
+  CUtensorMap b_map;
+  int n_taps;
+  int kblocks_per_tap;  // A channels / 64
+  int8_t tap_map[27];
+  int8_t tap_od[27], tap_oh[27], tap_ow[27];
+  int tap_kcoord[27];
+  // output tiling: view extents and box
+  int OD, OH, OW, ON;
+  int bw, bh, bd, bn;
+  int tw, th, td, tn, t_nblk;  // tiles per dim, N-blocks of BN
+  int64_t n_tiles;
+  // output addressing (elements)
+  bf16 *y;
+  int64_t s_n, s_d, s_h, s_w;
+  int ych;  // channels of y per voxel
+  const float *bias;
+  int accumulate;
+  const bf16 *res;
+  const bf16 *res_mask;
+};
+
+template <int BN, int STAGES>
+struct Smem {
+  static constexpr int A_BYTES = 128 * 128;      // 128 rows x 64 bf16
+  static constexpr int B_BYTES = BN * 128;       // BN rows x 64 bf16
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_constant__ TcParams p) {
+  using S = Smem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = (uint64_t *)(smem + S::BAR_OFF);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                  : (2 * BN <= 256) ? 256 : 512;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], 4);
+    }
+    tc::fence_barrier_init();
+    for (int i = 0; i < p.n_taps; ++i)
+      if (i == 0 || p.tap_map[i] != p.tap_map[i - 1]) tc::tma_prefetch(&p.a_map[p.tap_map[i]]);
+    tc::tma_prefetch(&p.b_map);
+  }
+  if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int nk = p.n_taps * p.kblocks_per_tap;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        int64_t r = tile;
+        const int nb = (int)(r % p.t_nblk); r /= p.t_nblk;
+        const int tw = (int)(r % p.tw); r /= p.tw;
+        const int th = (int)(r % p.th); r /= p.th;
+        const int td = (int)(r % p.td); r /= p.td;
+        const int tn = (int)r;
+        const int w0 = tw * p.bw, h0 = th * p.bh, d0 = td * p.bd, n0 = tn * p.bn;
+        for (int t = 0; t < p.n_taps; ++t) {
+          const CUtensorMap *am = &p.a_map[p.tap_map[t]];
+          for (int cb = 0; cb < p.kblocks_per_tap; ++cb) {
+            tc::mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t *sa = smem + stage * S::STAGE;
+            uint8_t *sb = sa + S::A_BYTES;
+            tc::mbar_arrive_expect_tx(&full[stage], S::STAGE);
+            tc::tma_load_5d(sa, am, &full[stage], cb * 64, w0 + p.tap_ow[t], h0 + p.tap_oh[t], d0 + p.tap_od[t], n0);
+            tc::tma_load_2d(sb, &p.b_map, &full[stage], p.tap_kcoord[t] + cb * 64, nb * BN);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t IDESC = tc::idesc_bf16(128, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < nk; ++kb) {
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = tc::smem_u32(smem + stage * S::STAGE);
+          const uint32_t sb = sa + S::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = tc::smem_desc(sa + k * 32, 16, 1024, 2);
+            const uint64_t bd = tc::smem_desc(sb + k * 32, 16, 1024, 2);
+            tc::mma_bf16(d_tmem, ad, bd, IDESC, (kb | k) != 0);
+          }
+          tc::mma_commit(&empty[stage]);
+          if (kb == nk - 1) tc::mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5) ----------------
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    const int wx = row % p.bw, hy = (row / p.bw) % p.bh, dz = (row / (p.bw * p.bh)) % p.bd,
+              nz = row / (p.bw * p.bh * p.bd);
+    int local = 0;
+    for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++local) {
+      int64_t r = tile;
+      const int nb = (int)(r % p.t_nblk); r /= p.t_nblk;
+      const int tw = (int)(r % p.tw); r /= p.tw;
+      const int th = (int)(r % p.th); r /= p.th;
+      const int td = (int)(r % p.td); r /= p.td;
+      const int tn = (int)r;
+      const int ow = tw * p.bw + wx, oh = th * p.bh + hy, od = td * p.bd + dz, on = tn * p.bn + nz;
+      const bool valid = ow < p.OW && oh < p.OH && od < p.OD && on < p.ON;
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      tc::mbar_wait(&tfull[acc], acc_phase);
+      tc::tc_fence_after();
+      const int64_t obase = on * p.s_n + od * p.s_d + oh * p.s_h + ow * p.s_w + (int64_t)nb * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
+        tc::tmem_wait_ld();
+        if (valid) {
+          float f[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+          if (p.bias) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[j] += p.bias[nb * BN + c0 + j];
+          }
+          bf16 *dst = p.y + obase + c0;
+          if (p.accumulate) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              float o[8];
+              load_vec(dst + j, o);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) f[j + e] += o[e];
+            }
+          }
+          if (p.res) {
+            const int64_t ro = obase + c0;
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              float rv[8], mv[8];
+              load_vec(p.res + ro + j, rv);
+              load_vec(p.res_mask + ro + j, mv);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) f[j + e] += mv[e] > 0.f ? rv[e] : 0.f;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) store_vec(dst + j, f + j);
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+void load_encode() {
+  if (g_encode) return;
+  cudaDriverEntryPointQueryResult q;
+  void *fn = nullptr;
+  CUDA_CHECK(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) throw Error(RN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+}
+
+// 5-D view of an NDHWC bf16 tensor: dims {C, W, H, D, N} with element strides
+// (sw, sh, sd, sn) in voxels (a parity sub-lattice uses doubled strides).
+void make_act_map(CUtensorMap *m, const void *base, int C, int W, int H, int D, int N, int64_t sw, int64_t sh,
+                  int64_t sd, int64_t sn, int bw, int bh, int bd, int bn) {
+  load_encode();
+  cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)D, (cuuint64_t)N};
+  cuuint64_t strides[4] = {(cuuint64_t)(sw * C * 2), (cuuint64_t)(sh * C * 2), (cuuint64_t)(sd * C * 2),
+                           (cuuint64_t)(sn * C * 2)};
+  cuuint32_t box[5] = {64, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bd, (cuuint32_t)bn};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(RN_ERR_CUDA, "cuTensorMapEncodeTiled (activation) failed: " + std::to_string(r));
+}
+
+void make_w_map(CUtensorMap *m, const void *base, int rows, int64_t ktot, int bn) {
+  load_encode();
+  cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ktot * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)bn};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(RN_ERR_CUDA, "cuTensorMapEncodeTiled (weights) failed: " + std::to_string(r));
+}
+
+// choose a 128-voxel box (bw, bh, bd, bn) minimising the padded volume
+void choose_box(int W, int H, int D, int N, int &bw, int &bh, int &bd, int &bn) {
+  double best = 1e30;
+  for (int a = 1; a <= 128; a *= 2)
+    for (int b = 1; a * b <= 128; b *= 2)
+      for (int c = 1; a * b * c <= 128; c *= 2) {
+        int e = 128 / (a * b * c);
+        if (a * b * c * e != 128) continue;
+        double pad = (double)((W + a - 1) / a * a) * ((H + b - 1) / b * b) * ((D + c - 1) / c * c) *
+                     ((N + e - 1) / e * e);
+        // prefer wider w (contiguous rows) on ties
+        double score = pad * (1.0 + 1e-6 * (8 - std::min(a, 8)));
+        if (score < best) { best = score; bw = a; bh = b; bd = c; bn = e; }
+      }
+}
+
+template <int BN, int STAGES>
+void launch(const TcParams &p, cudaStream_t st) {
+  using S = Smem<BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_CHECK(cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    S::TOTAL));
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::min<int64_t>(p.n_tiles, sms);
+  conv_tc_kernel<BN, STAGES><<<grid, TC_THREADS, S::TOTAL, st>>>(p);
+  LAUNCH_CHECK();
+}
+
+void run(const TcParams &p, int BN, cudaStream_t st) {
+  if (BN == 64) launch<64, 6>(p, st);
+  else if (BN == 128) launch<128, 5>(p, st);
+  else launch<256, 4>(p, st);
+}
+
+int pick_bn(int nout) {
+  if (nout % 256 == 0) return 256;
+  if (nout % 128 == 0) return 128;
+  return 64;
+}
+
+void fill_tiles(TcParams &p, int OW, int OH, int OD, int ON, int nout, int BN) {
+  p.OW = OW; p.OH = OH; p.OD = OD; p.ON = ON;
+  choose_box(OW, OH, OD, ON, p.bw, p.bh, p.bd, p.bn);
+  p.tw = (OW + p.bw - 1) / p.bw;
+  p.th = (OH + p.bh - 1) / p.bh;
+  p.td = (OD + p.bd - 1) / p.bd;
+  p.tn = (ON + p.bn - 1) / p.bn;
+  p.t_nblk = nout / BN;
+  p.n_tiles = (int64_t)p.tn * p.td * p.th * p.tw * p.t_nblk;
+}
+
+}  // namespace
+
+bool tc_conv_supported(const ConvGeom &g, bool dgrad) {
+  const int kc = dgrad ? g.Co : g.Ci;     // A channels
+  const int nout = dgrad ? g.Ci : g.Co;   // output channels
+  if (kc % 64 != 0 || nout % 64 != 0) return false;
+  if (g.k != 1 && g.k != 3) return false;
+  if (g.s != 1 && g.s != 2) return false;
+  if (g.k == 3 && g.p != 1) return false;
+  if (g.k == 1 && g.p != 0) return false;
+  if (g.s == 2) {  // output = ceil(in/2) lattice, every parity sub-lattice non-empty
+    if (g.Do != (g.Di + 1) / 2 || g.Ho != (g.Hi + 1) / 2 || g.Wo != (g.Wi + 1) / 2) return false;
+    if (g.Di < 2 || g.Hi < 2 || g.Wi < 2) return false;
+  }
+  return true;
+}
+
+// fprop: y[vo][co] = sum x[...] w[co][tap][ci] (+bias)
+void conv_fprop_tc(const ConvGeom &g, const bf16 *x, const bf16 *w, const float *bias, bf16 *y, cudaStream_t st) {
+  TcParams p;
+  memset(&p, 0, sizeof p);
+  const int BN = pick_bn(g.Co);
+  fill_tiles(p, g.Wo, g.Ho, g.Do, g.N, g.Co, BN);
+  const int taps = g.taps();
+  p.n_taps = taps;
+  p.kblocks_per_tap = g.Ci / 64;
+  if (g.s == 1) {
+    make_act_map(&p.a_map[0], x, g.Ci, g.Wi, g.Hi, g.Di, g.N, 1, g.Wi, (int64_t)g.Wi * g.Hi,
+                 (int64_t)g.Wi * g.Hi * g.Di, p.bw, p.bh, p.bd, p.bn);
+  } else {
+    // 8 parity sub-lattices: map index = (pd*2 + ph)*2 + pw ; base offset by the parity voxel
+    for (int pd = 0; pd < 2; ++pd)
+      for (int ph = 0; ph < 2; ++ph)
+        for (int pw = 0; pw < 2; ++pw) {
+          const int Wv = (g.Wi - pw + 1) / 2, Hv = (g.Hi - ph + 1) / 2, Dv = (g.Di - pd + 1) / 2;
+          const bf16 *b = x + (((int64_t)pd * g.Hi + ph) * g.Wi + pw) * g.Ci;
+          make_act_map(&p.a_map[(pd * 2 + ph) * 2 + pw], b, g.Ci, std::max(Wv, 1), std::max(Hv, 1), std::max(Dv, 1),
+                       g.N, 2, 2LL * g.Wi, 2LL * g.Wi * g.Hi, (int64_t)g.Wi * g.Hi * g.Di, p.bw, p.bh, p.bd, p.bn);
+        }
+  }
+  for (int t = 0; t < taps; ++t) {
+    const int kd = t / (g.k * g.k), kh = (t / g.k) % g.k, kw = t % g.k;
+    const int od = kd - g.p, oh = kh - g.p, ow = kw - g.p;  // input offset = s*o + (k - p)
+    if (g.s == 1) {
+      p.tap_map[t] = 0;
+      p.tap_od[t] = od; p.tap_oh[t] = oh; p.tap_ow[t] = ow;
+    } else {
+      // i = 2o + off: off = 0 -> even lattice at o; off = 1 -> odd at o; off = -1 -> odd at o-1
+      auto par = [](int off) { return off == 0 ? 0 : 1; };
+      auto sh = [](int off) { return off < 0 ? -1 : 0; };
+      p.tap_map[t] = (par(od) * 2 + par(oh)) * 2 + par(ow);
+      p.tap_od[t] = sh(od); p.tap_oh[t] = sh(oh); p.tap_ow[t] = sh(ow);
+    }
+    p.tap_kcoord[t] = t * g.Ci;
+  }
+  make_w_map(&p.b_map, w, g.Co, (int64_t)taps * g.Ci, BN);
+  p.y = y;
+  p.ych = g.Co;
+  p.s_w = g.Co;
+  p.s_h = (int64_t)g.Wo * g.Co;
+  p.s_d = (int64_t)g.Ho * g.Wo * g.Co;
+  p.s_n = (int64_t)g.Do * g.Ho * g.Wo * g.Co;
+  p.bias = bias;
+  run(p, BN, st);
+}
+
+// dgrad: dx[vi][ci] (=|+=) sum dy[vo][co] W[co][tap][ci]; wd = [ci][taps-1-tap][co]
+void conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, bool accumulate, const bf16 *res,
+                   const bf16 *res_mask, cudaStream_t st) {
+  const int taps = g.taps();
+  const int BN = pick_bn(g.Ci);
+  if (g.s == 1) {
+    TcParams p;
+    memset(&p, 0, sizeof p);
+    fill_tiles(p, g.Wi, g.Hi, g.Di, g.N, g.Ci, BN);
+    p.n_taps = taps;
+    p.kblocks_per_tap = g.Co / 64;
+    make_act_map(&p.a_map[0], dy, g.Co, g.Wo, g.Ho, g.Do, g.N, 1, g.Wo, (int64_t)g.Wo * g.Ho,
+                 (int64_t)g.Wo * g.Ho * g.Do, p.bw, p.bh, p.bd, p.bn);
+    for (int t = 0; t < taps; ++t) {
+      // dx[i] = sum_t dy[i + p - k_t] W[t]  ==  sum_t' dy[i + k_t' - p] Wflip[t'] with t' = taps-1-t
+      const int kd = t / (g.k * g.k), kh = (t / g.k) % g.k, kw = t % g.k;
+      p.tap_map[t] = 0;
+      p.tap_od[t] = kd - g.p; p.tap_oh[t] = kh - g.p; p.tap_ow[t] = kw - g.p;
+      p.tap_kcoord[t] = t * g.Co;  // wd row layout [ci][t'][co] indexed by t' = t here
+    }
+    make_w_map(&p.b_map, wd, g.Ci, (int64_t)taps * g.Co, BN);
+    p.y = dx;
+    p.ych = g.Ci;
+    p.s_w = g.Ci;
+    p.s_h = (int64_t)g.Wi * g.Ci;
+    p.s_d = (int64_t)g.Hi * g.Wi * g.Ci;
+    p.s_n = (int64_t)g.Di * g.Hi * g.Wi * g.Ci;
+    p.accumulate = accumulate;
+    p.res = res;
+    p.res_mask = res_mask;
+    run(p, BN, st);
+    return;
+  }
+  // stride 2: output parity classes (pd, ph, pw); input index i = 2a + par.
+  // Contributions: i = 2o + k - p  =>  for k=3,p=1: par 0 <- (k=1, o=a); par 1 <- (k=2, o=a), (k=0, o=a+1)
+  //                                    for k=1,p=0: par 0 <- (k=0, o=a); par 1 <- none
+  for (int pd = 0; pd < 2; ++pd)
+    for (int ph = 0; ph < 2; ++ph)
+      for (int pw = 0; pw < 2; ++pw) {
+        const int Wv = (g.Wi - pw + 1) / 2, Hv = (g.Hi - ph + 1) / 2, Dv = (g.Di - pd + 1) / 2;
+        if (Wv <= 0 || Hv <= 0 || Dv <= 0) continue;
+        TcParams p;
+        memset(&p, 0, sizeof p);
+        fill_tiles(p, Wv, Hv, Dv, g.N, g.Ci, BN);
+        p.kblocks_per_tap = g.Co / 64;
+        make_act_map(&p.a_map[0], dy, g.Co, g.Wo, g.Ho, g.Do, g.N, 1, g.Wo, (int64_t)g.Wo * g.Ho,
+                     (int64_t)g.Wo * g.Ho * g.Do, p.bw, p.bh, p.bd, p.bn);
+        int nt = 0;
+        for (int t = 0; t < taps; ++t) {
+          const int kk[3] = {t / (g.k * g.k), (t / g.k) % g.k, t % g.k};
+          const int par[3] = {pd, ph, pw};
+          int off[3];
+          bool ok = true;
+          for (int a = 0; a < 3; ++a) {
+            // need 2o + k - p = 2a' + par  ->  o = a' + (par + p - k)/2, integer
+            const int num = par[a] + g.p - kk[a];
+            if (num % 2 != 0) { ok = false; break; }
+            off[a] = num / 2;
+          }
+          if (!ok) continue;
+          p.tap_map[nt] = 0;
+          p.tap_od[nt] = off[0]; p.tap_oh[nt] = off[1]; p.tap_ow[nt] = off[2];
+          p.tap_kcoord[nt] = (taps - 1 - t) * g.Co;  // wd[ci][taps-1-t][co] == W[co][ci][t]
+          ++nt;
+        }
+        if (nt == 0) {
+          // no tap reaches this parity class (1x1x1 stride 2): its dx is zero
+          if (!accumulate) throw Error(RN_ERR_STATE, "conv_dgrad_tc: empty parity class needs accumulate");
+          continue;
+        }
+        p.n_taps = nt;
+        make_w_map(&p.b_map, wd, g.Ci, (int64_t)taps * g.Co, BN);
+        // strided output view: voxel (a_d, a_h, a_w) -> (2a_d+pd, 2a_h+ph, 2a_w+pw)
+        p.y = dx + (((int64_t)pd * g.Hi + ph) * g.Wi + pw) * g.Ci;
+        p.ych = g.Ci;
+        p.s_w = 2LL * g.Ci;
+        p.s_h = 2LL * g.Wi * g.Ci;
+        p.s_d = 2LL * g.Hi * g.Wi * g.Ci;
+        p.s_n = (int64_t)g.Di * g.Hi * g.Wi * g.Ci;
+        p.accumulate = accumulate;
+        if (res) {
+          p.res = res + (((int64_t)pd * g.Hi + ph) * g.Wi + pw) * g.Ci;
+          p.res_mask = res_mask + (((int64_t)pd * g.Hi + ph) * g.Wi + pw) * g.Ci;
+        }
+        run(p, BN, st);
+      }
+}
+
+}  // namespace rn

@@ -690,6 +690,22 @@ void repack_conv(DType dt, const float *w, int Co, int taps, int Ci, void *wf, v
   LAUNCH_CHECK();
 }
 
+template <typename T>
+__global__ void flip_k(const T *__restrict__ w, int Co, int taps, int Ci, T *__restrict__ wd) {
+  const int64_t n = (int64_t)Co * taps * Ci;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int ci = (int)(i % Ci);
+    const int tap = (int)((i / Ci) % taps);
+    const int co = (int)(i / ((int64_t)Ci * taps));
+    wd[((int64_t)ci * taps + (taps - 1 - tap)) * Co + co] = w[i];
+  }
+}
+
+void flip_weights(DType dt, const void *w, int Co, int taps, int Ci, void *wd, cudaStream_t st) {
+  DISPATCH(dt, flip_k<T><<<grid_for((int64_t)Co * taps * Ci), NT, 0, st>>>((const T *)w, Co, taps, Ci, (T *)wd));
+  LAUNCH_CHECK();
+}
+
 void check_finite(const float *v, int n, int *flag, cudaStream_t st) {
   check_finite_k<<<1, 256, 0, st>>>(v, n, flag);
   LAUNCH_CHECK();

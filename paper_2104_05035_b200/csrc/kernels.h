@@ -95,5 +95,7 @@ void sgd_update(float *w, const float *g, int64_t n, float lr, cudaStream_t st);
 // wf[co][tap][ci] = w, wd[ci][taps-1-tap][co] = w  (either may be null)
 void repack_conv(DType dt, const float *w, int Co, int taps, int Ci, void *wf, void *wd, cudaStream_t st);
 void check_finite(const float *v, int n, int *flag, cudaStream_t st);
+// wd[ci][taps-1-tap][co] = w[co][tap][ci] (element type dt)
+void flip_weights(DType dt, const void *w, int Co, int taps, int Ci, void *wd, cudaStream_t st);
 
 }  // namespace rn

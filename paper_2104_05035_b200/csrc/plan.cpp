@@ -18,6 +18,8 @@
 #include <vector>
 
 #include "error.h"
+#include "tc_conv.h"
+#include "util.cuh"
 
 namespace rn {
 
@@ -320,17 +322,31 @@ size_t Plan::tk_begin(int cls, double flops) {
 
 void Plan::tk_end(size_t i) { CUDA_CHECK(cudaEventRecord(ev_pool[i].b, stream)); }
 
+bool Plan::use_tc(const ConvGeom &g, bool dgrad) const {
+  if (dt != DT_BF16) return false;
+  auto it = opts.find("tc_conv");
+  if (it != opts.end() && it->second == 0) return false;
+  return tc_conv_supported(g, dgrad);
+}
+
 void Plan::conv_fwd(const ConvL &c, const void *x, void *y, const float *bias) {
   const bool t = timing();
   size_t e = t ? tk_begin(0, conv_flops(c.g)) : 0;
-  conv_fprop_simt(dt, c.g, x, wfwd(c.w_idx), bias, y, stream);
+  if (use_tc(c.g, false))
+    conv_fprop_tc(c.g, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, stream);
+  else
+    conv_fprop_simt(dt, c.g, x, wfwd(c.w_idx), bias, y, stream);
   if (t) tk_end(e);
 }
 void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumulate, const void *res,
                          const void *res_mask) {
   const bool t = timing();
   size_t e = t ? tk_begin(1, conv_flops(c.g)) : 0;
-  conv_dgrad_simt(dt, c.g, dy, wfwd(c.w_idx), dx, accumulate, res, res_mask, stream);
+  if (use_tc(c.g, true))
+    conv_dgrad_tc(c.g, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), (bf16 *)dx, accumulate,
+                  (const bf16 *)res, (const bf16 *)res_mask, stream);
+  else
+    conv_dgrad_simt(dt, c.g, dy, wfwd(c.w_idx), dx, accumulate, res, res_mask, stream);
   if (t) tk_end(e);
 }
 void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32) {

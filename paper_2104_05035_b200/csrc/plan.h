@@ -105,6 +105,7 @@ struct Plan {
   float *bn_stat(const BNL &b, int k, int which);
 
   // ops
+  bool use_tc(const ConvGeom &g, bool dgrad) const;
   void conv_fwd(const ConvL &c, const void *x, void *y, const float *bias = nullptr);
   void conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumulate, const void *res,
                      const void *res_mask);

@@ -1,0 +1,19 @@
+// tc_conv.h — tcgen05 implicit-GEMM convolution launchers (k_conv_tc.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace rn {
+
+// true if the tcgen05 kernels take this convolution (bf16, channels % 64 == 0,
+// k in {1, 3}, stride in {1, 2} with the 'same' ceil(in/2) lattice)
+bool tc_conv_supported(const ConvGeom &g, bool dgrad);
+void conv_fprop_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, const float *bias,
+                   __nv_bfloat16 *y, cudaStream_t st);
+// wd: [Ci][taps][Co] with the tap order flipped (repack_conv's wd)
+void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dy, const __nv_bfloat16 *wd, __nv_bfloat16 *dx,
+                   bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask, cudaStream_t st);
+
+}  // namespace rn

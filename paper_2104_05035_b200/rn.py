@@ -18,7 +18,7 @@ STATUS = {0: "RN_OK", 1: "RN_ERR_ARG", 2: "RN_ERR_SCHEMA", 3: "RN_ERR_INFEASIBLE
 EXPORTS = ["rn_ga_default", "rn_gabra_place", "rn_net_units", "rn_net_param_count", "rn_net_param_info",
            "rn_nccl_unique_id", "rn_plan", "rn_plan_bind", "rn_set_params", "rn_get_params", "rn_get_grads",
            "rn_get_bn_running", "rn_get_activation", "rn_forward", "rn_backward", "rn_step", "rn_train_step_host",
-           "rn_kernel_launches", "rn_set_option", "rn_query", "rn_plan_destroy", "rn_last_error"]
+           "rn_kernel_launches", "rn_set_option", "rn_query", "rn_op_conv3d", "rn_plan_destroy", "rn_last_error"]
 
 
 class RnError(RuntimeError):
@@ -224,3 +224,12 @@ class Plan:
 
 def kernel_launches() -> int:
     return lib().rn_kernel_launches(None)
+
+
+def op_conv3d(dtype, op, geom, a, b, out, impl=0, stream=None):
+    """rn_op_conv3d on torch CUDA tensors (see include/rn.h)."""
+    import torch
+    g = (C.c_int32 * 12)(*[int(v) for v in geom])
+    s = stream if stream is not None else torch.cuda.current_stream()
+    _check(lib().rn_op_conv3d(dtype, op, g, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                              C.c_void_p(out.data_ptr()), impl, C.c_void_p(s.cuda_stream)))

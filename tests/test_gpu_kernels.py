@@ -1,0 +1,82 @@
+"""Kernel-level parity through the C ABI (rn_op_conv3d): every convolution
+class of the r18 step at the full 91x109x91 sizes (batch 2), tcgen05 and SIMT,
+against the oracle's float64 convolution on the same bf16-valued inputs.
+Tolerance: fp32 accumulation + one bf16 rounding of the output ->
+per-tensor relative L2 error <= 4e-3."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import net as O
+from paper_2104_05035_b200 import rn
+
+pytestmark = pytest.mark.gpu
+
+# (name, Di,Hi,Wi, Ci, Co, k, s, p) — the r18 conv classes (reading X2-X5)
+CONVS = [
+    ("s1_k3", 23, 28, 23, 64, 64, 3, 1, 1),
+    ("s2_k3_s2", 23, 28, 23, 64, 128, 3, 2, 1),
+    ("s2_proj", 23, 28, 23, 64, 128, 1, 2, 0),
+    ("s2_k3", 12, 14, 12, 128, 128, 3, 1, 1),
+    ("s3_k3_s2", 12, 14, 12, 128, 256, 3, 2, 1),
+    ("s3_k3", 6, 7, 6, 256, 256, 3, 1, 1),
+    ("s4_k3_s2", 6, 7, 6, 256, 512, 3, 2, 1),
+    ("s4_k3", 3, 4, 3, 512, 512, 3, 1, 1),
+    ("att1_mask_k3", 12, 14, 12, 64, 64, 3, 1, 1),
+    ("att1_mconv", 23, 28, 23, 64, 64, 1, 1, 0),
+]
+
+
+def bf16_vals(shape, rng, scale=1.0):
+    t = torch.from_numpy((rng.standard_normal(shape) * scale).astype(np.float32)).to(torch.bfloat16)
+    return t
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("impl", [2, 1])
+@pytest.mark.parametrize("cv", CONVS, ids=[c[0] for c in CONVS])
+def test_conv_fprop_dgrad(cv, impl):
+    name, Di, Hi, Wi, Ci, Co, k, s, p = cv
+    N = 2
+    Do, Ho, Wo = (O.conv_out(v, k, s, p) for v in (Di, Hi, Wi))
+    rng = np.random.default_rng(0)
+    x = bf16_vals((N, Di, Hi, Wi, Ci), rng)
+    w = bf16_vals((Co, k * k * k, Ci), rng, scale=(2.0 / (Co * k ** 3)) ** 0.5)
+    dy = bf16_vals((N, Do, Ho, Wo, Co), rng)
+    geom = [N, Di, Hi, Wi, Ci, Do, Ho, Wo, Co, k, s, p]
+    y = torch.empty((N, Do, Ho, Wo, Co), dtype=torch.bfloat16, device="cuda")
+    dx = torch.empty((N, Di, Hi, Wi, Ci), dtype=torch.bfloat16, device="cuda")
+    xd, wd, dyd = x.cuda(), w.cuda(), dy.cuda()
+    rn.op_conv3d(rn.RN_BF16, 0, geom, xd, wd, y, impl)
+    rn.op_conv3d(rn.RN_BF16, 1, geom, dyd, wd, dx, impl)
+    torch.cuda.synchronize()
+    # oracle on the same bf16 values, float64
+    wc = w.float().numpy().astype(np.float64).reshape(Co, k, k, k, Ci).transpose(0, 4, 1, 2, 3)
+    xn = x.float().numpy().astype(np.float64)
+    dyn = dy.float().numpy().astype(np.float64)
+    y_ref = O.conv3d(xn, wc, s, p)
+    dx_ref, _ = O.conv3d_backward(xn, wc, dyn, s, p)
+    assert rel(y.float().cpu().numpy(), y_ref) < 4e-3
+    assert rel(dx.float().cpu().numpy(), dx_ref) < 4e-3
+
+
+@pytest.mark.parametrize("cv", CONVS[:3], ids=[c[0] for c in CONVS[:3]])
+def test_conv_wgrad(cv):
+    name, Di, Hi, Wi, Ci, Co, k, s, p = cv
+    N = 2
+    Do, Ho, Wo = (O.conv_out(v, k, s, p) for v in (Di, Hi, Wi))
+    rng = np.random.default_rng(1)
+    x = bf16_vals((N, Di, Hi, Wi, Ci), rng)
+    dy = bf16_vals((N, Do, Ho, Wo, Co), rng)
+    geom = [N, Di, Hi, Wi, Ci, Do, Ho, Wo, Co, k, s, p]
+    dw = torch.empty((Co, k ** 3, Ci), dtype=torch.float32, device="cuda")
+    rn.op_conv3d(rn.RN_BF16, 2, geom, x.cuda(), dy.cuda(), dw, 0)
+    torch.cuda.synchronize()
+    xn = x.float().numpy().astype(np.float64)
+    dyn = dy.float().numpy().astype(np.float64)
+    _, dw_ref = O.conv3d_backward(xn, np.zeros((Co, Ci, k, k, k)), dyn, s, p, need_dx=False)
+    got = dw.cpu().numpy().reshape(Co, k, k, k, Ci).transpose(0, 4, 1, 2, 3)
+    assert rel(got, dw_ref) < 1e-4
