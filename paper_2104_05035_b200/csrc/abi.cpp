@@ -320,7 +320,7 @@ rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const voi
     return set_error(RN_ERR_ARG, "rn_op_conv3d: inconsistent geometry");
   cudaStream_t st = (cudaStream_t)stream;
   const DType dt = dtype == RN_BF16 ? DT_BF16 : DT_F32;
-  const bool tc_ok = dt == DT_BF16 && op != 2 && tc_conv_supported(g, op == 1);
+  const bool tc_ok = dt == DT_BF16 && (op == 2 ? tc_wgrad_supported(g) : tc_conv_supported(g, op == 1));
   if (impl == 2 && !tc_ok) return set_error(RN_ERR_ARG, "rn_op_conv3d: tcgen05 kernel does not take this conv");
   const bool tc = tc_ok && impl != 1;
   if (op == 0) {
@@ -340,9 +340,11 @@ rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const voi
     }
   } else {
     float *ws = nullptr;
-    CUDA_CHECK(cudaMallocAsync((void **)&ws, sizeof(float) * conv_wgrad_ws_floats(g), st));
+    const size_t wsf = tc ? tc_wgrad_ws_floats(g) : conv_wgrad_ws_floats(g);
+    CUDA_CHECK(cudaMallocAsync((void **)&ws, sizeof(float) * wsf, st));
     CUDA_CHECK(cudaMemsetAsync(out_dev, 0, sizeof(float) * (size_t)g.Co * g.taps() * g.Ci, st));
-    conv_wgrad_simt(dt, false, g, a_dev, b_dev, (float *)out_dev, ws, st);
+    if (tc) conv_wgrad_tc(g, (const bf16 *)a_dev, (const bf16 *)b_dev, (float *)out_dev, ws, st);
+    else conv_wgrad_simt(dt, false, g, a_dev, b_dev, (float *)out_dev, ws, st);
     CUDA_CHECK(cudaFreeAsync(ws, st));
   }
   return RN_OK;

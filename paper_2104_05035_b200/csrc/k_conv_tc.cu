@@ -251,6 +251,8 @@ void load_encode() {
   g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
 }
 
+}  // namespace
+
 // 5-D view of an NDHWC bf16 tensor: dims {C, W, H, D, N} with element strides
 // (sw, sh, sd, sn) in voxels (a parity sub-lattice uses doubled strides).
 void make_act_map(CUtensorMap *m, const void *base, int C, int W, int H, int D, int N, int64_t sw, int64_t sh,
@@ -266,6 +268,8 @@ void make_act_map(CUtensorMap *m, const void *base, int C, int W, int H, int D, 
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(RN_ERR_CUDA, "cuTensorMapEncodeTiled (activation) failed: " + std::to_string(r));
 }
+
+namespace {
 
 void make_w_map(CUtensorMap *m, const void *base, int rows, int64_t ktot, int bn) {
   load_encode();

@@ -48,6 +48,7 @@ void Plan::make_conv(ConvL &c, int w_idx, int Ci, int Co, int k, int s, int p, D
   c.g.Do = out.d; c.g.Ho = out.h; c.g.Wo = out.w; c.g.Co = Co;
   c.g.k = k; c.g.s = s; c.g.p = p;
   size_t wsf = conv_wgrad_ws_floats(c.g);
+  if (dt == DT_BF16) wsf = std::max(wsf, tc_wgrad_ws_floats(c.g));
   if (wsf > wgrad_ws_floats) wgrad_ws_floats = wsf;
 }
 
@@ -352,7 +353,10 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
 void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32) {
   const bool t = timing();
   size_t e = t ? tk_begin(2, conv_flops(c.g)) : 0;
-  conv_wgrad_simt(dt, x_f32, c.g, x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), stream);
+  if (!x_f32 && use_tc(c.g, false) && tc_wgrad_supported(c.g))
+    conv_wgrad_tc(c.g, (const bf16 *)x, (const bf16 *)dy, grad(c.w_idx), (float *)P(off_wgrad_ws), stream);
+  else
+    conv_wgrad_simt(dt, x_f32, c.g, x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), stream);
   if (t) tk_end(e);
 }
 

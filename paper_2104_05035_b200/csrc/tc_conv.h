@@ -16,4 +16,10 @@ void conv_fprop_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat1
 void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dy, const __nv_bfloat16 *wd, __nv_bfloat16 *dx,
                    bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask, cudaStream_t st);
 
+// weight gradient dw[co][tap][ci] += sum dy x (fp32 partials in ws, fixed-order reduce)
+bool tc_wgrad_supported(const ConvGeom &g);
+size_t tc_wgrad_ws_floats(const ConvGeom &g);
+void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *dy, float *dw, float *ws,
+                   cudaStream_t st);
+
 }  // namespace rn

@@ -110,7 +110,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t *r) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Shared-memory matrix descriptor (tcgen05): start>>4 [0,14), LBO>>4 [16,30),
-// SBO>>4 [32,46), version 1 [46,48), base offset [49,52), layout [61,64).
+// SBO>>4 [32,46), version 1 [46,48), base offset [49,52) = 0, layout [61,64).
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
                                               uint32_t layout /*2 = SWIZZLE_128B*/) {
   uint64_t d = 0;
@@ -118,7 +118,9 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes
   d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)((saddr >> 7) & 7) << 49;  // base offset: row phase inside the 1024-B swizzle pattern
+  // base offset [49,52) stays 0: the swizzle phase of every row is taken from the
+  // absolute smem address (measured on B200: a start address at any 128-B row
+  // of a TMA-written SW128 tile reads correctly with base offset 0).
   d |= (uint64_t)(layout & 7) << 61;
   return d;
 }

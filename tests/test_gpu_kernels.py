@@ -63,8 +63,9 @@ def test_conv_fprop_dgrad(cv, impl):
     assert rel(dx.float().cpu().numpy(), dx_ref) < 4e-3
 
 
-@pytest.mark.parametrize("cv", CONVS[:3], ids=[c[0] for c in CONVS[:3]])
-def test_conv_wgrad(cv):
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("cv", CONVS, ids=[c[0] for c in CONVS])
+def test_conv_wgrad(cv, impl):
     name, Di, Hi, Wi, Ci, Co, k, s, p = cv
     N = 2
     Do, Ho, Wo = (O.conv_out(v, k, s, p) for v in (Di, Hi, Wi))
@@ -73,7 +74,7 @@ def test_conv_wgrad(cv):
     dy = bf16_vals((N, Do, Ho, Wo, Co), rng)
     geom = [N, Di, Hi, Wi, Ci, Do, Ho, Wo, Co, k, s, p]
     dw = torch.empty((Co, k ** 3, Ci), dtype=torch.float32, device="cuda")
-    rn.op_conv3d(rn.RN_BF16, 2, geom, x.cuda(), dy.cuda(), dw, 0)
+    rn.op_conv3d(rn.RN_BF16, 2, geom, x.cuda(), dy.cuda(), dw, impl)
     torch.cuda.synchronize()
     xn = x.float().numpy().astype(np.float64)
     dyn = dy.float().numpy().astype(np.float64)
