@@ -324,7 +324,13 @@ rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const voi
   if (impl == 2 && !tc_ok) return set_error(RN_ERR_ARG, "rn_op_conv3d: tcgen05 kernel does not take this conv");
   const bool tc = tc_ok && impl != 1;
   if (op == 0) {
-    if (tc) conv_fprop_tc(g, (const bf16 *)a_dev, (const bf16 *)b_dev, nullptr, (bf16 *)out_dev, st);
+    if (tc) {
+      const size_t wsf = tc_conv_ws_floats(g, false);
+      float *ws = nullptr;
+      if (wsf) CUDA_CHECK(cudaMallocAsync((void **)&ws, sizeof(float) * wsf, st));
+      conv_fprop_tc(g, (const bf16 *)a_dev, (const bf16 *)b_dev, nullptr, (bf16 *)out_dev, ws, wsf, st);
+      if (ws) CUDA_CHECK(cudaFreeAsync(ws, st));
+    }
     else conv_fprop_simt(dt, g, a_dev, b_dev, nullptr, out_dev, st);
   } else if (op == 1) {
     if (tc) {
@@ -333,7 +339,11 @@ rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const voi
       CUDA_CHECK(cudaMallocAsync(&wd, n * 2, st));
       flip_weights(dt, b_dev, g.Co, g.taps(), g.Ci, wd, st);
       CUDA_CHECK(cudaMemsetAsync(out_dev, 0, 2 * (size_t)g.in_vox() * g.Ci, st));
-      conv_dgrad_tc(g, (const bf16 *)a_dev, (const bf16 *)wd, (bf16 *)out_dev, true, nullptr, nullptr, st);
+      const size_t wsf = tc_conv_ws_floats(g, true);
+      float *ws = nullptr;
+      if (wsf) CUDA_CHECK(cudaMallocAsync((void **)&ws, sizeof(float) * wsf, st));
+      conv_dgrad_tc(g, (const bf16 *)a_dev, (const bf16 *)wd, (bf16 *)out_dev, true, nullptr, nullptr, ws, wsf, st);
+      if (ws) CUDA_CHECK(cudaFreeAsync(ws, st));
       CUDA_CHECK(cudaFreeAsync(wd, st));
     } else {
       conv_dgrad_simt(dt, g, a_dev, b_dev, out_dev, false, nullptr, nullptr, st);

@@ -60,6 +60,10 @@ struct __align__(64) TcParams {
   int accumulate;
   const bf16 *res;
   const bf16 *res_mask;
+  // split-K over the K blocks (layers with fewer tiles than SMs)
+  int ksplit;
+  float *part;
+  int64_t n_view_vox;
 };
 
 template <int BN, int STAGES>
@@ -107,31 +111,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
   const uint32_t tmem_base = *tmem_slot;
 
   const int nk = p.n_taps * p.kblocks_per_tap;
+  const int64_t n_items = p.n_tiles * p.ksplit;
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-        int64_t r = tile;
+      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+        int64_t r = item / p.ksplit;
+        const int split = (int)(item % p.ksplit);
         const int nb = (int)(r % p.t_nblk); r /= p.t_nblk;
         const int tw = (int)(r % p.tw); r /= p.tw;
         const int th = (int)(r % p.th); r /= p.th;
         const int td = (int)(r % p.td); r /= p.td;
         const int tn = (int)r;
         const int w0 = tw * p.bw, h0 = th * p.bh, d0 = td * p.bd, n0 = tn * p.bn;
-        for (int t = 0; t < p.n_taps; ++t) {
-          const CUtensorMap *am = &p.a_map[p.tap_map[t]];
-          for (int cb = 0; cb < p.kblocks_per_tap; ++cb) {
-            tc::mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t *sa = smem + stage * S::STAGE;
-            uint8_t *sb = sa + S::A_BYTES;
-            tc::mbar_arrive_expect_tx(&full[stage], S::STAGE);
-            tc::tma_load_5d(sa, am, &full[stage], cb * 64, w0 + p.tap_ow[t], h0 + p.tap_oh[t], d0 + p.tap_od[t], n0);
-            tc::tma_load_2d(sb, &p.b_map, &full[stage], p.tap_kcoord[t] + cb * 64, nb * BN);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          }
+        const int kb0 = split * nk / p.ksplit, kb1 = (split + 1) * nk / p.ksplit;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const int t = kb / p.kblocks_per_tap, cb = kb % p.kblocks_per_tap;
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t *sa = smem + stage * S::STAGE;
+          uint8_t *sb = sa + S::A_BYTES;
+          tc::mbar_arrive_expect_tx(&full[stage], S::STAGE);
+          tc::tma_load_5d(sa, &p.a_map[p.tap_map[t]], &full[stage], cb * 64, w0 + p.tap_ow[t], h0 + p.tap_oh[t],
+                          d0 + p.tap_od[t], n0);
+          tc::tma_load_2d(sb, &p.b_map, &full[stage], p.tap_kcoord[t] + cb * 64, nb * BN);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -141,13 +147,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++local) {
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+      const int split = (int)(item % p.ksplit);
+      const int kb0 = split * nk / p.ksplit, kb1 = (split + 1) * nk / p.ksplit;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc::tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < nk; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
         if (lane == 0) {
@@ -157,10 +165,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
           for (int k = 0; k < 4; ++k) {
             const uint64_t ad = tc::smem_desc(sa + k * 32, 16, 1024, 2);
             const uint64_t bd = tc::smem_desc(sb + k * 32, 16, 1024, 2);
-            tc::mma_bf16(d_tmem, ad, bd, IDESC, (kb | k) != 0);
+            tc::mma_bf16(d_tmem, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           tc::mma_commit(&empty[stage]);
-          if (kb == nk - 1) tc::mma_commit(&tfull[acc]);
+          if (kb == kb1 - 1) tc::mma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -173,8 +181,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
     const int wx = row % p.bw, hy = (row / p.bw) % p.bh, dz = (row / (p.bw * p.bh)) % p.bd,
               nz = row / (p.bw * p.bh * p.bd);
     int local = 0;
-    for (int64_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++local) {
-      int64_t r = tile;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
+      int64_t r = item / p.ksplit;
+      const int split = (int)(item % p.ksplit);
       const int nb = (int)(r % p.t_nblk); r /= p.t_nblk;
       const int tw = (int)(r % p.tw); r /= p.tw;
       const int th = (int)(r % p.th); r /= p.th;
@@ -192,7 +201,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
         uint32_t v[32];
         tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
         tc::tmem_wait_ld();
-        if (valid) {
+        if (valid && p.ksplit > 1) {
+          // split-K: raw fp32 partial [split][view voxel][Nout]; epilogue in conv_splitk_finish
+          const int64_t vidx = ((int64_t)(on * p.OD + od) * p.OH + oh) * p.OW + ow;
+          float *dst = p.part + ((int64_t)split * p.n_view_vox + vidx) * p.ych + nb * BN + c0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4 *>(dst + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                                               __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+        } else if (valid) {
           float f[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
@@ -255,8 +272,11 @@ void load_encode() {
 
 // 5-D view of an NDHWC bf16 tensor: dims {C, W, H, D, N} with element strides
 // (sw, sh, sd, sn) in voxels (a parity sub-lattice uses doubled strides).
+static thread_local size_t *g_dry_need = nullptr;  // non-null: size the split-K workspace only
+
 void make_act_map(CUtensorMap *m, const void *base, int C, int W, int H, int D, int N, int64_t sw, int64_t sh,
                   int64_t sd, int64_t sn, int bw, int bh, int bd, int bn) {
+  if (g_dry_need) return;
   load_encode();
   cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)D, (cuuint64_t)N};
   cuuint64_t strides[4] = {(cuuint64_t)(sw * C * 2), (cuuint64_t)(sh * C * 2), (cuuint64_t)(sd * C * 2),
@@ -272,6 +292,7 @@ void make_act_map(CUtensorMap *m, const void *base, int C, int W, int H, int D, 
 namespace {
 
 void make_w_map(CUtensorMap *m, const void *base, int rows, int64_t ktot, int bn) {
+  if (g_dry_need) return;
   load_encode();
   cuuint64_t dims[2] = {(cuuint64_t)ktot, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ktot * 2)};
@@ -311,15 +332,84 @@ void launch(const TcParams &p, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (int)std::min<int64_t>(p.n_tiles, sms);
+  const int grid = (int)std::min<int64_t>(p.n_tiles * p.ksplit, sms);
   conv_tc_kernel<BN, STAGES><<<grid, TC_THREADS, S::TOTAL, st>>>(p);
   LAUNCH_CHECK();
 }
 
-void run(const TcParams &p, int BN, cudaStream_t st) {
+// split-K finish: out = sum_s part[s] (+bias) (+existing) (+res*(mask>0)), bf16 store through the view
+__global__ void splitk_finish_k(const float *__restrict__ part, int ks, int64_t nvv, int ych, int OW, int OH, int OD,
+                                bf16 *__restrict__ y, int64_t s_n, int64_t s_d, int64_t s_h, int64_t s_w,
+                                const float *__restrict__ bias, int accumulate, const bf16 *__restrict__ res,
+                                const bf16 *__restrict__ res_mask) {
+  const int G = ych / 8;
+  const int64_t n = nvv * G;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i % G) * 8;
+    const int64_t vidx = i / G;
+    int64_t r = vidx;
+    const int ow = (int)(r % OW); r /= OW;
+    const int oh = (int)(r % OH); r /= OH;
+    const int od = (int)(r % OD); r /= OD;
+    const int on = (int)r;
+    float f[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = 0.f;
+    for (int s = 0; s < ks; ++s) {
+      const float *src = part + ((int64_t)s * nvv + vidx) * ych + c0;
+      const float4 a = *reinterpret_cast<const float4 *>(src);
+      const float4 b = *reinterpret_cast<const float4 *>(src + 4);
+      f[0] += a.x; f[1] += a.y; f[2] += a.z; f[3] += a.w;
+      f[4] += b.x; f[5] += b.y; f[6] += b.z; f[7] += b.w;
+    }
+    if (bias)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] += bias[c0 + j];
+    const int64_t o = on * s_n + od * s_d + oh * s_h + ow * s_w + c0;
+    if (accumulate) {
+      float e[8];
+      load_vec(y + o, e);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] += e[j];
+    }
+    if (res) {
+      float rv[8], mv[8];
+      load_vec(res + o, rv);
+      load_vec(res_mask + o, mv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] += mv[j] > 0.f ? rv[j] : 0.f;
+    }
+    store_vec(y + o, f);
+  }
+}
+
+int choose_ksplit(int64_t n_tiles, int nk) {
+  if (n_tiles >= 100) return 1;
+  int ks = (int)((2 * 148) / std::max<int64_t>(n_tiles, 1));
+  ks = std::min(ks, nk / 4);
+  return std::max(ks, 1);
+}
+
+void run(TcParams &p, int BN, float *ws, size_t ws_floats, cudaStream_t st) {
+  const int nk = p.n_taps * p.kblocks_per_tap;
+  p.n_view_vox = (int64_t)p.ON * p.OD * p.OH * p.OW;
+  p.ksplit = choose_ksplit(p.n_tiles, nk);
+  if (g_dry_need) {
+    if (p.ksplit > 1) *g_dry_need = std::max(*g_dry_need, (size_t)p.ksplit * p.n_view_vox * p.ych);
+    return;
+  }
+  if (!ws || (size_t)p.ksplit * p.n_view_vox * p.ych > ws_floats) p.ksplit = 1;
+  p.part = ws;
   if (BN == 64) launch<64, 6>(p, st);
   else if (BN == 128) launch<128, 5>(p, st);
   else launch<256, 4>(p, st);
+  if (p.ksplit > 1) {
+    const int64_t n = p.n_view_vox * (p.ych / 8);
+    splitk_finish_k<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(
+        ws, p.ksplit, p.n_view_vox, p.ych, p.OW, p.OH, p.OD, p.y, p.s_n, p.s_d, p.s_h, p.s_w, p.bias, p.accumulate,
+        p.res, p.res_mask);
+    LAUNCH_CHECK();
+  }
 }
 
 int pick_bn(int nout) {
@@ -357,7 +447,8 @@ bool tc_conv_supported(const ConvGeom &g, bool dgrad) {
 }
 
 // fprop: y[vo][co] = sum x[...] w[co][tap][ci] (+bias)
-void conv_fprop_tc(const ConvGeom &g, const bf16 *x, const bf16 *w, const float *bias, bf16 *y, cudaStream_t st) {
+void conv_fprop_tc(const ConvGeom &g, const bf16 *x, const bf16 *w, const float *bias, bf16 *y, float *ws,
+                   size_t ws_floats, cudaStream_t st) {
   TcParams p;
   memset(&p, 0, sizeof p);
   const int BN = pick_bn(g.Co);
@@ -402,12 +493,12 @@ void conv_fprop_tc(const ConvGeom &g, const bf16 *x, const bf16 *w, const float 
   p.s_d = (int64_t)g.Ho * g.Wo * g.Co;
   p.s_n = (int64_t)g.Do * g.Ho * g.Wo * g.Co;
   p.bias = bias;
-  run(p, BN, st);
+  run(p, BN, ws, ws_floats, st);
 }
 
 // dgrad: dx[vi][ci] (=|+=) sum dy[vo][co] W[co][tap][ci]; wd = [ci][taps-1-tap][co]
 void conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, bool accumulate, const bf16 *res,
-                   const bf16 *res_mask, cudaStream_t st) {
+                   const bf16 *res_mask, float *ws, size_t ws_floats, cudaStream_t st) {
   const int taps = g.taps();
   const int BN = pick_bn(g.Ci);
   if (g.s == 1) {
@@ -435,7 +526,7 @@ void conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, 
     p.accumulate = accumulate;
     p.res = res;
     p.res_mask = res_mask;
-    run(p, BN, st);
+    run(p, BN, ws, ws_floats, st);
     return;
   }
   // stride 2: output parity classes (pd, ph, pw); input index i = 2a + par.
@@ -489,8 +580,22 @@ void conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, 
           p.res = res + (((int64_t)pd * g.Hi + ph) * g.Wi + pw) * g.Ci;
           p.res_mask = res_mask + (((int64_t)pd * g.Hi + ph) * g.Wi + pw) * g.Ci;
         }
-        run(p, BN, st);
+        run(p, BN, ws, ws_floats, st);
       }
+}
+
+size_t tc_conv_ws_floats(const ConvGeom &g, bool dgrad) {
+  size_t need = 0;
+  g_dry_need = &need;
+  try {
+    if (!dgrad) conv_fprop_tc(g, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr);
+    else conv_dgrad_tc(g, nullptr, nullptr, nullptr, true, nullptr, nullptr, nullptr, 0, nullptr);
+  } catch (...) {
+    g_dry_need = nullptr;
+    throw;
+  }
+  g_dry_need = nullptr;
+  return need;
 }
 
 }  // namespace rn

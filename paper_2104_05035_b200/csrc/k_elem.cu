@@ -47,7 +47,14 @@ __global__ void __launch_bounds__(NT) chan_reduce_k(Op op, int64_t V, int C, flo
     op.init(cg * VEC);
     const int64_t r0 = (int64_t)blockIdx.x * rpb;
     const int64_t r1 = min(V, r0 + rpb);
-    for (int64_t r = r0 + rr; r < r1; r += RPI) op.row(r, cg * VEC, a1, a2);
+    int64_t r = r0 + rr;
+    for (; r + 3 * RPI < r1; r += 4 * RPI) {  // 4 independent rows per iteration (memory-level parallelism)
+      op.row(r, cg * VEC, a1, a2);
+      op.row(r + RPI, cg * VEC, a1, a2);
+      op.row(r + 2 * RPI, cg * VEC, a1, a2);
+      op.row(r + 3 * RPI, cg * VEC, a1, a2);
+    }
+    for (; r < r1; r += RPI) op.row(r, cg * VEC, a1, a2);
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
       sm[rr * C + cg * VEC + j] = a1[j];
@@ -155,61 +162,76 @@ struct AttBwdOp {
   }
 };
 
+// Sum of per-block partials for channel c: one warp per channel, lanes stride
+// over the blocks in double, fixed shuffle tree (deterministic).
+__device__ __forceinline__ void warp_partial_sums(const float *partial, int nblk, int C, int c, double &S1,
+                                                  double &S2) {
+  const int lane = threadIdx.x & 31;
+  double a = 0.0, b = 0.0;
+  for (int k = lane; k < nblk; k += 32) {
+    a += (double)partial[(int64_t)k * 2 * C + c];
+    b += (double)partial[(int64_t)k * 2 * C + C + c];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  S1 = a;
+  S2 = b;
+}
+
 template <typename T>
 __global__ void bn_finalize_k(const T *x, const float *partial, int nblk, int64_t V, int C, const float *gamma,
                               const float *beta, float *mean, float *invstd, float *scale, float *shift,
                               float *run_mean, float *run_var, float momentum, float eps) {
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    double S = 0.0, Q = 0.0;
-    for (int b = 0; b < nblk; ++b) {
-      S += (double)partial[(int64_t)b * 2 * C + c];
-      Q += (double)partial[(int64_t)b * 2 * C + C + c];
-    }
-    const double K = (double)to_f(x[c]);
-    const double ms = S / (double)V;
-    double var = Q / (double)V - ms * ms;
-    if (var < 0) var = 0;
-    const double mu = K + ms;
-    const double is = 1.0 / sqrt(var + (double)eps);
-    mean[c] = (float)mu;
-    invstd[c] = (float)is;
-    const double sc = (double)gamma[c] * is;
-    scale[c] = (float)sc;
-    shift[c] = (float)((double)beta[c] - mu * sc);
-    if (run_mean) {
-      const double unb = V > 1 ? var * (double)V / (double)(V - 1) : var;
-      run_mean[c] = (float)((1.0 - momentum) * run_mean[c] + momentum * mu);
-      run_var[c] = (float)((1.0 - momentum) * run_var[c] + momentum * unb);
-    }
+  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (c >= C) return;
+  double S, Q;
+  warp_partial_sums(partial, nblk, C, c, S, Q);
+  if ((threadIdx.x & 31) != 0) return;
+  const double K = (double)to_f(x[c]);
+  const double ms = S / (double)V;
+  double var = Q / (double)V - ms * ms;
+  if (var < 0) var = 0;
+  const double mu = K + ms;
+  const double is = 1.0 / sqrt(var + (double)eps);
+  mean[c] = (float)mu;
+  invstd[c] = (float)is;
+  const double sc = (double)gamma[c] * is;
+  scale[c] = (float)sc;
+  shift[c] = (float)((double)beta[c] - mu * sc);
+  if (run_mean) {
+    const double unb = V > 1 ? var * (double)V / (double)(V - 1) : var;
+    run_mean[c] = (float)((1.0 - momentum) * run_mean[c] + momentum * mu);
+    run_var[c] = (float)((1.0 - momentum) * run_var[c] + momentum * unb);
   }
 }
 
 __global__ void bn_bwd_finalize_k(const float *partial, int nblk, int64_t V, int C, const float *gamma,
                                   const float *mean, const float *invstd, float *dgamma, float *dbeta,
                                   float *coef) {
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    double S1 = 0.0, S2 = 0.0;
-    for (int b = 0; b < nblk; ++b) {
-      S1 += (double)partial[(int64_t)b * 2 * C + c];
-      S2 += (double)partial[(int64_t)b * 2 * C + C + c];
-    }
-    dgamma[c] += (float)S2;
-    dbeta[c] += (float)S1;
-    const double m1 = S1 / (double)V, m2 = S2 / (double)V;
-    const double is = invstd[c];
-    const double A = (double)gamma[c] * is;
-    coef[c] = (float)A;
-    coef[C + c] = (float)(-A * is * m2);
-    coef[2 * C + c] = (float)(-A * m1 + A * is * (double)mean[c] * m2);
-  }
+  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (c >= C) return;
+  double S1, S2;
+  warp_partial_sums(partial, nblk, C, c, S1, S2);
+  if ((threadIdx.x & 31) != 0) return;
+  dgamma[c] += (float)S2;
+  dbeta[c] += (float)S1;
+  const double m1 = S1 / (double)V, m2 = S2 / (double)V;
+  const double is = invstd[c];
+  const double A = (double)gamma[c] * is;
+  coef[c] = (float)A;
+  coef[C + c] = (float)(-A * is * m2);
+  coef[2 * C + c] = (float)(-A * m1 + A * is * (double)mean[c] * m2);
 }
 
 __global__ void chan_sum_finalize_k(const float *partial, int nblk, int C, float *out) {
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    double S = 0.0;
-    for (int b = 0; b < nblk; ++b) S += (double)partial[(int64_t)b * 2 * C + c];
-    out[c] += (float)S;
-  }
+  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (c >= C) return;
+  double S1, S2;
+  warp_partial_sums(partial, nblk, C, c, S1, S2);
+  if ((threadIdx.x & 31) == 0) out[c] += (float)S1;
 }
 
 template <typename T>
@@ -524,14 +546,25 @@ __global__ void sgd_k(float *__restrict__ w, const float *__restrict__ g, int64_
 template <typename T>
 __global__ void repack_k(const float *__restrict__ w, int Co, int taps, int Ci, T *__restrict__ wf,
                          T *__restrict__ wd) {
-  const int64_t n = (int64_t)Co * taps * Ci;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int ci = (int)(i % Ci);
-    const int tap = (int)((i / Ci) % taps);
-    const int co = (int)(i / ((int64_t)Ci * taps));
-    const T v = from_f<T>(w[i]);
-    if (wf) wf[i] = v;
-    if (wd) wd[((int64_t)ci * taps + (taps - 1 - tap)) * Co + co] = v;
+  // 32x32 tile of one tap: read/write wf along ci, write wd along co (smem transpose)
+  __shared__ float tile[32][33];
+  const int ci0 = blockIdx.x * 32, co0 = blockIdx.y * 32, tap = blockIdx.z;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int r = ty; r < 32; r += 8) {
+    const int co = co0 + r, ci = ci0 + tx;
+    float v = 0.f;
+    if (co < Co && ci < Ci) {
+      const int64_t i = ((int64_t)co * taps + tap) * Ci + ci;
+      v = w[i];
+      if (wf) wf[i] = from_f<T>(v);
+    }
+    tile[r][tx] = v;
+  }
+  if (!wd) return;
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int ci = ci0 + r, co = co0 + tx;
+    if (co < Co && ci < Ci) wd[((int64_t)ci * taps + (taps - 1 - tap)) * Co + co] = from_f<T>(tile[tx][r]);
   }
 }
 
@@ -543,8 +576,8 @@ __global__ void check_finite_k(const float *v, int n, int *flag) {
 }  // namespace
 
 int chan_reduce_blocks(int64_t V, int C) {
-  int64_t b = (V + 255) / 256;
-  if (b > 2 * 148) b = 2 * 148;
+  int64_t b = (V + 127) / 128;
+  if (b > 4 * 148) b = 4 * 148;
   if (b < 1) b = 1;
   return (int)b;
 }
@@ -574,8 +607,8 @@ void bn_stats(DType dt, const void *x, int64_t V, int C, float *partial, int nbl
 void bn_finalize(DType dt, const void *x, const float *partial, int nblk, int64_t V, int C, const float *gamma,
                  const float *beta, float *mean, float *invstd, float *scale, float *shift, float *run_mean,
                  float *run_var, float momentum, float eps, cudaStream_t st) {
-  DISPATCH(dt, bn_finalize_k<T><<<1, 512, 0, st>>>((const T *)x, partial, nblk, V, C, gamma, beta, mean, invstd,
-                                                    scale, shift, run_mean, run_var, momentum, eps));
+  DISPATCH(dt, bn_finalize_k<T><<<(C + 7) / 8, 256, 0, st>>>((const T *)x, partial, nblk, V, C, gamma, beta, mean,
+                                                             invstd, scale, shift, run_mean, run_var, momentum, eps));
   LAUNCH_CHECK();
 }
 
@@ -601,7 +634,7 @@ void bn_bwd_reduce(DType dt, const void *dy, const void *x, int64_t V, int C, in
 
 void bn_bwd_finalize(const float *partial, int nblk, int64_t V, int C, const float *gamma, const float *mean,
                      const float *invstd, float *dgamma, float *dbeta, float *coef, cudaStream_t st) {
-  bn_bwd_finalize_k<<<1, 512, 0, st>>>(partial, nblk, V, C, gamma, mean, invstd, dgamma, dbeta, coef);
+  bn_bwd_finalize_k<<<(C + 7) / 8, 256, 0, st>>>(partial, nblk, V, C, gamma, mean, invstd, dgamma, dbeta, coef);
   LAUNCH_CHECK();
 }
 
@@ -659,7 +692,7 @@ void att_bwd(DType dt, const void *dout, const void *m, const void *T_, int64_t 
 }
 
 void chan_sum_finalize(const float *partial, int nblk, int C, float *out, cudaStream_t st) {
-  chan_sum_finalize_k<<<1, 512, 0, st>>>(partial, nblk, C, out);
+  chan_sum_finalize_k<<<(C + 7) / 8, 256, 0, st>>>(partial, nblk, C, out);
   LAUNCH_CHECK();
 }
 
@@ -686,7 +719,8 @@ void sgd_update(float *w, const float *g, int64_t n, float lr, cudaStream_t st) 
 }
 
 void repack_conv(DType dt, const float *w, int Co, int taps, int Ci, void *wf, void *wd, cudaStream_t st) {
-  DISPATCH(dt, repack_k<T><<<grid_for((int64_t)Co * taps * Ci), NT, 0, st>>>(w, Co, taps, Ci, (T *)wf, (T *)wd));
+  dim3 grid((Ci + 31) / 32, (Co + 31) / 32, taps);
+  DISPATCH(dt, repack_k<T><<<grid, dim3(32, 8), 0, st>>>(w, Co, taps, Ci, (T *)wf, (T *)wd));
   LAUNCH_CHECK();
 }
 

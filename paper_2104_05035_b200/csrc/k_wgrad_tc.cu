@@ -37,7 +37,7 @@ namespace rn {
 namespace {
 
 constexpr int WG_THREADS = 192;
-constexpr int MAX_ATOMS = 64;  // atoms per CTA (2 per M-tile)
+constexpr int MAX_ATOMS = 128;  // M-tiles per problem (2 atoms each)
 
 struct __align__(64) WgParams {
   CUtensorMap x_map[8];
@@ -49,11 +49,11 @@ struct __align__(64) WgParams {
   int splits;
   // atoms of the whole problem: atom a = (tap, ci block); M-tile i = atoms 2i, 2i+1
   int n_mtiles;
-  int8_t atom_map[2 * 64];  // x map index (per-tap mode)
-  int8_t atom_od[2 * 64], atom_oh[2 * 64], atom_ow[2 * 64];
-  int16_t atom_tap[2 * 64];
-  int8_t atom_cb[2 * 64];
-  int8_t atom_valid[2 * 64];
+  int8_t atom_map[2 * MAX_ATOMS];  // x map index (per-tap mode)
+  int8_t atom_od[2 * MAX_ATOMS], atom_oh[2 * MAX_ATOMS], atom_ow[2 * MAX_ATOMS];
+  int16_t atom_tap[2 * MAX_ATOMS];
+  int8_t atom_cb[2 * MAX_ATOMS];
+  int8_t atom_valid[2 * MAX_ATOMS];
   // voxel tiles of dy
   int bw, bh, bd, bn;
   int tw, th, td, tn;

@@ -36,6 +36,12 @@ void conv_wgrad_simt(DType dt, bool x_is_f32, const ConvGeom &g, const void *x, 
                      float *ws, cudaStream_t st);
 // stem: Ci = 1, x fp32 [N][D][H][W], w fp32 [Co][27]
 void stem_conv_fprop(DType dt, const ConvGeom &g, const float *x, const float *w, void *y, cudaStream_t st);
+// k_stem.cu: Co in {8,16,32,64}
+bool stem_fast_supported(const ConvGeom &g);
+size_t stem_wgrad_ws_floats(const ConvGeom &g);
+void stem_fprop_fast(DType dt, const ConvGeom &g, const float *x, const float *w, void *y, cudaStream_t st);
+void stem_wgrad_fast(DType dt, const ConvGeom &g, const float *x, const void *dh, float *dw, float *ws,
+                     cudaStream_t st);
 
 // ---------------- BatchNorm (train mode), ReLU, residual ----------------
 int chan_reduce_blocks(int64_t V, int C);

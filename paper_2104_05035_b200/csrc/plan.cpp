@@ -49,6 +49,11 @@ void Plan::make_conv(ConvL &c, int w_idx, int Ci, int Co, int k, int s, int p, D
   c.g.k = k; c.g.s = s; c.g.p = p;
   size_t wsf = conv_wgrad_ws_floats(c.g);
   if (dt == DT_BF16) wsf = std::max(wsf, tc_wgrad_ws_floats(c.g));
+  if (Ci == 1 && stem_fast_supported(c.g)) wsf = std::max(wsf, stem_wgrad_ws_floats(c.g));
+  if (dt == DT_BF16) {
+    if (tc_conv_supported(c.g, false)) conv_ws_floats = std::max(conv_ws_floats, tc_conv_ws_floats(c.g, false));
+    if (tc_conv_supported(c.g, true)) conv_ws_floats = std::max(conv_ws_floats, tc_conv_ws_floats(c.g, true));
+  }
   if (wsf > wgrad_ws_floats) wgrad_ws_floats = wsf;
 }
 
@@ -220,10 +225,11 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
     }
   }
   // scratch
-  nblk_max = 2 * 148;
+  nblk_max = 4 * 148;
   off_partial = alloc(sizeof(float) * nblk_max * 2 * 512);
   off_coef = alloc(sizeof(float) * 3 * 512 * 2);
   off_wgrad_ws = alloc(sizeof(float) * (wgrad_ws_floats ? wgrad_ws_floats : 1));
+  off_conv_ws = alloc(sizeof(float) * (conv_ws_floats ? conv_ws_floats : 1));
 
   // --- communicators ---
   if (world > 1) {
@@ -334,7 +340,8 @@ void Plan::conv_fwd(const ConvL &c, const void *x, void *y, const float *bias) {
   const bool t = timing();
   size_t e = t ? tk_begin(0, conv_flops(c.g)) : 0;
   if (use_tc(c.g, false))
-    conv_fprop_tc(c.g, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, stream);
+    conv_fprop_tc(c.g, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y,
+                  (float *)P(off_conv_ws), conv_ws_floats, stream);
   else
     conv_fprop_simt(dt, c.g, x, wfwd(c.w_idx), bias, y, stream);
   if (t) tk_end(e);
@@ -345,7 +352,7 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
   size_t e = t ? tk_begin(1, conv_flops(c.g)) : 0;
   if (use_tc(c.g, true))
     conv_dgrad_tc(c.g, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), (bf16 *)dx, accumulate,
-                  (const bf16 *)res, (const bf16 *)res_mask, stream);
+                  (const bf16 *)res, (const bf16 *)res_mask, (float *)P(off_conv_ws), conv_ws_floats, stream);
   else
     conv_dgrad_simt(dt, c.g, dy, wfwd(c.w_idx), dx, accumulate, res, res_mask, stream);
   if (t) tk_end(e);
@@ -353,7 +360,9 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
 void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32) {
   const bool t = timing();
   size_t e = t ? tk_begin(2, conv_flops(c.g)) : 0;
-  if (!x_f32 && use_tc(c.g, false) && tc_wgrad_supported(c.g))
+  if (x_f32 && stem_fast_supported(c.g))
+    stem_wgrad_fast(dt, c.g, (const float *)x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), stream);
+  else if (!x_f32 && use_tc(c.g, false) && tc_wgrad_supported(c.g))
     conv_wgrad_tc(c.g, (const bf16 *)x, (const bf16 *)dy, grad(c.w_idx), (float *)P(off_wgrad_ws), stream);
   else
     conv_wgrad_simt(dt, x_f32, c.g, x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), stream);
@@ -440,7 +449,15 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
   UnitL &L = units[ui];
   const void *x = unit_input(ui, k, x_in);
   if (u.kind == U_STEM) {
-    stem_conv_fprop(dt, L.stem_conv.g, (const float *)x, master(L.stem_conv.w_idx), P(L.stem_h[k]), stream);
+    {
+      const bool t = timing();
+      size_t e = t ? tk_begin(0, conv_flops(L.stem_conv.g)) : 0;
+      if (stem_fast_supported(L.stem_conv.g))
+        stem_fprop_fast(dt, L.stem_conv.g, (const float *)x, master(L.stem_conv.w_idx), P(L.stem_h[k]), stream);
+      else
+        stem_conv_fprop(dt, L.stem_conv.g, (const float *)x, master(L.stem_conv.w_idx), P(L.stem_h[k]), stream);
+      if (t) tk_end(e);
+    }
     bn_forward_stats(L.stem_bn, k, P(L.stem_h[k]));
     if (u.pool) {
       maxpool_fwd(dt, P(L.stem_h[k]), mb, u.conv.d, u.conv.h, u.conv.w, u.cout, bn_stat(L.stem_bn, k, 2),

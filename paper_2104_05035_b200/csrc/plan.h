@@ -74,7 +74,7 @@ struct Plan {
   std::vector<size_t> shadow_f, shadow_d;
   size_t off_master = 0, off_grad = 0, off_run_mean = 0, off_run_var = 0, off_loss = 0, off_flag = 0;
   size_t off_partial = 0, off_coef = 0, off_wgrad_ws = 0, off_x = 0, off_y = 0;
-  size_t wgrad_ws_floats = 0;
+  size_t wgrad_ws_floats = 0, conv_ws_floats = 0, off_conv_ws = 0;
   int nblk_max = 0;
   size_t ws_bytes = 0;
   char *base = nullptr;

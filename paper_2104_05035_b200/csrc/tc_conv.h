@@ -10,11 +10,14 @@ namespace rn {
 // true if the tcgen05 kernels take this convolution (bf16, channels % 64 == 0,
 // k in {1, 3}, stride in {1, 2} with the 'same' ceil(in/2) lattice)
 bool tc_conv_supported(const ConvGeom &g, bool dgrad);
+// ws: fp32 split-K workspace of >= tc_conv_ws_floats(g, dgrad) floats (layers with few tiles)
+size_t tc_conv_ws_floats(const ConvGeom &g, bool dgrad);
 void conv_fprop_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, const float *bias,
-                   __nv_bfloat16 *y, cudaStream_t st);
+                   __nv_bfloat16 *y, float *ws, size_t ws_floats, cudaStream_t st);
 // wd: [Ci][taps][Co] with the tap order flipped (repack_conv's wd)
 void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dy, const __nv_bfloat16 *wd, __nv_bfloat16 *dx,
-                   bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask, cudaStream_t st);
+                   bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask, float *ws,
+                   size_t ws_floats, cudaStream_t st);
 
 // weight gradient dw[co][tap][ci] += sum dy x (fp32 partials in ws, fixed-order reduce)
 bool tc_wgrad_supported(const ConvGeom &g);
