@@ -21,7 +21,14 @@ rn_status gabra_place(int32_t n, const int64_t *loads, int32_t m, const int64_t 
 
 static thread_local std::string g_err;
 static std::atomic<int64_t> g_launches{0};
-void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// kernels launched by librn: counted at every eager launch; a CUDA-graph replay
+// adds the number of kernel nodes it contains (captured launches are not counted)
+static thread_local bool g_capturing = false;
+void count_launch() {
+  if (!g_capturing) g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+void add_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void set_capturing(bool c) { g_capturing = c; }
 int64_t launch_count() { return g_launches.load(); }
 rn_status set_error(rn_status s, const std::string &msg) {
   g_err = msg;

@@ -12,6 +12,8 @@ namespace rn {
 
 rn_status set_error(rn_status s, const std::string &msg);
 void count_launch();
+void add_launches(int64_t n);
+void set_capturing(bool c);
 int64_t launch_count();
 
 // Internal exception carrying an rn_status; converted at the ABI boundary.

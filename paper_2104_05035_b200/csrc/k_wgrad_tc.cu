@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -267,7 +268,10 @@ void choose_box_wg(int W, int H, int D, int N, int &bw, int &bh, int &bd, int &b
 WgShape wg_shape(const ConvGeom &g) {
   WgShape s;
   s.BN = g.Co % 256 == 0 ? 256 : g.Co % 128 == 0 ? 128 : 64;
-  s.haloed = (g.s == 1 && g.k == 3 && g.Ci == 64) ? 1 : 0;
+  // haloed staging cuts L2 traffic 9x but measured slower on B200 (MMAs reading
+  // operands from arbitrary row offsets, 252 vs 152 us on the stage-1 shape):
+  // opt-in only (RN_WG_HALO=1) until the MMA-side cost is understood.
+  s.haloed = (g.s == 1 && g.k == 3 && g.Ci == 64 && getenv("RN_WG_HALO")) ? 1 : 0;
   const int atoms = g.taps() * (g.Ci / 64);
   s.n_mtiles = (atoms + 1) / 2;
   if (s.haloed) {
@@ -366,7 +370,9 @@ void conv_wgrad_tc(const ConvGeom &g, const bf16 *x, const bf16 *dy, float *dw, 
   }
   if (na / 2 != s.n_mtiles) throw Error(RN_ERR_STATE, "wgrad: atom count mismatch");
   if (s.haloed) {
-    p.hw = s.bw + 2; p.hh = s.bh + 2; p.hd = s.bd + 2;
+    p.hw = getenv("RN_WG_HW16") ? 16 : s.bw + 2;
+    p.hh = s.bh + 2;
+    p.hd = s.bd + 2;
     make_act_map(&p.x_map[0], x, g.Ci, g.Wi, g.Hi, g.Di, g.N, 1, g.Wi, (int64_t)g.Wi * g.Hi,
                  (int64_t)g.Wi * g.Hi * g.Di, p.hw, p.hh, p.hd, 1);
   } else if (g.s == 1) {
@@ -385,7 +391,8 @@ void conv_wgrad_tc(const ConvGeom &g, const bf16 *x, const bf16 *dy, float *dw, 
   const int grid = s.n_mgroups * s.n_cob * s.splits;
   // the haloed region: 10 x 6 x 6 voxels x 128 B = 46080 B
   if (s.haloed) {
-    if (s.BN == 64) wg_launch<64, 3, 46080>(p, grid, st);
+    if (s.BN == 64 && p.hw == 16) wg_launch<64, 2, 73728>(p, grid, st);
+    else if (s.BN == 64) wg_launch<64, 3, 46080>(p, grid, st);
     else if (s.BN == 128) wg_launch<128, 2, 46080>(p, grid, st);
     else wg_launch<256, 2, 46080>(p, grid, st);
   } else {

@@ -240,6 +240,11 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
 }
 
 Plan::~Plan() {
+  drop_graphs();
+  for (auto &e : ev_pool) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
   for (auto &kv : up_dev) cudaFree(kv);
   nccl_destroy(dp_comm);
   nccl_destroy(pipe_comm);
@@ -549,7 +554,87 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
 // ---------------------------------------------------------------------------
 // step phases
 // ---------------------------------------------------------------------------
+// CUDA graphs: each phase is captured once (after one eager warm-up run that
+// also sets kernel attributes) and replayed; the pointers inside are fixed
+// because inputs are staged into plan-owned buffers.  Not used on the legacy
+// default stream (not capturable) or while kernel timing is on.
+bool Plan::graphs_on() const {
+  auto it = opts.find("graphs");
+  const bool on = it == opts.end() ? true : it->second != 0;
+  return on && stream != nullptr && stream != cudaStreamLegacy && stream != cudaStreamPerThread && !timing();
+}
+
+void Plan::drop_graphs() {
+  for (int i = 0; i < 3; ++i) {
+    if (gexec[i]) cudaGraphExecDestroy(gexec[i]);
+    gexec[i] = nullptr;
+    warm[i] = false;
+  }
+}
+
+void Plan::run_phase(int ph, const std::function<void()> &body) {
+  if (!graphs_on()) {
+    body();
+    return;
+  }
+  if (!gexec[ph]) {
+    if (!warm[ph]) {
+      body();
+      warm[ph] = true;
+      return;
+    }
+    cudaGraph_t g = nullptr;
+    CUDA_CHECK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    set_capturing(true);
+    try {
+      body();
+    } catch (...) {
+      set_capturing(false);
+      cudaStreamEndCapture(stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    set_capturing(false);
+    CUDA_CHECK(cudaStreamEndCapture(stream, &g));
+    size_t n = 0;
+    CUDA_CHECK(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CUDA_CHECK(cudaGraphGetNodes(g, nodes.data(), &n));
+    int kn = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      cudaGraphNodeGetType(nd, &t);
+      kn += t == cudaGraphNodeTypeKernel;
+    }
+    graph_kernels[ph] = kn;
+    const cudaError_t e = cudaGraphInstantiate(&gexec[ph], g, 0);
+    cudaGraphDestroy(g);
+    CUDA_CHECK(e);
+  }
+  CUDA_CHECK(cudaGraphLaunch(gexec[ph], stream));
+  add_launches(graph_kernels[ph]);
+}
+
 void Plan::forward(const float *x_in, const int32_t *y) {
+  run_phase(0, [&] { forward_body(x_in, y); });
+  fwd_done = true;
+}
+
+void Plan::backward(const float *x_in) {
+  run_phase(1, [&] { backward_body(x_in); });
+}
+
+void Plan::step(float lr) {
+  if (lr != graph_lr) {  // the learning rate is a kernel argument of the captured step
+    if (gexec[2]) cudaGraphExecDestroy(gexec[2]);
+    gexec[2] = nullptr;
+    warm[2] = false;
+    graph_lr = lr;
+  }
+  run_phase(2, [&] { step_body(lr); });
+}
+
+void Plan::forward_body(const float *x_in, const int32_t *y) {
   CUDA_CHECK(cudaMemsetAsync(P(off_loss), 0, sizeof(float), stream));
   const int nu = (int)net.units.size();
   for (int k = 0; k < Mb; ++k) {
@@ -567,10 +652,9 @@ void Plan::forward(const float *x_in, const int32_t *y) {
     }
   }
   if (S > 1) nccl_bcast_f32(pipe_comm, (float *)P(off_loss), 1, unit_stage[nu - 1], stream);
-  fwd_done = true;
 }
 
-void Plan::backward(const float *x_in) {
+void Plan::backward_body(const float *x_in) {
   CUDA_CHECK(cudaMemsetAsync(P(off_grad), 0, sizeof(float) * net.n_params, stream));
   const int nu = (int)net.units.size();
   for (int k = 0; k < Mb; ++k) {
@@ -607,7 +691,7 @@ std::vector<std::pair<int64_t, int64_t>> Plan::local_ranges() const {
   return r;
 }
 
-void Plan::step(float lr) {
+void Plan::step_body(float lr) {
   auto ranges = local_ranges();
   if (replicas > 1)
     for (auto &rg : ranges)
@@ -695,6 +779,7 @@ rn_status Plan::set_option(const std::string &k, int64_t v) {
   if (k != "graphs" && k != "tc_conv" && k != "time_kernels") return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;
+  drop_graphs();
   return RN_OK;
 }
 

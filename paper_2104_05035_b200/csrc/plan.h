@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <string>
 #include <utility>
@@ -126,6 +127,17 @@ struct Plan {
   void forward(const float *x_in, const int32_t *y);
   void backward(const float *x_in);
   void step(float lr);
+  void forward_body(const float *x_in, const int32_t *y);
+  void backward_body(const float *x_in);
+  void step_body(float lr);
+  // CUDA graphs per phase (0 forward, 1 backward, 2 step)
+  cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};
+  bool warm[3] = {false, false, false};
+  int graph_kernels[3] = {0, 0, 0};
+  float graph_lr = -1.f;
+  bool graphs_on() const;
+  void drop_graphs();
+  void run_phase(int ph, const std::function<void()> &body);
   void refresh_shadows();
   std::vector<std::pair<int64_t, int64_t>> local_ranges() const;
 

@@ -160,3 +160,26 @@ def test_per_unit_activations(depth, w, dims, dtype, tol):
         got = plan.get_activation(ui, 0, ref.shape)
         errs.append((ui, u.kind, rel(got, ref)))
     assert max(e[2] for e in errs) <= tol, errs
+
+
+def test_cuda_graph_replay_matches_eager():
+    """The captured forward/backward/step graphs replay exactly the eager step."""
+    dims = (40, 48, 40)
+    outs = []
+    for graphs in (1, 0):
+        st = torch.cuda.Stream()
+        plan = rn.Plan(rn.net_desc(18, 64, dims), 2, rn.RN_BF16, stream=st)
+        plan.set_option("graphs", graphs)
+        arrays = synthetic.init_params(plan.tensors, seed=0)
+        plan.set_params(np.concatenate([a.ravel() for a in arrays]).astype(np.float32))
+        x, y = synthetic.make_batch(2, *dims, seed=1)
+        with torch.cuda.stream(st):
+            xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+            losses = []
+            for _ in range(4):
+                losses.append(plan.forward(xd, yd))
+                plan.backward()
+                plan.step(LR)
+        outs.append((losses, plan.get_params()))
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][1], outs[1][1])
