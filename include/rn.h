@@ -159,6 +159,21 @@ rn_status rn_nccl_unique_id(uint8_t out[128]);
 rn_status rn_plan(const rn_net_desc *net, const rn_dist_desc *dist, int32_t local_batch,
                   int32_t dtype, void *cuda_stream, rn_plan_t *out, size_t *workspace_bytes);
 
+/* rn_plan_describe — the schedule rn_plan builds for this rank, computed on the
+ * host only (no GPU, no communicators): which units run here and, in forward
+ * order, the partition-boundary exchanges of P:156.
+ *  local_units[RN_MAX_UNITS] : 1 if the unit runs on this rank's stage (may be NULL)
+ *  n_xfer, xfer[4 * cap]     : {unit, peer stage, dir, bytes}; dir 0 = receive the
+ *                              input of `unit` (activation a^t of partition i-1),
+ *                              dir 1 = send the output of `unit`; backward does the
+ *                              mirror transfers (gradients) in reverse order
+ *  n_ranges, ranges[2 * cap] : canonical parameter ranges [begin, end) this rank
+ *                              all-reduces over its stage's data-parallel group
+ * Errors: RN_ERR_ARG, RN_ERR_SCHEMA, RN_ERR_SIZE (cap too small). */
+rn_status rn_plan_describe(const rn_net_desc *net, const rn_dist_desc *dist, int32_t local_batch, int32_t dtype,
+                           int32_t *local_units, int32_t cap, int32_t *n_xfer, int64_t *xfer, int32_t *n_ranges,
+                           int64_t *ranges);
+
 /* rn_plan_bind — give the plan its device workspace (>= *workspace_bytes,
  * 256-byte aligned, caller-owned, e.g. a torch uint8 tensor).  Must precede
  * every compute call.  Errors: RN_ERR_SIZE, RN_ERR_ARG. */

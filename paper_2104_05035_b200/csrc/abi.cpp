@@ -165,6 +165,32 @@ rn_status rn_plan(const rn_net_desc *net, const rn_dist_desc *dist, int32_t loca
   GUARD_END
 }
 
+rn_status rn_plan_describe(const rn_net_desc *net, const rn_dist_desc *dist, int32_t local_batch, int32_t dtype,
+                           int32_t *local_units, int32_t cap, int32_t *n_xfer, int64_t *xfer, int32_t *n_ranges,
+                           int64_t *ranges) {
+  GUARD_BEGIN
+  if (!net || !dist || !n_xfer || !n_ranges || cap < 0) return set_error(RN_ERR_ARG, "rn_plan_describe: null argument");
+  NetModel m = build_net(*net);
+  Schedule sc = make_schedule(m, *dist, local_batch, dtype == RN_BF16 ? DT_BF16 : DT_F32);
+  if ((int)sc.xfers.size() > cap || (int)sc.ranges.size() > cap) return set_error(RN_ERR_SIZE, "cap too small");
+  if (local_units)
+    for (size_t u = 0; u < m.units.size(); ++u) local_units[u] = sc.local[u];
+  *n_xfer = (int32_t)sc.xfers.size();
+  for (size_t i = 0; i < sc.xfers.size() && xfer; ++i) {
+    xfer[4 * i] = sc.xfers[i].unit;
+    xfer[4 * i + 1] = sc.xfers[i].peer_stage;
+    xfer[4 * i + 2] = sc.xfers[i].dir;
+    xfer[4 * i + 3] = sc.xfers[i].bytes;
+  }
+  *n_ranges = (int32_t)sc.ranges.size();
+  for (size_t i = 0; i < sc.ranges.size() && ranges; ++i) {
+    ranges[2 * i] = sc.ranges[i].first;
+    ranges[2 * i + 1] = sc.ranges[i].second;
+  }
+  return RN_OK;
+  GUARD_END
+}
+
 rn_status rn_plan_bind(rn_plan_t plan, void *dev, size_t bytes) {
   GUARD_BEGIN
   if (!plan || !dev) return set_error(RN_ERR_ARG, "rn_plan_bind: null argument");

@@ -576,8 +576,9 @@ __global__ void check_finite_k(const float *v, int n, int *flag) {
 }  // namespace
 
 int chan_reduce_blocks(int64_t V, int C) {
-  int64_t b = (V + 127) / 128;
-  if (b > 4 * 148) b = 4 * 148;
+  // ~2048 elements per block at least; at most one full wave (3 resident blocks/SM)
+  int64_t b = (V * C + 2047) / 2048;
+  if (b > 3 * 148) b = 3 * 148;
   if (b < 1) b = 1;
   return (int)b;
 }

@@ -113,21 +113,13 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
   replicas = world / S;
   stage = rank % S;
   replica = rank / S;
-  const int nparts = (int)net.part_loads.size();
-  genes.assign(nparts, 0);
-  if (S > 1) {
-    if (!dd.genes) throw Error(RN_ERR_ARG, "genes required when n_stages > 1");
-    for (int i = 0; i < nparts; ++i) {
-      genes[i] = dd.genes[i];
-      if (genes[i] < 0 || genes[i] >= S) throw Error(RN_ERR_ARG, "gene out of range");
-    }
+  {
+    Schedule sc = make_schedule(net, dd, local_batch, dt);
+    genes = sc.genes;
+    unit_stage = sc.unit_stage;
+    local = sc.local;
   }
   const int nu = (int)net.units.size();
-  unit_stage.assign(nu, 0);
-  for (int p = 0; p < nparts; ++p)
-    for (int u = net.part_first[p]; u < net.part_first[p + 1]; ++u) unit_stage[u] = genes[p];
-  local.assign(nu, 0);
-  for (int u = 0; u < nu; ++u) local[u] = unit_stage[u] == stage;
 
   // --- parameters (full model on every rank; only local ranges are used) ---
   const int np = (int)net.params.size();
@@ -673,8 +665,57 @@ void Plan::backward_body(const float *x_in) {
   }
 }
 
+// The rank's schedule (host logic only; shared by Plan and rn_plan_describe).
+// Partition p runs on stage genes[p]; unit u inherits its partition's stage.
+// Exchanges in forward order: a unit whose predecessor is on another stage
+// receives its input from there ("the partition output is sent to
+// partition (i+1)"); a unit whose successor is elsewhere sends its output.
+// Backward performs the mirror transfers in reverse order.
+Schedule make_schedule(const NetModel &net, const rn_dist_desc &dd, int local_batch, DType dt) {
+  Schedule sc;
+  const int S = dd.n_stages;
+  if (dd.world < 1 || dd.rank < 0 || dd.rank >= dd.world) throw Error(RN_ERR_ARG, "bad rank/world");
+  if (S < 1 || dd.world % S != 0) throw Error(RN_ERR_ARG, "world must be a multiple of n_stages");
+  if (dd.micro_batches < 1 || local_batch < 1 || local_batch % dd.micro_batches != 0)
+    throw Error(RN_ERR_ARG, "local_batch must be a positive multiple of micro_batches");
+  sc.stage = dd.rank % S;
+  sc.replica = dd.rank / S;
+  sc.replicas = dd.world / S;
+  sc.mb = local_batch / dd.micro_batches;
+  const int nparts = (int)net.part_loads.size();
+  sc.genes.assign(nparts, 0);
+  if (S > 1) {
+    if (!dd.genes) throw Error(RN_ERR_ARG, "genes required when n_stages > 1");
+    for (int i = 0; i < nparts; ++i) {
+      sc.genes[i] = dd.genes[i];
+      if (sc.genes[i] < 0 || sc.genes[i] >= S) throw Error(RN_ERR_ARG, "gene out of range");
+    }
+  }
+  const int nu = (int)net.units.size();
+  sc.unit_stage.assign(nu, 0);
+  for (int p = 0; p < nparts; ++p)
+    for (int u = net.part_first[p]; u < net.part_first[p + 1]; ++u) sc.unit_stage[u] = sc.genes[p];
+  sc.local.assign(nu, 0);
+  for (int u = 0; u < nu; ++u) sc.local[u] = sc.unit_stage[u] == sc.stage;
+  for (int u = 0; u < nu; ++u) {
+    if (!sc.local[u]) continue;
+    if (u > 0 && !sc.local[u - 1]) {
+      const Unit &pu = net.units[u - 1];
+      sc.xfers.push_back({u, sc.unit_stage[u - 1], 0, (int64_t)sc.mb * pu.out.vol() * pu.cout * (int64_t)dt_size(dt)});
+    }
+    if (u + 1 < nu && !sc.local[u + 1]) {
+      const Unit &cu = net.units[u];
+      sc.xfers.push_back({u, sc.unit_stage[u + 1], 1, (int64_t)sc.mb * cu.out.vol() * cu.cout * (int64_t)dt_size(dt)});
+    }
+  }
+  sc.ranges = local_param_ranges(net, sc.local);
+  return sc;
+}
+
+std::vector<std::pair<int64_t, int64_t>> Plan::local_ranges() const { return local_param_ranges(net, local); }
+
 // contiguous parameter ranges (in the flat buffer) of the local units
-std::vector<std::pair<int64_t, int64_t>> Plan::local_ranges() const {
+std::vector<std::pair<int64_t, int64_t>> local_param_ranges(const NetModel &net, const std::vector<char> &local) {
   std::vector<std::pair<int64_t, int64_t>> r;
   const int nu = (int)net.units.size();
   for (int ui = 0; ui < nu; ++ui) {

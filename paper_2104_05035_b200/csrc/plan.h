@@ -64,6 +64,20 @@ struct UnitL {
   std::vector<size_t> g, dz;
 };
 
+struct Schedule {
+  std::vector<int> genes, unit_stage;
+  std::vector<char> local;
+  int stage = 0, replica = 0, replicas = 1, mb = 1;
+  struct Xfer {
+    int unit, peer_stage, dir;  // dir 0: receive the input of `unit`; 1: send the output of `unit`
+    int64_t bytes;
+  };
+  std::vector<Xfer> xfers;                        // forward order
+  std::vector<std::pair<int64_t, int64_t>> ranges;  // parameter ranges all-reduced over the DP group
+};
+Schedule make_schedule(const NetModel &net, const rn_dist_desc &dd, int local_batch, DType dt);
+std::vector<std::pair<int64_t, int64_t>> local_param_ranges(const NetModel &net, const std::vector<char> &local);
+
 struct Plan {
   NetModel net;
   DType dt;

@@ -16,7 +16,7 @@ RN_F32, RN_BF16 = 0, 1
 STATUS = {0: "RN_OK", 1: "RN_ERR_ARG", 2: "RN_ERR_SCHEMA", 3: "RN_ERR_INFEASIBLE", 4: "RN_ERR_NUMERIC",
           5: "RN_ERR_CUDA", 6: "RN_ERR_NCCL", 7: "RN_ERR_STATE", 8: "RN_ERR_SIZE"}
 EXPORTS = ["rn_ga_default", "rn_gabra_place", "rn_net_units", "rn_net_param_count", "rn_net_param_info",
-           "rn_nccl_unique_id", "rn_plan", "rn_plan_bind", "rn_set_params", "rn_get_params", "rn_get_grads",
+           "rn_nccl_unique_id", "rn_plan", "rn_plan_describe", "rn_plan_bind", "rn_set_params", "rn_get_params", "rn_get_grads",
            "rn_get_bn_running", "rn_get_activation", "rn_forward", "rn_backward", "rn_step", "rn_train_step_host",
            "rn_kernel_launches", "rn_set_option", "rn_query", "rn_op_conv3d", "rn_plan_destroy", "rn_last_error"]
 
@@ -233,3 +233,24 @@ def op_conv3d(dtype, op, geom, a, b, out, impl=0, stream=None):
     s = stream if stream is not None else torch.cuda.current_stream()
     _check(lib().rn_op_conv3d(dtype, op, g, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
                               C.c_void_p(out.data_ptr()), impl, C.c_void_p(s.cuda_stream)))
+
+
+def plan_describe(desc: NetDesc, local_batch, dtype=RN_F32, rank=0, world=1, n_stages=1, genes=None,
+                  micro_batches=1):
+    """rn_plan_describe: (local unit mask, [(unit, peer_stage, dir, bytes)], [(begin, end)])."""
+    dd = DistDesc()
+    dd.rank, dd.world, dd.n_stages, dd.micro_batches = rank, world, n_stages, micro_batches
+    keep = None
+    if genes is not None:
+        keep = (C.c_int32 * len(genes))(*genes)
+        dd.genes = C.cast(keep, C.POINTER(C.c_int32))
+    cap = 256
+    lu = (C.c_int32 * 64)()
+    nx, nr = C.c_int32(), C.c_int32()
+    xf = (C.c_int64 * (4 * cap))()
+    rg = (C.c_int64 * (2 * cap))()
+    _check(lib().rn_plan_describe(C.byref(desc), C.byref(dd), local_batch, dtype, lu, cap, C.byref(nx), xf,
+                                  C.byref(nr), rg))
+    nu = len(net_units(desc)[0])
+    xfers = [tuple(xf[4 * i:4 * i + 4]) for i in range(nx.value)]
+    return [bool(v) for v in lu[:nu]], xfers, [tuple(rg[2 * i:2 * i + 2]) for i in range(nr.value)]
