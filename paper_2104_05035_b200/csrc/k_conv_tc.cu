@@ -385,7 +385,7 @@ __global__ void splitk_finish_k(const float *__restrict__ part, int ks, int64_t 
 
 int choose_ksplit(int64_t n_tiles, int nk) {
   if (n_tiles >= 100) return 1;
-  int ks = (int)((2 * 148) / std::max<int64_t>(n_tiles, 1));
+  int ks = (int)((148 + n_tiles - 1) / std::max<int64_t>(n_tiles, 1));
   ks = std::min(ks, nk / 4);
   return std::max(ks, 1);
 }
@@ -412,10 +412,17 @@ void run(TcParams &p, int BN, float *ws, size_t ws_floats, cudaStream_t st) {
   }
 }
 
-int pick_bn(int nout) {
-  if (nout % 256 == 0) return 256;
-  if (nout % 128 == 0) return 128;
-  return 64;
+// Largest N tile dividing nout, halved while the launch has fewer tiles than
+// SMs (small late-stage layers trade MMA width for parallelism before split-K).
+int pick_bn(int nout, int OW, int OH, int OD, int ON) {
+  int bw, bh, bd, bn;
+  choose_box(OW, OH, OD, ON, bw, bh, bd, bn);
+  const int64_t mt = (int64_t)((OW + bw - 1) / bw) * ((OH + bh - 1) / bh) * ((OD + bd - 1) / bd) * ((ON + bn - 1) / bn);
+  int BN = nout % 256 == 0 ? 256 : nout % 128 == 0 ? 128 : 64;
+  // halving BN for small layers measured slower overall (more A re-reads): only
+  // when even split-K cannot fill the machine (fewer than 16 tiles)
+  while (BN > 64 && mt * (nout / BN) < 16) BN /= 2;
+  return BN;
 }
 
 void fill_tiles(TcParams &p, int OW, int OH, int OD, int ON, int nout, int BN) {
@@ -451,7 +458,7 @@ void conv_fprop_tc(const ConvGeom &g, const bf16 *x, const bf16 *w, const float 
                    size_t ws_floats, cudaStream_t st) {
   TcParams p;
   memset(&p, 0, sizeof p);
-  const int BN = pick_bn(g.Co);
+  const int BN = pick_bn(g.Co, g.Wo, g.Ho, g.Do, g.N);
   fill_tiles(p, g.Wo, g.Ho, g.Do, g.N, g.Co, BN);
   const int taps = g.taps();
   p.n_taps = taps;
@@ -500,7 +507,8 @@ void conv_fprop_tc(const ConvGeom &g, const bf16 *x, const bf16 *w, const float 
 void conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, bool accumulate, const bf16 *res,
                    const bf16 *res_mask, float *ws, size_t ws_floats, cudaStream_t st) {
   const int taps = g.taps();
-  const int BN = pick_bn(g.Ci);
+  const int BN = g.s == 1 ? pick_bn(g.Ci, g.Wi, g.Hi, g.Di, g.N)
+                          : pick_bn(g.Ci, (g.Wi + 1) / 2, (g.Hi + 1) / 2, (g.Di + 1) / 2, g.N);
   if (g.s == 1) {
     TcParams p;
     memset(&p, 0, sizeof p);

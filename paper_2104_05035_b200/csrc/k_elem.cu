@@ -725,6 +725,58 @@ void repack_conv(DType dt, const float *w, int Co, int taps, int Ci, void *wf, v
   LAUNCH_CHECK();
 }
 
+__global__ void __launch_bounds__(256) sgd_repack_all_k(const ConvPack *__restrict__ tab, int n, float *master,
+                                                        const float *__restrict__ grad, float lr) {
+  __shared__ float tile[32][33];
+  __shared__ int ti;
+  const int64_t b = blockIdx.x;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {  // tensor of this tile: binary search on tile0
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) / 2;
+      if (tab[mid].tile0 <= b) lo = mid;
+      else hi = mid - 1;
+    }
+    ti = lo;
+  }
+  __syncthreads();
+  const ConvPack t = tab[ti];
+  int64_t r = b - t.tile0;
+  const int nci = (t.Ci + 31) / 32, nco = (t.Co + 31) / 32;
+  const int cit = (int)(r % nci); r /= nci;
+  const int cot = (int)(r % nco); r /= nco;
+  const int tap = (int)r;
+  const int ci0 = cit * 32, co0 = cot * 32, tx = threadIdx.x, ty = threadIdx.y;
+  float *w = master + t.off;
+  const float *g = grad ? grad + t.off : nullptr;
+  bf16 *wf = (bf16 *)t.wf, *wd = (bf16 *)t.wd;
+  for (int rr = ty; rr < 32; rr += 8) {
+    const int co = co0 + rr, ci = ci0 + tx;
+    float v = 0.f;
+    if (co < t.Co && ci < t.Ci) {
+      const int64_t i = ((int64_t)co * t.taps + tap) * t.Ci + ci;
+      v = w[i];
+      if (g) {
+        v -= lr * g[i];
+        w[i] = v;
+      }
+      wf[i] = __float2bfloat16_rn(v);
+    }
+    tile[rr][tx] = v;
+  }
+  __syncthreads();
+  for (int rr = ty; rr < 32; rr += 8) {
+    const int ci = ci0 + rr, co = co0 + tx;
+    if (co < t.Co && ci < t.Ci)
+      wd[((int64_t)ci * t.taps + (t.taps - 1 - tap)) * t.Co + co] = __float2bfloat16_rn(tile[tx][rr]);
+  }
+}
+
+__global__ void sgd_ranges_k(const int64_t *__restrict__ rg, float *master, const float *__restrict__ grad, float lr) {
+  const int64_t a = rg[2 * blockIdx.x], e = rg[2 * blockIdx.x + 1];
+  for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) master[i] -= lr * grad[i];
+}
+
 template <typename T>
 __global__ void flip_k(const T *__restrict__ w, int Co, int taps, int Ci, T *__restrict__ wd) {
   const int64_t n = (int64_t)Co * taps * Ci;
@@ -734,6 +786,19 @@ __global__ void flip_k(const T *__restrict__ w, int Co, int taps, int Ci, T *__r
     const int co = (int)(i / ((int64_t)Ci * taps));
     wd[((int64_t)ci * taps + (taps - 1 - tap)) * Co + co] = w[i];
   }
+}
+
+void sgd_repack_all(const ConvPack *table_dev, int n, int64_t total_tiles, float *master, const float *grad, float lr,
+                    cudaStream_t st) {
+  if (n <= 0 || total_tiles <= 0) return;
+  sgd_repack_all_k<<<(unsigned)total_tiles, dim3(32, 8), 0, st>>>(table_dev, n, master, grad, lr);
+  LAUNCH_CHECK();
+}
+
+void sgd_ranges(const int64_t *ranges_dev, int n, float *master, const float *grad, float lr, cudaStream_t st) {
+  if (n <= 0) return;
+  sgd_ranges_k<<<n, 256, 0, st>>>(ranges_dev, master, grad, lr);
+  LAUNCH_CHECK();
 }
 
 void flip_weights(DType dt, const void *w, int Co, int taps, int Ci, void *wd, cudaStream_t st) {

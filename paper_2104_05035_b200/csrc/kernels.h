@@ -100,6 +100,18 @@ void head_bwd(DType dt, const float *dz, const float *g, const float *W, int N, 
 void sgd_update(float *w, const float *g, int64_t n, float lr, cudaStream_t st);
 // wf[co][tap][ci] = w, wd[ci][taps-1-tap][co] = w  (either may be null)
 void repack_conv(DType dt, const float *w, int Co, int taps, int Ci, void *wf, void *wd, cudaStream_t st);
+// One launch for every conv tensor of the plan: w -= lr * g (g may be null: repack only),
+// then the bf16 forward copy wf and the flipped transposed dgrad copy wd (32x32 tiles per tap).
+struct ConvPack {
+  int64_t off;    // offset of the tensor in the master / gradient arrays
+  int64_t tile0;  // first tile index of this tensor in the launch
+  int Co, taps, Ci, pad;
+  void *wf, *wd;
+};
+void sgd_repack_all(const ConvPack *table_dev, int n, int64_t total_tiles, float *master, const float *grad, float lr,
+                    cudaStream_t st);
+// SGD over a device list of (offset, count) ranges, one block per range
+void sgd_ranges(const int64_t *ranges_dev, int n, float *master, const float *grad, float lr, cudaStream_t st);
 void check_finite(const float *v, int n, int *flag, cudaStream_t st);
 // wd[ci][taps-1-tap][co] = w[co][tap][ci] (element type dt)
 void flip_weights(DType dt, const void *w, int Co, int taps, int Ci, void *wd, cudaStream_t st);

@@ -148,6 +148,15 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
   }
   off_loss = alloc(64);
   off_flag = alloc(64);
+  max_pack = 0;
+  max_sgdrg = 0;
+  for (int i = 0; i < np; ++i) {
+    if (!local[net.params[i].unit]) continue;
+    if (net.params[i].kind == P_CONV) ++max_pack;
+    ++max_sgdrg;
+  }
+  off_pack = alloc(sizeof(ConvPack) * (max_pack + 1));
+  off_sgdrg = alloc(2 * sizeof(int64_t) * (max_sgdrg + 1));
   off_x = alloc(sizeof(float) * (size_t)b * net.units[0].in.vol());
   off_y = alloc(sizeof(int32_t) * (size_t)b);
 
@@ -732,31 +741,61 @@ std::vector<std::pair<int64_t, int64_t>> local_param_ranges(const NetModel &net,
   return r;
 }
 
+// SGD: ranges of the non-conv tensors in one launch; every conv tensor
+// (bf16 path) updated and repacked into its two bf16 copies in one more launch.
 void Plan::step_body(float lr) {
   auto ranges = local_ranges();
   if (replicas > 1)
     for (auto &rg : ranges)
       nccl_allreduce_sum_f32(dp_comm, (float *)P(off_grad) + rg.first, (size_t)(rg.second - rg.first), stream);
-  for (auto &rg : ranges)
-    sgd_update((float *)P(off_master) + rg.first, (const float *)P(off_grad) + rg.first, rg.second - rg.first, lr,
-               stream);
-  refresh_shadows();
+  sgd_ranges((const int64_t *)P(off_sgdrg), n_sgdrg, (float *)P(off_master), (const float *)P(off_grad), lr, stream);
+  if (dt == DT_BF16)
+    sgd_repack_all((const ConvPack *)P(off_pack), n_pack, pack_tiles, (float *)P(off_master),
+                   (const float *)P(off_grad), lr, stream);
 }
 
 void Plan::refresh_shadows() {
   if (dt != DT_BF16) return;
-  for (int i = 0; i < (int)net.params.size(); ++i) {
-    const ParamTensor &t = net.params[i];
-    if (t.kind != P_CONV || !local[t.unit]) continue;
-    const int taps = (int)(t.shape[2] * t.shape[3] * t.shape[4]);
-    repack_conv(dt, master(i), (int)t.shape[0], taps, (int)t.shape[1], P(shadow_f[i]), P(shadow_d[i]), stream);
-  }
+  sgd_repack_all((const ConvPack *)P(off_pack), n_pack, pack_tiles, (float *)P(off_master), nullptr, 0.f, stream);
 }
 
 void Plan::bind(void *dev, size_t bytes) {
   if (bytes < ws_bytes) throw Error(RN_ERR_SIZE, "workspace smaller than required");
   if (((uintptr_t)dev & 255) != 0) throw Error(RN_ERR_ARG, "workspace must be 256-byte aligned");
   base = (char *)dev;
+  // optimizer tables: conv tensors (bf16 copies) and plain SGD ranges, local units only
+  std::vector<ConvPack> packs;
+  std::vector<int64_t> rg;
+  int64_t tiles = 0;
+  for (int i = 0; i < (int)net.params.size(); ++i) {
+    const ParamTensor &t = net.params[i];
+    if (!local[t.unit]) continue;
+    if (t.kind == P_CONV && dt == DT_BF16) {
+      ConvPack c;
+      c.off = t.canon_off;
+      c.tile0 = tiles;
+      c.Co = (int)t.shape[0];
+      c.Ci = (int)t.shape[1];
+      c.taps = (int)(t.shape[2] * t.shape[3] * t.shape[4]);
+      c.pad = 0;
+      c.wf = P(shadow_f[i]);
+      c.wd = P(shadow_d[i]);
+      tiles += (int64_t)c.taps * ((c.Co + 31) / 32) * ((c.Ci + 31) / 32);
+      packs.push_back(c);
+    } else {
+      if (!rg.empty() && rg.back() == t.canon_off) rg.back() = t.canon_off + t.numel;
+      else {
+        rg.push_back(t.canon_off);
+        rg.push_back(t.canon_off + t.numel);
+      }
+    }
+  }
+  n_pack = (int)packs.size();
+  pack_tiles = tiles;
+  n_sgdrg = (int)rg.size() / 2;
+  if (n_pack > max_pack || n_sgdrg > max_sgdrg) throw Error(RN_ERR_STATE, "optimizer table overflow");
+  if (n_pack) CUDA_CHECK(cudaMemcpy(P(off_pack), packs.data(), sizeof(ConvPack) * n_pack, cudaMemcpyHostToDevice));
+  if (n_sgdrg) CUDA_CHECK(cudaMemcpy(P(off_sgdrg), rg.data(), sizeof(int64_t) * rg.size(), cudaMemcpyHostToDevice));
 }
 
 // canonical conv W[Co][Ci][kd][kh][kw] <-> internal [Co][tap][Ci]

@@ -90,6 +90,9 @@ struct Plan {
   size_t off_master = 0, off_grad = 0, off_run_mean = 0, off_run_var = 0, off_loss = 0, off_flag = 0;
   size_t off_partial = 0, off_coef = 0, off_wgrad_ws = 0, off_x = 0, off_y = 0;
   size_t wgrad_ws_floats = 0, conv_ws_floats = 0, off_conv_ws = 0;
+  size_t off_pack = 0, off_sgdrg = 0;
+  int n_pack = 0, n_sgdrg = 0, max_pack = 0, max_sgdrg = 0;
+  int64_t pack_tiles = 0;
   int nblk_max = 0;
   size_t ws_bytes = 0;
   char *base = nullptr;
