@@ -10,13 +10,18 @@
 // Layout: NDHWC, every thread owns one 16-byte channel vector (Vec<T>::N
 // channels) of one voxel; per-channel reductions write per-block partials that
 // a finalize kernel sums in a fixed order (deterministic, no float atomics).
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
+
+#include <algorithm>
 
 #include "error.h"
 #include "kernels.h"
 #include "util.cuh"
 
 namespace rn {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -33,9 +38,19 @@ inline unsigned grid_for(int64_t items, int per_block = NT, int64_t cap = 148 * 
 // generic per-channel block reduction: each block reduces rows [r0, r0 + rpb)
 // ---------------------------------------------------------------------------
 template <typename T, typename Op>
+__device__ __forceinline__ void chan_reduce_block(Op &op, int64_t V, int C, float *__restrict__ partial, int64_t rpb,
+                                                  float *sm);
+
+template <typename T, typename Op>
 __global__ void __launch_bounds__(NT) chan_reduce_k(Op op, int64_t V, int C, float *__restrict__ partial,
                                                     int64_t rpb) {
   extern __shared__ float sm[];
+  chan_reduce_block<T>(op, V, C, partial, rpb, sm);
+}
+
+template <typename T, typename Op>
+__device__ __forceinline__ void chan_reduce_block(Op &op, int64_t V, int C, float *__restrict__ partial, int64_t rpb,
+                                                  float *sm) {
   constexpr int VEC = Vec<T>::N;
   const int G = C / VEC;
   const int RPI = NT / G;
@@ -182,11 +197,10 @@ __device__ __forceinline__ void warp_partial_sums(const float *partial, int nblk
 }
 
 template <typename T>
-__global__ void bn_finalize_k(const T *x, const float *partial, int nblk, int64_t V, int C, const float *gamma,
-                              const float *beta, float *mean, float *invstd, float *scale, float *shift,
-                              float *run_mean, float *run_var, float momentum, float eps) {
-  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  if (c >= C) return;
+__device__ __forceinline__ void bn_finalize_channel(int c, const T *x, const float *partial, int nblk, int64_t V,
+                                                    int C, const float *gamma, const float *beta, float *mean,
+                                                    float *invstd, float *scale, float *shift, float *run_mean,
+                                                    float *run_var, float momentum, float eps) {
   double S, Q;
   warp_partial_sums(partial, nblk, C, c, S, Q);
   if ((threadIdx.x & 31) != 0) return;
@@ -208,11 +222,19 @@ __global__ void bn_finalize_k(const T *x, const float *partial, int nblk, int64_
   }
 }
 
-__global__ void bn_bwd_finalize_k(const float *partial, int nblk, int64_t V, int C, const float *gamma,
-                                  const float *mean, const float *invstd, float *dgamma, float *dbeta,
-                                  float *coef) {
+template <typename T>
+__global__ void bn_finalize_k(const T *x, const float *partial, int nblk, int64_t V, int C, const float *gamma,
+                              const float *beta, float *mean, float *invstd, float *scale, float *shift,
+                              float *run_mean, float *run_var, float momentum, float eps) {
   const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (c >= C) return;
+  bn_finalize_channel<T>(c, x, partial, nblk, V, C, gamma, beta, mean, invstd, scale, shift, run_mean, run_var,
+                         momentum, eps);
+}
+
+__device__ __forceinline__ void bn_bwd_finalize_channel(int c, const float *partial, int nblk, int64_t V, int C,
+                                                        const float *gamma, const float *mean, const float *invstd,
+                                                        float *dgamma, float *dbeta, float *coef) {
   double S1, S2;
   warp_partial_sums(partial, nblk, C, c, S1, S2);
   if ((threadIdx.x & 31) != 0) return;
@@ -224,6 +246,167 @@ __global__ void bn_bwd_finalize_k(const float *partial, int nblk, int64_t V, int
   coef[c] = (float)A;
   coef[C + c] = (float)(-A * is * m2);
   coef[2 * C + c] = (float)(-A * m1 + A * is * (double)mean[c] * m2);
+}
+
+__global__ void bn_bwd_finalize_k(const float *partial, int nblk, int64_t V, int C, const float *gamma,
+                                  const float *mean, const float *invstd, float *dgamma, float *dbeta,
+                                  float *coef) {
+  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (c >= C) return;
+  bn_bwd_finalize_channel(c, partial, nblk, V, C, gamma, mean, invstd, dgamma, dbeta, coef);
+}
+
+// ---------------------------------------------------------------------------
+// Fused BatchNorm passes (one cooperative launch per BN layer):
+//   forward : per-block channel sums -> grid sync -> finalize (warp per channel)
+//             -> grid sync -> y = act(x*scale + shift + R) on the block's rows
+//   backward: per-block (sum dy', sum dy'*xhat) -> grid sync -> finalize
+//             (dgamma, dbeta, coefficients) -> grid sync -> dx on the block's rows
+// The apply pass re-reads rows this block just reduced (L2-resident), and the
+// three launches of the unfused version become one.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct BnFwdArgs {
+  const T *x;
+  int64_t V, rpb;
+  int C;
+  float *partial;
+  const float *gamma, *beta;
+  float *mean, *invstd, *scale, *shift, *run_mean, *run_var;
+  float momentum, eps;
+  const T *res;
+  const float *rscale, *rshift;
+  int relu;
+  T *y;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(NT) bn_fwd_fused_k(BnFwdArgs<T> a) {
+  extern __shared__ float sm[];
+  cg::grid_group grid = cg::this_grid();
+  StatsOp<T> op{a.x, a.C, {}};
+  chan_reduce_block<T>(op, a.V, a.C, a.partial, a.rpb, sm);
+  grid.sync();
+  const int warps = blockDim.x / 32;
+  for (int c = blockIdx.x * warps + threadIdx.x / 32; c < a.C; c += gridDim.x * warps)
+    bn_finalize_channel<T>(c, a.x, a.partial, gridDim.x, a.V, a.C, a.gamma, a.beta, a.mean, a.invstd, a.scale,
+                           a.shift, a.run_mean, a.run_var, a.momentum, a.eps);
+  if (!a.y) return;
+  grid.sync();
+  constexpr int VEC = Vec<T>::N;
+  const int G = a.C / VEC;
+  const int c0 = (threadIdx.x % G) * VEC;  // fixed per thread (blockDim % G == 0)
+  float sc[VEC], sh[VEC], rs[VEC], rh[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    sc[j] = __ldcg(a.scale + c0 + j);
+    sh[j] = __ldcg(a.shift + c0 + j);
+    rs[j] = a.rscale ? __ldcg(a.rscale + c0 + j) : 1.f;
+    rh[j] = a.rscale ? __ldcg(a.rshift + c0 + j) : 0.f;
+  }
+  const int64_t r0 = (int64_t)blockIdx.x * a.rpb, r1 = min(a.V, r0 + a.rpb);
+  for (int64_t i = r0 * G + threadIdx.x; i < r1 * G; i += blockDim.x) {
+    const int64_t off = (i / G) * a.C + c0;
+    float v[VEC];
+    load_vec(a.x + off, v);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) v[j] = fmaf(v[j], sc[j], sh[j]);
+    if (a.res) {
+      float r[VEC];
+      load_vec(a.res + off, r);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[j] += fmaf(r[j], rs[j], rh[j]);
+    }
+    if (a.relu) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[j] = fmaxf(v[j], 0.f);
+    }
+    store_vec(a.y + off, v);
+  }
+}
+
+template <typename T>
+struct BnBwdArgs {
+  const T *dy, *x, *mask_t;
+  int64_t V, rpb;
+  int C, mode;
+  float *partial;
+  const float *scale, *shift, *mean, *invstd, *gamma;
+  float *dgamma, *dbeta, *coef;
+  T *dx;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(NT) bn_bwd_fused_k(BnBwdArgs<T> a) {
+  extern __shared__ float sm[];
+  cg::grid_group grid = cg::this_grid();
+  BwdOp<T> op{a.dy, a.x, a.mask_t, a.mode, a.C, a.scale, a.shift, a.mean, a.invstd};
+  chan_reduce_block<T>(op, a.V, a.C, a.partial, a.rpb, sm);
+  grid.sync();
+  const int warps = blockDim.x / 32;
+  for (int c = blockIdx.x * warps + threadIdx.x / 32; c < a.C; c += gridDim.x * warps)
+    bn_bwd_finalize_channel(c, a.partial, gridDim.x, a.V, a.C, a.gamma, a.mean, a.invstd, a.dgamma, a.dbeta, a.coef);
+  grid.sync();
+  constexpr int VEC = Vec<T>::N;
+  const int G = a.C / VEC;
+  const int c0 = (threadIdx.x % G) * VEC;
+  float A[VEC], B[VEC], Cc[VEC], sc[VEC], sh[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    A[j] = __ldcg(a.coef + c0 + j);
+    B[j] = __ldcg(a.coef + a.C + c0 + j);
+    Cc[j] = __ldcg(a.coef + 2 * a.C + c0 + j);
+    sc[j] = a.scale[c0 + j];
+    sh[j] = a.shift[c0 + j];
+  }
+  const int64_t r0 = (int64_t)blockIdx.x * a.rpb, r1 = min(a.V, r0 + a.rpb);
+  for (int64_t i = r0 * G + threadIdx.x; i < r1 * G; i += blockDim.x) {
+    const int64_t off = (i / G) * a.C + c0;
+    float d[VEC], xv[VEC], o[VEC];
+    load_vec(a.dy + off, d);
+    load_vec(a.x + off, xv);
+    if (a.mode == MASK_TENSOR) {
+      float m[VEC];
+      load_vec(a.mask_t + off, m);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) d[j] = m[j] > 0.f ? d[j] : 0.f;
+    } else if (a.mode == MASK_RECOMPUTE) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) d[j] = fmaf(xv[j], sc[j], sh[j]) > 0.f ? d[j] : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) o[j] = fmaf(A[j], d[j], fmaf(B[j], xv[j], Cc[j]));
+    store_vec(a.dx + off, o);
+  }
+}
+
+template <typename K>
+int coop_grid(K kernel, size_t smem, int64_t V, int C) {
+  static int max_blocks = 0;
+  if (!max_blocks) {
+    int per_sm = 0, dev = 0, sms = 148;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, NT, smem));
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    max_blocks = std::max(1, std::min(per_sm, 3)) * sms;
+  }
+  const int want = chan_reduce_blocks(V, C);
+  return std::max(1, std::min(want, max_blocks));
+}
+
+template <typename K, typename A>
+void coop_launch(K kernel, int grid, size_t smem, const A &args, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, args));
 }
 
 __global__ void chan_sum_finalize_k(const float *partial, int nblk, int C, float *out) {
@@ -637,6 +820,38 @@ void bn_bwd_finalize(const float *partial, int nblk, int64_t V, int C, const flo
                      const float *invstd, float *dgamma, float *dbeta, float *coef, cudaStream_t st) {
   bn_bwd_finalize_k<<<(C + 7) / 8, 256, 0, st>>>(partial, nblk, V, C, gamma, mean, invstd, dgamma, dbeta, coef);
   LAUNCH_CHECK();
+}
+
+void bn_forward_fused(DType dt, const void *x, int64_t V, int C, float *partial, const float *gamma,
+                      const float *beta, float *mean, float *invstd, float *scale, float *shift, float *run_mean,
+                      float *run_var, float momentum, float eps, const void *res, const float *rscale,
+                      const float *rshift, bool relu, void *y, cudaStream_t st) {
+  DISPATCH(dt, {
+    int64_t rpb;
+    size_t smem;
+    const int grid = coop_grid(bn_fwd_fused_k<T>, (size_t)2 * NT * Vec<T>::N * sizeof(float), V, C);
+    launch_chan_reduce_dims<T>(V, C, grid, rpb, smem);
+    BnFwdArgs<T> a{(const T *)x, V, rpb, C, partial, gamma, beta, mean, invstd, scale, shift, run_mean, run_var,
+                   momentum, eps, (const T *)res, rscale, rshift, relu ? 1 : 0, (T *)y};
+    coop_launch(bn_fwd_fused_k<T>, grid, smem, a, st);
+  });
+  count_launch();
+}
+
+void bn_backward_fused(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,
+                       const float *scale, const float *shift, const float *mean, const float *invstd,
+                       const float *gamma, float *partial, float *dgamma, float *dbeta, float *coef, void *dx,
+                       cudaStream_t st) {
+  DISPATCH(dt, {
+    int64_t rpb;
+    size_t smem;
+    const int grid = coop_grid(bn_bwd_fused_k<T>, (size_t)2 * NT * Vec<T>::N * sizeof(float), V, C);
+    launch_chan_reduce_dims<T>(V, C, grid, rpb, smem);
+    BnBwdArgs<T> a{(const T *)dy, (const T *)x, (const T *)mask_t, V, rpb, C, mask_mode, partial, scale, shift,
+                   mean, invstd, gamma, dgamma, dbeta, coef, (T *)dx};
+    coop_launch(bn_bwd_fused_k<T>, grid, smem, a, st);
+  });
+  count_launch();
 }
 
 void bn_bwd_apply(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,

@@ -64,6 +64,15 @@ void bn_bwd_finalize(const float *partial, int nblk, int64_t V, int C, const flo
                      const float *invstd, float *dgamma, float *dbeta, float *coef, cudaStream_t st);
 void bn_bwd_apply(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,
                   const float *scale, const float *shift, const float *coef, void *dx, cudaStream_t st);
+// fused cooperative versions (stats + finalize [+ apply] in one launch); y == nullptr: statistics only
+void bn_forward_fused(DType dt, const void *x, int64_t V, int C, float *partial, const float *gamma,
+                      const float *beta, float *mean, float *invstd, float *scale, float *shift, float *run_mean,
+                      float *run_var, float momentum, float eps, const void *res, const float *rscale,
+                      const float *rshift, bool relu, void *y, cudaStream_t st);
+void bn_backward_fused(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,
+                       const float *scale, const float *shift, const float *mean, const float *invstd,
+                       const float *gamma, float *partial, float *dgamma, float *dbeta, float *coef, void *dx,
+                       cudaStream_t st);
 
 // ---------------- pooling / upsampling / attention ----------------
 // y = maxpool3(act(x*scale+shift)) (scale == nullptr: identity, no act); argmax uint8 (0..26)

@@ -377,13 +377,33 @@ void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x
 
 float *Plan::bn_stat(const BNL &b, int k, int which) { return (float *)P(b.stat_off[k]) + which * b.C; }
 
-void Plan::bn_forward_stats(const BNL &b, int k, const void *h) {
-  const int nblk = chan_reduce_blocks(b.V, b.C);
+// Cooperative fused BN (one launch per layer) measured slower than the 3-launch
+// path on B200 (7.3 vs 6.2 ms/step: 444-block grid, serial apply loop), so it
+// is opt-in ("fuse_bn" = 1) until its apply phase is reworked.
+bool Plan::fuse_bn() const {
+  auto it = opts.find("fuse_bn");
+  return it != opts.end() && it->second != 0;
+}
+
+void Plan::bn_forward_stats(const BNL &b, int k, const void *h) { bn_fwd(b, k, h, nullptr, nullptr, nullptr, false, nullptr); }
+
+// Train-mode BN (reading X8): statistics of h, then (if y) y = act(BN(h) + R) where
+// R = res (identity skip) or res*rscale + rshift (the projection's BN).
+void Plan::bn_fwd(const BNL &b, int k, const void *h, const void *res, const float *rscale, const float *rshift,
+                  bool relu, void *y) {
   float *part = (float *)P(off_partial);
+  if (fuse_bn()) {
+    bn_forward_fused(dt, h, b.V, b.C, part, master(b.gamma_idx), master(b.gamma_idx + 1), bn_stat(b, k, 0),
+                     bn_stat(b, k, 1), bn_stat(b, k, 2), bn_stat(b, k, 3), (float *)P(off_run_mean) + b.run_off,
+                     (float *)P(off_run_var) + b.run_off, BN_MOMENTUM, BN_EPS, res, rscale, rshift, relu, y, stream);
+    return;
+  }
+  const int nblk = chan_reduce_blocks(b.V, b.C);
   bn_stats(dt, h, b.V, b.C, part, nblk, stream);
   bn_finalize(dt, h, part, nblk, b.V, b.C, master(b.gamma_idx), master(b.gamma_idx + 1), bn_stat(b, k, 0),
               bn_stat(b, k, 1), bn_stat(b, k, 2), bn_stat(b, k, 3), (float *)P(off_run_mean) + b.run_off,
               (float *)P(off_run_var) + b.run_off, BN_MOMENTUM, BN_EPS, stream);
+  if (y) bn_apply(dt, h, b.V, b.C, bn_stat(b, k, 2), bn_stat(b, k, 3), res, rscale, rshift, relu, y, stream);
 }
 
 // dx = BN-backward of dy' = dy * mask ; coef scratch slot `slot`
@@ -392,6 +412,12 @@ void Plan::bn_backward(const BNL &b, int k, const void *dy, const void *h, int m
   const int nblk = chan_reduce_blocks(b.V, b.C);
   float *part = (float *)P(off_partial);
   float *coef = (float *)P(off_coef) + slot * 3 * 512;
+  if (fuse_bn()) {
+    bn_backward_fused(dt, dy, h, b.V, b.C, mask_mode, mask_t, bn_stat(b, k, 2), bn_stat(b, k, 3), bn_stat(b, k, 0),
+                      bn_stat(b, k, 1), master(b.gamma_idx), part, grad(b.gamma_idx), grad(b.gamma_idx + 1), coef, dx,
+                      stream);
+    return;
+  }
   bn_bwd_reduce(dt, dy, h, b.V, b.C, mask_mode, mask_t, bn_stat(b, k, 2), bn_stat(b, k, 3), bn_stat(b, k, 0),
                 bn_stat(b, k, 1), part, nblk, stream);
   bn_bwd_finalize(part, nblk, b.V, b.C, master(b.gamma_idx), bn_stat(b, k, 0), bn_stat(b, k, 1),
@@ -404,20 +430,14 @@ void Plan::bn_backward(const BNL &b, int k, const void *dy, const void *h, int m
 // ---------------------------------------------------------------------------
 void Plan::block_fwd(BlockL &B, int k, const void *x) {
   conv_fwd(B.c1, x, P(B.h1[k]));
-  bn_forward_stats(B.b1, k, P(B.h1[k]));
-  const int64_t V = B.b1.V;
-  bn_apply(dt, P(B.h1[k]), V, B.cout, bn_stat(B.b1, k, 2), bn_stat(B.b1, k, 3), nullptr, nullptr, nullptr, true,
-           P(B.a1[k]), stream);
+  bn_fwd(B.b1, k, P(B.h1[k]), nullptr, nullptr, nullptr, true, P(B.a1[k]));
   conv_fwd(B.c2, P(B.a1[k]), P(B.h2[k]));
-  bn_forward_stats(B.b2, k, P(B.h2[k]));
   if (B.proj) {
     conv_fwd(B.cp, x, P(B.hp[k]));
     bn_forward_stats(B.bp, k, P(B.hp[k]));
-    bn_apply(dt, P(B.h2[k]), V, B.cout, bn_stat(B.b2, k, 2), bn_stat(B.b2, k, 3), P(B.hp[k]), bn_stat(B.bp, k, 2),
-             bn_stat(B.bp, k, 3), true, P(B.out_[k]), stream);
+    bn_fwd(B.b2, k, P(B.h2[k]), P(B.hp[k]), bn_stat(B.bp, k, 2), bn_stat(B.bp, k, 3), true, P(B.out_[k]));
   } else {
-    bn_apply(dt, P(B.h2[k]), V, B.cout, bn_stat(B.b2, k, 2), bn_stat(B.b2, k, 3), x, nullptr, nullptr, true,
-             P(B.out_[k]), stream);
+    bn_fwd(B.b2, k, P(B.h2[k]), x, nullptr, nullptr, true, P(B.out_[k]));
   }
 }
 
@@ -464,14 +484,13 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
         stem_conv_fprop(dt, L.stem_conv.g, (const float *)x, master(L.stem_conv.w_idx), P(L.stem_h[k]), stream);
       if (t) tk_end(e);
     }
-    bn_forward_stats(L.stem_bn, k, P(L.stem_h[k]));
     if (u.pool) {
+      bn_forward_stats(L.stem_bn, k, P(L.stem_h[k]));
       maxpool_fwd(dt, P(L.stem_h[k]), mb, u.conv.d, u.conv.h, u.conv.w, u.cout, bn_stat(L.stem_bn, k, 2),
                   bn_stat(L.stem_bn, k, 3), true, P(L.out[k]), (uint8_t *)P(L.am[k]), u.out.d, u.out.h, u.out.w,
                   stream);
     } else {
-      bn_apply(dt, P(L.stem_h[k]), L.stem_bn.V, u.cout, bn_stat(L.stem_bn, k, 2), bn_stat(L.stem_bn, k, 3), nullptr,
-               nullptr, nullptr, true, P(L.out[k]), stream);
+      bn_fwd(L.stem_bn, k, P(L.stem_h[k]), nullptr, nullptr, nullptr, true, P(L.out[k]));
     }
   } else if (u.kind == U_BLOCK) {
     block_fwd(L.blk, k, x);
@@ -485,9 +504,7 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
     upsample_fwd(dt, P(L.mask.out_[k]), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.up[k]), u.in.d, u.in.h, u.in.w,
                  L.tab, stream);
     conv_fwd(L.mc1, P(L.up[k]), P(L.mh[k]));
-    bn_forward_stats(L.mbn, k, P(L.mh[k]));
-    bn_apply(dt, P(L.mh[k]), V, C, bn_stat(L.mbn, k, 2), bn_stat(L.mbn, k, 3), nullptr, nullptr, nullptr, true,
-             P(L.r[k]), stream);
+    bn_fwd(L.mbn, k, P(L.mh[k]), nullptr, nullptr, nullptr, true, P(L.r[k]));
     conv_fwd(L.mc2, P(L.r[k]), P(L.m[k]), master(L.bias_idx));
     att_fwd(dt, P(L.m[k]), P(L.trunk.out_[k]), V, C, P(L.out[k]), stream);
   } else {
@@ -856,7 +873,8 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 }
 
 rn_status Plan::set_option(const std::string &k, int64_t v) {
-  if (k != "graphs" && k != "tc_conv" && k != "time_kernels") return set_error(RN_ERR_ARG, "unknown option " + k);
+  if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "fuse_bn")
+    return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;
   drop_graphs();

@@ -129,6 +129,9 @@ struct Plan {
                      const void *res_mask);
   void conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32);
   void bn_forward_stats(const BNL &b, int k, const void *h);
+  void bn_fwd(const BNL &b, int k, const void *h, const void *res, const float *rscale, const float *rshift, bool relu,
+              void *y);
+  bool fuse_bn() const;
   void bn_backward(const BNL &b, int k, const void *dy, const void *h, int mask_mode, const void *mask_t, void *dx,
                    int slot);
   void block_fwd(BlockL &B, int k, const void *x);
