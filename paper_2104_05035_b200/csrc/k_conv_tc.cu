@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -76,7 +77,7 @@ struct Smem {
 };
 
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_constant__ TcParams p) {
+__global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_constant__ TcParams p) {
   using S = Smem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -158,17 +159,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
       for (int kb = kb0; kb < kb1; ++kb) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
-        if (lane == 0) {
+        {
           const uint32_t sa = tc::smem_u32(smem + stage * S::STAGE);
           const uint32_t sb = sa + S::A_BYTES;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint64_t ad = tc::smem_desc(sa + k * 32, 16, 1024, 2);
             const uint64_t bd = tc::smem_desc(sb + k * 32, 16, 1024, 2);
-            tc::mma_bf16(d_tmem, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
+            tc::mma_bf16_warp(d_tmem, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
           }
-          tc::mma_commit(&empty[stage]);
-          if (kb == kb1 - 1) tc::mma_commit(&tfull[acc]);
+          tc::mma_commit_warp(&empty[stage]);
+          if (kb == kb1 - 1) tc::mma_commit_warp(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -289,8 +290,6 @@ void make_act_map(CUtensorMap *m, const void *base, int C, int W, int H, int D, 
   if (r != CUDA_SUCCESS) throw Error(RN_ERR_CUDA, "cuTensorMapEncodeTiled (activation) failed: " + std::to_string(r));
 }
 
-namespace {
-
 void make_w_map(CUtensorMap *m, const void *base, int rows, int64_t ktot, int bn) {
   if (g_dry_need) return;
   load_encode();
@@ -303,6 +302,8 @@ void make_w_map(CUtensorMap *m, const void *base, int rows, int64_t ktot, int bn
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(RN_ERR_CUDA, "cuTensorMapEncodeTiled (weights) failed: " + std::to_string(r));
 }
+
+namespace {
 
 // choose a 128-voxel box (bw, bh, bd, bn) minimising the padded volume
 void choose_box(int W, int H, int D, int N, int &bw, int &bh, int &bd, int &bn) {
@@ -332,7 +333,14 @@ void launch(const TcParams &p, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (int)std::min<int64_t>(p.n_tiles * p.ksplit, sms);
+  // resident CTAs per SM: smem and TMEM (2*BN columns each, 512 per SM) permitting
+  static int per_sm = 0;
+  if (!per_sm) {
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_tc_kernel<BN, STAGES>, TC_THREADS,
+                                                             S::TOTAL));
+    per_sm = std::max(1, std::min(per_sm, 512 / (2 * BN)));
+  }
+  const int grid = (int)std::min<int64_t>(p.n_tiles * p.ksplit, (int64_t)sms * per_sm);
   conv_tc_kernel<BN, STAGES><<<grid, TC_THREADS, S::TOTAL, st>>>(p);
   LAUNCH_CHECK();
 }
@@ -400,9 +408,18 @@ void run(TcParams &p, int BN, float *ws, size_t ws_floats, cudaStream_t st) {
   }
   if (!ws || (size_t)p.ksplit * p.n_view_vox * p.ych > ws_floats) p.ksplit = 1;
   p.part = ws;
-  if (BN == 64) launch<64, 6>(p, st);
-  else if (BN == 128) launch<128, 5>(p, st);
-  else launch<256, 4>(p, st);
+  // two CTAs per SM (each with its own TMA/MMA pipeline) hide the TMA latency the
+  // small N=64/128 MMAs cannot cover alone; N=256 needs all 512 TMEM columns
+  static const bool occ1 = getenv("RN_TC_OCC1") != nullptr;
+  if (BN == 64) {
+    if (occ1) launch<64, 6>(p, st);
+    else launch<64, 4>(p, st);
+  } else if (BN == 128) {
+    if (occ1) launch<128, 5>(p, st);
+    else launch<128, 3>(p, st);
+  } else {
+    launch<256, 4>(p, st);
+  }
   if (p.ksplit > 1) {
     const int64_t n = p.n_view_vox * (p.ych / 8);
     splitk_finish_k<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(

@@ -149,12 +149,12 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
       for (int64_t vt = vt0; vt < vt1; ++vt) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
-        if (lane == 0) {
+        {
           const uint32_t sdy = tc::smem_u32(smem + stage * STAGE);
           const uint32_t sx = sdy + DYB;
           for (int i = 0; i < G; ++i) {
             const int a0 = 2 * (mt0 + i), a1 = a0 + 1;
-#pragma unroll 1
+#pragma unroll
             for (int j = 0; j < 8; ++j) {  // K = 16 voxels = 2 row groups per MMA
               uint64_t ad;
               if (p.haloed) {
@@ -169,16 +169,16 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
                 ad = tc::smem_desc(sx + (2 * i) * 16384 + j * 2048, 16384, 1024, 2);
               }
               const uint64_t bd = tc::smem_desc(sdy + j * 2048, 16384, 1024, 2);
-              tc::mma_bf16(tmem_base + i * BN, ad, bd, IDESC, (first && j == 0) ? 0u : 1u);
+              tc::mma_bf16_warp(tmem_base + i * BN, ad, bd, IDESC, (first && j == 0) ? 0u : 1u);
             }
           }
-          tc::mma_commit(&empty[stage]);
+          tc::mma_commit_warp(&empty[stage]);
         }
         __syncwarp();
         first = false;
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (lane == 0) tc::mma_commit(done);
+      tc::mma_commit_warp(done);
       __syncwarp();
     }
   } else {

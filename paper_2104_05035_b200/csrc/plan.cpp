@@ -335,6 +335,11 @@ size_t Plan::tk_begin(int cls, double flops) {
 
 void Plan::tk_end(size_t i) { CUDA_CHECK(cudaEventRecord(ev_pool[i].b, stream)); }
 
+bool Plan::use_halo() const {
+  auto it = opts.find("halo_conv");
+  return it == opts.end() || it->second != 0;
+}
+
 bool Plan::use_tc(const ConvGeom &g, bool dgrad) const {
   if (dt != DT_BF16) return false;
   auto it = opts.find("tc_conv");
@@ -345,7 +350,10 @@ bool Plan::use_tc(const ConvGeom &g, bool dgrad) const {
 void Plan::conv_fwd(const ConvL &c, const void *x, void *y, const float *bias) {
   const bool t = timing();
   size_t e = t ? tk_begin(0, conv_flops(c.g)) : 0;
-  if (use_tc(c.g, false))
+  if (use_tc(c.g, false) && use_halo() && halo_conv_supported(c.g, false))
+    conv_halo(c.g, false, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, false, nullptr,
+              nullptr, stream);
+  else if (use_tc(c.g, false))
     conv_fprop_tc(c.g, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y,
                   (float *)P(off_conv_ws), conv_ws_floats, stream);
   else
@@ -356,7 +364,10 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
                          const void *res_mask) {
   const bool t = timing();
   size_t e = t ? tk_begin(1, conv_flops(c.g)) : 0;
-  if (use_tc(c.g, true))
+  if (use_tc(c.g, true) && use_halo() && halo_conv_supported(c.g, true))
+    conv_halo(c.g, true, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx, accumulate,
+              (const bf16 *)res, (const bf16 *)res_mask, stream);
+  else if (use_tc(c.g, true))
     conv_dgrad_tc(c.g, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), (bf16 *)dx, accumulate,
                   (const bf16 *)res, (const bf16 *)res_mask, (float *)P(off_conv_ws), conv_ws_floats, stream);
   else
@@ -873,7 +884,7 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 }
 
 rn_status Plan::set_option(const std::string &k, int64_t v) {
-  if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "fuse_bn")
+  if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "fuse_bn" && k != "halo_conv")
     return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;

@@ -19,6 +19,12 @@ void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dy, const __nv_bfloat
                    bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask, float *ws,
                    size_t ws_floats, cudaStream_t st);
 
+// haloed-A kernel for the 64 -> 64 channel stride-1 3x3x3 convs (k_conv_halo.cu)
+bool halo_conv_supported(const ConvGeom &g, bool dgrad);
+void conv_halo(const ConvGeom &g, bool dgrad, const __nv_bfloat16 *src, const __nv_bfloat16 *w, const float *bias,
+               __nv_bfloat16 *out, bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask,
+               cudaStream_t st);
+
 // weight gradient dw[co][tap][ci] += sum dy x (fp32 partials in ws, fixed-order reduce)
 bool tc_wgrad_supported(const ConvGeom &g);
 size_t tc_wgrad_ws_floats(const ConvGeom &g);
