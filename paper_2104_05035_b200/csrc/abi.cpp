@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -30,6 +31,15 @@ void count_launch() {
 void add_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 void set_capturing(bool c) { g_capturing = c; }
 int64_t launch_count() { return g_launches.load(); }
+// Programmatic Dependent Launch for every kernel (launch.h): opt-in (RN_PDL=1);
+// measured 4% slower per step with the trigger at kernel entry
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("RN_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 rn_status set_error(rn_status s, const std::string &msg) {
   g_err = msg;
   return s;

@@ -23,6 +23,7 @@
 #include <cstring>
 
 #include "error.h"
+#include "launch.h"
 #include "kernels.h"
 #include "tc_conv.h"
 #include "tc_ptx.cuh"
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_halo_kernel(const __grid_cons
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_begin();  // prologue above overlaps the predecessor's tail
 
   if (warp == 0) {
     if (lane == 0) {
@@ -260,7 +262,7 @@ void conv_halo(const ConvGeom &g, bool dgrad, const bf16 *src, const bf16 *w, co
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>(p.n_items, sms);
-  conv_halo_kernel<<<grid, THREADS, SMEM, st>>>(p);
+  launch_k(conv_halo_kernel, grid, THREADS, SMEM, st, p);
   LAUNCH_CHECK();
 }
 

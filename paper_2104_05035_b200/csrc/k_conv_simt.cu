@@ -9,6 +9,7 @@
 #include <algorithm>
 
 #include "error.h"
+#include "launch.h"
 #include "kernels.h"
 #include "util.cuh"
 
@@ -25,6 +26,7 @@ __global__ void __launch_bounds__(NT) conv_simt_kernel(ConvGeom g, const T *__re
                                                        const T *__restrict__ w, const float *__restrict__ bias,
                                                        T *__restrict__ out, int accumulate,
                                                        const T *__restrict__ res, const T *__restrict__ res_mask) {
+  pdl_begin();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int t = threadIdx.x;
@@ -140,6 +142,7 @@ template <typename TX, typename TY>
 __global__ void __launch_bounds__(NT) wgrad_simt_kernel(ConvGeom g, const TX *__restrict__ x,
                                                         const TY *__restrict__ dy, float *__restrict__ part,
                                                         int64_t chunks_per_split) {
+  pdl_begin();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int t = threadIdx.x, tx = t % 16, ty = t / 16;
@@ -222,6 +225,7 @@ __global__ void __launch_bounds__(NT) wgrad_simt_kernel(ConvGeom g, const TX *__
 }
 
 __global__ void split_reduce_add(const float *__restrict__ part, int splits, int64_t n, float *__restrict__ out) {
+  pdl_begin();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int z = 0; z < splits; ++z) s += part[(int64_t)z * n + i];
@@ -245,6 +249,7 @@ void wgrad_split(const ConvGeom &g, int &splits, int64_t &chunks_per_split) {
 template <typename T>
 __global__ void stem_kernel(ConvGeom g, const float *__restrict__ x, const float *__restrict__ w,
                             T *__restrict__ y) {
+  pdl_begin();
   extern __shared__ float ws[];  // [27][Co]
   for (int i = threadIdx.x; i < 27 * g.Co; i += blockDim.x) {
     int co = i % g.Co, tap = i / g.Co;
@@ -284,10 +289,10 @@ void conv_fprop_simt(DType dt, const ConvGeom &g, const void *x, const void *w, 
                      cudaStream_t st) {
   dim3 grid((unsigned)((g.out_vox() + BM - 1) / BM), (g.Co + BN - 1) / BN);
   if (dt == DT_F32)
-    conv_simt_kernel<float, 0><<<grid, NT, 0, st>>>(g, (const float *)x, (const float *)w, bias, (float *)y, 0,
+    launch_k(conv_simt_kernel<float, 0>, grid, NT, 0, st, g, (const float *)x, (const float *)w, bias, (float *)y, 0,
                                                      nullptr, nullptr);
   else
-    conv_simt_kernel<bf16, 0><<<grid, NT, 0, st>>>(g, (const bf16 *)x, (const bf16 *)w, bias, (bf16 *)y, 0,
+    launch_k(conv_simt_kernel<bf16, 0>, grid, NT, 0, st, g, (const bf16 *)x, (const bf16 *)w, bias, (bf16 *)y, 0,
                                                     nullptr, nullptr);
   LAUNCH_CHECK();
 }
@@ -296,10 +301,10 @@ void conv_dgrad_simt(DType dt, const ConvGeom &g, const void *dy, const void *w,
                      const void *res, const void *res_mask, cudaStream_t st) {
   dim3 grid((unsigned)((g.in_vox() + BM - 1) / BM), (g.Ci + BN - 1) / BN);
   if (dt == DT_F32)
-    conv_simt_kernel<float, 1><<<grid, NT, 0, st>>>(g, (const float *)dy, (const float *)w, nullptr, (float *)dx,
+    launch_k(conv_simt_kernel<float, 1>, grid, NT, 0, st, g, (const float *)dy, (const float *)w, nullptr, (float *)dx,
                                                      accumulate, (const float *)res, (const float *)res_mask);
   else
-    conv_simt_kernel<bf16, 1><<<grid, NT, 0, st>>>(g, (const bf16 *)dy, (const bf16 *)w, nullptr, (bf16 *)dx,
+    launch_k(conv_simt_kernel<bf16, 1>, grid, NT, 0, st, g, (const bf16 *)dy, (const bf16 *)w, nullptr, (bf16 *)dx,
                                                     accumulate, (const bf16 *)res, (const bf16 *)res_mask);
   LAUNCH_CHECK();
 }
@@ -318,14 +323,14 @@ void conv_wgrad_simt(DType dt, bool x_is_f32, const ConvGeom &g, const void *x, 
   wgrad_split(g, splits, cps);
   dim3 grid((g.Co + BM - 1) / BM, (g.taps() * g.Ci + BN - 1) / BN, splits);
   if (dt == DT_F32)
-    wgrad_simt_kernel<float, float><<<grid, NT, 0, st>>>(g, (const float *)x, (const float *)dy, ws, cps);
+    launch_k(wgrad_simt_kernel<float, float>, grid, NT, 0, st, g, (const float *)x, (const float *)dy, ws, cps);
   else if (x_is_f32)
-    wgrad_simt_kernel<float, bf16><<<grid, NT, 0, st>>>(g, (const float *)x, (const bf16 *)dy, ws, cps);
+    launch_k(wgrad_simt_kernel<float, bf16>, grid, NT, 0, st, g, (const float *)x, (const bf16 *)dy, ws, cps);
   else
-    wgrad_simt_kernel<bf16, bf16><<<grid, NT, 0, st>>>(g, (const bf16 *)x, (const bf16 *)dy, ws, cps);
+    launch_k(wgrad_simt_kernel<bf16, bf16>, grid, NT, 0, st, g, (const bf16 *)x, (const bf16 *)dy, ws, cps);
   LAUNCH_CHECK();
   int64_t n = (int64_t)g.Co * g.taps() * g.Ci;
-  split_reduce_add<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(ws, splits, n, dw);
+  launch_k(split_reduce_add, (unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st, ws, splits, n, dw);
   LAUNCH_CHECK();
 }
 
@@ -334,9 +339,9 @@ void stem_conv_fprop(DType dt, const ConvGeom &g, const float *x, const float *w
   unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
   size_t sm = 27 * g.Co * sizeof(float);
   if (dt == DT_F32)
-    stem_kernel<float><<<blocks, 256, sm, st>>>(g, x, w, (float *)y);
+    launch_k(stem_kernel<float>, blocks, 256, sm, st, g, x, w, (float *)y);
   else
-    stem_kernel<bf16><<<blocks, 256, sm, st>>>(g, x, w, (bf16 *)y);
+    launch_k(stem_kernel<bf16>, blocks, 256, sm, st, g, x, w, (bf16 *)y);
   LAUNCH_CHECK();
 }
 

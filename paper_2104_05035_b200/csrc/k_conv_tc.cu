@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "error.h"
+#include "launch.h"
 #include "kernels.h"
 #include "tc_conv.h"
 #include "tc_ptx.cuh"
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_begin();  // prologue above overlaps the predecessor's tail
 
   const int nk = p.n_taps * p.kblocks_per_tap;
   const int64_t n_items = p.n_tiles * p.ksplit;
@@ -341,7 +343,7 @@ void launch(const TcParams &p, cudaStream_t st) {
     per_sm = std::max(1, std::min(per_sm, 512 / (2 * BN)));
   }
   const int grid = (int)std::min<int64_t>(p.n_tiles * p.ksplit, (int64_t)sms * per_sm);
-  conv_tc_kernel<BN, STAGES><<<grid, TC_THREADS, S::TOTAL, st>>>(p);
+  launch_k(conv_tc_kernel<BN, STAGES>, grid, TC_THREADS, S::TOTAL, st, p);
   LAUNCH_CHECK();
 }
 
@@ -350,6 +352,7 @@ __global__ void splitk_finish_k(const float *__restrict__ part, int ks, int64_t 
                                 bf16 *__restrict__ y, int64_t s_n, int64_t s_d, int64_t s_h, int64_t s_w,
                                 const float *__restrict__ bias, int accumulate, const bf16 *__restrict__ res,
                                 const bf16 *__restrict__ res_mask) {
+  pdl_begin();
   const int G = ych / 8;
   const int64_t n = nvv * G;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -391,9 +394,12 @@ __global__ void splitk_finish_k(const float *__restrict__ part, int ks, int64_t 
   }
 }
 
+// split-K factor for launches with fewer tiles than SMs: as many splits as fit
+// in ONE wave of 148 CTAs (rounding up leaves a few CTAs with two items and
+// doubles the launch time)
 int choose_ksplit(int64_t n_tiles, int nk) {
   if (n_tiles >= 100) return 1;
-  int ks = (int)((148 + n_tiles - 1) / std::max<int64_t>(n_tiles, 1));
+  int ks = (int)(148 / std::max<int64_t>(n_tiles, 1));
   ks = std::min(ks, nk / 4);
   return std::max(ks, 1);
 }
@@ -422,7 +428,7 @@ void run(TcParams &p, int BN, float *ws, size_t ws_floats, cudaStream_t st) {
   }
   if (p.ksplit > 1) {
     const int64_t n = p.n_view_vox * (p.ych / 8);
-    splitk_finish_k<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(
+    launch_k(splitk_finish_k, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st, 
         ws, p.ksplit, p.n_view_vox, p.ych, p.OW, p.OH, p.OD, p.y, p.s_n, p.s_d, p.s_h, p.s_w, p.bias, p.accumulate,
         p.res, p.res_mask);
     LAUNCH_CHECK();

@@ -10,18 +10,16 @@
 // Layout: NDHWC, every thread owns one 16-byte channel vector (Vec<T>::N
 // channels) of one voxel; per-channel reductions write per-block partials that
 // a finalize kernel sums in a fixed order (deterministic, no float atomics).
-#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
 #include <algorithm>
 
 #include "error.h"
+#include "launch.h"
 #include "kernels.h"
 #include "util.cuh"
 
 namespace rn {
-
-namespace cg = cooperative_groups;
 
 namespace {
 
@@ -35,141 +33,233 @@ inline unsigned grid_for(int64_t items, int per_block = NT, int64_t cap = 148 * 
 }
 
 // ---------------------------------------------------------------------------
-// generic per-channel block reduction: each block reduces rows [r0, r0 + rpb)
+// Per-channel reductions over the rows (voxels) of an NDHWC tensor, with the
+// finalize in the same launch.  Block b reduces rows [b*rpb, (b+1)*rpb): each
+// thread owns one 16-byte channel vector and walks rows RPI apart, loading
+// U rows before accumulating (all U loads in flight: memory-level parallelism),
+// then a fixed-order smem tree gives the block's partial [2][C].  The last block
+// to finish (atomic ticket, reset afterwards for the next launch / graph
+// replay) sums all partials in block order — fixed order, so the result is
+// deterministic (reading X24) — and applies `fin` per channel.  The partials
+// are read with plain weak loads after the ticket's __threadfence (which also
+// invalidates L1): strong ld.global.cg loads measured fully serialised on B200
+// (~0.3 us each, 45 us for 148 partials).
 // ---------------------------------------------------------------------------
-template <typename T, typename Op>
-__device__ __forceinline__ void chan_reduce_block(Op &op, int64_t V, int C, float *__restrict__ partial, int64_t rpb,
-                                                  float *sm);
+constexpr int NTR = 512;  // threads of a reduction block
+constexpr int RU = 8;     // rows in flight per thread
 
-template <typename T, typename Op>
-__global__ void __launch_bounds__(NT) chan_reduce_k(Op op, int64_t V, int C, float *__restrict__ partial,
-                                                    int64_t rpb) {
-  extern __shared__ float sm[];
-  chan_reduce_block<T>(op, V, C, partial, rpb, sm);
+// 16-byte read-only load as a volatile asm: the compiler keeps a batch of these
+// ahead of the arithmetic that consumes them (plain __ldg loads were sunk next
+// to their uses, one L2/HBM round trip per row)
+template <typename T>
+__device__ __forceinline__ uint4 ld16(const T *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void unpack16(const uint4 &u, float *v, const float *) {
+  v[0] = __uint_as_float(u.x); v[1] = __uint_as_float(u.y); v[2] = __uint_as_float(u.z); v[3] = __uint_as_float(u.w);
+}
+__device__ __forceinline__ void unpack16(const uint4 &u, float *v, const bf16 *) {
+  const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
 }
 
-template <typename T, typename Op>
-__device__ __forceinline__ void chan_reduce_block(Op &op, int64_t V, int C, float *__restrict__ partial, int64_t rpb,
-                                                  float *sm) {
+template <typename T, typename Op, typename Fin>
+__global__ void __launch_bounds__(NTR) chan_reduce_fin_k(Op op, Fin fin, int64_t V, int C, float *__restrict__ partial,
+                                                         int64_t rpb, unsigned *counter) {
+  extern __shared__ float sm[];
+  pdl_begin();
   constexpr int VEC = Vec<T>::N;
   const int G = C / VEC;
-  const int RPI = NT / G;
-  const int t = threadIdx.x, rr = t / G, cg = t % G;
+  const int RPI = NTR / G;
+  const int t = threadIdx.x, rr = t / G, c0 = (t % G) * VEC;
   float a1[VEC], a2[VEC];
 #pragma unroll
   for (int j = 0; j < VEC; ++j) a1[j] = a2[j] = 0.f;
   if (rr < RPI) {
-    op.init(cg * VEC);
+    op.init(c0);
     const int64_t r0 = (int64_t)blockIdx.x * rpb;
     const int64_t r1 = min(V, r0 + rpb);
     int64_t r = r0 + rr;
-    for (; r + 3 * RPI < r1; r += 4 * RPI) {  // 4 independent rows per iteration (memory-level parallelism)
-      op.row(r, cg * VEC, a1, a2);
-      op.row(r + RPI, cg * VEC, a1, a2);
-      op.row(r + 2 * RPI, cg * VEC, a1, a2);
-      op.row(r + 3 * RPI, cg * VEC, a1, a2);
+    for (; r < r1; r += RU * RPI) {  // the last batch is predicated, not a serial remainder
+      typename Op::Buf b[RU];
+#pragma unroll
+      for (int q = 0; q < RU; ++q)
+        if (r + q * RPI < r1) op.load(r + q * RPI, c0, b[q]);
+#pragma unroll
+      for (int q = 0; q < RU; ++q)
+        if (r + q * RPI < r1) op.acc(b[q], r + q * RPI, c0, a1, a2);
     }
-    for (; r < r1; r += RPI) op.row(r, cg * VEC, a1, a2);
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
-      sm[rr * C + cg * VEC + j] = a1[j];
-      sm[RPI * C + rr * C + cg * VEC + j] = a2[j];
+      sm[rr * C + c0 + j] = a1[j];
+      sm[RPI * C + rr * C + c0 + j] = a2[j];
     }
   }
   __syncthreads();
-  for (int c = t; c < C; c += NT) {
+  for (int c = t; c < C; c += NTR) {
     float s1 = 0.f, s2 = 0.f;
-    for (int r = 0; r < RPI; ++r) {
-      s1 += sm[r * C + c];
-      s2 += sm[RPI * C + r * C + c];
+    for (int q = 0; q < RPI; ++q) {
+      s1 += sm[q * C + c];
+      s2 += sm[RPI * C + q * C + c];
     }
     partial[(int64_t)blockIdx.x * 2 * C + c] = s1;
     partial[(int64_t)blockIdx.x * 2 * C + C + c] = s2;
   }
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  double *dsm = reinterpret_cast<double *>(sm);  // 2 * NTR doubles <= the reduce scratch
+  const int Cb = C < NTR ? C : NTR, P = NTR / Cb;
+  const int s = t / Cb, cc = t % Cb;
+  const int nb = (int)gridDim.x;
+  for (int cb = 0; cb < C; cb += Cb) {
+    const int c = cb + cc;
+    if (s < P && c < C) {
+      // batches of 8 independent loads per operand: one L2 round trip per batch
+      double a = 0.0, b = 0.0;
+      for (int k0 = s; k0 < nb; k0 += 8 * P) {
+        float va[8], vb[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = k0 + j * P;
+          va[j] = k < nb ? partial[(int64_t)k * 2 * C + c] : 0.f;
+          vb[j] = k < nb ? partial[(int64_t)k * 2 * C + C + c] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          a += (double)va[j];
+          b += (double)vb[j];
+        }
+      }
+      dsm[s * Cb + cc] = a;
+      dsm[NTR + s * Cb + cc] = b;
+    }
+    __syncthreads();
+    if (s == 0 && c < C) {
+      double A = 0.0, B = 0.0;
+      for (int q = 0; q < P; ++q) {
+        A += dsm[q * Cb + cc];
+        B += dsm[NTR + q * Cb + cc];
+      }
+      fin(c, A, B);
+    }
+    __syncthreads();
+  }
+  if (t == 0) *counter = 0u;
 }
 
 template <typename T>
-void launch_chan_reduce_dims(int64_t V, int C, int nblk, int64_t &rpb, size_t &smem) {
-  constexpr int VEC = Vec<T>::N;
-  const int G = C / VEC;
-  const int RPI = NT / G;
+void chan_reduce_dims(int64_t V, int C, int nblk, int64_t &rpb, size_t &smem) {
+  const int G = C / Vec<T>::N;
+  const int RPI = NTR / G;
   rpb = (V + nblk - 1) / nblk;
-  smem = (size_t)2 * RPI * C * sizeof(float);
+  smem = std::max((size_t)2 * RPI * C * sizeof(float), (size_t)2 * NTR * sizeof(double));
 }
 
+// forward statistics of x, shifted by K = x[0][c] (cancellation-safe variance)
 template <typename T>
 struct StatsOp {
   const T *x;
   int C;
   float K[Vec<T>::N];
+  struct Buf {
+    uint4 v;
+  };
   __device__ void init(int c0) { load_vec(x + c0, K); }
-  __device__ void row(int64_t r, int c0, float *a1, float *a2) {
+  __device__ void load(int64_t r, int c0, Buf &b) const { b.v = ld16(x + r * C + c0); }
+  __device__ void acc(const Buf &b, int64_t, int, float *a1, float *a2) const {
     float v[Vec<T>::N];
-    load_vec(x + r * C + c0, v);
+    unpack16(b.v, v, x);
 #pragma unroll
     for (int j = 0; j < Vec<T>::N; ++j) {
-      float d = v[j] - K[j];
+      const float d = v[j] - K[j];
       a1[j] += d;
       a2[j] = fmaf(d, d, a2[j]);
     }
   }
 };
 
-template <typename T>
-__device__ __forceinline__ void masked_dy(const T *dy, const T *x, const T *mask_t, int mode, const float *scale,
-                                          const float *shift, int64_t off, int c0, float *d, float *xv) {
-  constexpr int VEC = Vec<T>::N;
-  load_vec(dy + off, d);
-  load_vec(x + off, xv);
-  if (mode == MASK_TENSOR) {
-    float m[VEC];
-    load_vec(mask_t + off, m);
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) d[j] = m[j] > 0.f ? d[j] : 0.f;
-  } else if (mode == MASK_RECOMPUTE) {
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) d[j] = fmaf(xv[j], scale[c0 + j], shift[c0 + j]) > 0.f ? d[j] : 0.f;
-  }
-}
-
+// BN backward sums over dy' = dy * mask: (sum dy', sum dy' * xhat)
 template <typename T>
 struct BwdOp {
   const T *dy, *x, *mask_t;
   int mode, C;
   const float *scale, *shift, *mean, *invstd;
+  struct Buf {
+    uint4 d, x, m;
+  };
   __device__ void init(int) {}
-  __device__ void row(int64_t r, int c0, float *a1, float *a2) {
+  __device__ void load(int64_t r, int c0, Buf &b) const {
+    const int64_t off = r * C + c0;
+    b.d = ld16(dy + off);
+    b.x = ld16(x + off);
+    if (mode == MASK_TENSOR) b.m = ld16(mask_t + off);
+  }
+  __device__ void acc(const Buf &b, int64_t, int c0, float *a1, float *a2) const {
     constexpr int VEC = Vec<T>::N;
     float d[VEC], xv[VEC];
-    masked_dy(dy, x, mask_t, mode, scale, shift, r * C + c0, c0, d, xv);
+    unpack16(b.d, d, dy);
+    unpack16(b.x, xv, x);
+    if (mode == MASK_TENSOR) {
+      float m[VEC];
+      unpack16(b.m, m, x);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) d[j] = m[j] > 0.f ? d[j] : 0.f;
+    } else if (mode == MASK_RECOMPUTE) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) d[j] = fmaf(xv[j], scale[c0 + j], shift[c0 + j]) > 0.f ? d[j] : 0.f;
+    }
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
-      float xh = (xv[j] - mean[c0 + j]) * invstd[c0 + j];
+      const float xh = (xv[j] - mean[c0 + j]) * invstd[c0 + j];
       a1[j] += d[j];
       a2[j] = fmaf(d[j], xh, a2[j]);
     }
   }
 };
 
+// attention backward: dT = dout (1 + s), dm = dout T s (1 - s), s = sigmoid(m); sums dm
 template <typename T>
 struct AttBwdOp {
   const T *dout, *m, *Tt;
   T *dT, *dm;
   int C;
+  struct Buf {
+    uint4 g, m, t;
+  };
   __device__ void init(int) {}
-  __device__ void row(int64_t r, int c0, float *a1, float *a2) {
+  __device__ void load(int64_t r, int c0, Buf &b) const {
+    const int64_t off = r * C + c0;
+    b.g = ld16(dout + off);
+    b.m = ld16(m + off);
+    b.t = ld16(Tt + off);
+  }
+  __device__ void acc(const Buf &b, int64_t r, int c0, float *a1, float *) const {
     constexpr int VEC = Vec<T>::N;
     float g[VEC], mv[VEC], tv[VEC], o1[VEC], o2[VEC];
-    const int64_t off = r * C + c0;
-    load_vec(dout + off, g);
-    load_vec(m + off, mv);
-    load_vec(Tt + off, tv);
+    unpack16(b.g, g, dout);
+    unpack16(b.m, mv, m);
+    unpack16(b.t, tv, Tt);
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
-      float s = 1.f / (1.f + __expf(-mv[j]));
+      const float s = 1.f / (1.f + __expf(-mv[j]));
       o1[j] = g[j] * (1.f + s);
       o2[j] = g[j] * tv[j] * s * (1.f - s);
     }
+    const int64_t off = r * C + c0;
     store_vec(dT + off, o1);
     store_vec(dm + off, o2);
 #pragma unroll
@@ -177,375 +267,308 @@ struct AttBwdOp {
   }
 };
 
-// Sum of per-block partials for channel c: one warp per channel, lanes stride
-// over the blocks in double, fixed shuffle tree (deterministic).
-__device__ __forceinline__ void warp_partial_sums(const float *partial, int nblk, int C, int c, double &S1,
-                                                  double &S2) {
-  const int lane = threadIdx.x & 31;
-  double a = 0.0, b = 0.0;
-  for (int k = lane; k < nblk; k += 32) {
-    a += (double)partial[(int64_t)k * 2 * C + c];
-    b += (double)partial[(int64_t)k * 2 * C + C + c];
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-  }
-  S1 = a;
-  S2 = b;
-}
-
+// forward statistics -> mean / invstd / scale / shift, running-stat momentum update
 template <typename T>
-__device__ __forceinline__ void bn_finalize_channel(int c, const T *x, const float *partial, int nblk, int64_t V,
-                                                    int C, const float *gamma, const float *beta, float *mean,
-                                                    float *invstd, float *scale, float *shift, float *run_mean,
-                                                    float *run_var, float momentum, float eps) {
-  double S, Q;
-  warp_partial_sums(partial, nblk, C, c, S, Q);
-  if ((threadIdx.x & 31) != 0) return;
-  const double K = (double)to_f(x[c]);
-  const double ms = S / (double)V;
-  double var = Q / (double)V - ms * ms;
-  if (var < 0) var = 0;
-  const double mu = K + ms;
-  const double is = 1.0 / sqrt(var + (double)eps);
-  mean[c] = (float)mu;
-  invstd[c] = (float)is;
-  const double sc = (double)gamma[c] * is;
-  scale[c] = (float)sc;
-  shift[c] = (float)((double)beta[c] - mu * sc);
-  if (run_mean) {
-    const double unb = V > 1 ? var * (double)V / (double)(V - 1) : var;
-    run_mean[c] = (float)((1.0 - momentum) * run_mean[c] + momentum * mu);
-    run_var[c] = (float)((1.0 - momentum) * run_var[c] + momentum * unb);
-  }
-}
-
-template <typename T>
-__global__ void bn_finalize_k(const T *x, const float *partial, int nblk, int64_t V, int C, const float *gamma,
-                              const float *beta, float *mean, float *invstd, float *scale, float *shift,
-                              float *run_mean, float *run_var, float momentum, float eps) {
-  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  if (c >= C) return;
-  bn_finalize_channel<T>(c, x, partial, nblk, V, C, gamma, beta, mean, invstd, scale, shift, run_mean, run_var,
-                         momentum, eps);
-}
-
-__device__ __forceinline__ void bn_bwd_finalize_channel(int c, const float *partial, int nblk, int64_t V, int C,
-                                                        const float *gamma, const float *mean, const float *invstd,
-                                                        float *dgamma, float *dbeta, float *coef) {
-  double S1, S2;
-  warp_partial_sums(partial, nblk, C, c, S1, S2);
-  if ((threadIdx.x & 31) != 0) return;
-  dgamma[c] += (float)S2;
-  dbeta[c] += (float)S1;
-  const double m1 = S1 / (double)V, m2 = S2 / (double)V;
-  const double is = invstd[c];
-  const double A = (double)gamma[c] * is;
-  coef[c] = (float)A;
-  coef[C + c] = (float)(-A * is * m2);
-  coef[2 * C + c] = (float)(-A * m1 + A * is * (double)mean[c] * m2);
-}
-
-__global__ void bn_bwd_finalize_k(const float *partial, int nblk, int64_t V, int C, const float *gamma,
-                                  const float *mean, const float *invstd, float *dgamma, float *dbeta,
-                                  float *coef) {
-  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  if (c >= C) return;
-  bn_bwd_finalize_channel(c, partial, nblk, V, C, gamma, mean, invstd, dgamma, dbeta, coef);
-}
-
-// ---------------------------------------------------------------------------
-// Fused BatchNorm passes (one cooperative launch per BN layer):
-//   forward : per-block channel sums -> grid sync -> finalize (warp per channel)
-//             -> grid sync -> y = act(x*scale + shift + R) on the block's rows
-//   backward: per-block (sum dy', sum dy'*xhat) -> grid sync -> finalize
-//             (dgamma, dbeta, coefficients) -> grid sync -> dx on the block's rows
-// The apply pass re-reads rows this block just reduced (L2-resident), and the
-// three launches of the unfused version become one.
-// ---------------------------------------------------------------------------
-template <typename T>
-struct BnFwdArgs {
+struct StatsFin {
   const T *x;
-  int64_t V, rpb;
-  int C;
-  float *partial;
+  int64_t V;
   const float *gamma, *beta;
   float *mean, *invstd, *scale, *shift, *run_mean, *run_var;
   float momentum, eps;
-  const T *res;
-  const float *rscale, *rshift;
-  int relu;
-  T *y;
+  __device__ void operator()(int c, double S, double Q) const {
+    const double K = (double)to_f(x[c]);  // the shift of StatsOp
+    const double ms = S / (double)V;
+    double var = Q / (double)V - ms * ms;
+    if (var < 0) var = 0;
+    const double mu = K + ms;
+    const double is = 1.0 / sqrt(var + (double)eps);
+    mean[c] = (float)mu;
+    invstd[c] = (float)is;
+    const double sc = (double)gamma[c] * is;
+    scale[c] = (float)sc;
+    shift[c] = (float)((double)beta[c] - mu * sc);
+    if (run_mean) {
+      const double unb = V > 1 ? var * (double)V / (double)(V - 1) : var;
+      run_mean[c] = (float)((1.0 - momentum) * run_mean[c] + momentum * mu);
+      run_var[c] = (float)((1.0 - momentum) * run_var[c] + momentum * unb);
+    }
+  }
 };
 
+// backward sums (S1 = sum dy', S2 = sum dy' xhat) -> dgamma, dbeta, dx coefficients
+// dx = A dy' + B x + Cc with A = gamma invstd, B = -A invstd S2/V, Cc = -A S1/V + A invstd mean S2/V
+struct BwdFin {
+  int64_t V;
+  int C;
+  const float *gamma, *mean, *invstd;
+  float *dgamma, *dbeta, *coef;
+  __device__ void operator()(int c, double S1, double S2) const {
+    dgamma[c] += (float)S2;
+    dbeta[c] += (float)S1;
+    const double m1 = S1 / (double)V, m2 = S2 / (double)V;
+    const double is = invstd[c];
+    const double A = (double)gamma[c] * is;
+    coef[c] = (float)A;
+    coef[C + c] = (float)(-A * is * m2);
+    coef[2 * C + c] = (float)(-A * m1 + A * is * (double)mean[c] * m2);
+  }
+};
+
+struct SumFin {
+  float *out;
+  __device__ void operator()(int c, double S1, double) const { out[c] += (float)S1; }
+};
+
+// Elementwise BN passes: each thread owns a fixed 16-byte channel vector
+// (grid stride is a multiple of C/VEC, so its per-channel coefficients stay in
+// registers) and loads EU vectors before computing (memory-level parallelism).
+constexpr int EU = 4;
+
+inline unsigned grid_elem(int64_t vecs) {
+  int64_t b = (vecs + (int64_t)NT * EU - 1) / ((int64_t)NT * EU);
+  if (b > 148 * 8) b = 148 * 8;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+// y = act(x*scale + shift + R), R = 0 | res | res*rscale + rshift
 template <typename T>
-__global__ void __launch_bounds__(NT) bn_fwd_fused_k(BnFwdArgs<T> a) {
-  extern __shared__ float sm[];
-  cg::grid_group grid = cg::this_grid();
-  StatsOp<T> op{a.x, a.C, {}};
-  chan_reduce_block<T>(op, a.V, a.C, a.partial, a.rpb, sm);
-  grid.sync();
-  const int warps = blockDim.x / 32;
-  for (int c = blockIdx.x * warps + threadIdx.x / 32; c < a.C; c += gridDim.x * warps)
-    bn_finalize_channel<T>(c, a.x, a.partial, gridDim.x, a.V, a.C, a.gamma, a.beta, a.mean, a.invstd, a.scale,
-                           a.shift, a.run_mean, a.run_var, a.momentum, a.eps);
-  if (!a.y) return;
-  grid.sync();
+__global__ void __launch_bounds__(NT) bn_apply_k(const T *__restrict__ x, int64_t V, int C,
+                                                 const float *__restrict__ scale, const float *__restrict__ shift,
+                                                 const T *__restrict__ res, const float *__restrict__ rscale,
+                                                 const float *__restrict__ rshift, int relu, T *__restrict__ y) {
+  pdl_begin();
   constexpr int VEC = Vec<T>::N;
-  const int G = a.C / VEC;
-  const int c0 = (threadIdx.x % G) * VEC;  // fixed per thread (blockDim % G == 0)
+  const int G = C / VEC;
+  const int64_t n = V * G;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int c0 = (int)(i0 % G) * VEC;
   float sc[VEC], sh[VEC], rs[VEC], rh[VEC];
 #pragma unroll
   for (int j = 0; j < VEC; ++j) {
-    sc[j] = __ldcg(a.scale + c0 + j);
-    sh[j] = __ldcg(a.shift + c0 + j);
-    rs[j] = a.rscale ? __ldcg(a.rscale + c0 + j) : 1.f;
-    rh[j] = a.rscale ? __ldcg(a.rshift + c0 + j) : 0.f;
+    sc[j] = scale[c0 + j];
+    sh[j] = shift[c0 + j];
+    rs[j] = rscale ? rscale[c0 + j] : 1.f;
+    rh[j] = rscale ? rshift[c0 + j] : 0.f;
   }
-  const int64_t r0 = (int64_t)blockIdx.x * a.rpb, r1 = min(a.V, r0 + a.rpb);
-  for (int64_t i = r0 * G + threadIdx.x; i < r1 * G; i += blockDim.x) {
-    const int64_t off = (i / G) * a.C + c0;
-    float v[VEC];
-    load_vec(a.x + off, v);
+  for (int64_t i = i0; i < n; i += EU * stride) {
+    uint4 xv[EU], rv[EU];
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) v[j] = fmaf(v[j], sc[j], sh[j]);
-    if (a.res) {
-      float r[VEC];
-      load_vec(a.res + off, r);
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) v[j] += fmaf(r[j], rs[j], rh[j]);
+    for (int q = 0; q < EU; ++q) {
+      const int64_t k = i + q * stride;
+      if (k < n) {
+        xv[q] = ld16(x + k * VEC);
+        if (res) rv[q] = ld16(res + k * VEC);
+      }
     }
-    if (a.relu) {
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) v[j] = fmaxf(v[j], 0.f);
+    for (int q = 0; q < EU; ++q) {
+      const int64_t k = i + q * stride;
+      if (k >= n) break;
+      float v[VEC];
+      unpack16(xv[q], v, x);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[j] = fmaf(v[j], sc[j], sh[j]);
+      if (res) {
+        float r[VEC];
+        unpack16(rv[q], r, x);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) v[j] += fmaf(r[j], rs[j], rh[j]);
+      }
+      if (relu) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) v[j] = fmaxf(v[j], 0.f);
+      }
+      store_vec(y + k * VEC, v);
     }
-    store_vec(a.y + off, v);
   }
 }
 
+// dx = A dy' + B x + Cc, dy' = dy * mask (mask tensor > 0, or recomputed ReLU of BN(x))
 template <typename T>
-struct BnBwdArgs {
-  const T *dy, *x, *mask_t;
-  int64_t V, rpb;
-  int C, mode;
-  float *partial;
-  const float *scale, *shift, *mean, *invstd, *gamma;
-  float *dgamma, *dbeta, *coef;
-  T *dx;
-};
-
-template <typename T>
-__global__ void __launch_bounds__(NT) bn_bwd_fused_k(BnBwdArgs<T> a) {
-  extern __shared__ float sm[];
-  cg::grid_group grid = cg::this_grid();
-  BwdOp<T> op{a.dy, a.x, a.mask_t, a.mode, a.C, a.scale, a.shift, a.mean, a.invstd};
-  chan_reduce_block<T>(op, a.V, a.C, a.partial, a.rpb, sm);
-  grid.sync();
-  const int warps = blockDim.x / 32;
-  for (int c = blockIdx.x * warps + threadIdx.x / 32; c < a.C; c += gridDim.x * warps)
-    bn_bwd_finalize_channel(c, a.partial, gridDim.x, a.V, a.C, a.gamma, a.mean, a.invstd, a.dgamma, a.dbeta, a.coef);
-  grid.sync();
+__global__ void __launch_bounds__(NT) bn_bwd_apply_k(const T *__restrict__ dy, const T *__restrict__ x, int64_t V,
+                                                     int C, int mode, const T *__restrict__ mask_t,
+                                                     const float *__restrict__ scale, const float *__restrict__ shift,
+                                                     const float *__restrict__ coef, T *__restrict__ dx) {
+  pdl_begin();
   constexpr int VEC = Vec<T>::N;
-  const int G = a.C / VEC;
-  const int c0 = (threadIdx.x % G) * VEC;
+  const int G = C / VEC;
+  const int64_t n = V * G;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int c0 = (int)(i0 % G) * VEC;
   float A[VEC], B[VEC], Cc[VEC], sc[VEC], sh[VEC];
 #pragma unroll
   for (int j = 0; j < VEC; ++j) {
-    A[j] = __ldcg(a.coef + c0 + j);
-    B[j] = __ldcg(a.coef + a.C + c0 + j);
-    Cc[j] = __ldcg(a.coef + 2 * a.C + c0 + j);
-    sc[j] = a.scale[c0 + j];
-    sh[j] = a.shift[c0 + j];
+    A[j] = coef[c0 + j];
+    B[j] = coef[C + c0 + j];
+    Cc[j] = coef[2 * C + c0 + j];
+    sc[j] = mode == MASK_RECOMPUTE ? scale[c0 + j] : 0.f;
+    sh[j] = mode == MASK_RECOMPUTE ? shift[c0 + j] : 0.f;
   }
-  const int64_t r0 = (int64_t)blockIdx.x * a.rpb, r1 = min(a.V, r0 + a.rpb);
-  for (int64_t i = r0 * G + threadIdx.x; i < r1 * G; i += blockDim.x) {
-    const int64_t off = (i / G) * a.C + c0;
-    float d[VEC], xv[VEC], o[VEC];
-    load_vec(a.dy + off, d);
-    load_vec(a.x + off, xv);
-    if (a.mode == MASK_TENSOR) {
-      float m[VEC];
-      load_vec(a.mask_t + off, m);
+  for (int64_t i = i0; i < n; i += EU * stride) {
+    uint4 dv[EU], xv[EU], mv[EU];
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) d[j] = m[j] > 0.f ? d[j] : 0.f;
-    } else if (a.mode == MASK_RECOMPUTE) {
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) d[j] = fmaf(xv[j], sc[j], sh[j]) > 0.f ? d[j] : 0.f;
-    }
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) o[j] = fmaf(A[j], d[j], fmaf(B[j], xv[j], Cc[j]));
-    store_vec(a.dx + off, o);
-  }
-}
-
-template <typename K>
-int coop_grid(K kernel, size_t smem, int64_t V, int C) {
-  static int max_blocks = 0;
-  if (!max_blocks) {
-    int per_sm = 0, dev = 0, sms = 148;
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, NT, smem));
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    max_blocks = std::max(1, std::min(per_sm, 3)) * sms;
-  }
-  const int want = chan_reduce_blocks(V, C);
-  return std::max(1, std::min(want, max_blocks));
-}
-
-template <typename K, typename A>
-void coop_launch(K kernel, int grid, size_t smem, const A &args, cudaStream_t st) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, args));
-}
-
-__global__ void chan_sum_finalize_k(const float *partial, int nblk, int C, float *out) {
-  const int c = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  if (c >= C) return;
-  double S1, S2;
-  warp_partial_sums(partial, nblk, C, c, S1, S2);
-  if ((threadIdx.x & 31) == 0) out[c] += (float)S1;
-}
-
-template <typename T>
-__global__ void bn_apply_k(const T *__restrict__ x, int64_t V, int C, const float *__restrict__ scale,
-                           const float *__restrict__ shift, const T *__restrict__ res,
-                           const float *__restrict__ rscale, const float *__restrict__ rshift, int relu,
-                           T *__restrict__ y) {
-  constexpr int VEC = Vec<T>::N;
-  const int G = C / VEC;
-  const int64_t n = V * G;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i % G) * VEC;
-    const int64_t off = (i / G) * C + c0;
-    float v[VEC];
-    load_vec(x + off, v);
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) v[j] = fmaf(v[j], scale[c0 + j], shift[c0 + j]);
-    if (res) {
-      float r[VEC];
-      load_vec(res + off, r);
-      if (rscale) {
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) v[j] += fmaf(r[j], rscale[c0 + j], rshift[c0 + j]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) v[j] += r[j];
+    for (int q = 0; q < EU; ++q) {
+      const int64_t k = i + q * stride;
+      if (k < n) {
+        dv[q] = ld16(dy + k * VEC);
+        xv[q] = ld16(x + k * VEC);
+        if (mode == MASK_TENSOR) mv[q] = ld16(mask_t + k * VEC);
       }
     }
-    if (relu) {
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) v[j] = fmaxf(v[j], 0.f);
+    for (int q = 0; q < EU; ++q) {
+      const int64_t k = i + q * stride;
+      if (k >= n) break;
+      float d[VEC], xf[VEC], o[VEC];
+      unpack16(dv[q], d, dy);
+      unpack16(xv[q], xf, x);
+      if (mode == MASK_TENSOR) {
+        float m[VEC];
+        unpack16(mv[q], m, x);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) d[j] = m[j] > 0.f ? d[j] : 0.f;
+      } else if (mode == MASK_RECOMPUTE) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) d[j] = fmaf(xf[j], sc[j], sh[j]) > 0.f ? d[j] : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) o[j] = fmaf(A[j], d[j], fmaf(B[j], xf[j], Cc[j]));
+      store_vec(dx + k * VEC, o);
     }
-    store_vec(y + off, v);
   }
 }
 
+// max-pool k3 s2 p1, -inf padding; first maximum in (kd,kh,kw) order (reading X10).
+// One thread per (output voxel, 16-byte channel vector); the 9 taps of each kd
+// plane are loaded as one predicated batch before comparing (memory-level
+// parallelism); argmax codes of the vector go out as one 8-/4-byte store.
+template <int VEC>
+struct ArgVec;
+template <>
+struct ArgVec<8> {
+  typedef uint2 type;
+};
+template <>
+struct ArgVec<4> {
+  typedef uint32_t type;
+};
+
 template <typename T>
-__global__ void bn_bwd_apply_k(const T *__restrict__ dy, const T *__restrict__ x, int64_t V, int C, int mode,
-                               const T *__restrict__ mask_t, const float *__restrict__ scale,
-                               const float *__restrict__ shift, const float *__restrict__ coef,
-                               T *__restrict__ dx) {
+__global__ void __launch_bounds__(NT) maxpool_fwd_k(const T *__restrict__ x, int N, int D, int H, int W, int C,
+                                                    const float *__restrict__ scale, const float *__restrict__ shift,
+                                                    int relu, T *__restrict__ y, uint8_t *__restrict__ am, int Do,
+                                                    int Ho, int Wo) {
+  pdl_begin();
   constexpr int VEC = Vec<T>::N;
-  const int G = C / VEC;
-  const int64_t n = V * G;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i % G) * VEC;
-    const int64_t off = (i / G) * C + c0;
-    float d[VEC], xv[VEC], o[VEC];
-    masked_dy(dy, x, mask_t, mode, scale, shift, off, c0, d, xv);
+  typedef typename ArgVec<VEC>::type AT;
+  // one block per output row (n, od, oh); 32-bit index math, G = C/VEC a power of two
+  const int lg = __ffs(C / VEC) - 1;
+  const int oh = (int)(blockIdx.x % (unsigned)Ho), od = (int)((blockIdx.x / (unsigned)Ho) % (unsigned)Do);
+  const int nn = (int)(blockIdx.x / ((unsigned)Ho * Do));
+  const int items = Wo << lg;
+  for (int t = threadIdx.x; t < items; t += blockDim.x) {
+    const int ow = t >> lg, c0 = (t & ((1 << lg) - 1)) * VEC;
+    const int64_t vo = (int64_t)blockIdx.x * Wo + ow;
+    float sc[VEC], sh[VEC];
 #pragma unroll
-    for (int j = 0; j < VEC; ++j)
-      o[j] = fmaf(coef[c0 + j], d[j], fmaf(coef[C + c0 + j], xv[j], coef[2 * C + c0 + j]));
-    store_vec(dx + off, o);
-  }
-}
-
-// max-pool k3 s2 p1, -inf padding; first maximum in (kd,kh,kw) order (reading X10)
-template <typename T>
-__global__ void maxpool_fwd_k(const T *__restrict__ x, int N, int D, int H, int W, int C,
-                              const float *__restrict__ scale, const float *__restrict__ shift, int relu,
-                              T *__restrict__ y, uint8_t *__restrict__ am, int Do, int Ho, int Wo) {
-  constexpr int VEC = Vec<T>::N;
-  const int G = C / VEC;
-  const int64_t n = (int64_t)N * Do * Ho * Wo * G;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i % G) * VEC;
-    int64_t r = i / G;
-    const int64_t vo = r;
-    const int ow = (int)(r % Wo); r /= Wo;
-    const int oh = (int)(r % Ho); r /= Ho;
-    const int od = (int)(r % Do); r /= Do;
-    const int nn = (int)r;
+    for (int j = 0; j < VEC; ++j) {
+      sc[j] = scale ? scale[c0 + j] : 1.f;
+      sh[j] = scale ? shift[c0 + j] : 0.f;
+    }
     float best[VEC];
     uint8_t arg[VEC];
 #pragma unroll
-    for (int j = 0; j < VEC; ++j) { best[j] = -INFINITY; arg[j] = 0; }
-    for (int tap = 0; tap < 27; ++tap) {
-      const int id = 2 * od + tap / 9 - 1, ih = 2 * oh + (tap / 3) % 3 - 1, iw = 2 * ow + tap % 3 - 1;
-      if (id < 0 || id >= D || ih < 0 || ih >= H || iw < 0 || iw >= W) continue;
-      float v[VEC];
-      load_vec(x + ((((int64_t)nn * D + id) * H + ih) * W + iw) * C + c0, v);
-      if (scale) {
+    for (int j = 0; j < VEC; ++j) {
+      best[j] = -INFINITY;
+      arg[j] = 0;
+    }
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) {
-          v[j] = fmaf(v[j], scale[c0 + j], shift[c0 + j]);
-          if (relu) v[j] = fmaxf(v[j], 0.f);
-        }
+    for (int kd = 0; kd < 3; ++kd) {
+      const int id = 2 * od + kd - 1;
+      uint4 v[9];
+      bool ok[9];
+#pragma unroll
+      for (int tp = 0; tp < 9; ++tp) {
+        const int ih = 2 * oh + tp / 3 - 1, iw = 2 * ow + tp % 3 - 1;
+        ok[tp] = id >= 0 && id < D && ih >= 0 && ih < H && iw >= 0 && iw < W;
+        if (ok[tp]) v[tp] = ld16(x + ((int64_t)((nn * D + id) * H + ih) * W + iw) * C + c0);
       }
 #pragma unroll
-      for (int j = 0; j < VEC; ++j)
-        if (v[j] > best[j]) { best[j] = v[j]; arg[j] = (uint8_t)tap; }
+      for (int tp = 0; tp < 9; ++tp) {
+        if (!ok[tp]) continue;
+        float f[VEC];
+        unpack16(v[tp], f, x);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) {
+          float e = fmaf(f[j], sc[j], sh[j]);
+          if (relu) e = fmaxf(e, 0.f);
+          if (e > best[j]) {
+            best[j] = e;
+            arg[j] = (uint8_t)(kd * 9 + tp);
+          }
+        }
+      }
     }
     store_vec(y + vo * C + c0, best);
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) am[vo * C + c0 + j] = arg[j];
+    AT packed;
+    memcpy(&packed, arg, sizeof(AT));
+    *reinterpret_cast<AT *>(am + vo * C + c0) = packed;
   }
 }
 
-// gather-form adjoint: each input voxel sums dy of the (<= 8) windows whose argmax is it
+// gather-form adjoint: each input voxel sums dy of the (<= 8) windows whose
+// argmax is it.  Per dimension the covering windows are o = floor(i/2) and
+// o = floor((i+1)/2) (one window when i is even); all candidates are loaded as
+// one predicated batch.
 template <typename T>
-__global__ void maxpool_bwd_k(const T *__restrict__ dy, const uint8_t *__restrict__ am, int N, int D, int H,
-                              int W, int C, int Do, int Ho, int Wo, T *__restrict__ dx, int accumulate) {
+__global__ void __launch_bounds__(NT) maxpool_bwd_k(const T *__restrict__ dy, const uint8_t *__restrict__ am, int N,
+                                                    int D, int H, int W, int C, int Do, int Ho, int Wo,
+                                                    T *__restrict__ dx, int accumulate) {
+  pdl_begin();
   constexpr int VEC = Vec<T>::N;
-  const int G = C / VEC;
-  const int64_t n = (int64_t)N * D * H * W * G;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i % G) * VEC;
-    int64_t r = i / G;
-    const int64_t vi = r;
-    const int iw = (int)(r % W); r /= W;
-    const int ih = (int)(r % H); r /= H;
-    const int id = (int)(r % D); r /= D;
-    const int nn = (int)r;
+  typedef typename ArgVec<VEC>::type AT;
+  // one block per input row (n, id, ih); 32-bit index math
+  const int lg = __ffs(C / VEC) - 1;
+  const int ih = (int)(blockIdx.x % (unsigned)H), id = (int)((blockIdx.x / (unsigned)H) % (unsigned)D);
+  const int nn = (int)(blockIdx.x / ((unsigned)H * D));
+  const int items = W << lg;
+  for (int t = threadIdx.x; t < items; t += blockDim.x) {
+    const int iw = t >> lg, c0 = (t & ((1 << lg) - 1)) * VEC;
+    const int64_t vi = (int64_t)blockIdx.x * W + iw;
+    uint4 g[8];
+    AT a[8];
+    bool ok[8];
+    int tap[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int od = (id + (q >> 2 & 1)) >> 1, oh = (ih + (q >> 1 & 1)) >> 1, ow = (iw + (q & 1)) >> 1;
+      // the second candidate of a dimension exists only for odd i (else it repeats the first)
+      ok[q] = od < Do && oh < Ho && ow < Wo && (!(q & 4) || (id & 1)) && (!(q & 2) || (ih & 1)) &&
+              (!(q & 1) || (iw & 1));
+      tap[q] = ((id - 2 * od + 1) * 3 + (ih - 2 * oh + 1)) * 3 + (iw - 2 * ow + 1);
+      if (ok[q]) {
+        const int64_t o = ((int64_t)((nn * Do + od) * Ho + oh) * Wo + ow) * C + c0;
+        g[q] = ld16(dy + o);
+        a[q] = *reinterpret_cast<const AT *>(am + o);
+      }
+    }
     float acc[VEC];
 #pragma unroll
     for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
-    // windows o with 2o-1 <= i <= 2o+1  <=>  o in [ceil((i-1)/2), floor((i+1)/2)]
-    const int d_lo = max(0, id / 2), d_hi = min(Do - 1, (id + 1) / 2);
-    const int h_lo = max(0, ih / 2), h_hi = min(Ho - 1, (ih + 1) / 2);
-    const int w_lo = max(0, iw / 2), w_hi = min(Wo - 1, (iw + 1) / 2);
-    for (int od = d_lo; od <= d_hi; ++od)
-      for (int oh = h_lo; oh <= h_hi; ++oh)
-        for (int ow = w_lo; ow <= w_hi; ++ow) {
-          const int tap = ((id - 2 * od + 1) * 3 + (ih - 2 * oh + 1)) * 3 + (iw - 2 * ow + 1);
-          const int64_t o = ((((int64_t)nn * Do + od) * Ho + oh) * Wo + ow) * C + c0;
-          float g[VEC];
-          load_vec(dy + o, g);
 #pragma unroll
-          for (int j = 0; j < VEC; ++j)
-            if (am[o + j] == tap) acc[j] += g[j];
-        }
+    for (int q = 0; q < 8; ++q) {
+      if (!ok[q]) continue;
+      float f[VEC];
+      unpack16(g[q], f, dy);
+      uint8_t code[VEC];
+      memcpy(code, &a[q], sizeof(AT));
+#pragma unroll
+      for (int j = 0; j < VEC; ++j)
+        if (code[j] == tap[q]) acc[j] += f[j];
+    }
     if (accumulate) {
       float p[VEC];
       load_vec(dx + vi * C + c0, p);
@@ -559,6 +582,7 @@ __global__ void maxpool_bwd_k(const T *__restrict__ dy, const uint8_t *__restric
 template <typename T>
 __global__ void upsample_fwd_k(const T *__restrict__ x, int N, int Di, int Hi, int Wi, int C, T *__restrict__ y,
                                int Do, int Ho, int Wo, UpTables t) {
+  pdl_begin();
   constexpr int VEC = Vec<T>::N;
   const int G = C / VEC;
   const int64_t n = (int64_t)N * Do * Ho * Wo * G;
@@ -596,6 +620,7 @@ __global__ void upsample_fwd_k(const T *__restrict__ x, int N, int Di, int Hi, i
 template <typename T>
 __global__ void upsample_bwd_k(const T *__restrict__ dy, int N, int Di, int Hi, int Wi, int C, T *__restrict__ dx,
                                int Do, int Ho, int Wo, UpTables t) {
+  pdl_begin();
   constexpr int VEC = Vec<T>::N;
   const int G = C / VEC;
   const int64_t n = (int64_t)N * Di * Hi * Wi * G;
@@ -632,6 +657,7 @@ __global__ void upsample_bwd_k(const T *__restrict__ dy, int N, int Di, int Hi, 
 
 template <typename T>
 __global__ void att_fwd_k(const T *__restrict__ m, const T *__restrict__ Tt, int64_t V, int C, T *__restrict__ out) {
+  pdl_begin();
   constexpr int VEC = Vec<T>::N;
   const int64_t n = V * (C / VEC);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -648,6 +674,7 @@ __global__ void att_fwd_k(const T *__restrict__ m, const T *__restrict__ Tt, int
 // GAP: g[n][c] = mean_v x[n][v][c]; block per (n, 256-channel chunk)
 template <typename T>
 __global__ void gap_k(const T *__restrict__ x, int V, int C, float *__restrict__ g) {
+  pdl_begin();
   const int nn = blockIdx.x;
   for (int c = blockIdx.y * blockDim.x + threadIdx.x; c < C; c += gridDim.y * blockDim.x) {
     float s = 0.f;
@@ -660,6 +687,7 @@ __global__ void gap_k(const T *__restrict__ x, int V, int C, float *__restrict__
 __global__ void ce_k(const float *__restrict__ g, int N, int C, const float *__restrict__ W,
                      const float *__restrict__ b, const int32_t *__restrict__ y, float dz_scale, float loss_scale,
                      float *__restrict__ dz, float *__restrict__ loss_acc) {
+  pdl_begin();
   __shared__ float z[64][2];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   for (int p = warp; p < N * 2; p += nw) {
@@ -688,6 +716,7 @@ __global__ void ce_k(const float *__restrict__ g, int N, int C, const float *__r
 
 __global__ void head_wgrad_k(const float *__restrict__ dz, const float *__restrict__ g, int N, int C,
                              float *__restrict__ dW, float *__restrict__ db) {
+  pdl_begin();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * C; i += gridDim.x * blockDim.x) {
     const int k = i / C, c = i % C;
     float s = 0.f;
@@ -704,6 +733,7 @@ __global__ void head_wgrad_k(const float *__restrict__ dz, const float *__restri
 template <typename T>
 __global__ void head_dx_k(const float *__restrict__ dz, const float *__restrict__ W, int N, int V, int C,
                           T *__restrict__ dx) {
+  pdl_begin();
   const int64_t n = (int64_t)N * V * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % C);
@@ -714,6 +744,7 @@ __global__ void head_dx_k(const float *__restrict__ dz, const float *__restrict_
 }
 
 __global__ void sgd_k(float *__restrict__ w, const float *__restrict__ g, int64_t n, float lr) {
+  pdl_begin();
   const int64_t n4 = n / 4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 a = reinterpret_cast<float4 *>(w)[i];
@@ -729,6 +760,7 @@ __global__ void sgd_k(float *__restrict__ w, const float *__restrict__ g, int64_
 template <typename T>
 __global__ void repack_k(const float *__restrict__ w, int Co, int taps, int Ci, T *__restrict__ wf,
                          T *__restrict__ wd) {
+  pdl_begin();
   // 32x32 tile of one tap: read/write wf along ci, write wd along co (smem transpose)
   __shared__ float tile[32][33];
   const int ci0 = blockIdx.x * 32, co0 = blockIdx.y * 32, tap = blockIdx.z;
@@ -752,19 +784,12 @@ __global__ void repack_k(const float *__restrict__ w, int Co, int taps, int Ci, 
 }
 
 __global__ void check_finite_k(const float *v, int n, int *flag) {
+  pdl_begin();
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     if (!isfinite(v[i])) *flag = 1;
 }
 
 }  // namespace
-
-int chan_reduce_blocks(int64_t V, int C) {
-  // ~2048 elements per block at least; at most one full wave (3 resident blocks/SM)
-  int64_t b = (V * C + 2047) / 2048;
-  if (b > 3 * 148) b = 3 * 148;
-  if (b < 1) b = 1;
-  return (int)b;
-}
 
 #define DISPATCH(dt, ...)                      \
   do {                                         \
@@ -777,223 +802,199 @@ int chan_reduce_blocks(int64_t V, int C) {
     }                                          \
   } while (0)
 
-void bn_stats(DType dt, const void *x, int64_t V, int C, float *partial, int nblk, cudaStream_t st) {
+int chan_fin_blocks(int64_t V, int C) {
+  // one block per ~4096 elements, at most one per SM: the last block's
+  // finalize reads every partial, so fewer, fuller blocks
+  int64_t b = (V * C + 4095) / 4096;
+  if (b > 148) b = 148;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+void bn_stats_finalize(DType dt, const void *x, int64_t V, int C, float *partial, unsigned *counter,
+                       const float *gamma, const float *beta, float *mean, float *invstd, float *scale, float *shift,
+                       float *run_mean, float *run_var, float momentum, float eps, cudaStream_t st) {
+  const int nblk = chan_fin_blocks(V, C);
   DISPATCH(dt, {
     int64_t rpb;
     size_t smem;
-    launch_chan_reduce_dims<T>(V, C, nblk, rpb, smem);
+    chan_reduce_dims<T>(V, C, nblk, rpb, smem);
     StatsOp<T> op{(const T *)x, C, {}};
-    chan_reduce_k<T, StatsOp<T>><<<nblk, NT, smem, st>>>(op, V, C, partial, rpb);
+    StatsFin<T> fin{(const T *)x, V, gamma, beta, mean, invstd, scale, shift, run_mean, run_var, momentum, eps};
+    launch_k(chan_reduce_fin_k<T, StatsOp<T>, StatsFin<T>>, nblk, NTR, smem, st, op, fin, V, C, partial, rpb, counter);
   });
   LAUNCH_CHECK();
 }
 
-void bn_finalize(DType dt, const void *x, const float *partial, int nblk, int64_t V, int C, const float *gamma,
-                 const float *beta, float *mean, float *invstd, float *scale, float *shift, float *run_mean,
-                 float *run_var, float momentum, float eps, cudaStream_t st) {
-  DISPATCH(dt, bn_finalize_k<T><<<(C + 7) / 8, 256, 0, st>>>((const T *)x, partial, nblk, V, C, gamma, beta, mean,
-                                                             invstd, scale, shift, run_mean, run_var, momentum, eps));
+void bn_bwd_reduce_finalize(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode,
+                            const void *mask_t, const float *scale, const float *shift, const float *mean,
+                            const float *invstd, const float *gamma, float *partial, unsigned *counter, float *dgamma,
+                            float *dbeta, float *coef, cudaStream_t st) {
+  const int nblk = chan_fin_blocks(V, C);
+  DISPATCH(dt, {
+    int64_t rpb;
+    size_t smem;
+    chan_reduce_dims<T>(V, C, nblk, rpb, smem);
+    BwdOp<T> op{(const T *)dy, (const T *)x, (const T *)mask_t, mask_mode, C, scale, shift, mean, invstd};
+    BwdFin fin{V, C, gamma, mean, invstd, dgamma, dbeta, coef};
+    launch_k(chan_reduce_fin_k<T, BwdOp<T>, BwdFin>, nblk, NTR, smem, st, op, fin, V, C, partial, rpb, counter);
+  });
+  LAUNCH_CHECK();
+}
+
+void att_bwd_finalize(DType dt, const void *dout, const void *m, const void *T_, int64_t V, int C, void *dT, void *dm,
+                      float *partial, unsigned *counter, float *dbias, cudaStream_t st) {
+  const int nblk = chan_fin_blocks(V, C);
+  DISPATCH(dt, {
+    int64_t rpb;
+    size_t smem;
+    chan_reduce_dims<T>(V, C, nblk, rpb, smem);
+    AttBwdOp<T> op{(const T *)dout, (const T *)m, (const T *)T_, (T *)dT, (T *)dm, C};
+    SumFin fin{dbias};
+    launch_k(chan_reduce_fin_k<T, AttBwdOp<T>, SumFin>, nblk, NTR, smem, st, op, fin, V, C, partial, rpb, counter);
+  });
   LAUNCH_CHECK();
 }
 
 void bn_apply(DType dt, const void *x, int64_t V, int C, const float *scale, const float *shift, const void *res,
               const float *rscale, const float *rshift, bool relu, void *y, cudaStream_t st) {
-  DISPATCH(dt, bn_apply_k<T><<<grid_for(V * C / Vec<T>::N), NT, 0, st>>>(
+  DISPATCH(dt, launch_k(bn_apply_k<T>, grid_elem(V * C / Vec<T>::N), NT, 0, st, 
                    (const T *)x, V, C, scale, shift, (const T *)res, rscale, rshift, relu ? 1 : 0, (T *)y));
   LAUNCH_CHECK();
 }
 
-void bn_bwd_reduce(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,
-                   const float *scale, const float *shift, const float *mean, const float *invstd, float *partial,
-                   int nblk, cudaStream_t st) {
-  DISPATCH(dt, {
-    int64_t rpb;
-    size_t smem;
-    launch_chan_reduce_dims<T>(V, C, nblk, rpb, smem);
-    BwdOp<T> op{(const T *)dy, (const T *)x, (const T *)mask_t, mask_mode, C, scale, shift, mean, invstd};
-    chan_reduce_k<T, BwdOp<T>><<<nblk, NT, smem, st>>>(op, V, C, partial, rpb);
-  });
-  LAUNCH_CHECK();
-}
-
-void bn_bwd_finalize(const float *partial, int nblk, int64_t V, int C, const float *gamma, const float *mean,
-                     const float *invstd, float *dgamma, float *dbeta, float *coef, cudaStream_t st) {
-  bn_bwd_finalize_k<<<(C + 7) / 8, 256, 0, st>>>(partial, nblk, V, C, gamma, mean, invstd, dgamma, dbeta, coef);
-  LAUNCH_CHECK();
-}
-
-void bn_forward_fused(DType dt, const void *x, int64_t V, int C, float *partial, const float *gamma,
-                      const float *beta, float *mean, float *invstd, float *scale, float *shift, float *run_mean,
-                      float *run_var, float momentum, float eps, const void *res, const float *rscale,
-                      const float *rshift, bool relu, void *y, cudaStream_t st) {
-  DISPATCH(dt, {
-    int64_t rpb;
-    size_t smem;
-    const int grid = coop_grid(bn_fwd_fused_k<T>, (size_t)2 * NT * Vec<T>::N * sizeof(float), V, C);
-    launch_chan_reduce_dims<T>(V, C, grid, rpb, smem);
-    BnFwdArgs<T> a{(const T *)x, V, rpb, C, partial, gamma, beta, mean, invstd, scale, shift, run_mean, run_var,
-                   momentum, eps, (const T *)res, rscale, rshift, relu ? 1 : 0, (T *)y};
-    coop_launch(bn_fwd_fused_k<T>, grid, smem, a, st);
-  });
-  count_launch();
-}
-
-void bn_backward_fused(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,
-                       const float *scale, const float *shift, const float *mean, const float *invstd,
-                       const float *gamma, float *partial, float *dgamma, float *dbeta, float *coef, void *dx,
-                       cudaStream_t st) {
-  DISPATCH(dt, {
-    int64_t rpb;
-    size_t smem;
-    const int grid = coop_grid(bn_bwd_fused_k<T>, (size_t)2 * NT * Vec<T>::N * sizeof(float), V, C);
-    launch_chan_reduce_dims<T>(V, C, grid, rpb, smem);
-    BnBwdArgs<T> a{(const T *)dy, (const T *)x, (const T *)mask_t, V, rpb, C, mask_mode, partial, scale, shift,
-                   mean, invstd, gamma, dgamma, dbeta, coef, (T *)dx};
-    coop_launch(bn_bwd_fused_k<T>, grid, smem, a, st);
-  });
-  count_launch();
-}
-
 void bn_bwd_apply(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,
                   const float *scale, const float *shift, const float *coef, void *dx, cudaStream_t st) {
-  DISPATCH(dt, bn_bwd_apply_k<T><<<grid_for(V * C / Vec<T>::N), NT, 0, st>>>(
+  DISPATCH(dt, launch_k(bn_bwd_apply_k<T>, grid_elem(V * C / Vec<T>::N), NT, 0, st, 
                    (const T *)dy, (const T *)x, V, C, mask_mode, (const T *)mask_t, scale, shift, coef, (T *)dx));
   LAUNCH_CHECK();
 }
 
 void maxpool_fwd(DType dt, const void *x, int N, int D, int H, int W, int C, const float *scale, const float *shift,
                  bool relu, void *y, uint8_t *argmax, int Do, int Ho, int Wo, cudaStream_t st) {
-  DISPATCH(dt, maxpool_fwd_k<T><<<grid_for((int64_t)N * Do * Ho * Wo * C / Vec<T>::N), NT, 0, st>>>(
+  DISPATCH(dt, launch_k(maxpool_fwd_k<T>, (unsigned)(N * Do * Ho), NT, 0, st, 
                    (const T *)x, N, D, H, W, C, scale, shift, relu ? 1 : 0, (T *)y, argmax, Do, Ho, Wo));
   LAUNCH_CHECK();
 }
 
 void maxpool_bwd(DType dt, const void *dy, const uint8_t *argmax, int N, int D, int H, int W, int C, int Do, int Ho,
                  int Wo, void *dx, bool accumulate, cudaStream_t st) {
-  DISPATCH(dt, maxpool_bwd_k<T><<<grid_for((int64_t)N * D * H * W * C / Vec<T>::N), NT, 0, st>>>(
+  DISPATCH(dt, launch_k(maxpool_bwd_k<T>, (unsigned)(N * D * H), NT, 0, st, 
                    (const T *)dy, argmax, N, D, H, W, C, Do, Ho, Wo, (T *)dx, accumulate ? 1 : 0));
   LAUNCH_CHECK();
 }
 
 void upsample_fwd(DType dt, const void *x, int N, int Di, int Hi, int Wi, int C, void *y, int Do, int Ho, int Wo,
                   const UpTables &t, cudaStream_t st) {
-  DISPATCH(dt, upsample_fwd_k<T><<<grid_for((int64_t)N * Do * Ho * Wo * C / Vec<T>::N), NT, 0, st>>>(
+  DISPATCH(dt, launch_k(upsample_fwd_k<T>, grid_for((int64_t)N * Do * Ho * Wo * C / Vec<T>::N), NT, 0, st, 
                    (const T *)x, N, Di, Hi, Wi, C, (T *)y, Do, Ho, Wo, t));
   LAUNCH_CHECK();
 }
 
 void upsample_bwd(DType dt, const void *dy, int N, int Di, int Hi, int Wi, int C, void *dx, int Do, int Ho, int Wo,
                   const UpTables &t, cudaStream_t st) {
-  DISPATCH(dt, upsample_bwd_k<T><<<grid_for((int64_t)N * Di * Hi * Wi * C / Vec<T>::N), NT, 0, st>>>(
+  DISPATCH(dt, launch_k(upsample_bwd_k<T>, grid_for((int64_t)N * Di * Hi * Wi * C / Vec<T>::N), NT, 0, st, 
                    (const T *)dy, N, Di, Hi, Wi, C, (T *)dx, Do, Ho, Wo, t));
   LAUNCH_CHECK();
 }
 
 void att_fwd(DType dt, const void *m, const void *T_, int64_t V, int C, void *out, cudaStream_t st) {
-  DISPATCH(dt, att_fwd_k<T><<<grid_for(V * C / Vec<T>::N), NT, 0, st>>>((const T *)m, (const T *)T_, V, C,
+  DISPATCH(dt, launch_k(att_fwd_k<T>, grid_for(V * C / Vec<T>::N), NT, 0, st, (const T *)m, (const T *)T_, V, C,
                                                                           (T *)out));
-  LAUNCH_CHECK();
-}
-
-void att_bwd(DType dt, const void *dout, const void *m, const void *T_, int64_t V, int C, void *dT, void *dm,
-             float *partial, int nblk, cudaStream_t st) {
-  DISPATCH(dt, {
-    int64_t rpb;
-    size_t smem;
-    launch_chan_reduce_dims<T>(V, C, nblk, rpb, smem);
-    AttBwdOp<T> op{(const T *)dout, (const T *)m, (const T *)T_, (T *)dT, (T *)dm, C};
-    chan_reduce_k<T, AttBwdOp<T>><<<nblk, NT, smem, st>>>(op, V, C, partial, rpb);
-  });
-  LAUNCH_CHECK();
-}
-
-void chan_sum_finalize(const float *partial, int nblk, int C, float *out, cudaStream_t st) {
-  chan_sum_finalize_k<<<(C + 7) / 8, 256, 0, st>>>(partial, nblk, C, out);
   LAUNCH_CHECK();
 }
 
 void head_fwd(DType dt, const void *x, int N, int V, int C, const float *W, const float *b, const int32_t *y,
               float dz_scale, float loss_scale, float *g, float *dz, float *loss_acc, cudaStream_t st) {
   dim3 grid(N, (C + 255) / 256);
-  DISPATCH(dt, gap_k<T><<<grid, 256, 0, st>>>((const T *)x, V, C, g));
+  DISPATCH(dt, launch_k(gap_k<T>, grid, 256, 0, st, (const T *)x, V, C, g));
   LAUNCH_CHECK();
-  ce_k<<<1, 256, 0, st>>>(g, N, C, W, b, y, dz_scale, loss_scale, dz, loss_acc);
+  launch_k(ce_k, 1, 256, 0, st, g, N, C, W, b, y, dz_scale, loss_scale, dz, loss_acc);
   LAUNCH_CHECK();
 }
 
 void head_bwd(DType dt, const float *dz, const float *g, const float *W, int N, int V, int C, float *dW, float *db,
               void *dx, cudaStream_t st) {
-  head_wgrad_k<<<(2 * C + 255) / 256, 256, 0, st>>>(dz, g, N, C, dW, db);
+  launch_k(head_wgrad_k, (2 * C + 255) / 256, 256, 0, st, dz, g, N, C, dW, db);
   LAUNCH_CHECK();
-  DISPATCH(dt, head_dx_k<T><<<grid_for((int64_t)N * V * C), 256, 0, st>>>(dz, W, N, V, C, (T *)dx));
+  DISPATCH(dt, launch_k(head_dx_k<T>, grid_for((int64_t)N * V * C), 256, 0, st, dz, W, N, V, C, (T *)dx));
   LAUNCH_CHECK();
 }
 
 void sgd_update(float *w, const float *g, int64_t n, float lr, cudaStream_t st) {
-  sgd_k<<<grid_for((n + 3) / 4), NT, 0, st>>>(w, g, n, lr);
+  launch_k(sgd_k, grid_for((n + 3) / 4), NT, 0, st, w, g, n, lr);
   LAUNCH_CHECK();
 }
 
 void repack_conv(DType dt, const float *w, int Co, int taps, int Ci, void *wf, void *wd, cudaStream_t st) {
   dim3 grid((Ci + 31) / 32, (Co + 31) / 32, taps);
-  DISPATCH(dt, repack_k<T><<<grid, dim3(32, 8), 0, st>>>(w, Co, taps, Ci, (T *)wf, (T *)wd));
+  DISPATCH(dt, launch_k(repack_k<T>, grid, dim3(32, 8), 0, st, w, Co, taps, Ci, (T *)wf, (T *)wd));
   LAUNCH_CHECK();
 }
 
-__global__ void __launch_bounds__(256) sgd_repack_all_k(const ConvPack *__restrict__ tab, int n, float *master,
-                                                        const float *__restrict__ grad, float lr) {
+__global__ void __launch_bounds__(256) sgd_repack_all_k(const ConvPack *__restrict__ tab, int n, int64_t total_tiles,
+                                                        float *master, const float *__restrict__ grad, float lr) {
+  pdl_begin();
   __shared__ float tile[32][33];
-  __shared__ int ti;
-  const int64_t b = blockIdx.x;
-  if (threadIdx.x == 0 && threadIdx.y == 0) {  // tensor of this tile: binary search on tile0
-    int lo = 0, hi = n - 1;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  // persistent: blocks stride over the 32x32 (co, ci) tiles of every tap of every conv tensor
+  for (int64_t b = blockIdx.x; b < total_tiles; b += gridDim.x) {
+    int lo = 0, hi = n - 1;  // tensor of this tile: binary search on tile0 (uniform across the block)
     while (lo < hi) {
       const int mid = (lo + hi + 1) / 2;
       if (tab[mid].tile0 <= b) lo = mid;
       else hi = mid - 1;
     }
-    ti = lo;
-  }
-  __syncthreads();
-  const ConvPack t = tab[ti];
-  int64_t r = b - t.tile0;
-  const int nci = (t.Ci + 31) / 32, nco = (t.Co + 31) / 32;
-  const int cit = (int)(r % nci); r /= nci;
-  const int cot = (int)(r % nco); r /= nco;
-  const int tap = (int)r;
-  const int ci0 = cit * 32, co0 = cot * 32, tx = threadIdx.x, ty = threadIdx.y;
-  float *w = master + t.off;
-  const float *g = grad ? grad + t.off : nullptr;
-  bf16 *wf = (bf16 *)t.wf, *wd = (bf16 *)t.wd;
-  for (int rr = ty; rr < 32; rr += 8) {
-    const int co = co0 + rr, ci = ci0 + tx;
-    float v = 0.f;
-    if (co < t.Co && ci < t.Ci) {
-      const int64_t i = ((int64_t)co * t.taps + tap) * t.Ci + ci;
-      v = w[i];
-      if (g) {
-        v -= lr * g[i];
-        w[i] = v;
-      }
-      wf[i] = __float2bfloat16_rn(v);
+    const ConvPack t = tab[lo];
+    int64_t r = b - t.tile0;
+    const int nci = (t.Ci + 31) / 32, nco = (t.Co + 31) / 32;
+    const int cit = (int)(r % nci); r /= nci;
+    const int cot = (int)(r % nco); r /= nco;
+    const int tap = (int)r;
+    const int ci0 = cit * 32, co0 = cot * 32;
+    float *w = master + t.off;
+    const float *g = grad ? grad + t.off : nullptr;
+    bf16 *wf = (bf16 *)t.wf, *wd = (bf16 *)t.wd;
+    float v[4], gv[4];
+    int64_t idx[4];
+    bool ok[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // all loads first
+      const int co = co0 + ty + 8 * q, ci = ci0 + tx;
+      ok[q] = co < t.Co && ci < t.Ci;
+      idx[q] = ((int64_t)co * t.taps + tap) * t.Ci + ci;
+      v[q] = ok[q] ? w[idx[q]] : 0.f;
+      gv[q] = ok[q] && g ? g[idx[q]] : 0.f;
     }
-    tile[rr][tx] = v;
-  }
-  __syncthreads();
-  for (int rr = ty; rr < 32; rr += 8) {
-    const int ci = ci0 + rr, co = co0 + tx;
-    if (co < t.Co && ci < t.Ci)
-      wd[((int64_t)ci * t.taps + (t.taps - 1 - tap)) * t.Co + co] = __float2bfloat16_rn(tile[tx][rr]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (g) v[q] -= lr * gv[q];
+      if (ok[q]) {
+        if (g) w[idx[q]] = v[q];
+        wf[idx[q]] = __float2bfloat16_rn(v[q]);
+      }
+      tile[ty + 8 * q][tx] = v[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int ci = ci0 + ty + 8 * q, co = co0 + tx;
+      if (co < t.Co && ci < t.Ci)
+        wd[((int64_t)ci * t.taps + (t.taps - 1 - tap)) * t.Co + co] = __float2bfloat16_rn(tile[tx][ty + 8 * q]);
+    }
+    __syncthreads();
   }
 }
 
 __global__ void sgd_ranges_k(const int64_t *__restrict__ rg, float *master, const float *__restrict__ grad, float lr) {
+  pdl_begin();
   const int64_t a = rg[2 * blockIdx.x], e = rg[2 * blockIdx.x + 1];
   for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) master[i] -= lr * grad[i];
 }
 
 template <typename T>
 __global__ void flip_k(const T *__restrict__ w, int Co, int taps, int Ci, T *__restrict__ wd) {
+  pdl_begin();
   const int64_t n = (int64_t)Co * taps * Ci;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int ci = (int)(i % Ci);
@@ -1006,23 +1007,24 @@ __global__ void flip_k(const T *__restrict__ w, int Co, int taps, int Ci, T *__r
 void sgd_repack_all(const ConvPack *table_dev, int n, int64_t total_tiles, float *master, const float *grad, float lr,
                     cudaStream_t st) {
   if (n <= 0 || total_tiles <= 0) return;
-  sgd_repack_all_k<<<(unsigned)total_tiles, dim3(32, 8), 0, st>>>(table_dev, n, master, grad, lr);
+  const unsigned grid = (unsigned)std::min<int64_t>(total_tiles, 148 * 8);
+  launch_k(sgd_repack_all_k, grid, dim3(32, 8), 0, st, table_dev, n, total_tiles, master, grad, lr);
   LAUNCH_CHECK();
 }
 
 void sgd_ranges(const int64_t *ranges_dev, int n, float *master, const float *grad, float lr, cudaStream_t st) {
   if (n <= 0) return;
-  sgd_ranges_k<<<n, 256, 0, st>>>(ranges_dev, master, grad, lr);
+  launch_k(sgd_ranges_k, n, 256, 0, st, ranges_dev, master, grad, lr);
   LAUNCH_CHECK();
 }
 
 void flip_weights(DType dt, const void *w, int Co, int taps, int Ci, void *wd, cudaStream_t st) {
-  DISPATCH(dt, flip_k<T><<<grid_for((int64_t)Co * taps * Ci), NT, 0, st>>>((const T *)w, Co, taps, Ci, (T *)wd));
+  DISPATCH(dt, launch_k(flip_k<T>, grid_for((int64_t)Co * taps * Ci), NT, 0, st, (const T *)w, Co, taps, Ci, (T *)wd));
   LAUNCH_CHECK();
 }
 
 void check_finite(const float *v, int n, int *flag, cudaStream_t st) {
-  check_finite_k<<<1, 256, 0, st>>>(v, n, flag);
+  launch_k(check_finite_k, 1, 256, 0, st, v, n, flag);
   LAUNCH_CHECK();
 }
 

@@ -17,6 +17,7 @@
 #include <algorithm>
 
 #include "error.h"
+#include "launch.h"
 #include "kernels.h"
 #include "util.cuh"
 
@@ -27,6 +28,7 @@ namespace {
 template <typename T, int CO>
 __global__ void __launch_bounds__(128) stem_fprop_k(ConvGeom g, const float *__restrict__ x,
                                                    const float *__restrict__ w, T *__restrict__ y) {
+  pdl_begin();
   __shared__ __align__(16) float ws[27 * CO];
   for (int i = threadIdx.x; i < 27 * CO; i += blockDim.x) {
     const int co = i % CO, tap = i / CO;
@@ -88,6 +90,7 @@ template <typename T, int CO>
 __global__ void __launch_bounds__(256) stem_wgrad_k(ConvGeom g, const float *__restrict__ x,
                                                    const T *__restrict__ dh, float *__restrict__ part,
                                                    int64_t vox_per_block) {
+  pdl_begin();
   constexpr int G = CO / 8;
   __shared__ __align__(16) float sdh[WV][CO];
   __shared__ float sx[WV][28];
@@ -169,6 +172,7 @@ template <typename T, int CO>
 __global__ void __launch_bounds__(256) stem_wgrad_warp_k(ConvGeom g, const float *__restrict__ x,
                                                         const T *__restrict__ dh, float *__restrict__ part,
                                                         int64_t vox_per_warp) {
+  pdl_begin();
   const int lane = threadIdx.x & 31;
   const int64_t wid = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int64_t total = g.out_vox();
@@ -224,6 +228,7 @@ __global__ void __launch_bounds__(256) stem_wgrad_warp_k(ConvGeom g, const float
 }
 
 __global__ void stem_reduce_k(const float *__restrict__ part, int nblk, int n, float *__restrict__ dw) {
+  pdl_begin();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * n + i];
@@ -235,7 +240,7 @@ template <typename T, int CO>
 void stem_fprop_launch(const ConvGeom &g, const float *x, const float *w, void *y, cudaStream_t st) {
   const int64_t total = g.out_vox();
   const unsigned blocks = (unsigned)std::min<int64_t>((total + 127) / 128, 148 * 16);
-  stem_fprop_k<T, CO><<<blocks, 128, 0, st>>>(g, x, w, (T *)y);
+  launch_k(stem_fprop_k<T, CO>, blocks, 128, 0, st, g, x, w, (T *)y);
 }
 
 int stem_wgrad_blocks(const ConvGeom &g) {
@@ -249,9 +254,9 @@ void stem_wgrad_launch(const ConvGeom &g, const float *x, const void *dh, float 
   // the r18 stem: latency-bound with 16 warps/SM; kept for reference)
   const int nb = stem_wgrad_blocks(g);
   const int64_t vpb = (g.out_vox() + nb - 1) / nb;
-  stem_wgrad_k<T, CO><<<nb, 256, 0, st>>>(g, x, (const T *)dh, ws, vpb);
+  launch_k(stem_wgrad_k<T, CO>, nb, 256, 0, st, g, x, (const T *)dh, ws, vpb);
   LAUNCH_CHECK();
-  stem_reduce_k<<<(CO * 27 + 255) / 256, 256, 0, st>>>(ws, nb, CO * 27, dw);
+  launch_k(stem_reduce_k, (CO * 27 + 255) / 256, 256, 0, st, ws, nb, CO * 27, dw);
 }
 
 }  // namespace

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "error.h"
+#include "launch.h"
 #include "kernels.h"
 #include "tc_conv.h"
 #include "tc_ptx.cuh"
@@ -48,6 +49,7 @@ struct __align__(64) WgParams {
   int n_mgroups;  // CTA groups over M
   int n_cob;      // co blocks of BN
   int splits;
+  int accum;  // splits == 1: part is dW itself and the epilogue accumulates
   // atoms of the whole problem: atom a = (tap, ci block); M-tile i = atoms 2i, 2i+1
   int n_mtiles;
   int8_t atom_map[2 * MAX_ATOMS];  // x map index (per-tap mode)
@@ -107,6 +109,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_begin();  // prologue above overlaps the predecessor's tail
 
   if (warp == 0) {
     if (lane == 0 && G > 0) {
@@ -200,10 +203,17 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
           tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + i * BN + c0, v);
           tc::tmem_wait_ld();
           if (ok) {
+            float *dst = P + ((int64_t)(cob * BN + c0) * p.taps + tap) * p.Ci + ci;
+            const int64_t cs = (int64_t)p.taps * p.Ci;  // stride between co
+            if (p.accum) {  // single split: straight into dW (all 32 loads issued before the stores)
+              float old[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int co = cob * BN + c0 + j;
-              P[((int64_t)co * p.taps + tap) * p.Ci + ci] = __uint_as_float(v[j]);
+              for (int j = 0; j < 32; ++j) old[j] = dst[j * cs];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) dst[j * cs] = old[j] + __uint_as_float(v[j]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) dst[j * cs] = __uint_as_float(v[j]);
             }
           }
         }
@@ -219,11 +229,13 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
 }
 
 __global__ void zero_rows_k(float *part, int64_t n) {
+  pdl_begin();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     part[i] = 0.f;
 }
 
 __global__ void wg_reduce_add(const float *__restrict__ part, int splits, int64_t n, float *__restrict__ out) {
+  pdl_begin();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int z = 0; z < splits; ++z) s += part[(int64_t)z * n + i];
@@ -241,7 +253,7 @@ void wg_launch(const WgParams &p, int grid, cudaStream_t st) {
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     attr = true;
   }
-  wgrad_tc_kernel<BN, STAGES, XBYTES><<<grid, WG_THREADS, SMEM, st>>>(p);
+  launch_k(wgrad_tc_kernel<BN, STAGES, XBYTES>, grid, WG_THREADS, SMEM, st, p);
   LAUNCH_CHECK();
 }
 
@@ -291,8 +303,19 @@ WgShape wg_shape(const ConvGeom &g) {
   s.td = (g.Do + s.bd - 1) / s.bd;
   s.tn = (g.N + s.bn - 1) / s.bn;
   s.n_vtiles = (int64_t)s.tw * s.th * s.td * s.tn;
+  if (!s.haloed && s.n_vtiles <= 24) {
+    // short K (late stages): no split (its fp32 partials would be as large as
+    // dW itself); one M-tile per CTA and narrower N blocks supply the CTAs
+    s.G = 1;
+    while (s.BN > 64 && (int64_t)s.n_mtiles * (g.Co / s.BN) < 100) s.BN /= 2;
+    s.n_mgroups = s.n_mtiles;
+    s.n_cob = g.Co / s.BN;
+    s.splits = 1;
+    s.vt_per_split = (int)s.n_vtiles;
+    return s;
+  }
   const int ctas0 = s.n_mgroups * s.n_cob;
-  int splits = (148 + ctas0 - 1) / ctas0;
+  int splits = std::max(1, 148 / ctas0);  // one wave: every CTA resident (a 2nd partial wave doubles the time)
   splits = (int)std::max<int64_t>(1, std::min<int64_t>(splits, s.n_vtiles));
   s.vt_per_split = (int)((s.n_vtiles + splits - 1) / splits);
   s.splits = (int)((s.n_vtiles + s.vt_per_split - 1) / s.vt_per_split);
@@ -315,7 +338,7 @@ bool tc_wgrad_supported(const ConvGeom &g) {
 size_t tc_wgrad_ws_floats(const ConvGeom &g) {
   if (!tc_wgrad_supported(g)) return 0;
   WgShape s = wg_shape(g);
-  return (size_t)s.splits * g.Co * g.taps() * g.Ci;
+  return s.splits > 1 ? (size_t)s.splits * g.Co * g.taps() * g.Ci : 0;
 }
 
 void conv_wgrad_tc(const ConvGeom &g, const bf16 *x, const bf16 *dy, float *dw, float *ws, cudaStream_t st) {
@@ -332,7 +355,8 @@ void conv_wgrad_tc(const ConvGeom &g, const bf16 *x, const bf16 *dy, float *dw, 
   p.tw = s.tw; p.th = s.th; p.td = s.td; p.tn = s.tn;
   p.n_vtiles = s.n_vtiles;
   p.vt_per_split = s.vt_per_split;
-  p.part = ws;
+  p.accum = s.splits == 1;
+  p.part = p.accum ? dw : ws;
   p.Co = g.Co; p.Ci = g.Ci; p.taps = g.taps();
   // dy map: NDHWC [N][Do][Ho][Wo][Co]
   make_act_map(&p.dy_map, dy, g.Co, g.Wo, g.Ho, g.Do, g.N, 1, g.Wo, (int64_t)g.Wo * g.Ho,
@@ -400,8 +424,9 @@ void conv_wgrad_tc(const ConvGeom &g, const bf16 *x, const bf16 *dy, float *dw, 
     else if (s.BN == 128) wg_launch<128, 2, 2 * 32768>(p, grid, st);  // G <= 2
     else wg_launch<256, 2, 1 * 32768>(p, grid, st);                   // G <= 1
   }
+  if (p.accum) return;
   const int64_t n = (int64_t)g.Co * g.taps() * g.Ci;
-  wg_reduce_add<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(ws, s.splits, n, dw);
+  launch_k(wg_reduce_add, (unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st, ws, s.splits, n, dw);
   LAUNCH_CHECK();
 }
 

@@ -44,36 +44,31 @@ void stem_wgrad_fast(DType dt, const ConvGeom &g, const float *x, const void *dh
                      cudaStream_t st);
 
 // ---------------- BatchNorm (train mode), ReLU, residual ----------------
-int chan_reduce_blocks(int64_t V, int C);
-// partial[blk][2][C] = (sum (x-K), sum (x-K)^2), K[c] = x[0][c]
-void bn_stats(DType dt, const void *x, int64_t V, int C, float *partial, int nblk, cudaStream_t st);
-// mean/invstd/scale/shift per channel; running stats momentum update (unbiased var)
-void bn_finalize(DType dt, const void *x, const float *partial, int nblk, int64_t V, int C, const float *gamma,
-                 const float *beta, float *mean, float *invstd, float *scale, float *shift, float *run_mean,
-                 float *run_var, float momentum, float eps, cudaStream_t st);
 // y = act(x*scale + shift + R), R = 0 | res | res*rscale + rshift ; act = relu if relu
 void bn_apply(DType dt, const void *x, int64_t V, int C, const float *scale, const float *shift, const void *res,
               const float *rscale, const float *rshift, bool relu, void *y, cudaStream_t st);
 enum MaskMode { MASK_NONE = 0, MASK_TENSOR = 1, MASK_RECOMPUTE = 2 };
-// partial[blk][2][C] = (sum dy', sum dy'*xhat), dy' = dy * mask
-void bn_bwd_reduce(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,
-                   const float *scale, const float *shift, const float *mean, const float *invstd, float *partial,
-                   int nblk, cudaStream_t st);
-// dgamma += S2, dbeta += S1; coef[0..C) = A, [C..2C) = B, [2C..3C) = Cc with dx = A dy' + B x + Cc
-void bn_bwd_finalize(const float *partial, int nblk, int64_t V, int C, const float *gamma, const float *mean,
-                     const float *invstd, float *dgamma, float *dbeta, float *coef, cudaStream_t st);
+// dx = A dy' + B x + Cc with the coefficients of bn_bwd_reduce_finalize, dy' = dy * mask
 void bn_bwd_apply(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,
                   const float *scale, const float *shift, const float *coef, void *dx, cudaStream_t st);
-// fused cooperative versions (stats + finalize [+ apply] in one launch); y == nullptr: statistics only
-void bn_forward_fused(DType dt, const void *x, int64_t V, int C, float *partial, const float *gamma,
-                      const float *beta, float *mean, float *invstd, float *scale, float *shift, float *run_mean,
-                      float *run_var, float momentum, float eps, const void *res, const float *rscale,
-                      const float *rshift, bool relu, void *y, cudaStream_t st);
-void bn_backward_fused(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,
-                       const float *scale, const float *shift, const float *mean, const float *invstd,
-                       const float *gamma, float *partial, float *dgamma, float *dbeta, float *coef, void *dx,
-                       cudaStream_t st);
-
+// Reduction + finalize in one launch (last-block finalize, deterministic order);
+// counter: a zero-initialised uint32 in device memory, left at zero afterwards.
+// bn_stats_finalize: statistics of x (shifted by x[0][c]) -> mean / invstd /
+//   scale = gamma*invstd / shift = beta - mean*scale, running stats (momentum,
+//   unbiased variance).
+// bn_bwd_reduce_finalize: S1 = sum dy', S2 = sum dy'*xhat -> dgamma += S2,
+//   dbeta += S1, coef[0..C) = A, [C..2C) = B, [2C..3C) = Cc.
+int chan_fin_blocks(int64_t V, int C);
+void bn_stats_finalize(DType dt, const void *x, int64_t V, int C, float *partial, unsigned *counter,
+                       const float *gamma, const float *beta, float *mean, float *invstd, float *scale, float *shift,
+                       float *run_mean, float *run_var, float momentum, float eps, cudaStream_t st);
+void bn_bwd_reduce_finalize(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode,
+                            const void *mask_t, const float *scale, const float *shift, const float *mean,
+                            const float *invstd, const float *gamma, float *partial, unsigned *counter, float *dgamma,
+                            float *dbeta, float *coef, cudaStream_t st);
+// attention backward + dbias (sum of dm) in one launch
+void att_bwd_finalize(DType dt, const void *dout, const void *m, const void *T_, int64_t V, int C, void *dT, void *dm,
+                      float *partial, unsigned *counter, float *dbias, cudaStream_t st);
 // ---------------- pooling / upsampling / attention ----------------
 // y = maxpool3(act(x*scale+shift)) (scale == nullptr: identity, no act); argmax uint8 (0..26)
 void maxpool_fwd(DType dt, const void *x, int N, int D, int H, int W, int C, const float *scale, const float *shift,
@@ -94,10 +89,7 @@ void upsample_bwd(DType dt, const void *dy, int N, int Di, int Hi, int Wi, int C
 // out = (1 + sigmoid(m)) * T
 void att_fwd(DType dt, const void *m, const void *T, int64_t V, int C, void *out, cudaStream_t st);
 // dT = dout*(1+s), dm = dout*T*s*(1-s); partial[blk][2][C] = (sum dm, 0)
-void att_bwd(DType dt, const void *dout, const void *m, const void *T, int64_t V, int C, void *dT, void *dm,
-             float *partial, int nblk, cudaStream_t st);
 // out[c] += sum_blk partial[blk][0][c]
-void chan_sum_finalize(const float *partial, int nblk, int C, float *out, cudaStream_t st);
 
 // ---------------- head: GAP + FC + softmax cross-entropy ----------------
 void head_fwd(DType dt, const void *x, int N, int V, int C, const float *W, const float *b, const int32_t *y,

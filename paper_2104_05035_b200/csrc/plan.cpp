@@ -229,6 +229,7 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
   nblk_max = 4 * 148;
   off_partial = alloc(sizeof(float) * nblk_max * 2 * 512);
   off_coef = alloc(sizeof(float) * 3 * 512 * 2);
+  off_counter = alloc(256);  // last-block tickets of the fused reduce+finalize kernels (zeroed at bind)
   off_wgrad_ws = alloc(sizeof(float) * (wgrad_ws_floats ? wgrad_ws_floats : 1));
   off_conv_ws = alloc(sizeof(float) * (conv_ws_floats ? conv_ws_floats : 1));
 
@@ -388,14 +389,6 @@ void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x
 
 float *Plan::bn_stat(const BNL &b, int k, int which) { return (float *)P(b.stat_off[k]) + which * b.C; }
 
-// Cooperative fused BN (one launch per layer) measured slower than the 3-launch
-// path on B200 (7.3 vs 6.2 ms/step: 444-block grid, serial apply loop), so it
-// is opt-in ("fuse_bn" = 1) until its apply phase is reworked.
-bool Plan::fuse_bn() const {
-  auto it = opts.find("fuse_bn");
-  return it != opts.end() && it->second != 0;
-}
-
 void Plan::bn_forward_stats(const BNL &b, int k, const void *h) { bn_fwd(b, k, h, nullptr, nullptr, nullptr, false, nullptr); }
 
 // Train-mode BN (reading X8): statistics of h, then (if y) y = act(BN(h) + R) where
@@ -403,36 +396,21 @@ void Plan::bn_forward_stats(const BNL &b, int k, const void *h) { bn_fwd(b, k, h
 void Plan::bn_fwd(const BNL &b, int k, const void *h, const void *res, const float *rscale, const float *rshift,
                   bool relu, void *y) {
   float *part = (float *)P(off_partial);
-  if (fuse_bn()) {
-    bn_forward_fused(dt, h, b.V, b.C, part, master(b.gamma_idx), master(b.gamma_idx + 1), bn_stat(b, k, 0),
-                     bn_stat(b, k, 1), bn_stat(b, k, 2), bn_stat(b, k, 3), (float *)P(off_run_mean) + b.run_off,
-                     (float *)P(off_run_var) + b.run_off, BN_MOMENTUM, BN_EPS, res, rscale, rshift, relu, y, stream);
-    return;
-  }
-  const int nblk = chan_reduce_blocks(b.V, b.C);
-  bn_stats(dt, h, b.V, b.C, part, nblk, stream);
-  bn_finalize(dt, h, part, nblk, b.V, b.C, master(b.gamma_idx), master(b.gamma_idx + 1), bn_stat(b, k, 0),
-              bn_stat(b, k, 1), bn_stat(b, k, 2), bn_stat(b, k, 3), (float *)P(off_run_mean) + b.run_off,
-              (float *)P(off_run_var) + b.run_off, BN_MOMENTUM, BN_EPS, stream);
+  bn_stats_finalize(dt, h, b.V, b.C, part, counter(), master(b.gamma_idx), master(b.gamma_idx + 1),
+                    bn_stat(b, k, 0), bn_stat(b, k, 1), bn_stat(b, k, 2), bn_stat(b, k, 3),
+                    (float *)P(off_run_mean) + b.run_off, (float *)P(off_run_var) + b.run_off, BN_MOMENTUM, BN_EPS,
+                    stream);
   if (y) bn_apply(dt, h, b.V, b.C, bn_stat(b, k, 2), bn_stat(b, k, 3), res, rscale, rshift, relu, y, stream);
 }
 
 // dx = BN-backward of dy' = dy * mask ; coef scratch slot `slot`
 void Plan::bn_backward(const BNL &b, int k, const void *dy, const void *h, int mask_mode, const void *mask_t,
                        void *dx, int slot) {
-  const int nblk = chan_reduce_blocks(b.V, b.C);
   float *part = (float *)P(off_partial);
   float *coef = (float *)P(off_coef) + slot * 3 * 512;
-  if (fuse_bn()) {
-    bn_backward_fused(dt, dy, h, b.V, b.C, mask_mode, mask_t, bn_stat(b, k, 2), bn_stat(b, k, 3), bn_stat(b, k, 0),
-                      bn_stat(b, k, 1), master(b.gamma_idx), part, grad(b.gamma_idx), grad(b.gamma_idx + 1), coef, dx,
-                      stream);
-    return;
-  }
-  bn_bwd_reduce(dt, dy, h, b.V, b.C, mask_mode, mask_t, bn_stat(b, k, 2), bn_stat(b, k, 3), bn_stat(b, k, 0),
-                bn_stat(b, k, 1), part, nblk, stream);
-  bn_bwd_finalize(part, nblk, b.V, b.C, master(b.gamma_idx), bn_stat(b, k, 0), bn_stat(b, k, 1),
-                  grad(b.gamma_idx), grad(b.gamma_idx + 1), coef, stream);
+  bn_bwd_reduce_finalize(dt, dy, h, b.V, b.C, mask_mode, mask_t, bn_stat(b, k, 2), bn_stat(b, k, 3),
+                         bn_stat(b, k, 0), bn_stat(b, k, 1), master(b.gamma_idx), part, counter(),
+                         grad(b.gamma_idx), grad(b.gamma_idx + 1), coef, stream);
   bn_bwd_apply(dt, dy, h, b.V, b.C, mask_mode, mask_t, bn_stat(b, k, 2), bn_stat(b, k, 3), coef, dx, stream);
 }
 
@@ -559,10 +537,8 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
   } else if (u.kind == U_ATT) {
     const int C = u.cout;
     const int64_t V = (int64_t)mb * u.in.vol();
-    const int nblk = chan_reduce_blocks(V, C);
-    float *part = (float *)P(off_partial);
-    att_bwd(dt, P(L.dout), P(L.m[k]), P(L.trunk.out_[k]), V, C, P(L.dT), P(L.dm), part, nblk, stream);
-    chan_sum_finalize(part, nblk, C, grad(L.bias_idx), stream);
+    att_bwd_finalize(dt, P(L.dout), P(L.m[k]), P(L.trunk.out_[k]), V, C, P(L.dT), P(L.dm), (float *)P(off_partial),
+                     counter(), grad(L.bias_idx), stream);
     conv_bwd_weight(L.mc2, P(L.r[k]), P(L.dm), false);
     conv_bwd_data(L.mc2, P(L.dm), P(L.dr), false, nullptr, nullptr);
     bn_backward(L.mbn, k, P(L.dr), P(L.mh[k]), MASK_TENSOR, P(L.r[k]), P(L.dmh), 0);
@@ -791,6 +767,7 @@ void Plan::bind(void *dev, size_t bytes) {
   if (bytes < ws_bytes) throw Error(RN_ERR_SIZE, "workspace smaller than required");
   if (((uintptr_t)dev & 255) != 0) throw Error(RN_ERR_ARG, "workspace must be 256-byte aligned");
   base = (char *)dev;
+  CUDA_CHECK(cudaMemset(P(off_counter), 0, 256));
   // optimizer tables: conv tensors (bf16 copies) and plain SGD ranges, local units only
   std::vector<ConvPack> packs;
   std::vector<int64_t> rg;
@@ -884,7 +861,7 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 }
 
 rn_status Plan::set_option(const std::string &k, int64_t v) {
-  if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "fuse_bn" && k != "halo_conv")
+  if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv")
     return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;

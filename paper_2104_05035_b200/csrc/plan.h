@@ -88,6 +88,8 @@ struct Plan {
   std::vector<int64_t> bn_run_off;
   std::vector<size_t> shadow_f, shadow_d;
   size_t off_master = 0, off_grad = 0, off_run_mean = 0, off_run_var = 0, off_loss = 0, off_flag = 0;
+  size_t off_counter = 0;
+  unsigned *counter() { return (unsigned *)P(off_counter); }
   size_t off_partial = 0, off_coef = 0, off_wgrad_ws = 0, off_x = 0, off_y = 0;
   size_t wgrad_ws_floats = 0, conv_ws_floats = 0, off_conv_ws = 0;
   size_t off_pack = 0, off_sgdrg = 0;
@@ -132,7 +134,6 @@ struct Plan {
   void bn_forward_stats(const BNL &b, int k, const void *h);
   void bn_fwd(const BNL &b, int k, const void *h, const void *res, const float *rscale, const float *rshift, bool relu,
               void *y);
-  bool fuse_bn() const;
   void bn_backward(const BNL &b, int k, const void *dy, const void *h, int mask_mode, const void *mask_t, void *dx,
                    int slot);
   void block_fwd(BlockL &B, int k, const void *x);

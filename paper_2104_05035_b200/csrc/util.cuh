@@ -58,6 +58,15 @@ __device__ __forceinline__ void store8(float *p, const float *v) {
 }
 __device__ __forceinline__ void store8(bf16 *p, const float *v) { store_vec(p, v); }
 
+// Programmatic Dependent Launch (see launch.h): wait for the predecessor grid
+// (no-op when launched without PDL), then allow the successor to launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_begin() {
+  pdl_wait();
+  pdl_trigger();
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

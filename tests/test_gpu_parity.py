@@ -183,24 +183,3 @@ def test_cuda_graph_replay_matches_eager():
         outs.append((losses, plan.get_params()))
     assert outs[0][0] == outs[1][0]
     assert np.array_equal(outs[0][1], outs[1][1])
-
-
-@pytest.mark.parametrize("dtype", [rn.RN_F32, rn.RN_BF16])
-def test_fused_bn_matches_unfused(dtype):
-    """The cooperative fused BN kernels compute what the 3-launch path computes
-    (same partial order; fp32 path additionally checked against the oracle)."""
-    dims = (40, 48, 40)
-    outs = []
-    for fuse in (1, 0):
-        plan = rn.Plan(rn.net_desc(18, 16, dims), 2, dtype)
-        plan.set_option("fuse_bn", fuse)
-        arrays = synthetic.perturb_params(plan.tensors, synthetic.init_params(plan.tensors, seed=0))
-        plan.set_params(np.concatenate([a.ravel() for a in arrays]).astype(np.float32))
-        x, y = synthetic.make_batch(2, *dims, seed=1)
-        loss = plan.forward(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
-        plan.backward()
-        outs.append((loss, plan.get_grads(), plan.get_bn_running()))
-    assert abs(outs[0][0] - outs[1][0]) <= 1e-6 * abs(outs[1][0])
-    tol = 1e-5 if dtype == rn.RN_F32 else 2e-2
-    assert rel(outs[0][1], outs[1][1]) <= tol
-    assert rel(outs[0][2][1], outs[1][2][1]) <= 1e-5
