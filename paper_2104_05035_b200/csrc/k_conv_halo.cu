@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cstring>
 
+#include "bnstats.cuh"
 #include "error.h"
 #include "launch.h"
 #include "kernels.h"
@@ -41,7 +42,8 @@ constexpr int HW = 10, HH = 18, HD = 4;              // haloed box (w, h, d)
 constexpr int A_BYTES = HW * HH * HD * 128;          // 92160
 constexpr int B_BYTES = 64 * 128;                    // one tap: 64 out channels x 64 in channels
 constexpr int BSTAGES = 4;
-constexpr int SMEM = 2 * A_BYTES + BSTAGES * B_BYTES + 256 + 1024;
+constexpr int RED_BYTES = 4 * 2 * 64 * 4;  // [4 warps][2][64] BN-statistics accumulators
+constexpr int SMEM = 2 * A_BYTES + BSTAGES * B_BYTES + RED_BYTES + 256 + 1024;
 constexpr int THREADS = 192;
 
 struct __align__(64) HaloParams {
@@ -56,6 +58,7 @@ struct __align__(64) HaloParams {
   const float *bias;
   int accumulate;
   const bf16 *res, *res_mask;
+  EpiStats st;
 };
 
 __global__ void __launch_bounds__(THREADS, 1) conv_halo_kernel(const __grid_constant__ HaloParams p) {
@@ -63,7 +66,8 @@ __global__ void __launch_bounds__(THREADS, 1) conv_halo_kernel(const __grid_cons
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *sA = smem;                       // 2 x A_BYTES
   uint8_t *sB = smem + 2 * A_BYTES;         // BSTAGES x B_BYTES
-  uint64_t *bar = (uint64_t *)(sB + BSTAGES * B_BYTES);
+  float *red = (float *)(sB + BSTAGES * B_BYTES);
+  uint64_t *bar = (uint64_t *)(sB + BSTAGES * B_BYTES + RED_BYTES);
   uint64_t *a_full = bar, *a_empty = bar + 2, *b_full = bar + 4, *b_empty = b_full + BSTAGES;
   uint64_t *t_full = b_empty + BSTAGES, *t_empty = t_full + 2;
   uint32_t *tmem_slot = (uint32_t *)(t_empty + 2);
@@ -156,6 +160,11 @@ __global__ void __launch_bounds__(THREADS, 1) conv_halo_kernel(const __grid_cons
     const int q = warp & 3;
     const int row = q * 32 + lane;  // output row in a slice: w = row % 8, h = row / 8
     const int wx = row % 8, hy = row / 8;
+    const int et = threadIdx.x - 64;
+    if (p.st.mode) {
+      for (int i = et; i < 8 * 64; i += 128) red[i] = 0.f;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
     int local = 0;
     for (int64_t it = blockIdx.x; it < p.n_items; it += gridDim.x, ++local) {
       int64_t r = it;
@@ -164,55 +173,67 @@ __global__ void __launch_bounds__(THREADS, 1) conv_halo_kernel(const __grid_cons
       const int td = (int)(r % p.td); r /= p.td;
       const int n = (int)r;
       const int acc = local & 1;
+      const int ow = tw * 8 + wx, oh = th * 16 + hy;
+      // chunk ch = (slice, 32-channel half); mask / h of the next chunk are prefetched
+      auto chunk_valid = [&](int sl) { return ow < p.OW && oh < p.OH && td * 2 + sl < p.OD; };
+      auto chunk_base = [&](int sl) { return n * p.s_n + (td * 2 + sl) * p.s_d + oh * p.s_h + ow * p.s_w; };
+      StatsPf pf_cur, pf_nxt;
+      epi_stats_prefetch(p.st, chunk_valid(0), chunk_base(0), pf_cur);
       tc::mbar_wait(&t_full[acc], (local >> 1) & 1);
       tc::tc_fence_after();
-      const int ow = tw * 8 + wx, oh = th * 16 + hy;
 #pragma unroll 1
       for (int sl = 0; sl < 2; ++sl) {
-        const int od = td * 2 + sl;
-        const bool valid = ow < p.OW && oh < p.OH && od < p.OD;
-        const int64_t obase = n * p.s_n + od * p.s_d + oh * p.s_h + ow * p.s_w;
+        const bool valid = chunk_valid(sl);
+        const int64_t obase = chunk_base(sl);
 #pragma unroll 1
         for (int c0 = 0; c0 < 64; c0 += 32) {
+          if (c0 == 0) epi_stats_prefetch(p.st, valid, obase + 32, pf_nxt);
+          else if (sl == 0) epi_stats_prefetch(p.st, chunk_valid(1), chunk_base(1), pf_nxt);
           uint32_t v[32];
           tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * 128 + sl * 64 + c0, v);
           tc::tmem_wait_ld();
-          if (!valid) continue;
           float f[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-          if (p.bias) {
+          if (valid) {
+            if (p.bias) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) f[j] += p.bias[c0 + j];
-          }
-          bf16 *dst = p.y + obase + c0;
-          if (p.accumulate) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              float o[8];
-              load_vec(dst + j, o);
-#pragma unroll
-              for (int e = 0; e < 8; ++e) f[j + e] += o[e];
+              for (int j = 0; j < 32; ++j) f[j] += p.bias[c0 + j];
             }
-          }
-          if (p.res) {
+            bf16 *dst = p.y + obase + c0;
+            if (p.accumulate) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              float rv[8], mv[8];
-              load_vec(p.res + obase + c0 + j, rv);
-              load_vec(p.res_mask + obase + c0 + j, mv);
+              for (int j = 0; j < 32; j += 8) {
+                float o[8];
+                load_vec(dst + j, o);
 #pragma unroll
-              for (int e = 0; e < 8; ++e) f[j + e] += mv[e] > 0.f ? rv[e] : 0.f;
+                for (int e = 0; e < 8; ++e) f[j + e] += o[e];
+              }
             }
-          }
+            if (p.res) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 8) store_vec(dst + j, f + j);
+              for (int j = 0; j < 32; j += 8) {
+                float rv[8], mv[8];
+                load_vec(p.res + obase + c0 + j, rv);
+                load_vec(p.res_mask + obase + c0 + j, mv);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) f[j + e] += mv[e] > 0.f ? rv[e] : 0.f;
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) store_vec(dst + j, f + j);
+          }
+          if (p.st.mode) {
+            epi_stats_add(p.st, f, valid, pf_cur, lane, red + (q * 2) * 64 + c0, red + (q * 2 + 1) * 64 + c0);
+            pf_cur = pf_nxt;
+          }
         }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&t_empty[acc]);
     }
+    if (p.st.mode) epi_stats_flush(p.st, red, 64, 64, et);
   }
   __syncthreads();
   if (warp == 1) {
@@ -230,8 +251,8 @@ bool halo_conv_supported(const ConvGeom &g, bool dgrad) {
 
 // fprop (w = [Co][27][Ci]) or stride-1 dgrad (src = dy, w = flipped [Ci][27][Co]):
 // out[v][n] (=|+=) sum_t src[v + off_t][:] . w[n][t][:]  (+ bias) (+ res*(mask>0))
-void conv_halo(const ConvGeom &g, bool dgrad, const bf16 *src, const bf16 *w, const float *bias, bf16 *out,
-               bool accumulate, const bf16 *res, const bf16 *res_mask, cudaStream_t st) {
+int conv_halo(const ConvGeom &g, bool dgrad, const bf16 *src, const bf16 *w, const float *bias, bf16 *out,
+              bool accumulate, const bf16 *res, const bf16 *res_mask, cudaStream_t st, const EpiStats *est) {
   HaloParams p;
   memset(&p, 0, sizeof p);
   // output grid == input grid (stride 1, pad 1)
@@ -253,6 +274,7 @@ void conv_halo(const ConvGeom &g, bool dgrad, const bf16 *src, const bf16 *w, co
   p.accumulate = accumulate;
   p.res = res;
   p.res_mask = res_mask;
+  if (est && est->mode) p.st = *est;
   static bool attr = false;
   if (!attr) {
     CUDA_CHECK(cudaFuncSetAttribute(conv_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -264,6 +286,7 @@ void conv_halo(const ConvGeom &g, bool dgrad, const bf16 *src, const bf16 *w, co
   const int grid = (int)std::min<int64_t>(p.n_items, sms);
   launch_k(conv_halo_kernel, grid, THREADS, SMEM, st, p);
   LAUNCH_CHECK();
+  return p.st.mode ? grid : 0;
 }
 
 }  // namespace rn

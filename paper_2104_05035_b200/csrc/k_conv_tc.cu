@@ -28,6 +28,7 @@
 #include <cstring>
 #include <vector>
 
+#include "bnstats.cuh"
 #include "error.h"
 #include "launch.h"
 #include "kernels.h"
@@ -66,6 +67,7 @@ struct __align__(64) TcParams {
   int ksplit;
   float *part;
   int64_t n_view_vox;
+  EpiStats st;  // fused BN statistics of the stored output (needs ksplit == 1, t_nblk == 1)
 };
 
 template <int BN, int STAGES>
@@ -73,7 +75,8 @@ struct Smem {
   static constexpr int A_BYTES = 128 * 128;      // 128 rows x 64 bf16
   static constexpr int B_BYTES = BN * 128;       // BN rows x 64 bf16
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFF = STAGES * STAGE;
+  static constexpr int RED_OFF = STAGES * STAGE;   // [4 warps][2][BN] fp32 BN-statistics accumulators
+  static constexpr int BAR_OFF = RED_OFF + 4 * 2 * BN * 4;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
 };
 
@@ -181,6 +184,12 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
     // ---------------- epilogue (warps 2..5) ----------------
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
+    const int et = threadIdx.x - 64;  // 0..127
+    float *red = (float *)(smem + S::RED_OFF);
+    if (p.st.mode) {
+      for (int i = et; i < 8 * BN; i += 128) red[i] = 0.f;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
     const int wx = row % p.bw, hy = (row / p.bw) % p.bh, dz = (row / (p.bw * p.bh)) % p.bd,
               nz = row / (p.bw * p.bh * p.bd);
     int local = 0;
@@ -196,11 +205,14 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
       const bool valid = ow < p.OW && oh < p.OH && od < p.OD && on < p.ON;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
+      const int64_t obase = on * p.s_n + od * p.s_d + oh * p.s_h + ow * p.s_w + (int64_t)nb * BN;
+      StatsPf pf_cur, pf_nxt;
+      epi_stats_prefetch(p.st, valid, obase, pf_cur);  // before the accumulator wait
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::tc_fence_after();
-      const int64_t obase = on * p.s_n + od * p.s_d + oh * p.s_h + ow * p.s_w + (int64_t)nb * BN;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
+        if (c0 + 32 < BN) epi_stats_prefetch(p.st, valid, obase + c0 + 32, pf_nxt);
         uint32_t v[32];
         tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
         tc::tmem_wait_ld();
@@ -212,10 +224,12 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
           for (int j = 0; j < 32; j += 4)
             *reinterpret_cast<float4 *>(dst + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
                                                                __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-        } else if (valid) {
-          float f[32];
+          continue;
+        }
+        float f[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+        if (valid) {
           if (p.bias) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) f[j] += p.bias[nb * BN + c0 + j];
@@ -244,11 +258,16 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
 #pragma unroll
           for (int j = 0; j < 32; j += 8) store_vec(dst + j, f + j);
         }
+        if (p.st.mode) {
+          epi_stats_add(p.st, f, valid, pf_cur, lane, red + (q * 2) * BN + c0, red + (q * 2 + 1) * BN + c0);
+          pf_cur = pf_nxt;
+        }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
     }
+    if (p.st.mode) epi_stats_flush(p.st, red, BN, BN, et);
   }
   __syncthreads();
   if (warp == 1) {
@@ -324,7 +343,7 @@ void choose_box(int W, int H, int D, int N, int &bw, int &bh, int &bd, int &bn) 
 }
 
 template <int BN, int STAGES>
-void launch(const TcParams &p, cudaStream_t st) {
+int launch(const TcParams &p, cudaStream_t st) {
   using S = Smem<BN, STAGES>;
   static bool attr = false;
   if (!attr) {
@@ -345,6 +364,7 @@ void launch(const TcParams &p, cudaStream_t st) {
   const int grid = (int)std::min<int64_t>(p.n_tiles * p.ksplit, (int64_t)sms * per_sm);
   launch_k(conv_tc_kernel<BN, STAGES>, grid, TC_THREADS, S::TOTAL, st, p);
   LAUNCH_CHECK();
+  return grid;
 }
 
 // split-K finish: out = sum_s part[s] (+bias) (+existing) (+res*(mask>0)), bf16 store through the view
@@ -404,27 +424,32 @@ int choose_ksplit(int64_t n_tiles, int nk) {
   return std::max(ks, 1);
 }
 
-void run(TcParams &p, int BN, float *ws, size_t ws_floats, cudaStream_t st) {
+// returns the number of BN-statistics partials written (0: statistics not fused)
+int run(TcParams &p, int BN, float *ws, size_t ws_floats, const EpiStats *est, cudaStream_t st) {
   const int nk = p.n_taps * p.kblocks_per_tap;
   p.n_view_vox = (int64_t)p.ON * p.OD * p.OH * p.OW;
   p.ksplit = choose_ksplit(p.n_tiles, nk);
   if (g_dry_need) {
     if (p.ksplit > 1) *g_dry_need = std::max(*g_dry_need, (size_t)p.ksplit * p.n_view_vox * p.ych);
-    return;
+    return 0;
   }
   if (!ws || (size_t)p.ksplit * p.n_view_vox * p.ych > ws_floats) p.ksplit = 1;
   p.part = ws;
+  // fused statistics need whole-K tiles (no split) covering every output channel
+  const bool stats = est && est->mode && p.ksplit == 1 && p.t_nblk == 1;
+  if (stats) p.st = *est;
   // two CTAs per SM (each with its own TMA/MMA pipeline) hide the TMA latency the
   // small N=64/128 MMAs cannot cover alone; N=256 needs all 512 TMEM columns
   static const bool occ1 = getenv("RN_TC_OCC1") != nullptr;
+  int grid;
   if (BN == 64) {
-    if (occ1) launch<64, 6>(p, st);
-    else launch<64, 4>(p, st);
+    if (occ1) grid = launch<64, 6>(p, st);
+    else grid = launch<64, 4>(p, st);
   } else if (BN == 128) {
-    if (occ1) launch<128, 5>(p, st);
-    else launch<128, 3>(p, st);
+    if (occ1) grid = launch<128, 5>(p, st);
+    else grid = launch<128, 3>(p, st);
   } else {
-    launch<256, 4>(p, st);
+    grid = launch<256, 4>(p, st);
   }
   if (p.ksplit > 1) {
     const int64_t n = p.n_view_vox * (p.ych / 8);
@@ -433,6 +458,7 @@ void run(TcParams &p, int BN, float *ws, size_t ws_floats, cudaStream_t st) {
         p.res, p.res_mask);
     LAUNCH_CHECK();
   }
+  return stats ? grid : 0;
 }
 
 // Largest N tile dividing nout, halved while the launch has fewer tiles than
@@ -477,8 +503,8 @@ bool tc_conv_supported(const ConvGeom &g, bool dgrad) {
 }
 
 // fprop: y[vo][co] = sum x[...] w[co][tap][ci] (+bias)
-void conv_fprop_tc(const ConvGeom &g, const bf16 *x, const bf16 *w, const float *bias, bf16 *y, float *ws,
-                   size_t ws_floats, cudaStream_t st) {
+int conv_fprop_tc(const ConvGeom &g, const bf16 *x, const bf16 *w, const float *bias, bf16 *y, float *ws,
+                  size_t ws_floats, cudaStream_t st, const EpiStats *est) {
   TcParams p;
   memset(&p, 0, sizeof p);
   const int BN = pick_bn(g.Co, g.Wo, g.Ho, g.Do, g.N);
@@ -523,12 +549,12 @@ void conv_fprop_tc(const ConvGeom &g, const bf16 *x, const bf16 *w, const float 
   p.s_d = (int64_t)g.Ho * g.Wo * g.Co;
   p.s_n = (int64_t)g.Do * g.Ho * g.Wo * g.Co;
   p.bias = bias;
-  run(p, BN, ws, ws_floats, st);
+  return run(p, BN, ws, ws_floats, est, st);
 }
 
 // dgrad: dx[vi][ci] (=|+=) sum dy[vo][co] W[co][tap][ci]; wd = [ci][taps-1-tap][co]
-void conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, bool accumulate, const bf16 *res,
-                   const bf16 *res_mask, float *ws, size_t ws_floats, cudaStream_t st) {
+int conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, bool accumulate, const bf16 *res,
+                  const bf16 *res_mask, float *ws, size_t ws_floats, cudaStream_t st, const EpiStats *est) {
   const int taps = g.taps();
   const int BN = g.s == 1 ? pick_bn(g.Ci, g.Wi, g.Hi, g.Di, g.N)
                           : pick_bn(g.Ci, (g.Wi + 1) / 2, (g.Hi + 1) / 2, (g.Di + 1) / 2, g.N);
@@ -557,8 +583,7 @@ void conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, 
     p.accumulate = accumulate;
     p.res = res;
     p.res_mask = res_mask;
-    run(p, BN, ws, ws_floats, st);
-    return;
+    return run(p, BN, ws, ws_floats, est, st);
   }
   // stride 2: output parity classes (pd, ph, pw); input index i = 2a + par.
   // Contributions: i = 2o + k - p  =>  for k=3,p=1: par 0 <- (k=1, o=a); par 1 <- (k=2, o=a), (k=0, o=a+1)
@@ -611,16 +636,17 @@ void conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, 
           p.res = res + (((int64_t)pd * g.Hi + ph) * g.Wi + pw) * g.Ci;
           p.res_mask = res_mask + (((int64_t)pd * g.Hi + ph) * g.Wi + pw) * g.Ci;
         }
-        run(p, BN, ws, ws_floats, st);
+        run(p, BN, ws, ws_floats, nullptr, st);  // stride-2 dgrad outputs never feed a BN directly
       }
+  return 0;
 }
 
 size_t tc_conv_ws_floats(const ConvGeom &g, bool dgrad) {
   size_t need = 0;
   g_dry_need = &need;
   try {
-    if (!dgrad) conv_fprop_tc(g, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr);
-    else conv_dgrad_tc(g, nullptr, nullptr, nullptr, true, nullptr, nullptr, nullptr, 0, nullptr);
+    if (!dgrad) conv_fprop_tc(g, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr);
+    else conv_dgrad_tc(g, nullptr, nullptr, nullptr, true, nullptr, nullptr, nullptr, 0, nullptr, nullptr);
   } catch (...) {
     g_dry_need = nullptr;
     throw;

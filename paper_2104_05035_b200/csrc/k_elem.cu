@@ -72,11 +72,9 @@ __device__ __forceinline__ void unpack16(const uint4 &u, float *v, const bf16 *)
   }
 }
 
-template <typename T, typename Op, typename Fin>
-__global__ void __launch_bounds__(NTR) chan_reduce_fin_k(Op op, Fin fin, int64_t V, int C, float *__restrict__ partial,
-                                                         int64_t rpb, unsigned *counter) {
-  extern __shared__ float sm[];
-  pdl_begin();
+template <typename T, typename Op>
+__device__ __forceinline__ void chan_reduce_body(Op &op, int64_t V, int C, float *__restrict__ partial, int64_t rpb,
+                                                 float *sm) {
   constexpr int VEC = Vec<T>::N;
   const int G = C / VEC;
   const int RPI = NTR / G;
@@ -114,6 +112,24 @@ __global__ void __launch_bounds__(NTR) chan_reduce_fin_k(Op op, Fin fin, int64_t
     partial[(int64_t)blockIdx.x * 2 * C + c] = s1;
     partial[(int64_t)blockIdx.x * 2 * C + C + c] = s2;
   }
+}
+
+// per-block partials only (the BN apply kernels finalize them: bn_*_part_k)
+template <typename T, typename Op>
+__global__ void __launch_bounds__(NTR) chan_partials_k(Op op, int64_t V, int C, float *__restrict__ partial,
+                                                       int64_t rpb) {
+  extern __shared__ float sm[];
+  pdl_begin();
+  chan_reduce_body<T>(op, V, C, partial, rpb, sm);
+}
+
+template <typename T, typename Op, typename Fin>
+__global__ void __launch_bounds__(NTR) chan_reduce_fin_k(Op op, Fin fin, int64_t V, int C, float *__restrict__ partial,
+                                                         int64_t rpb, unsigned *counter) {
+  extern __shared__ float sm[];
+  pdl_begin();
+  chan_reduce_body<T>(op, V, C, partial, rpb, sm);
+  const int t = threadIdx.x;
   __shared__ bool is_last;
   __threadfence();
   __syncthreads();
@@ -178,7 +194,13 @@ struct StatsOp {
   struct Buf {
     uint4 v;
   };
-  __device__ void init(int c0) { load_vec(x + c0, K); }
+  bool shifted = true;  // false: plain sums (the convention of the fused conv-epilogue partials)
+  __device__ void init(int c0) {
+    if (shifted) load_vec(x + c0, K);
+    else
+#pragma unroll
+      for (int j = 0; j < Vec<T>::N; ++j) K[j] = 0.f;
+  }
   __device__ void load(int64_t r, int c0, Buf &b) const { b.v = ld16(x + r * C + c0); }
   __device__ void acc(const Buf &b, int64_t, int, float *a1, float *a2) const {
     float v[Vec<T>::N];
@@ -227,6 +249,36 @@ struct BwdOp {
       const float xh = (xv[j] - mean[c0 + j]) * invstd[c0 + j];
       a1[j] += d[j];
       a2[j] = fmaf(d[j], xh, a2[j]);
+    }
+  }
+};
+
+// BN backward sums in the fused-partials convention: (sum dy', sum dy' h), dy' = dy * (mask > 0)
+template <typename T>
+struct BwdHOp {
+  const T *dy, *x, *mask_t;
+  int C;
+  struct Buf {
+    uint4 d, x, m;
+  };
+  __device__ void init(int) {}
+  __device__ void load(int64_t r, int c0, Buf &b) const {
+    const int64_t off = r * C + c0;
+    b.d = ld16(dy + off);
+    b.x = ld16(x + off);
+    b.m = ld16(mask_t + off);
+  }
+  __device__ void acc(const Buf &b, int64_t, int, float *a1, float *a2) const {
+    constexpr int VEC = Vec<T>::N;
+    float d[VEC], xv[VEC], m[VEC];
+    unpack16(b.d, d, dy);
+    unpack16(b.x, xv, x);
+    unpack16(b.m, m, x);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      const float dd = m[j] > 0.f ? d[j] : 0.f;
+      a1[j] += dd;
+      a2[j] = fmaf(dd, xv[j], a2[j]);
     }
   }
 };
@@ -439,6 +491,238 @@ __global__ void __launch_bounds__(NT) bn_bwd_apply_k(const T *__restrict__ dy, c
       store_vec(dx + k * VEC, o);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// BN apply passes fed by per-CTA statistics partials of the producing
+// convolution (bnstats.cuh).  Every block finalizes the statistics it needs in
+// its prologue (all partials, CTA order, fp64: identical in every block, so
+// deterministic) and block 0 publishes them (mean / invstd / scale / shift,
+// running statistics; dgamma / dbeta in backward).  No separate statistics pass
+// over the tensor and no serial finalize launch.
+// ---------------------------------------------------------------------------
+constexpr int NTA = 512;
+
+// per-channel sums over the P partials [P][2][C] -> dscr[0..C) / dscr[C..2C) (fp64)
+__device__ __forceinline__ void reduce_partials(const float *part, int P, int C, double *out, double *scr) {
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int Cb = C < nt ? C : nt, S = nt / Cb;
+  for (int cb = 0; cb < C; cb += Cb) {
+    const int c = cb + t % Cb, s = t / Cb;
+    if (s < S && c < C) {
+      // fp32 chain within a batch of 8 (short dependent-add latency), fp64 across batches
+      double a = 0.0, b = 0.0;
+      for (int k0 = s; k0 < P; k0 += 8 * S) {
+        float va[8], vb[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = k0 + j * S;
+          va[j] = k < P ? part[(int64_t)k * 2 * C + c] : 0.f;
+          vb[j] = k < P ? part[(int64_t)k * 2 * C + C + c] : 0.f;
+        }
+        float fa = 0.f, fb = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          fa += va[j];
+          fb += vb[j];
+        }
+        a += (double)fa;
+        b += (double)fb;
+      }
+      scr[s * Cb + t % Cb] = a;
+      scr[nt + s * Cb + t % Cb] = b;
+    }
+    __syncthreads();
+    if (s == 0 && c < C) {
+      double A = 0.0, B = 0.0;
+      for (int q = 0; q < S; ++q) {
+        A += scr[q * Cb + t % Cb];
+        B += scr[nt + q * Cb + t % Cb];
+      }
+      out[c] = A;
+      out[C + c] = B;
+    }
+    __syncthreads();
+  }
+}
+
+struct BnPart {
+  const float *part;  // [P][2][C]: (sum y, sum y^2) of the stored conv output
+  int P;
+  int64_t V;
+  const float *gamma, *beta;
+  float *mean, *invstd, *scale, *shift, *run_mean, *run_var;
+  float momentum, eps;
+};
+
+// sc/sh (smem) = scale/shift of the set; block 0 publishes the statistics
+__device__ __forceinline__ void bn_part_finalize(const BnPart &b, int C, float *sc, float *sh, double *sums,
+                                                 double *scr) {
+  reduce_partials(b.part, b.P, C, sums, scr);
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const double mu = sums[c] / (double)b.V;
+    double var = sums[C + c] / (double)b.V - mu * mu;
+    if (var < 0) var = 0;
+    const double is = 1.0 / sqrt(var + (double)b.eps);
+    const double scd = (double)b.gamma[c] * is;
+    const float s_ = (float)scd, h_ = (float)((double)b.beta[c] - mu * scd);
+    sc[c] = s_;
+    sh[c] = h_;
+    if (blockIdx.x == 0) {
+      b.mean[c] = (float)mu;
+      b.invstd[c] = (float)is;
+      b.scale[c] = s_;
+      b.shift[c] = h_;
+      if (b.run_mean) {
+        const double unb = b.V > 1 ? var * (double)b.V / (double)(b.V - 1) : var;
+        b.run_mean[c] = (float)((1.0 - b.momentum) * b.run_mean[c] + b.momentum * mu);
+        b.run_var[c] = (float)((1.0 - b.momentum) * b.run_var[c] + b.momentum * unb);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// y = act(x*scale + shift + R), R = 0 | res | BN_r(res) (set r.part != null)
+template <typename T>
+__global__ void __launch_bounds__(NTA) bn_apply_part_k(const T *__restrict__ x, int64_t V, int C, BnPart b,
+                                                       BnPart rb, const T *__restrict__ res, int relu,
+                                                       T *__restrict__ y) {
+  extern __shared__ double dsm[];
+  pdl_begin();
+  double *sums = dsm, *scr = dsm + 2 * C;  // 2C + 2*NTA doubles
+  float *fs = (float *)(scr + 2 * NTA);     // sc, sh, rsc, rsh: 4C floats
+  float *sc = fs, *sh = fs + C, *rsc = fs + 2 * C, *rsh = fs + 3 * C;
+  bn_part_finalize(b, C, sc, sh, sums, scr);
+  const bool rbn = rb.part != nullptr;
+  if (rbn) bn_part_finalize(rb, C, rsc, rsh, sums, scr);
+  constexpr int VEC = Vec<T>::N;
+  const int G = C / VEC;
+  const int64_t n = V * G;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // multiple of G
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int c0 = (int)(i0 % G) * VEC;
+  float a[VEC], bb[VEC], ra[VEC], rbv[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    a[j] = sc[c0 + j];
+    bb[j] = sh[c0 + j];
+    ra[j] = rbn ? rsc[c0 + j] : 1.f;
+    rbv[j] = rbn ? rsh[c0 + j] : 0.f;
+  }
+  for (int64_t i = i0; i < n; i += EU * stride) {
+    uint4 xv[EU], rv[EU];
+#pragma unroll
+    for (int q = 0; q < EU; ++q) {
+      const int64_t k = i + q * stride;
+      if (k < n) {
+        xv[q] = ld16(x + k * VEC);
+        if (res) rv[q] = ld16(res + k * VEC);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < EU; ++q) {
+      const int64_t k = i + q * stride;
+      if (k >= n) break;
+      float v[VEC];
+      unpack16(xv[q], v, x);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) v[j] = fmaf(v[j], a[j], bb[j]);
+      if (res) {
+        float r[VEC];
+        unpack16(rv[q], r, x);
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) v[j] += fmaf(r[j], ra[j], rbv[j]);
+      }
+      if (relu) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) v[j] = fmaxf(v[j], 0.f);
+      }
+      store_vec(y + k * VEC, v);
+    }
+  }
+}
+
+struct BnBwdPart {
+  const float *part;  // [P][2][C]: (sum dy', sum dy' h), dy' = dy * (mask > 0)
+  int P;
+  int64_t V;
+  const float *gamma, *mean, *invstd;
+  float *dgamma, *dbeta;
+};
+
+// dx = A dy' + B h + Cc with the coefficients finalized from the partials
+template <typename T>
+__global__ void __launch_bounds__(NTA) bn_bwd_apply_part_k(const T *__restrict__ dy, const T *__restrict__ h,
+                                                           const T *__restrict__ mask_t, int64_t V, int C,
+                                                           BnBwdPart b, T *__restrict__ dx) {
+  extern __shared__ double dsm[];
+  pdl_begin();
+  double *sums = dsm, *scr = dsm + 2 * C;
+  float *fs = (float *)(scr + 2 * NTA);
+  float *cA = fs, *cB = fs + C, *cC = fs + 2 * C;
+  reduce_partials(b.part, b.P, C, sums, scr);
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const double S1 = sums[c], is = b.invstd[c], mu = b.mean[c];
+    const double S2 = is * (sums[C + c] - mu * S1);  // sum dy' * xhat
+    const double m1 = S1 / (double)b.V, m2 = S2 / (double)b.V;
+    const double A = (double)b.gamma[c] * is;
+    cA[c] = (float)A;
+    cB[c] = (float)(-A * is * m2);
+    cC[c] = (float)(-A * m1 + A * is * mu * m2);
+    if (blockIdx.x == 0) {
+      b.dgamma[c] += (float)S2;
+      b.dbeta[c] += (float)S1;
+    }
+  }
+  __syncthreads();
+  constexpr int VEC = Vec<T>::N;
+  const int G = C / VEC;
+  const int64_t n = V * G;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int c0 = (int)(i0 % G) * VEC;
+  float A[VEC], B[VEC], Cc[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    A[j] = cA[c0 + j];
+    B[j] = cB[c0 + j];
+    Cc[j] = cC[c0 + j];
+  }
+  for (int64_t i = i0; i < n; i += EU * stride) {
+    uint4 dv[EU], xv[EU], mv[EU];
+#pragma unroll
+    for (int q = 0; q < EU; ++q) {
+      const int64_t k = i + q * stride;
+      if (k < n) {
+        dv[q] = ld16(dy + k * VEC);
+        xv[q] = ld16(h + k * VEC);
+        mv[q] = ld16(mask_t + k * VEC);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < EU; ++q) {
+      const int64_t k = i + q * stride;
+      if (k >= n) break;
+      float d[VEC], xf[VEC], m[VEC], o[VEC];
+      unpack16(dv[q], d, dy);
+      unpack16(xv[q], xf, h);
+      unpack16(mv[q], m, h);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        const float dd = m[j] > 0.f ? d[j] : 0.f;
+        o[j] = fmaf(A[j], dd, fmaf(B[j], xf[j], Cc[j]));
+      }
+      store_vec(dx + k * VEC, o);
+    }
+  }
+}
+
+inline unsigned grid_part(int64_t vecs) {
+  int64_t b = (vecs + (int64_t)NTA * EU - 1) / ((int64_t)NTA * EU);
+  if (b > 148) b = 148;
+  if (b < 1) b = 1;
+  return (unsigned)b;
 }
 
 // max-pool k3 s2 p1, -inf padding; first maximum in (kd,kh,kw) order (reading X10).
@@ -803,9 +1087,9 @@ __global__ void check_finite_k(const float *v, int n, int *flag) {
   } while (0)
 
 int chan_fin_blocks(int64_t V, int C) {
-  // one block per ~4096 elements, at most one per SM: the last block's
-  // finalize reads every partial, so fewer, fuller blocks
-  int64_t b = (V * C + 4095) / 4096;
+  // one block per ~32K elements, at most one per SM: whoever finalizes reads
+  // every partial (a small tensor needs few)
+  int64_t b = (V * C + 32767) / 32768;
   if (b > 148) b = 148;
   if (b < 1) b = 1;
   return (int)b;
@@ -819,7 +1103,7 @@ void bn_stats_finalize(DType dt, const void *x, int64_t V, int C, float *partial
     int64_t rpb;
     size_t smem;
     chan_reduce_dims<T>(V, C, nblk, rpb, smem);
-    StatsOp<T> op{(const T *)x, C, {}};
+    StatsOp<T> op{(const T *)x, C, {}, true};
     StatsFin<T> fin{(const T *)x, V, gamma, beta, mean, invstd, scale, shift, run_mean, run_var, momentum, eps};
     launch_k(chan_reduce_fin_k<T, StatsOp<T>, StatsFin<T>>, nblk, NTR, smem, st, op, fin, V, C, partial, rpb, counter);
   });
@@ -867,6 +1151,58 @@ void bn_bwd_apply(DType dt, const void *dy, const void *x, int64_t V, int C, int
                   const float *scale, const float *shift, const float *coef, void *dx, cudaStream_t st) {
   DISPATCH(dt, launch_k(bn_bwd_apply_k<T>, grid_elem(V * C / Vec<T>::N), NT, 0, st, 
                    (const T *)dy, (const T *)x, V, C, mask_mode, (const T *)mask_t, scale, shift, coef, (T *)dx));
+  LAUNCH_CHECK();
+}
+
+int bn_stats_partials(DType dt, const void *x, int64_t V, int C, float *part, cudaStream_t st) {
+  const int nblk = chan_fin_blocks(V, C);
+  DISPATCH(dt, {
+    int64_t rpb;
+    size_t smem;
+    chan_reduce_dims<T>(V, C, nblk, rpb, smem);
+    StatsOp<T> op{(const T *)x, C, {}, false};
+    launch_k(chan_partials_k<T, StatsOp<T>>, nblk, NTR, smem, st, op, V, C, part, rpb);
+  });
+  LAUNCH_CHECK();
+  return nblk;
+}
+
+int bn_bwd_partials(DType dt, const void *dy, const void *h, const void *mask_t, int64_t V, int C, float *part,
+                    cudaStream_t st) {
+  const int nblk = chan_fin_blocks(V, C);
+  DISPATCH(dt, {
+    int64_t rpb;
+    size_t smem;
+    chan_reduce_dims<T>(V, C, nblk, rpb, smem);
+    BwdHOp<T> op{(const T *)dy, (const T *)h, (const T *)mask_t, C};
+    launch_k(chan_partials_k<T, BwdHOp<T>>, nblk, NTR, smem, st, op, V, C, part, rpb);
+  });
+  LAUNCH_CHECK();
+  return nblk;
+}
+
+void bn_apply_fused(DType dt, const void *x, int64_t V, int C, const BnFinal &f, const BnFinal *rf, const void *res,
+                    bool relu, void *y, cudaStream_t st) {
+  auto mk = [&](const BnFinal &q) {
+    return BnPart{q.part, q.P, V, q.gamma, q.beta, q.mean, q.invstd, q.scale, q.shift, q.run_mean, q.run_var,
+                  q.momentum, q.eps};
+  };
+  const BnPart b = mk(f);
+  BnPart r{};
+  if (rf) r = mk(*rf);
+  const size_t smem = (2 * (size_t)C + 2 * NTA) * sizeof(double) + 4 * (size_t)C * sizeof(float);
+  DISPATCH(dt, launch_k(bn_apply_part_k<T>, grid_part(V * C / Vec<T>::N), NTA, smem, st, (const T *)x, V, C, b, r,
+                        (const T *)res, relu ? 1 : 0, (T *)y));
+  LAUNCH_CHECK();
+}
+
+void bn_bwd_apply_fused(DType dt, const void *dy, const void *h, const void *mask_t, int64_t V, int C,
+                        const float *part, int P, const float *gamma, const float *mean, const float *invstd,
+                        float *dgamma, float *dbeta, void *dx, cudaStream_t st) {
+  const BnBwdPart b{part, P, V, gamma, mean, invstd, dgamma, dbeta};
+  const size_t smem = (2 * (size_t)C + 2 * NTA) * sizeof(double) + 3 * (size_t)C * sizeof(float);
+  DISPATCH(dt, launch_k(bn_bwd_apply_part_k<T>, grid_part(V * C / Vec<T>::N), NTA, smem, st, (const T *)dy,
+                        (const T *)h, (const T *)mask_t, V, C, b, (T *)dx));
   LAUNCH_CHECK();
 }
 

@@ -66,6 +66,29 @@ void bn_bwd_reduce_finalize(DType dt, const void *dy, const void *x, int64_t V, 
                             const void *mask_t, const float *scale, const float *shift, const float *mean,
                             const float *invstd, const float *gamma, float *partial, unsigned *counter, float *dgamma,
                             float *dbeta, float *coef, cudaStream_t st);
+// BN apply fed by per-CTA statistics partials of the producing convolution
+// (bnstats.cuh): part [P][2][C] = (sum y, sum y^2); the kernel finalizes them
+// in every block and block 0 publishes mean / invstd / scale / shift and the
+// running statistics.  rf (optional): a second BN applied to `res` (projection).
+struct BnFinal {
+  const float *part;
+  int P;
+  const float *gamma, *beta;
+  float *mean, *invstd, *scale, *shift, *run_mean, *run_var;
+  float momentum, eps;
+};
+void bn_apply_fused(DType dt, const void *x, int64_t V, int C, const BnFinal &f, const BnFinal *rf, const void *res,
+                    bool relu, void *y, cudaStream_t st);
+// the same partials from a standalone pass over the tensor (layers whose conv
+// could not fuse them: split-K, SIMT); returns P
+int bn_stats_partials(DType dt, const void *x, int64_t V, int C, float *part, cudaStream_t st);
+int bn_bwd_partials(DType dt, const void *dy, const void *h, const void *mask_t, int64_t V, int C, float *part,
+                    cudaStream_t st);
+// BN backward apply fed by partials (sum dy', sum dy' h), dy' = dy * (mask > 0):
+// dgamma += sum dy' xhat, dbeta += sum dy', dx = BN-backward(dy')
+void bn_bwd_apply_fused(DType dt, const void *dy, const void *h, const void *mask_t, int64_t V, int C,
+                        const float *part, int P, const float *gamma, const float *mean, const float *invstd,
+                        float *dgamma, float *dbeta, void *dx, cudaStream_t st);
 // attention backward + dbias (sum of dm) in one launch
 void att_bwd_finalize(DType dt, const void *dout, const void *m, const void *T_, int64_t V, int C, void *dT, void *dm,
                       float *partial, unsigned *counter, float *dbias, cudaStream_t st);

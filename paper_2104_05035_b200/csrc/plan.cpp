@@ -39,6 +39,10 @@ void Plan::make_bn(BNL &b, int gamma_idx, int C, int64_t V) {
   b.run_off = bn_run_off[gamma_idx];
   b.stat_off.resize(Mb);
   for (int k = 0; k < Mb; ++k) b.stat_off[k] = alloc(4 * sizeof(float) * C);
+  if (dt == DT_BF16) {  // up to 2 CTAs per SM in the producing conv
+    b.fpart = alloc(sizeof(float) * 2 * 148 * 2 * C);
+    b.bpart = alloc(sizeof(float) * 2 * 148 * 2 * C);
+  }
 }
 
 void Plan::make_conv(ConvL &c, int w_idx, int Ci, int Co, int k, int s, int p, Dims in, Dims out) {
@@ -348,31 +352,57 @@ bool Plan::use_tc(const ConvGeom &g, bool dgrad) const {
   return tc_conv_supported(g, dgrad);
 }
 
-void Plan::conv_fwd(const ConvL &c, const void *x, void *y, const float *bias) {
+// fused BN statistics in the conv epilogues (bf16 tensor-core path; option
+// "fused_stats" = 0 restores the separate reduction kernels)
+bool Plan::fused_stats() const {
+  auto it = opts.find("fused_stats");
+  return dt == DT_BF16 && (it == opts.end() || it->second != 0);
+}
+
+void Plan::conv_fwd(const ConvL &c, const void *x, void *y, const float *bias, BNL *stats) {
   const bool t = timing();
   size_t e = t ? tk_begin(0, conv_flops(c.g)) : 0;
+  EpiStats es;
+  const bool want = stats && fused_stats();
+  if (want) {
+    es.part = (float *)P(stats->fpart);
+    es.mode = 1;
+  }
+  int parts = 0;
   if (use_tc(c.g, false) && use_halo() && halo_conv_supported(c.g, false))
-    conv_halo(c.g, false, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, false, nullptr,
-              nullptr, stream);
+    parts = conv_halo(c.g, false, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, false,
+                      nullptr, nullptr, stream, want ? &es : nullptr);
   else if (use_tc(c.g, false))
-    conv_fprop_tc(c.g, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y,
-                  (float *)P(off_conv_ws), conv_ws_floats, stream);
+    parts = conv_fprop_tc(c.g, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y,
+                          (float *)P(off_conv_ws), conv_ws_floats, stream, want ? &es : nullptr);
   else
     conv_fprop_simt(dt, c.g, x, wfwd(c.w_idx), bias, y, stream);
+  if (stats) stats->fP = parts;
   if (t) tk_end(e);
 }
 void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumulate, const void *res,
-                         const void *res_mask) {
+                         const void *res_mask, const StatsTarget &stats) {
   const bool t = timing();
   size_t e = t ? tk_begin(1, conv_flops(c.g)) : 0;
+  EpiStats es;
+  const bool want = stats.bn && fused_stats();
+  if (want) {
+    es.part = (float *)P(stats.bn->bpart);
+    es.mode = 2;
+    es.mask = (const bf16 *)stats.mask;
+    es.h = (const bf16 *)stats.h;
+  }
+  int parts = 0;
   if (use_tc(c.g, true) && use_halo() && halo_conv_supported(c.g, true))
-    conv_halo(c.g, true, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx, accumulate,
-              (const bf16 *)res, (const bf16 *)res_mask, stream);
+    parts = conv_halo(c.g, true, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx,
+                      accumulate, (const bf16 *)res, (const bf16 *)res_mask, stream, want ? &es : nullptr);
   else if (use_tc(c.g, true))
-    conv_dgrad_tc(c.g, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), (bf16 *)dx, accumulate,
-                  (const bf16 *)res, (const bf16 *)res_mask, (float *)P(off_conv_ws), conv_ws_floats, stream);
+    parts = conv_dgrad_tc(c.g, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), (bf16 *)dx, accumulate,
+                          (const bf16 *)res, (const bf16 *)res_mask, (float *)P(off_conv_ws), conv_ws_floats, stream,
+                          want ? &es : nullptr);
   else
     conv_dgrad_simt(dt, c.g, dy, wfwd(c.w_idx), dx, accumulate, res, res_mask, stream);
+  if (stats.bn) stats.bn->bP = parts;
   if (t) tk_end(e);
 }
 void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32) {
@@ -391,10 +421,35 @@ float *Plan::bn_stat(const BNL &b, int k, int which) { return (float *)P(b.stat_
 
 void Plan::bn_forward_stats(const BNL &b, int k, const void *h) { bn_fwd(b, k, h, nullptr, nullptr, nullptr, false, nullptr); }
 
+BnFinal Plan::bn_final(const BNL &b, int k) {
+  BnFinal f;
+  f.part = (const float *)P(b.fpart);
+  f.P = b.fP;
+  f.gamma = master(b.gamma_idx);
+  f.beta = master(b.gamma_idx + 1);
+  f.mean = bn_stat(b, k, 0);
+  f.invstd = bn_stat(b, k, 1);
+  f.scale = bn_stat(b, k, 2);
+  f.shift = bn_stat(b, k, 3);
+  f.run_mean = (float *)P(off_run_mean) + b.run_off;
+  f.run_var = (float *)P(off_run_var) + b.run_off;
+  f.momentum = BN_MOMENTUM;
+  f.eps = BN_EPS;
+  return f;
+}
+
 // Train-mode BN (reading X8): statistics of h, then (if y) y = act(BN(h) + R) where
-// R = res (identity skip) or res*rscale + rshift (the projection's BN).
+// R = res (identity skip) or res*rscale + rshift (the projection's BN).  When
+// the producing conv fused the statistics (b.fP > 0) one kernel finalizes and
+// applies them.
 void Plan::bn_fwd(const BNL &b, int k, const void *h, const void *res, const float *rscale, const float *rshift,
                   bool relu, void *y) {
+  if (fused_stats() && y && !rscale) {
+    BNL &m = const_cast<BNL &>(b);
+    if (m.fP <= 0) m.fP = bn_stats_partials(dt, h, b.V, b.C, (float *)P(b.fpart), stream);
+    bn_apply_fused(dt, h, b.V, b.C, bn_final(b, k), nullptr, res, relu, y, stream);
+    return;
+  }
   float *part = (float *)P(off_partial);
   bn_stats_finalize(dt, h, b.V, b.C, part, counter(), master(b.gamma_idx), master(b.gamma_idx + 1),
                     bn_stat(b, k, 0), bn_stat(b, k, 1), bn_stat(b, k, 2), bn_stat(b, k, 3),
@@ -403,9 +458,19 @@ void Plan::bn_fwd(const BNL &b, int k, const void *h, const void *res, const flo
   if (y) bn_apply(dt, h, b.V, b.C, bn_stat(b, k, 2), bn_stat(b, k, 3), res, rscale, rshift, relu, y, stream);
 }
 
-// dx = BN-backward of dy' = dy * mask ; coef scratch slot `slot`
+// dx = BN-backward of dy' = dy * mask ; coef scratch slot `slot`.  bf16 path:
+// the sums come from the producer of dy (b.bP > 0) or one standalone pass,
+// and the apply kernel finalizes them.
 void Plan::bn_backward(const BNL &b, int k, const void *dy, const void *h, int mask_mode, const void *mask_t,
                        void *dx, int slot) {
+  if (fused_stats() && mask_mode == MASK_TENSOR) {
+    BNL &m = const_cast<BNL &>(b);
+    if (m.bP <= 0) m.bP = bn_bwd_partials(dt, dy, h, mask_t, b.V, b.C, (float *)P(b.bpart), stream);
+    bn_bwd_apply_fused(dt, dy, h, mask_t, b.V, b.C, (const float *)P(b.bpart), b.bP, master(b.gamma_idx),
+                       bn_stat(b, k, 0), bn_stat(b, k, 1), grad(b.gamma_idx), grad(b.gamma_idx + 1), dx, stream);
+    m.bP = 0;  // consumed: the next producer decides again
+    return;
+  }
   float *part = (float *)P(off_partial);
   float *coef = (float *)P(off_coef) + slot * 3 * 512;
   bn_bwd_reduce_finalize(dt, dy, h, b.V, b.C, mask_mode, mask_t, bn_stat(b, k, 2), bn_stat(b, k, 3),
@@ -418,33 +483,49 @@ void Plan::bn_backward(const BNL &b, int k, const void *dy, const void *h, int m
 // residual network layer (two Conv blocks + skip)
 // ---------------------------------------------------------------------------
 void Plan::block_fwd(BlockL &B, int k, const void *x) {
-  conv_fwd(B.c1, x, P(B.h1[k]));
+  conv_fwd(B.c1, x, P(B.h1[k]), nullptr, &B.b1);
   bn_fwd(B.b1, k, P(B.h1[k]), nullptr, nullptr, nullptr, true, P(B.a1[k]));
-  conv_fwd(B.c2, P(B.a1[k]), P(B.h2[k]));
+  conv_fwd(B.c2, P(B.a1[k]), P(B.h2[k]), nullptr, &B.b2);
   if (B.proj) {
-    conv_fwd(B.cp, x, P(B.hp[k]));
-    bn_forward_stats(B.bp, k, P(B.hp[k]));
-    bn_fwd(B.b2, k, P(B.h2[k]), P(B.hp[k]), bn_stat(B.bp, k, 2), bn_stat(B.bp, k, 3), true, P(B.out_[k]));
+    conv_fwd(B.cp, x, P(B.hp[k]), nullptr, &B.bp);
+    if (fused_stats()) {
+      // out = ReLU(BN2(h2) + BNp(hp)): both statistics finalized in the apply kernel
+      if (B.b2.fP <= 0) B.b2.fP = bn_stats_partials(dt, P(B.h2[k]), B.b2.V, B.b2.C, (float *)P(B.b2.fpart), stream);
+      if (B.bp.fP <= 0) B.bp.fP = bn_stats_partials(dt, P(B.hp[k]), B.bp.V, B.bp.C, (float *)P(B.bp.fpart), stream);
+      const BnFinal fp = bn_final(B.bp, k);
+      bn_apply_fused(dt, P(B.h2[k]), B.b2.V, B.b2.C, bn_final(B.b2, k), &fp, P(B.hp[k]), true, P(B.out_[k]), stream);
+    } else {
+      bn_forward_stats(B.bp, k, P(B.hp[k]));
+      bn_fwd(B.b2, k, P(B.h2[k]), P(B.hp[k]), bn_stat(B.bp, k, 2), bn_stat(B.bp, k, 3), true, P(B.out_[k]));
+    }
   } else {
     bn_fwd(B.b2, k, P(B.h2[k]), x, nullptr, nullptr, true, P(B.out_[k]));
   }
 }
 
-void Plan::block_bwd(BlockL &B, int k, const void *x, const void *dout, void *dx, bool accumulate) {
+// dx_stats: the BN that consumes dx (the previous unit's last BN), whose backward
+// sums the final writer of dx computes in its epilogue
+void Plan::block_bwd(BlockL &B, int k, const void *x, const void *dout, void *dx, bool accumulate,
+                     const StatsTarget &dx_stats) {
   const void *out = P(B.out_[k]);
   bn_backward(B.b2, k, dout, P(B.h2[k]), MASK_TENSOR, out, P(B.dh2), 0);
   if (B.proj) bn_backward(B.bp, k, dout, P(B.hp[k]), MASK_TENSOR, out, P(B.dhp), 1);
   conv_bwd_weight(B.c2, P(B.a1[k]), P(B.dh2), false);
-  conv_bwd_data(B.c2, P(B.dh2), P(B.da1), false, nullptr, nullptr);
+  StatsTarget t1;
+  t1.bn = &B.b1;
+  t1.mode = 2;
+  t1.mask = P(B.a1[k]);
+  t1.h = P(B.h1[k]);
+  conv_bwd_data(B.c2, P(B.dh2), P(B.da1), false, nullptr, nullptr, t1);
   bn_backward(B.b1, k, P(B.da1), P(B.h1[k]), MASK_TENSOR, P(B.a1[k]), P(B.dh1), 0);
   conv_bwd_weight(B.c1, x, P(B.dh1), false);
   if (dx) {
     if (B.proj) {
       conv_bwd_data(B.c1, P(B.dh1), dx, accumulate, nullptr, nullptr);
-      conv_bwd_data(B.cp, P(B.dhp), dx, true, nullptr, nullptr);
+      conv_bwd_data(B.cp, P(B.dhp), dx, true, nullptr, nullptr, dx_stats);
     } else {
       // identity skip: dx (+)= dgrad(dh1) + dout * (out > 0)
-      conv_bwd_data(B.c1, P(B.dh1), dx, accumulate, dout, out);
+      conv_bwd_data(B.c1, P(B.dh1), dx, accumulate, dout, out, dx_stats);
     }
   }
   if (B.proj) conv_bwd_weight(B.cp, x, P(B.dhp), false);
@@ -492,7 +573,7 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
     block_fwd(L.mask, k, P(L.u0[k]));
     upsample_fwd(dt, P(L.mask.out_[k]), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.up[k]), u.in.d, u.in.h, u.in.w,
                  L.tab, stream);
-    conv_fwd(L.mc1, P(L.up[k]), P(L.mh[k]));
+    conv_fwd(L.mc1, P(L.up[k]), P(L.mh[k]), nullptr, &L.mbn);
     bn_fwd(L.mbn, k, P(L.mh[k]), nullptr, nullptr, nullptr, true, P(L.r[k]));
     conv_fwd(L.mc2, P(L.r[k]), P(L.m[k]), master(L.bias_idx));
     att_fwd(dt, P(L.m[k]), P(L.trunk.out_[k]), V, C, P(L.out[k]), stream);
@@ -502,6 +583,20 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
              master(net.unit_param_begin[ui] + 1), y + (int64_t)k * mb, dz_scale, 1.0f / (float)Mb,
              (float *)P(L.g[k]), (float *)P(L.dz[k]), (float *)P(off_loss), stream);
   }
+}
+
+// the BN that consumes unit ui's input gradient (the previous unit's dout): the
+// last BN of a local residual block; its backward sums are fused into the conv
+// that writes dout last
+StatsTarget Plan::dout_consumer(int ui, int k) {
+  StatsTarget t;
+  if (ui == 0 || !local[ui - 1] || net.units[ui - 1].kind != U_BLOCK) return t;
+  BlockL &B = units[ui - 1].blk;
+  t.bn = &B.b2;
+  t.mode = 2;
+  t.mask = P(B.out_[k]);
+  t.h = P(B.h2[k]);
+  return t;
 }
 
 // dx target for unit ui's backward: previous unit's dout (local) or the send buffer
@@ -533,14 +628,19 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
     bn_backward(L.stem_bn, k, dy, P(L.stem_h[k]), mode, mt, P(L.tmp1), 0);
     conv_bwd_weight(L.stem_conv, x, P(L.tmp1), true);
   } else if (u.kind == U_BLOCK) {
-    block_bwd(L.blk, k, x, P(L.dout), dx, false);
+    block_bwd(L.blk, k, x, P(L.dout), dx, false, dout_consumer(ui, k));
   } else if (u.kind == U_ATT) {
     const int C = u.cout;
     const int64_t V = (int64_t)mb * u.in.vol();
     att_bwd_finalize(dt, P(L.dout), P(L.m[k]), P(L.trunk.out_[k]), V, C, P(L.dT), P(L.dm), (float *)P(off_partial),
                      counter(), grad(L.bias_idx), stream);
     conv_bwd_weight(L.mc2, P(L.r[k]), P(L.dm), false);
-    conv_bwd_data(L.mc2, P(L.dm), P(L.dr), false, nullptr, nullptr);
+    StatsTarget tm;
+    tm.bn = &L.mbn;
+    tm.mode = 2;
+    tm.mask = P(L.r[k]);
+    tm.h = P(L.mh[k]);
+    conv_bwd_data(L.mc2, P(L.dm), P(L.dr), false, nullptr, nullptr, tm);
     bn_backward(L.mbn, k, P(L.dr), P(L.mh[k]), MASK_TENSOR, P(L.r[k]), P(L.dmh), 0);
     conv_bwd_weight(L.mc1, P(L.up[k]), P(L.dmh), false);
     conv_bwd_data(L.mc1, P(L.dmh), P(L.dup), false, nullptr, nullptr);
@@ -548,7 +648,7 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
     block_bwd(L.mask, k, P(L.u0[k]), P(L.dum), P(L.du0), false);
     maxpool_bwd(dt, P(L.du0), (const uint8_t *)P(L.am[k]), mb, u.in.d, u.in.h, u.in.w, C, u.mask.d, u.mask.h,
                 u.mask.w, dx, false, stream);
-    block_bwd(L.trunk, k, x, P(L.dT), dx, true);
+    block_bwd(L.trunk, k, x, P(L.dT), dx, true, dout_consumer(ui, k));
   } else {
     const int p0 = net.unit_param_begin[ui];
     head_bwd(dt, (const float *)P(L.dz[k]), (const float *)P(L.g[k]), master(p0), mb, (int)u.in.vol(), u.cin,
@@ -861,7 +961,7 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 }
 
 rn_status Plan::set_option(const std::string &k, int64_t v) {
-  if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv")
+  if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv" && k != "fused_stats")
     return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;

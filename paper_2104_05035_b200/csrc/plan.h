@@ -22,6 +22,19 @@ struct BNL {
   int64_t V = 0;       // voxels per micro-batch
   int64_t run_off = 0;
   std::vector<size_t> stat_off;  // per micro-batch: mean, invstd, scale, shift [4][C]
+  // statistics partials fused into the producing convolution's epilogue
+  // (bnstats.cuh): forward (sum h, sum h^2) and backward (sum dy', sum dy' h),
+  // [P][2][C] with P = the producing launch's CTA count (0: not fused)
+  size_t fpart = 0, bpart = 0;
+  int fP = 0, bP = 0;
+};
+
+// where a convolution's epilogue sends the statistics of its output
+struct StatsTarget {
+  BNL *bn = nullptr;
+  int mode = 0;                 // 1 forward, 2 backward
+  const void *mask = nullptr;   // backward: the consumer's ReLU output
+  const void *h = nullptr;      // backward: the consumer's BN input
 };
 
 struct ConvL {
@@ -127,9 +140,12 @@ struct Plan {
   // ops
   bool use_tc(const ConvGeom &g, bool dgrad) const;
   bool use_halo() const;
-  void conv_fwd(const ConvL &c, const void *x, void *y, const float *bias = nullptr);
+  void conv_fwd(const ConvL &c, const void *x, void *y, const float *bias = nullptr, BNL *stats = nullptr);
   void conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumulate, const void *res,
-                     const void *res_mask);
+                     const void *res_mask, const StatsTarget &stats = StatsTarget());
+  bool fused_stats() const;
+  BnFinal bn_final(const BNL &b, int k);
+  StatsTarget dout_consumer(int ui, int k);
   void conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32);
   void bn_forward_stats(const BNL &b, int k, const void *h);
   void bn_fwd(const BNL &b, int k, const void *h, const void *res, const float *rscale, const float *rshift, bool relu,
@@ -137,7 +153,8 @@ struct Plan {
   void bn_backward(const BNL &b, int k, const void *dy, const void *h, int mask_mode, const void *mask_t, void *dx,
                    int slot);
   void block_fwd(BlockL &B, int k, const void *x);
-  void block_bwd(BlockL &B, int k, const void *x, const void *dout, void *dx, bool accumulate);
+  void block_bwd(BlockL &B, int k, const void *x, const void *dout, void *dx, bool accumulate,
+                 const StatsTarget &dx_stats = StatsTarget());
   const void *unit_input(int ui, int k, const float *x_in);
   void *unit_dx_target(int ui);
   void unit_fwd(int ui, int k, const float *x_in, const int32_t *y);

@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "bnstats.cuh"
 #include "kernels.h"
 
 namespace rn {
@@ -12,18 +13,21 @@ namespace rn {
 bool tc_conv_supported(const ConvGeom &g, bool dgrad);
 // ws: fp32 split-K workspace of >= tc_conv_ws_floats(g, dgrad) floats (layers with few tiles)
 size_t tc_conv_ws_floats(const ConvGeom &g, bool dgrad);
-void conv_fprop_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, const float *bias,
-                   __nv_bfloat16 *y, float *ws, size_t ws_floats, cudaStream_t st);
+// est (optional): fused BN statistics of the stored output (bnstats.cuh); the
+// return value is the number of per-CTA partials written, 0 when not fused
+// (split-K or multi-N-block launches, stride-2 dgrad)
+int conv_fprop_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, const float *bias,
+                  __nv_bfloat16 *y, float *ws, size_t ws_floats, cudaStream_t st, const EpiStats *est = nullptr);
 // wd: [Ci][taps][Co] with the tap order flipped (repack_conv's wd)
-void conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dy, const __nv_bfloat16 *wd, __nv_bfloat16 *dx,
-                   bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask, float *ws,
-                   size_t ws_floats, cudaStream_t st);
+int conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dy, const __nv_bfloat16 *wd, __nv_bfloat16 *dx,
+                  bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask, float *ws,
+                  size_t ws_floats, cudaStream_t st, const EpiStats *est = nullptr);
 
 // haloed-A kernel for the 64 -> 64 channel stride-1 3x3x3 convs (k_conv_halo.cu)
 bool halo_conv_supported(const ConvGeom &g, bool dgrad);
-void conv_halo(const ConvGeom &g, bool dgrad, const __nv_bfloat16 *src, const __nv_bfloat16 *w, const float *bias,
-               __nv_bfloat16 *out, bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask,
-               cudaStream_t st);
+int conv_halo(const ConvGeom &g, bool dgrad, const __nv_bfloat16 *src, const __nv_bfloat16 *w, const float *bias,
+              __nv_bfloat16 *out, bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask,
+              cudaStream_t st, const EpiStats *est = nullptr);
 
 // weight gradient dw[co][tap][ci] += sum dy x (fp32 partials in ws, fixed-order reduce)
 bool tc_wgrad_supported(const ConvGeom &g);
