@@ -3,7 +3,8 @@
 // over the layer output of the micro-batch).  Instead of a separate pass that
 // re-reads the conv output, every CTA of the conv reduces the values it stores:
 //   forward  (mode 1): S1 = sum y,   S2 = sum y^2           (y as stored, bf16)
-//   backward (mode 2): S1 = sum dy', S2 = sum dy' * h,  dy' = y * (mask > 0)
+//   backward (mode 2): S1 = sum dy', S2 = sum dy' * (h - mean),  dy' = y * (mask > 0)
+//   (centred by the consumer BN's batch mean: no cancellation in the apply)
 // and writes one fp32 partial [2][C] per CTA; the BN apply kernel reduces the
 // partials in CTA order (deterministic) in fp64 and finalizes.
 #pragma once
@@ -17,6 +18,7 @@ struct EpiStats {
   float *part = nullptr;       // [gridDim.x][2][C]
   const bf16 *mask = nullptr;  // mode 2
   const bf16 *h = nullptr;     // mode 2
+  const float *mean = nullptr; // mode 2: the consumer BN's batch mean per channel
   int mode = 0;                // 0 off, 1 forward, 2 backward
 };
 
@@ -64,7 +66,7 @@ __device__ __forceinline__ void unpack_bf16x8(const uint4 &u, float *v) {
 // the row's prefetched mask / h (mode 2), red = this warp's smem accumulators
 // [2][BN] at channel c0.
 __device__ __forceinline__ void epi_stats_add(const EpiStats &st, const float *f, bool valid, const StatsPf &pf,
-                                              int lane, float *red0, float *red1) {
+                                              int c0, int lane, float *red0, float *red1) {
   float x1[32], x2[32];
   if (st.mode == 1) {
 #pragma unroll
@@ -79,6 +81,14 @@ __device__ __forceinline__ void epi_stats_add(const EpiStats &st, const float *f
     for (int i = 0; i < 4; ++i) {
       unpack_bf16x8(pf.m[i], m + 8 * i);
       unpack_bf16x8(pf.h[i], h + 8 * i);
+    }
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      const float4 mu = __ldg(reinterpret_cast<const float4 *>(st.mean + c0 + j));
+      h[j] -= mu.x;
+      h[j + 1] -= mu.y;
+      h[j + 2] -= mu.z;
+      h[j + 3] -= mu.w;
     }
 #pragma unroll
     for (int j = 0; j < 32; ++j) {

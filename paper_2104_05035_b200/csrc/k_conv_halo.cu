@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_halo_kernel(const __grid_cons
             for (int j = 0; j < 32; j += 8) store_vec(dst + j, f + j);
           }
           if (p.st.mode) {
-            epi_stats_add(p.st, f, valid, pf_cur, lane, red + (q * 2) * 64 + c0, red + (q * 2 + 1) * 64 + c0);
+            epi_stats_add(p.st, f, valid, pf_cur, c0, lane, red + (q * 2) * 64 + c0, red + (q * 2 + 1) * 64 + c0);
             pf_cur = pf_nxt;
           }
         }

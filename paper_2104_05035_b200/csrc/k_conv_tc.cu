@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
           for (int j = 0; j < 32; j += 8) store_vec(dst + j, f + j);
         }
         if (p.st.mode) {
-          epi_stats_add(p.st, f, valid, pf_cur, lane, red + (q * 2) * BN + c0, red + (q * 2 + 1) * BN + c0);
+          epi_stats_add(p.st, f, valid, pf_cur, c0, lane, red + (q * 2) * BN + c0, red + (q * 2 + 1) * BN + c0);
           pf_cur = pf_nxt;
         }
       }

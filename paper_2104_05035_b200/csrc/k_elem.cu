@@ -253,11 +253,12 @@ struct BwdOp {
   }
 };
 
-// BN backward sums in the fused-partials convention: (sum dy', sum dy' h), dy' = dy * (mask > 0)
+// BN backward sums in the fused-partials convention: (sum dy', sum dy' (h - mean)), dy' = dy * (mask > 0)
 template <typename T>
 struct BwdHOp {
   const T *dy, *x, *mask_t;
   int C;
+  const float *mean;
   struct Buf {
     uint4 d, x, m;
   };
@@ -268,7 +269,7 @@ struct BwdHOp {
     b.x = ld16(x + off);
     b.m = ld16(mask_t + off);
   }
-  __device__ void acc(const Buf &b, int64_t, int, float *a1, float *a2) const {
+  __device__ void acc(const Buf &b, int64_t, int c0, float *a1, float *a2) const {
     constexpr int VEC = Vec<T>::N;
     float d[VEC], xv[VEC], m[VEC];
     unpack16(b.d, d, dy);
@@ -278,7 +279,7 @@ struct BwdHOp {
     for (int j = 0; j < VEC; ++j) {
       const float dd = m[j] > 0.f ? d[j] : 0.f;
       a1[j] += dd;
-      a2[j] = fmaf(dd, xv[j], a2[j]);
+      a2[j] = fmaf(dd, xv[j] - mean[c0 + j], a2[j]);
     }
   }
 };
@@ -644,7 +645,7 @@ __global__ void __launch_bounds__(NTA) bn_apply_part_k(const T *__restrict__ x, 
 }
 
 struct BnBwdPart {
-  const float *part;  // [P][2][C]: (sum dy', sum dy' h), dy' = dy * (mask > 0)
+  const float *part;  // [P][2][C]: (sum dy', sum dy' (h - mean)), dy' = dy * (mask > 0)
   int P;
   int64_t V;
   const float *gamma, *mean, *invstd;
@@ -664,7 +665,7 @@ __global__ void __launch_bounds__(NTA) bn_bwd_apply_part_k(const T *__restrict__
   reduce_partials(b.part, b.P, C, sums, scr);
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     const double S1 = sums[c], is = b.invstd[c], mu = b.mean[c];
-    const double S2 = is * (sums[C + c] - mu * S1);  // sum dy' * xhat
+    const double S2 = is * sums[C + c];  // sum dy' * xhat
     const double m1 = S1 / (double)b.V, m2 = S2 / (double)b.V;
     const double A = (double)b.gamma[c] * is;
     cA[c] = (float)A;
@@ -1167,14 +1168,14 @@ int bn_stats_partials(DType dt, const void *x, int64_t V, int C, float *part, cu
   return nblk;
 }
 
-int bn_bwd_partials(DType dt, const void *dy, const void *h, const void *mask_t, int64_t V, int C, float *part,
-                    cudaStream_t st) {
+int bn_bwd_partials(DType dt, const void *dy, const void *h, const void *mask_t, const float *mean, int64_t V, int C,
+                    float *part, cudaStream_t st) {
   const int nblk = chan_fin_blocks(V, C);
   DISPATCH(dt, {
     int64_t rpb;
     size_t smem;
     chan_reduce_dims<T>(V, C, nblk, rpb, smem);
-    BwdHOp<T> op{(const T *)dy, (const T *)h, (const T *)mask_t, C};
+    BwdHOp<T> op{(const T *)dy, (const T *)h, (const T *)mask_t, C, mean};
     launch_k(chan_partials_k<T, BwdHOp<T>>, nblk, NTR, smem, st, op, V, C, part, rpb);
   });
   LAUNCH_CHECK();

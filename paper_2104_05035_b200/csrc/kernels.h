@@ -82,9 +82,9 @@ void bn_apply_fused(DType dt, const void *x, int64_t V, int C, const BnFinal &f,
 // the same partials from a standalone pass over the tensor (layers whose conv
 // could not fuse them: split-K, SIMT); returns P
 int bn_stats_partials(DType dt, const void *x, int64_t V, int C, float *part, cudaStream_t st);
-int bn_bwd_partials(DType dt, const void *dy, const void *h, const void *mask_t, int64_t V, int C, float *part,
-                    cudaStream_t st);
-// BN backward apply fed by partials (sum dy', sum dy' h), dy' = dy * (mask > 0):
+int bn_bwd_partials(DType dt, const void *dy, const void *h, const void *mask_t, const float *mean, int64_t V, int C,
+                    float *part, cudaStream_t st);
+// BN backward apply fed by partials (sum dy', sum dy' (h - mean)), dy' = dy * (mask > 0):
 // dgamma += sum dy' xhat, dbeta += sum dy', dx = BN-backward(dy')
 void bn_bwd_apply_fused(DType dt, const void *dy, const void *h, const void *mask_t, int64_t V, int C,
                         const float *part, int P, const float *gamma, const float *mean, const float *invstd,

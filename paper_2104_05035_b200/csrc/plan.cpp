@@ -391,6 +391,7 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
     es.mode = 2;
     es.mask = (const bf16 *)stats.mask;
     es.h = (const bf16 *)stats.h;
+    es.mean = stats.mean;
   }
   int parts = 0;
   if (use_tc(c.g, true) && use_halo() && halo_conv_supported(c.g, true))
@@ -465,7 +466,7 @@ void Plan::bn_backward(const BNL &b, int k, const void *dy, const void *h, int m
                        void *dx, int slot) {
   if (fused_stats() && mask_mode == MASK_TENSOR) {
     BNL &m = const_cast<BNL &>(b);
-    if (m.bP <= 0) m.bP = bn_bwd_partials(dt, dy, h, mask_t, b.V, b.C, (float *)P(b.bpart), stream);
+    if (m.bP <= 0) m.bP = bn_bwd_partials(dt, dy, h, mask_t, bn_stat(b, k, 0), b.V, b.C, (float *)P(b.bpart), stream);
     bn_bwd_apply_fused(dt, dy, h, mask_t, b.V, b.C, (const float *)P(b.bpart), b.bP, master(b.gamma_idx),
                        bn_stat(b, k, 0), bn_stat(b, k, 1), grad(b.gamma_idx), grad(b.gamma_idx + 1), dx, stream);
     m.bP = 0;  // consumed: the next producer decides again
@@ -516,6 +517,7 @@ void Plan::block_bwd(BlockL &B, int k, const void *x, const void *dout, void *dx
   t1.mode = 2;
   t1.mask = P(B.a1[k]);
   t1.h = P(B.h1[k]);
+  t1.mean = bn_stat(B.b1, k, 0);
   conv_bwd_data(B.c2, P(B.dh2), P(B.da1), false, nullptr, nullptr, t1);
   bn_backward(B.b1, k, P(B.da1), P(B.h1[k]), MASK_TENSOR, P(B.a1[k]), P(B.dh1), 0);
   conv_bwd_weight(B.c1, x, P(B.dh1), false);
@@ -596,6 +598,7 @@ StatsTarget Plan::dout_consumer(int ui, int k) {
   t.mode = 2;
   t.mask = P(B.out_[k]);
   t.h = P(B.h2[k]);
+  t.mean = bn_stat(B.b2, k, 0);
   return t;
 }
 
@@ -640,6 +643,7 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
     tm.mode = 2;
     tm.mask = P(L.r[k]);
     tm.h = P(L.mh[k]);
+    tm.mean = bn_stat(L.mbn, k, 0);
     conv_bwd_data(L.mc2, P(L.dm), P(L.dr), false, nullptr, nullptr, tm);
     bn_backward(L.mbn, k, P(L.dr), P(L.mh[k]), MASK_TENSOR, P(L.r[k]), P(L.dmh), 0);
     conv_bwd_weight(L.mc1, P(L.up[k]), P(L.dmh), false);

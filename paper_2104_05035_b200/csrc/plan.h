@@ -35,6 +35,7 @@ struct StatsTarget {
   int mode = 0;                 // 1 forward, 2 backward
   const void *mask = nullptr;   // backward: the consumer's ReLU output
   const void *h = nullptr;      // backward: the consumer's BN input
+  const float *mean = nullptr;  // backward: the consumer's batch mean
 };
 
 struct ConvL {
