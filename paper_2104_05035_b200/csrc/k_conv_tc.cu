@@ -438,15 +438,17 @@ int run(TcParams &p, int BN, float *ws, size_t ws_floats, const EpiStats *est, c
   // fused statistics need whole-K tiles (no split) covering every output channel
   const bool stats = est && est->mode && p.ksplit == 1 && p.t_nblk == 1;
   if (stats) p.st = *est;
-  // two CTAs per SM (each with its own TMA/MMA pipeline) hide the TMA latency the
-  // small N=64/128 MMAs cannot cover alone; N=256 needs all 512 TMEM columns
-  static const bool occ1 = getenv("RN_TC_OCC1") != nullptr;
+  // The TMA ring must hold ~latency x bandwidth (measured ~1600 cycles x ~85 B/clk
+  // per SM from L2): launches with more work items than SMs run two CTAs per SM
+  // (two rings of 96 KB); launches with at most one item per SM run one CTA with
+  // a 192 KB ring (a 96 KB ring measured latency-bound: 29 us vs ~15 us)
+  const bool one_wave = p.n_tiles * p.ksplit <= 148;
   int grid;
   if (BN == 64) {
-    if (occ1) grid = launch<64, 6>(p, st);
+    if (one_wave) grid = launch<64, 8>(p, st);
     else grid = launch<64, 4>(p, st);
   } else if (BN == 128) {
-    if (occ1) grid = launch<128, 5>(p, st);
+    if (one_wave) grid = launch<128, 6>(p, st);
     else grid = launch<128, 3>(p, st);
   } else {
     grid = launch<256, 4>(p, st);

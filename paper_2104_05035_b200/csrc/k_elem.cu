@@ -259,10 +259,14 @@ struct BwdHOp {
   const T *dy, *x, *mask_t;
   int C;
   const float *mean;
+  float mu[Vec<T>::N];  // this thread's channels (fixed per thread)
   struct Buf {
     uint4 d, x, m;
   };
-  __device__ void init(int) {}
+  __device__ void init(int c0) {
+#pragma unroll
+    for (int j = 0; j < Vec<T>::N; ++j) mu[j] = mean[c0 + j];
+  }
   __device__ void load(int64_t r, int c0, Buf &b) const {
     const int64_t off = r * C + c0;
     b.d = ld16(dy + off);
@@ -279,7 +283,7 @@ struct BwdHOp {
     for (int j = 0; j < VEC; ++j) {
       const float dd = m[j] > 0.f ? d[j] : 0.f;
       a1[j] += dd;
-      a2[j] = fmaf(dd, xv[j] - mean[c0 + j], a2[j]);
+      a2[j] = fmaf(dd, xv[j] - mu[j], a2[j]);
     }
   }
 };
@@ -1175,7 +1179,7 @@ int bn_bwd_partials(DType dt, const void *dy, const void *h, const void *mask_t,
     int64_t rpb;
     size_t smem;
     chan_reduce_dims<T>(V, C, nblk, rpb, smem);
-    BwdHOp<T> op{(const T *)dy, (const T *)h, (const T *)mask_t, C, mean};
+    BwdHOp<T> op{(const T *)dy, (const T *)h, (const T *)mask_t, C, mean, {}};
     launch_k(chan_partials_k<T, BwdHOp<T>>, nblk, NTR, smem, st, op, V, C, part, rpb);
   });
   LAUNCH_CHECK();
