@@ -25,10 +25,14 @@ namespace rn {
 
 namespace {
 
+// part (optional): fused BN statistics of the stored output, [gridDim.x][2][CO] = (sum y, sum y^2)
 template <typename T, int CO>
 __global__ void __launch_bounds__(128) stem_fprop_k(ConvGeom g, const float *__restrict__ x,
-                                                   const float *__restrict__ w, T *__restrict__ y) {
+                                                   const float *__restrict__ w, T *__restrict__ y,
+                                                   float *__restrict__ part) {
   pdl_begin();
+  constexpr int HG = 128 / CO;  // thread groups summing one channel
+  float s1 = 0.f, s2 = 0.f;
   __shared__ __align__(16) float ws[27 * CO];
   for (int i = threadIdx.x; i < 27 * CO; i += blockDim.x) {
     const int co = i % CO, tap = i / CO;
@@ -77,10 +81,33 @@ __global__ void __launch_bounds__(128) stem_fprop_k(ConvGeom g, const float *__r
     __syncthreads();
     constexpr int VE = 16 / sizeof(T);  // elements per 16-B chunk
     const int64_t nvox = min((int64_t)blockDim.x, total - vb);
+    if (part) {  // statistics of the stored (rounded) values, channel t % CO
+      const int c = threadIdx.x % CO;
+      for (int v = threadIdx.x / CO; v < nvox; v += HG) {
+        const float f = to_f(so[v * CO + c]);
+        s1 += f;
+        s2 = fmaf(f, f, s2);
+      }
+    }
     const int nchunk = (int)(nvox * CO / VE);
     for (int i = threadIdx.x; i < nchunk; i += blockDim.x)
       reinterpret_cast<uint4 *>(y + vb * CO)[i] = reinterpret_cast<const uint4 *>(so)[i];
     __syncthreads();
+  }
+  if (part) {
+    __shared__ float r1[128], r2[128];
+    r1[threadIdx.x] = s1;
+    r2[threadIdx.x] = s2;
+    __syncthreads();
+    if (threadIdx.x < CO) {
+      float a = 0.f, b = 0.f;
+      for (int q = 0; q < HG; ++q) {
+        a += r1[q * CO + threadIdx.x];
+        b += r2[q * CO + threadIdx.x];
+      }
+      part[(int64_t)blockIdx.x * 2 * CO + threadIdx.x] = a;
+      part[(int64_t)blockIdx.x * 2 * CO + CO + threadIdx.x] = b;
+    }
   }
 }
 
@@ -237,10 +264,12 @@ __global__ void stem_reduce_k(const float *__restrict__ part, int nblk, int n, f
 }
 
 template <typename T, int CO>
-void stem_fprop_launch(const ConvGeom &g, const float *x, const float *w, void *y, cudaStream_t st) {
+int stem_fprop_launch(const ConvGeom &g, const float *x, const float *w, void *y, float *part, cudaStream_t st) {
   const int64_t total = g.out_vox();
-  const unsigned blocks = (unsigned)std::min<int64_t>((total + 127) / 128, 148 * 16);
-  launch_k(stem_fprop_k<T, CO>, blocks, 128, 0, st, g, x, w, (T *)y);
+  // with fused statistics the grid is the partial count: 4 blocks per SM
+  const unsigned blocks = (unsigned)std::min<int64_t>((total + 127) / 128, part ? 4 * 148 : 148 * 16);
+  launch_k(stem_fprop_k<T, CO>, blocks, 128, 0, st, g, x, w, (T *)y, part);
+  return part ? (int)blocks : 0;
 }
 
 int stem_wgrad_blocks(const ConvGeom &g) {
@@ -267,15 +296,18 @@ bool stem_fast_supported(const ConvGeom &g) {
 
 size_t stem_wgrad_ws_floats(const ConvGeom &g) { return (size_t)stem_wgrad_blocks(g) * g.Co * 27; }
 
-void stem_fprop_fast(DType dt, const ConvGeom &g, const float *x, const float *w, void *y, cudaStream_t st) {
-#define STEM_F(CO)                                                      \
-  if (g.Co == CO) {                                                     \
-    if (dt == DT_F32) stem_fprop_launch<float, CO>(g, x, w, y, st);     \
-    else stem_fprop_launch<bf16, CO>(g, x, w, y, st);                   \
+int stem_fprop_fast(DType dt, const ConvGeom &g, const float *x, const float *w, void *y, cudaStream_t st,
+                    float *part) {
+  int P = 0;
+#define STEM_F(CO)                                                              \
+  if (g.Co == CO) {                                                             \
+    if (dt == DT_F32) P = stem_fprop_launch<float, CO>(g, x, w, y, part, st);   \
+    else P = stem_fprop_launch<bf16, CO>(g, x, w, y, part, st);                 \
   }
   STEM_F(8) STEM_F(16) STEM_F(32) STEM_F(64)
 #undef STEM_F
   LAUNCH_CHECK();
+  return P;
 }
 
 void stem_wgrad_fast(DType dt, const ConvGeom &g, const float *x, const void *dh, float *dw, float *ws,

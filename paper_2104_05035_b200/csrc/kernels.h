@@ -39,7 +39,9 @@ void stem_conv_fprop(DType dt, const ConvGeom &g, const float *x, const float *w
 // k_stem.cu: Co in {8,16,32,64}
 bool stem_fast_supported(const ConvGeom &g);
 size_t stem_wgrad_ws_floats(const ConvGeom &g);
-void stem_fprop_fast(DType dt, const ConvGeom &g, const float *x, const float *w, void *y, cudaStream_t st);
+// part (optional): fused BN statistics partials [P][2][Co] of the stored output; returns P
+int stem_fprop_fast(DType dt, const ConvGeom &g, const float *x, const float *w, void *y, cudaStream_t st,
+                    float *part = nullptr);
 void stem_wgrad_fast(DType dt, const ConvGeom &g, const float *x, const void *dh, float *dw, float *ws,
                      cudaStream_t st);
 
@@ -89,6 +91,10 @@ int bn_bwd_partials(DType dt, const void *dy, const void *h, const void *mask_t,
 void bn_bwd_apply_fused(DType dt, const void *dy, const void *h, const void *mask_t, int64_t V, int C,
                         const float *part, int P, const float *gamma, const float *mean, const float *invstd,
                         float *dgamma, float *dbeta, void *dx, cudaStream_t st);
+// stem tail, bf16 (reading X4): y = maxpool(ReLU(BN(h))) with the BN statistics
+// finalized from the stem conv's partials (f.part, f.P) and published; argmax uint8
+void stem_pool_fwd(const void *h, int N, int D, int H, int W, int C, const BnFinal &f, int64_t V, void *y,
+                   uint8_t *am, int Do, int Ho, int Wo, cudaStream_t st);
 // attention backward + dbias (sum of dm) in one launch
 void att_bwd_finalize(DType dt, const void *dout, const void *m, const void *T_, int64_t V, int C, void *dT, void *dm,
                       float *partial, unsigned *counter, float *dbias, cudaStream_t st);

@@ -40,7 +40,7 @@ void Plan::make_bn(BNL &b, int gamma_idx, int C, int64_t V) {
   b.stat_off.resize(Mb);
   for (int k = 0; k < Mb; ++k) b.stat_off[k] = alloc(4 * sizeof(float) * C);
   if (dt == DT_BF16) {  // up to 2 CTAs per SM in the producing conv
-    b.fpart = alloc(sizeof(float) * 2 * 148 * 2 * C);
+    b.fpart = alloc(sizeof(float) * 4 * 148 * 2 * C);  // up to 4 producer blocks per SM (stem)
     b.bpart = alloc(sizeof(float) * 2 * 148 * 2 * C);
   }
 }
@@ -550,13 +550,19 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
     {
       const bool t = timing();
       size_t e = t ? tk_begin(0, conv_flops(L.stem_conv.g)) : 0;
+      const bool fuse = fused_stats() && u.pool && u.cout % 8 == 0;
       if (stem_fast_supported(L.stem_conv.g))
-        stem_fprop_fast(dt, L.stem_conv.g, (const float *)x, master(L.stem_conv.w_idx), P(L.stem_h[k]), stream);
+        L.stem_bn.fP = stem_fprop_fast(dt, L.stem_conv.g, (const float *)x, master(L.stem_conv.w_idx),
+                                       P(L.stem_h[k]), stream, fuse ? (float *)P(L.stem_bn.fpart) : nullptr);
       else
         stem_conv_fprop(dt, L.stem_conv.g, (const float *)x, master(L.stem_conv.w_idx), P(L.stem_h[k]), stream);
       if (t) tk_end(e);
     }
-    if (u.pool) {
+    if (u.pool && L.stem_bn.fP > 0) {
+      // BN statistics fused into the stem conv; finalize + BN + ReLU + pool in one kernel
+      stem_pool_fwd(P(L.stem_h[k]), mb, u.conv.d, u.conv.h, u.conv.w, u.cout, bn_final(L.stem_bn, k), L.stem_bn.V,
+                    P(L.out[k]), (uint8_t *)P(L.am[k]), u.out.d, u.out.h, u.out.w, stream);
+    } else if (u.pool) {
       bn_forward_stats(L.stem_bn, k, P(L.stem_h[k]));
       maxpool_fwd(dt, P(L.stem_h[k]), mb, u.conv.d, u.conv.h, u.conv.w, u.cout, bn_stat(L.stem_bn, k, 2),
                   bn_stat(L.stem_bn, k, 3), true, P(L.out[k]), (uint8_t *)P(L.am[k]), u.out.d, u.out.h, u.out.w,

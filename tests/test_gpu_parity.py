@@ -188,9 +188,9 @@ def test_cuda_graph_replay_matches_eager():
 def test_fused_bn_statistics_match_separate_pass():
     """BN statistics fused into the conv epilogues (per-CTA partials, finalized
     in the apply kernels) compute what the separate reduction kernels compute.
-    The first fused layer (unit 1's first BN: its input is identical in both
-    modes) must agree to fp32 summation-order level; everything downstream is
-    subject to bf16 re-rounding chaos, so it gets the bf16 bounds."""
+    The first fused layers (stem BN, unit 1's first BN) must agree to fp32
+    summation-order level; everything downstream is subject to bf16 re-rounding
+    chaos, so it gets the bf16 bounds."""
     dims = (91, 109, 91)  # stage 4 = 3x4x3 per sample (BN over 72 values: well conditioned)
     outs = []
     for fused in (1, 0):
@@ -203,9 +203,11 @@ def test_fused_bn_statistics_match_separate_pass():
         plan.backward()
         outs.append((loss, plan.get_grads(), plan.get_bn_running()))
     (m1, v1), (m0, v0) = outs[0][2], outs[1][2]
-    # channels 0..63: stem BN (not fused, identical); 64..127: unit 1's first BN (fused)
-    assert np.array_equal(m1[:64], m0[:64]) and np.array_equal(v1[:64], v0[:64])
-    assert rel(m1[64:128], m0[64:128]) <= 1e-5 and rel(v1[64:128], v0[64:128]) <= 1e-5
+    # channels 0..63: stem BN (statistics fused into the stem conv); 64..127: unit
+    # 1's first BN (fused into its tensor-core conv); their inputs are identical
+    # in both modes up to the stem statistics' summation order
+    assert rel(m1[:64], m0[:64]) <= 1e-5 and rel(v1[:64], v0[:64]) <= 1e-5
+    assert rel(m1[64:128], m0[64:128]) <= 1e-4 and rel(v1[64:128], v0[64:128]) <= 1e-4
     assert abs(outs[0][0] - outs[1][0]) <= 1e-2 * abs(outs[1][0])
     assert rel(v1, v0) <= 2e-2
     # backward: the head gradient depends on the forward only; the BN-backward
