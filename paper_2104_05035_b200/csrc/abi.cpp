@@ -352,7 +352,7 @@ rn_status rn_query(rn_plan_t plan, const char *key, double *value) {
 rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const void *a_dev, const void *b_dev,
                        void *out_dev, int32_t impl, void *stream) {
   GUARD_BEGIN
-  if (!geom || !a_dev || !b_dev || !out_dev || op < 0 || op > 2 || impl < 0 || impl > 3 ||
+  if (!geom || !a_dev || !b_dev || !out_dev || op < 0 || op > 2 || impl < 0 || impl > 4 ||
       (dtype != RN_F32 && dtype != RN_BF16))
     return set_error(RN_ERR_ARG, "rn_op_conv3d: bad arguments");
   ConvGeom g;
@@ -368,7 +368,22 @@ rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const voi
   const bool tc = tc_ok && impl != 1;
   const bool halo_ok = dt == DT_BF16 && op != 2 && halo_conv_supported(g, op == 1);
   if (impl == 3 && !halo_ok) return set_error(RN_ERR_ARG, "rn_op_conv3d: haloed kernel does not take this conv");
-  if ((impl == 3 || impl == 0) && halo_ok) {
+  const bool pair_ok = dt == DT_BF16 && op != 2 && pair_conv_supported(g, op == 1);
+  if (impl == 4 && !pair_ok) return set_error(RN_ERR_ARG, "rn_op_conv3d: CTA-pair kernel does not take this conv");
+  if ((impl == 4 || impl == 0) && pair_ok) {
+    if (op == 0) {
+      conv_pair(g, false, (const bf16 *)a_dev, (const bf16 *)b_dev, nullptr, (bf16 *)out_dev, false, nullptr, nullptr,
+                st);
+    } else {
+      void *wd = nullptr;
+      CUDA_CHECK(cudaMallocAsync(&wd, (size_t)g.Co * g.taps() * g.Ci * 2, st));
+      flip_weights(dt, b_dev, g.Co, g.taps(), g.Ci, wd, st);
+      conv_pair(g, true, (const bf16 *)a_dev, (const bf16 *)wd, nullptr, (bf16 *)out_dev, false, nullptr, nullptr, st);
+      CUDA_CHECK(cudaFreeAsync(wd, st));
+    }
+    return RN_OK;
+  }
+  if (impl == 3 && halo_ok) {
     if (op == 0) {
       conv_halo(g, false, (const bf16 *)a_dev, (const bf16 *)b_dev, nullptr, (bf16 *)out_dev, false, nullptr, nullptr,
                 st);

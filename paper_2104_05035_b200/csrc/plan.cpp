@@ -345,6 +345,11 @@ bool Plan::use_halo() const {
   return it == opts.end() || it->second != 0;
 }
 
+bool Plan::use_pair() const {
+  auto it = opts.find("pair_conv");
+  return it == opts.end() || it->second != 0;
+}
+
 bool Plan::use_tc(const ConvGeom &g, bool dgrad) const {
   if (dt != DT_BF16) return false;
   auto it = opts.find("tc_conv");
@@ -369,7 +374,10 @@ void Plan::conv_fwd(const ConvL &c, const void *x, void *y, const float *bias, B
     es.mode = 1;
   }
   int parts = 0;
-  if (use_tc(c.g, false) && use_halo() && halo_conv_supported(c.g, false))
+  if (use_tc(c.g, false) && use_pair() && pair_conv_supported(c.g, false))
+    parts = conv_pair(c.g, false, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, false,
+                      nullptr, nullptr, stream, want ? &es : nullptr);
+  else if (use_tc(c.g, false) && use_halo() && halo_conv_supported(c.g, false))
     parts = conv_halo(c.g, false, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, false,
                       nullptr, nullptr, stream, want ? &es : nullptr);
   else if (use_tc(c.g, false))
@@ -394,7 +402,10 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
     es.mean = stats.mean;
   }
   int parts = 0;
-  if (use_tc(c.g, true) && use_halo() && halo_conv_supported(c.g, true))
+  if (use_tc(c.g, true) && use_pair() && pair_conv_supported(c.g, true))
+    parts = conv_pair(c.g, true, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx,
+                      accumulate, (const bf16 *)res, (const bf16 *)res_mask, stream, want ? &es : nullptr);
+  else if (use_tc(c.g, true) && use_halo() && halo_conv_supported(c.g, true))
     parts = conv_halo(c.g, true, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx,
                       accumulate, (const bf16 *)res, (const bf16 *)res_mask, stream, want ? &es : nullptr);
   else if (use_tc(c.g, true))
@@ -971,7 +982,8 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 }
 
 rn_status Plan::set_option(const std::string &k, int64_t v) {
-  if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv" && k != "fused_stats")
+  if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv" && k != "fused_stats" &&
+      k != "pair_conv")
     return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;

@@ -29,6 +29,13 @@ int conv_halo(const ConvGeom &g, bool dgrad, const __nv_bfloat16 *src, const __n
               __nv_bfloat16 *out, bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask,
               cudaStream_t st, const EpiStats *est = nullptr);
 
+// CTA-pair kernel (cta_group::2, resident weights) for the same 64 -> 64 stride-1
+// 3x3x3 convs (k_conv_pair.cu); returns the BN-statistics partial count (0: none)
+bool pair_conv_supported(const ConvGeom &g, bool dgrad);
+int conv_pair(const ConvGeom &g, bool dgrad, const __nv_bfloat16 *src, const __nv_bfloat16 *w, const float *bias,
+              __nv_bfloat16 *out, bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask,
+              cudaStream_t st, const EpiStats *est = nullptr);
+
 // weight gradient dw[co][tap][ci] += sum dy x (fp32 partials in ws, fixed-order reduce)
 bool tc_wgrad_supported(const ConvGeom &g);
 size_t tc_wgrad_ws_floats(const ConvGeom &g);

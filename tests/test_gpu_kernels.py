@@ -36,12 +36,12 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-@pytest.mark.parametrize("impl", [3, 2, 1])
+@pytest.mark.parametrize("impl", [4, 3, 2, 1])
 @pytest.mark.parametrize("cv", CONVS, ids=[c[0] for c in CONVS])
 def test_conv_fprop_dgrad(cv, impl):
     name, Di, Hi, Wi, Ci, Co, k, s, p = cv
-    if impl == 3 and not (Ci == 64 and Co == 64 and k == 3 and s == 1):
-        pytest.skip("haloed kernel: 64->64 stride-1 3x3x3 only")
+    if impl in (3, 4) and not (Ci == 64 and Co == 64 and k == 3 and s == 1):
+        pytest.skip("haloed / CTA-pair kernels: 64->64 stride-1 3x3x3 only")
     N = 2
     Do, Ho, Wo = (O.conv_out(v, k, s, p) for v in (Di, Hi, Wi))
     rng = np.random.default_rng(0)
