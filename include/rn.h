@@ -223,6 +223,17 @@ rn_status rn_step(rn_plan_t plan, float lr);
 rn_status rn_train_step_host(rn_plan_t plan, const float *x_host, const int32_t *y_host, float lr,
                              float *loss_host);
 
+/* rn_train_steps_host — n_steps training steps from host inputs (x_host[i],
+ * y_host[i]: step i's batch, same layout as rn_forward's; pinned memory lets
+ * the copies run asynchronously).  The host->device copy of step i+1 runs on a
+ * plan-owned side stream while step i computes (double-buffered staging in the
+ * workspace); losses_host[i] (optional, n_steps floats) receives step i's loss.
+ * Returns when all steps are complete.  Semantics per step = rn_train_step_host.
+ * Errors: RN_ERR_ARG (null inputs), RN_ERR_STATE, RN_ERR_NUMERIC (a non-finite
+ * loss), RN_ERR_CUDA / RN_ERR_NCCL. */
+rn_status rn_train_steps_host(rn_plan_t plan, const float *const *x_host, const int32_t *const *y_host,
+                              int32_t n_steps, float lr, float *losses_host);
+
 /* Introspection for tests/bench: number of GPU kernels launched by this plan so
  * far, and the plan's conv-kernel time accounting. */
 int64_t rn_kernel_launches(rn_plan_t plan);

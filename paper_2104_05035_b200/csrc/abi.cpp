@@ -333,6 +333,24 @@ rn_status rn_train_step_host(rn_plan_t plan, const float *x_host, const int32_t 
   GUARD_END
 }
 
+rn_status rn_train_steps_host(rn_plan_t plan, const float *const *x_host, const int32_t *const *y_host,
+                              int32_t n_steps, float lr, float *losses_host) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  Plan *p = plan->p;
+  if (!p->params_set) return set_error(RN_ERR_STATE, "rn_set_params must precede a step");
+  if (n_steps < 0 || (n_steps > 0 && (!x_host || !y_host))) return set_error(RN_ERR_ARG, "bad step inputs");
+  for (int i = 0; i < n_steps; ++i)
+    if ((p->local[0] && !x_host[i]) || (p->local[p->net.units.size() - 1] && !y_host[i]))
+      return set_error(RN_ERR_ARG, "null host input");
+  p->train_steps_host(x_host, y_host, n_steps, lr, losses_host);
+  if (losses_host)
+    for (int i = 0; i < n_steps; ++i)
+      if (!std::isfinite(losses_host[i])) return set_error(RN_ERR_NUMERIC, "non-finite loss");
+  return RN_OK;
+  GUARD_END
+}
+
 int64_t rn_kernel_launches(rn_plan_t) { return rn::launch_count(); }
 
 rn_status rn_set_option(rn_plan_t plan, const char *key, int64_t value) {

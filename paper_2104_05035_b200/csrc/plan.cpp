@@ -163,6 +163,8 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
   off_sgdrg = alloc(2 * sizeof(int64_t) * (max_sgdrg + 1));
   off_x = alloc(sizeof(float) * (size_t)b * net.units[0].in.vol());
   off_y = alloc(sizeof(int32_t) * (size_t)b);
+  for (int i = 0; i < 2; ++i)  // staging slots of the pipelined host-input loop: x then y
+    off_stage[i] = alloc(sizeof(float) * (size_t)b * net.units[0].in.vol() + 256 + sizeof(int32_t) * (size_t)b);
 
   // --- units ---
   units.resize(nu);
@@ -247,6 +249,12 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
 
 Plan::~Plan() {
   drop_graphs();
+  if (copy_stream) cudaStreamDestroy(copy_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (ev_copied[i]) cudaEventDestroy(ev_copied[i]);
+    if (ev_free[i]) cudaEventDestroy(ev_free[i]);
+  }
+  if (loss_pinned) cudaFreeHost(loss_pinned);
   for (auto &e : ev_pool) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
@@ -973,6 +981,55 @@ void Plan::get_flat(size_t off, float *host) {
 
 // inputs are copied into plan-owned buffers so the step's pointers are fixed
 // (CUDA-graph capturable) and x stays valid for the stem's weight gradient.
+// n training steps from host inputs: step i+1's H2D copy (side stream, into
+// staging slot (i+1)%2) overlaps step i; each step starts with a device-side copy
+// staging -> plan input buffers (the captured graphs keep fixed pointers) and
+// ends with an async copy of its loss into pinned memory.  Every step's inputs
+// still cross PCIe inside the call.
+void Plan::train_steps_host(const float *const *x_host, const int32_t *const *y_host, int n, float lr,
+                            float *losses) {
+  if (n <= 0) return;
+  if (!copy_stream) {
+    CUDA_CHECK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CUDA_CHECK(cudaEventCreateWithFlags(&ev_copied[i], cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming));
+    }
+  }
+  if (loss_pinned_n < n) {
+    if (loss_pinned) CUDA_CHECK(cudaFreeHost(loss_pinned));
+    CUDA_CHECK(cudaMallocHost((void **)&loss_pinned, sizeof(float) * n));
+    loss_pinned_n = n;
+  }
+  const size_t xb = sizeof(float) * (size_t)b * net.units[0].in.vol();
+  const size_t yoff = (xb + 255) / 256 * 256;
+  const bool hx = local[0], hy = local[net.units.size() - 1];
+  auto h2d = [&](int i) {
+    char *slot = (char *)P(off_stage[i % 2]);
+    if (i >= 2) CUDA_CHECK(cudaStreamWaitEvent(copy_stream, ev_free[i % 2], 0));
+    if (hx) CUDA_CHECK(cudaMemcpyAsync(slot, x_host[i], xb, cudaMemcpyHostToDevice, copy_stream));
+    if (hy) CUDA_CHECK(cudaMemcpyAsync(slot + yoff, y_host[i], sizeof(int32_t) * (size_t)b, cudaMemcpyHostToDevice,
+                                       copy_stream));
+    CUDA_CHECK(cudaEventRecord(ev_copied[i % 2], copy_stream));
+  };
+  h2d(0);
+  for (int i = 0; i < n; ++i) {
+    if (i + 1 < n) h2d(i + 1);
+    const char *slot = (const char *)P(off_stage[i % 2]);
+    CUDA_CHECK(cudaStreamWaitEvent(stream, ev_copied[i % 2], 0));
+    if (hx) CUDA_CHECK(cudaMemcpyAsync(P(off_x), slot, xb, cudaMemcpyDeviceToDevice, stream));
+    if (hy) CUDA_CHECK(cudaMemcpyAsync(P(off_y), slot + yoff, sizeof(int32_t) * (size_t)b, cudaMemcpyDeviceToDevice,
+                                       stream));
+    CUDA_CHECK(cudaEventRecord(ev_free[i % 2], stream));
+    forward((const float *)P(off_x), (const int32_t *)P(off_y));
+    backward((const float *)P(off_x));
+    step(lr);
+    CUDA_CHECK(cudaMemcpyAsync(loss_pinned + i, P(off_loss), sizeof(float), cudaMemcpyDeviceToHost, stream));
+  }
+  CUDA_CHECK(cudaStreamSynchronize(stream));
+  if (losses) memcpy(losses, loss_pinned, sizeof(float) * n);
+}
+
 void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
   const cudaMemcpyKind kind = from_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   if (local[0] && x)

@@ -165,6 +165,14 @@ struct Plan {
   // phases
   void bind(void *dev, size_t bytes);
   void stage_inputs(const float *x_dev, const int32_t *y_dev, bool from_host);
+  // pipelined host-input training loop (inputs of step i+1 copied on a side
+  // stream into a staging buffer while step i computes)
+  size_t off_stage[2] = {0, 0};
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  float *loss_pinned = nullptr;
+  int loss_pinned_n = 0;
+  void train_steps_host(const float *const *x_host, const int32_t *const *y_host, int n, float lr, float *losses);
   void forward(const float *x_in, const int32_t *y);
   void backward(const float *x_in);
   void step(float lr);

@@ -18,6 +18,7 @@ STATUS = {0: "RN_OK", 1: "RN_ERR_ARG", 2: "RN_ERR_SCHEMA", 3: "RN_ERR_INFEASIBLE
 EXPORTS = ["rn_ga_default", "rn_gabra_place", "rn_net_units", "rn_net_param_count", "rn_net_param_info",
            "rn_nccl_unique_id", "rn_plan", "rn_plan_describe", "rn_plan_bind", "rn_set_params", "rn_get_params", "rn_get_grads",
            "rn_get_bn_running", "rn_get_activation", "rn_forward", "rn_backward", "rn_step", "rn_train_step_host",
+           "rn_train_steps_host",
            "rn_kernel_launches", "rn_set_option", "rn_query", "rn_op_conv3d", "rn_plan_destroy", "rn_last_error"]
 
 
@@ -212,6 +213,18 @@ class Plan:
         _check(lib().rn_train_step_host(self.h, C.c_void_p(x_host.ctypes.data), C.c_void_p(y_host.ctypes.data),
                                         C.c_float(lr), C.byref(loss)))
         return loss.value
+
+    def train_steps_host(self, xs, ys, lr: float) -> np.ndarray:
+        """len(xs) steps from host batches (pinned numpy views recommended); the
+        copy of batch i+1 overlaps step i.  Returns the per-step losses."""
+        n = len(xs)
+        assert len(ys) == n
+        xp = (C.c_void_p * n)(*[C.c_void_p(x.ctypes.data) for x in xs])
+        yp = (C.c_void_p * n)(*[C.c_void_p(y.ctypes.data) for y in ys])
+        out = np.empty(n, dtype=np.float32)
+        _check(lib().rn_train_steps_host(self.h, xp, yp, C.c_int32(n), C.c_float(lr),
+                                         out.ctypes.data_as(C.POINTER(C.c_float))))
+        return out
 
     def set_option(self, key: str, value: int):
         _check(lib().rn_set_option(self.h, key.encode(), C.c_int64(value)))

@@ -221,3 +221,26 @@ def test_fused_bn_statistics_match_separate_pass():
         idx[name] = slice(off, off + n)
         off += n
     assert rel(g1[idx["u12.fc.weight"]], g0[idx["u12.fc.weight"]]) <= 2e-2
+
+
+def test_pipelined_host_steps_match_single_steps():
+    """rn_train_steps_host (step i+1's H2D overlapped with step i) computes
+    exactly what the same number of rn_train_step_host calls computes."""
+    dims = (40, 48, 40)
+    x, y = synthetic.make_batch(2, *dims, seed=1)
+    x2, y2 = synthetic.make_batch(2, *dims, seed=2)
+    xs = [torch.from_numpy(v).pin_memory().numpy() for v in (x, x2, x)]
+    ys = [torch.from_numpy(v).pin_memory().numpy() for v in (y, y2, y)]
+    outs = []
+    for pipelined in (True, False):
+        st = torch.cuda.Stream()
+        plan = rn.Plan(rn.net_desc(18, 64, dims), 2, rn.RN_BF16, stream=st)
+        arrays = synthetic.init_params(plan.tensors, seed=0)
+        plan.set_params(np.concatenate([a.ravel() for a in arrays]).astype(np.float32))
+        if pipelined:
+            losses = list(plan.train_steps_host(xs, ys, LR))
+        else:
+            losses = [plan.train_step_host(xv, yv, LR) for xv, yv in zip(xs, ys)]
+        outs.append((losses, plan.get_params()))
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][1], outs[1][1])
