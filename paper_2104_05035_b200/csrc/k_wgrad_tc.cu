@@ -144,7 +144,52 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
       }
     }
   } else if (warp == 1) {
-    if (G > 0) {
+    if (G > 0 && p.haloed) {
+      // Haloed x: every descriptor is precomputed — A of M-tile i at K-step j is
+      // dA[i] (the two taps' rows at LBO distance) + goff[j] (the j-th pair of
+      // 8-voxel row groups) + the stage offset; per MMA only an add remains
+      // (the issue loop must sustain one MMA per ~48 cycles)
+      constexpr uint32_t IDESC = tc::idesc_bf16(128, BN, 1, 1);
+      const uint32_t sdy0 = tc::smem_u32(smem), sx0 = sdy0 + DYB;
+      uint64_t dA[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        dA[i] = 0;
+        if (i < G) {
+          const int t0 = p.atom_tap[2 * (mt0 + i)], t1 = p.atom_tap[2 * (mt0 + i) + 1];
+          const int r0 = ((t0 / 9) * p.hh + (t0 / 3) % 3) * p.hw + t0 % 3;
+          const int r1 = ((t1 / 9) * p.hh + (t1 / 3) % 3) * p.hw + t1 % 3;
+          dA[i] = tc::smem_desc(sx0 + r0 * 128, (r1 - r0) * 128, p.hw * 128, 2);
+        }
+      }
+      uint32_t goff[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) goff[j] = (uint32_t)((((2 * j) / p.bh) * p.hh + (2 * j) % p.bh) * p.hw * 8);
+      const uint64_t dB0 = tc::smem_desc(sdy0, 16384, 1024, 2);
+      int stage = 0;
+      uint32_t phase = 0;
+      bool first = true;
+      for (int64_t vt = vt0; vt < vt1; ++vt) {
+        tc::mbar_wait(&full[stage], phase);
+        tc::tc_fence_after();
+        const uint32_t sadd = (uint32_t)(stage * STAGE) >> 4;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i < G) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              tc::mma_bf16_warp(tmem_base + i * BN, dA[i] + sadd + goff[j], dB0 + sadd + j * 128, IDESC,
+                                (first && j == 0) ? 0u : 1u);
+          }
+        }
+        tc::mma_commit_warp(&empty[stage]);
+        __syncwarp();
+        first = false;
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      tc::mma_commit_warp(done);
+      __syncwarp();
+    } else if (G > 0) {
       constexpr uint32_t IDESC = tc::idesc_bf16(128, BN, 1, 1);
       int stage = 0;
       uint32_t phase = 0;
@@ -156,21 +201,9 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
           const uint32_t sdy = tc::smem_u32(smem + stage * STAGE);
           const uint32_t sx = sdy + DYB;
           for (int i = 0; i < G; ++i) {
-            const int a0 = 2 * (mt0 + i), a1 = a0 + 1;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {  // K = 16 voxels = 2 row groups per MMA
-              uint64_t ad;
-              if (p.haloed) {
-                // group g = 2j (+1): h = g % bh, d = g / bh (bw == 8 voxels per group)
-                const int g0 = 2 * j;
-                const int hh = g0 % p.bh, dd = g0 / p.bh;
-                const int t0 = p.atom_tap[a0], t1 = p.atom_tap[a1];
-                const int r0 = ((dd + t0 / 9) * p.hh + hh + (t0 / 3) % 3) * p.hw + t0 % 3;
-                const int r1 = ((dd + t1 / 9) * p.hh + hh + (t1 / 3) % 3) * p.hw + t1 % 3;
-                ad = tc::smem_desc(sx + r0 * 128, (r1 - r0) * 128, p.hw * 128, 2);
-              } else {
-                ad = tc::smem_desc(sx + (2 * i) * 16384 + j * 2048, 16384, 1024, 2);
-              }
+              const uint64_t ad = tc::smem_desc(sx + (2 * i) * 16384 + j * 2048, 16384, 1024, 2);
               const uint64_t bd = tc::smem_desc(sdy + j * 2048, 16384, 1024, 2);
               tc::mma_bf16_warp(tmem_base + i * BN, ad, bd, IDESC, (first && j == 0) ? 0u : 1u);
             }
@@ -280,15 +313,17 @@ void choose_box_wg(int W, int H, int D, int N, int &bw, int &bh, int &bd, int &b
 WgShape wg_shape(const ConvGeom &g) {
   WgShape s;
   s.BN = g.Co % 256 == 0 ? 256 : g.Co % 128 == 0 ? 128 : 64;
-  // haloed staging cuts L2 traffic 9x but measured slower on B200 (MMAs reading
-  // operands from arbitrary row offsets, 252 vs 152 us on the stage-1 shape):
-  // opt-in only (RN_WG_HALO=1) until the MMA-side cost is understood.
-  s.haloed = (g.s == 1 && g.k == 3 && g.Ci == 64 && getenv("RN_WG_HALO")) ? 1 : 0;
+  // haloed staging cuts L2 traffic 9x; its MMAs read operands from arbitrary
+  // row offsets at full speed (tools/micro/tc_probe.cu) — it first measured
+  // slower only because the issue loop recomputed the descriptors with integer
+  // divisions per MMA (now precomputed).  RN_WG_NOHALO=1: per-tap staging.
+  s.haloed = (g.s == 1 && g.k == 3 && g.Ci == 64 && !getenv("RN_WG_NOHALO")) ? 1 : 0;
   const int atoms = g.taps() * (g.Ci / 64);
   s.n_mtiles = (atoms + 1) / 2;
   if (s.haloed) {
     s.bw = 8; s.bh = 4; s.bd = 4; s.bn = 1;
-    s.G = std::min(512 / s.BN, s.n_mtiles);
+    const int groups = (s.n_mtiles + 512 / s.BN - 1) / (512 / s.BN);  // balanced M-groups (14 tiles -> 7 + 7)
+    s.G = (s.n_mtiles + groups - 1) / groups;
   } else {
     choose_box_wg(g.Wo, g.Ho, g.Do, g.N, s.bw, s.bh, s.bd, s.bn);
     const int dyb = (s.BN / 64) * 16;

@@ -133,6 +133,14 @@ int main() {
   run<128, 1>("SW128 MN-major aligned", d, mn);
   Cfg mno = mn; mno.aoff = 128; mno.asbo = 1280;
   run<64, 1>("SW128 MN-major A +1 row (haloed wgrad)", d, mno);
+  Cfg mnh = {2, 128 * 7, 128 * 37, 1280, 16384, 1024, 1, 1, 2560, 2048};
+  run<64, 1>("SW128 MN-major A haloed (+7 rows, LBO 37 rows, SBO 10 rows)", d, mnh);
+  Cfg mnh2 = mnh; mnh2.aoff = 0; mnh2.alo = 128 * 40; mnh2.asbo = 1280;
+  run<64, 1>("SW128 MN-major A (LBO 40 rows, SBO 10 rows)", d, mnh2);
+  Cfg mnh3 = mnh; mnh3.aoff = 0; mnh3.alo = 16384; mnh3.asbo = 1280;
+  run<64, 1>("SW128 MN-major A (LBO 16K, SBO 10 rows)", d, mnh3);
+  Cfg mnh4 = mnh; mnh4.aoff = 128 * 3; mnh4.alo = 16384; mnh4.asbo = 1024;
+  run<64, 1>("SW128 MN-major A (+3 rows, LBO 16K, SBO 8 rows)", d, mnh4);
   Cfg mnn = {0, 16, 160, 180 * 16, 128, 128 * 16, 1, 1, 2 * 160, 256};
   run<64, 1>("NOSWZ MN-major A +16B LBO 160", d, mnn);
   run<128, 1>("NOSWZ MN-major A +16B LBO 160", d, mnn);
