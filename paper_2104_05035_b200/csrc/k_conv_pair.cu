@@ -142,6 +142,10 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
   } else if (warp == 1) {
     if (rank == 0) {
       constexpr uint32_t IDESC = tc::idesc_bf16(256, 64);
+      // precomputed descriptors: A(plane, kh, kw, k) = dA0 + (pl*PLANE_SLOT + (kh*PW+kw)*128 + 32k) >> 4,
+      // B(tap, k) = dB0 + (tap*B_TAP + 32k) >> 4
+      const uint64_t dA0 = tc::smem_desc(tc::smem_u32(sA), 16, PW * 128, 2);
+      const uint64_t dB0 = tc::smem_desc(tc::smem_u32(sB), 16, 1024, 2);
       tc::mbar_wait_cluster(b_full, 0);
       tc::tc_fence_after();
       int local = 0;
@@ -156,20 +160,18 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
               tc::mbar_wait_cluster(&a_full[pl], local & 1);
               tc::tc_fence_after();
             }
-            const uint32_t a0 = tc::smem_u32(sA + pl * PLANE_SLOT);
+            const uint64_t dAp = dA0 + (uint32_t)(pl * PLANE_SLOT >> 4);
+            const uint32_t dtm = tmem_base + acc * 128 + sl * 64;
 #pragma unroll
             for (int kh = 0; kh < 3; ++kh) {
 #pragma unroll
               for (int kw = 0; kw < 3; ++kw) {
                 const int tap = (kd * 3 + kh) * 3 + kw;
-                const uint32_t arow = a0 + (uint32_t)((kh * PW + kw) * 128);
-                const uint32_t b0 = tc::smem_u32(sB + tap * B_TAP);
+                const uint64_t ad = dAp + (uint32_t)((kh * PW + kw) * 8);
+                const uint64_t bd = dB0 + (uint32_t)(tap * (B_TAP >> 4));
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const uint64_t ad = tc::smem_desc(arow + k * 32, 16, PW * 128, 2);
-                  const uint64_t bd = tc::smem_desc(b0 + k * 32, 16, 1024, 2);
-                  tc::mma_bf16_pair(tmem_base + acc * 128 + sl * 64, ad, bd, IDESC, (kd | kh | kw | k) != 0);
-                }
+                for (int k = 0; k < 4; ++k)
+                  tc::mma_bf16_pair(dtm, ad + 2 * k, bd + 2 * k, IDESC, (kd | kh | kw | k) != 0);
               }
             }
             // last uses: plane 0 after (0,0); plane 1 after (1,0); plane 2 after (1,1); plane 3 after (1,2)

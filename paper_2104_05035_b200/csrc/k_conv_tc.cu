@@ -149,7 +149,11 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
+    // descriptors precomputed: stage s, k-step k = base + (s * STAGE + 32 k) >> 4
+    // (the issue loop must sustain one MMA per 32-64 tensor cycles)
     constexpr uint32_t IDESC = tc::idesc_bf16(128, BN);
+    const uint64_t dA0 = tc::smem_desc(tc::smem_u32(smem), 16, 1024, 2);
+    const uint64_t dB0 = tc::smem_desc(tc::smem_u32(smem) + S::A_BYTES, 16, 1024, 2);
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
@@ -161,21 +165,18 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
       tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc::tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
+      uint32_t accum = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
-        {
-          const uint32_t sa = tc::smem_u32(smem + stage * S::STAGE);
-          const uint32_t sb = sa + S::A_BYTES;
+        const uint32_t soff = (uint32_t)(stage * S::STAGE) >> 4;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t ad = tc::smem_desc(sa + k * 32, 16, 1024, 2);
-            const uint64_t bd = tc::smem_desc(sb + k * 32, 16, 1024, 2);
-            tc::mma_bf16_warp(d_tmem, ad, bd, IDESC, (kb != kb0 || k != 0) ? 1u : 0u);
-          }
-          tc::mma_commit_warp(&empty[stage]);
-          if (kb == kb1 - 1) tc::mma_commit_warp(&tfull[acc]);
+        for (int k = 0; k < 4; ++k) {
+          tc::mma_bf16_warp(d_tmem, dA0 + soff + 2 * k, dB0 + soff + 2 * k, IDESC, accum);
+          accum = 1;
         }
+        tc::mma_commit_warp(&empty[stage]);
+        if (kb == kb1 - 1) tc::mma_commit_warp(&tfull[acc]);
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }

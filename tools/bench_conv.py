@@ -17,8 +17,11 @@ CONVS = [("s1_k3", 23, 28, 23, 64, 64, 3, 1, 1), ("s2_k3_s2", 23, 28, 23, 64, 12
          ("att1_mask_k3", 12, 14, 12, 64, 64, 3, 1, 1), ("att1_mconv", 23, 28, 23, 64, 64, 1, 1, 0)]
 ops = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "0,1,2").split(",")]
 impl = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+only = sys.argv[3].split(",") if len(sys.argv) > 3 else None
 N = 8
 for name, Di, Hi, Wi, Ci, Co, k, s, p in CONVS:
+    if only and name not in only:
+        continue
     Do, Ho, Wo = (conv_out(v, k, s, p) for v in (Di, Hi, Wi))
     geom = [N, Di, Hi, Wi, Ci, Do, Ho, Wo, Co, k, s, p]
     x = torch.randn(N, Di, Hi, Wi, Ci, device="cuda").to(torch.bfloat16)
