@@ -598,15 +598,25 @@ __global__ void __launch_bounds__(NTA) bn_apply_part_k(const T *__restrict__ x, 
   double *sums = dsm, *scr = dsm + 2 * C;  // 2C + 2*NTA doubles
   float *fs = (float *)(scr + 2 * NTA);     // sc, sh, rsc, rsh: 4C floats
   float *sc = fs, *sh = fs + C, *rsc = fs + 2 * C, *rsh = fs + 3 * C;
-  bn_part_finalize(b, C, sc, sh, sums, scr);
-  const bool rbn = rb.part != nullptr;
-  if (rbn) bn_part_finalize(rb, C, rsc, rsh, sums, scr);
   constexpr int VEC = Vec<T>::N;
   const int G = C / VEC;
   const int64_t n = V * G;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // multiple of G
   const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int c0 = (int)(i0 % G) * VEC;
+  // the first batch of the stream is in flight while the statistics are finalized
+  uint4 xv[EU], rv[EU];
+#pragma unroll
+  for (int q = 0; q < EU; ++q) {
+    const int64_t k = i0 + q * stride;
+    if (k < n) {
+      xv[q] = ld16(x + k * VEC);
+      if (res) rv[q] = ld16(res + k * VEC);
+    }
+  }
+  bn_part_finalize(b, C, sc, sh, sums, scr);
+  const bool rbn = rb.part != nullptr;
+  if (rbn) bn_part_finalize(rb, C, rsc, rsh, sums, scr);
   float a[VEC], bb[VEC], ra[VEC], rbv[VEC];
 #pragma unroll
   for (int j = 0; j < VEC; ++j) {
@@ -616,13 +626,14 @@ __global__ void __launch_bounds__(NTA) bn_apply_part_k(const T *__restrict__ x, 
     rbv[j] = rbn ? rsh[c0 + j] : 0.f;
   }
   for (int64_t i = i0; i < n; i += EU * stride) {
-    uint4 xv[EU], rv[EU];
+    if (i != i0) {
 #pragma unroll
-    for (int q = 0; q < EU; ++q) {
-      const int64_t k = i + q * stride;
-      if (k < n) {
-        xv[q] = ld16(x + k * VEC);
-        if (res) rv[q] = ld16(res + k * VEC);
+      for (int q = 0; q < EU; ++q) {
+        const int64_t k = i + q * stride;
+        if (k < n) {
+          xv[q] = ld16(x + k * VEC);
+          if (res) rv[q] = ld16(res + k * VEC);
+        }
       }
     }
 #pragma unroll
@@ -666,6 +677,23 @@ __global__ void __launch_bounds__(NTA) bn_bwd_apply_part_k(const T *__restrict__
   double *sums = dsm, *scr = dsm + 2 * C;
   float *fs = (float *)(scr + 2 * NTA);
   float *cA = fs, *cB = fs + C, *cC = fs + 2 * C;
+  constexpr int VEC = Vec<T>::N;
+  const int G = C / VEC;
+  const int64_t n = V * G;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int c0 = (int)(i0 % G) * VEC;
+  // the first batch of the stream is in flight while the coefficients are finalized
+  uint4 dv[EU], xv[EU], mv[EU];
+#pragma unroll
+  for (int q = 0; q < EU; ++q) {
+    const int64_t k = i0 + q * stride;
+    if (k < n) {
+      dv[q] = ld16(dy + k * VEC);
+      xv[q] = ld16(h + k * VEC);
+      mv[q] = ld16(mask_t + k * VEC);
+    }
+  }
   reduce_partials(b.part, b.P, C, sums, scr);
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     const double S1 = sums[c], is = b.invstd[c], mu = b.mean[c];
@@ -681,12 +709,6 @@ __global__ void __launch_bounds__(NTA) bn_bwd_apply_part_k(const T *__restrict__
     }
   }
   __syncthreads();
-  constexpr int VEC = Vec<T>::N;
-  const int G = C / VEC;
-  const int64_t n = V * G;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int c0 = (int)(i0 % G) * VEC;
   float A[VEC], B[VEC], Cc[VEC];
 #pragma unroll
   for (int j = 0; j < VEC; ++j) {
@@ -695,14 +717,15 @@ __global__ void __launch_bounds__(NTA) bn_bwd_apply_part_k(const T *__restrict__
     Cc[j] = cC[c0 + j];
   }
   for (int64_t i = i0; i < n; i += EU * stride) {
-    uint4 dv[EU], xv[EU], mv[EU];
+    if (i != i0) {
 #pragma unroll
-    for (int q = 0; q < EU; ++q) {
-      const int64_t k = i + q * stride;
-      if (k < n) {
-        dv[q] = ld16(dy + k * VEC);
-        xv[q] = ld16(h + k * VEC);
-        mv[q] = ld16(mask_t + k * VEC);
+      for (int q = 0; q < EU; ++q) {
+        const int64_t k = i + q * stride;
+        if (k < n) {
+          dv[q] = ld16(dy + k * VEC);
+          xv[q] = ld16(h + k * VEC);
+          mv[q] = ld16(mask_t + k * VEC);
+        }
       }
     }
 #pragma unroll
@@ -1378,17 +1401,22 @@ void repack_conv(DType dt, const float *w, int Co, int taps, int Ci, void *wf, v
   LAUNCH_CHECK();
 }
 
+constexpr int SGD_MAX_TENSORS = 512;
+
 __global__ void __launch_bounds__(256) sgd_repack_all_k(const ConvPack *__restrict__ tab, int n, int64_t total_tiles,
                                                         float *master, const float *__restrict__ grad, float lr) {
   pdl_begin();
   __shared__ float tile[32][33];
+  __shared__ int64_t t0s[SGD_MAX_TENSORS];  // tile0 of every tensor, searched in smem (not L2)
   const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int i = ty * 32 + tx; i < n; i += 256) t0s[i] = tab[i].tile0;
+  __syncthreads();
   // persistent: blocks stride over the 32x32 (co, ci) tiles of every tap of every conv tensor
   for (int64_t b = blockIdx.x; b < total_tiles; b += gridDim.x) {
     int lo = 0, hi = n - 1;  // tensor of this tile: binary search on tile0 (uniform across the block)
     while (lo < hi) {
       const int mid = (lo + hi + 1) / 2;
-      if (tab[mid].tile0 <= b) lo = mid;
+      if (t0s[mid] <= b) lo = mid;
       else hi = mid - 1;
     }
     const ConvPack t = tab[lo];
@@ -1453,6 +1481,7 @@ __global__ void flip_k(const T *__restrict__ w, int Co, int taps, int Ci, T *__r
 void sgd_repack_all(const ConvPack *table_dev, int n, int64_t total_tiles, float *master, const float *grad, float lr,
                     cudaStream_t st) {
   if (n <= 0 || total_tiles <= 0) return;
+  if (n > SGD_MAX_TENSORS) throw Error(RN_ERR_STATE, "sgd_repack_all: too many conv tensors");
   const unsigned grid = (unsigned)std::min<int64_t>(total_tiles, 148 * 8);
   launch_k(sgd_repack_all_k, grid, dim3(32, 8), 0, st, table_dev, n, total_tiles, master, grad, lr);
   LAUNCH_CHECK();

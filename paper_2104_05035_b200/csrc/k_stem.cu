@@ -15,6 +15,9 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
 
 #include "error.h"
 #include "launch.h"
@@ -254,6 +257,137 @@ __global__ void __launch_bounds__(256) stem_wgrad_warp_k(ConvGeom g, const float
   }
 }
 
+// wgrad on the legacy warp tensor cores (mma.sync m16n8k16, bf16 -> fp32) for the
+// bf16 path: dW[co][tap] = sum_v dh[v][co] * x[v + off(tap)] is a thin GEMM
+// (M = 64 channels, N = 27 taps padded to 32, K = voxels).  dh is bf16 already;
+// the fp32 input is split x = x_hi + x_lo (two bf16, |x - x_hi - x_lo| <= 2^-17 |x|)
+// and both halves go through the MMA, so every product dh*x is formed exactly
+// to ~2^-17 and accumulated in fp32 — the fp32-input reading of the stem.
+// Block = 8 warps over chunks of 256 voxels: dh tile [256][64] (16-B chunks
+// XOR-swizzled by row for conflict-free ldmatrix.trans) and the 27-tap input
+// patches [256][36] fp32 in smem; warp w takes k-steps w and w+8 (16 voxels
+// each): 4 m-tiles x 4 n-tiles x (hi, lo) = 32 MMAs.  Per-block partials are
+// reduced in a fixed order (stem_reduce_k).
+constexpr int SW_CH = 256;     // voxels per chunk
+constexpr int SW_PS = 36;      // patch row stride (floats): conflict-free fragment reads
+constexpr int SW_SMEM = SW_CH * 128 + SW_CH * SW_PS * 4;
+
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo_k, float hi_k) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo_k, hi_k);  // .x (low half) = first k
+  uint32_t u;
+  memcpy(&u, &v, 4);
+  return u;
+}
+
+__global__ void __launch_bounds__(256) stem_wgrad_mma_k(ConvGeom g, const float *__restrict__ x,
+                                                       const bf16 *__restrict__ dh, float *__restrict__ part) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  pdl_begin();
+  uint8_t *sdh = sm;                                  // [256][128 B], chunk c of row v at ((c ^ (v & 7)) * 16)
+  float *sp = reinterpret_cast<float *>(sm + SW_CH * 128);  // [256][36]
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gq = lane >> 2, tq = lane & 3;
+  float acc[4][4][4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[m][n][r] = 0.f;
+  const int64_t total = g.out_vox();
+  for (int64_t v0 = (int64_t)blockIdx.x * SW_CH; v0 < total; v0 += (int64_t)gridDim.x * SW_CH) {
+    __syncthreads();
+    // dh tile: 256 rows x 8 chunks of 16 B
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = t + 256 * j, row = i >> 3, c = i & 7;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (v0 + row < total) v = __ldg(reinterpret_cast<const uint4 *>(dh + (v0 + row) * 64) + c);
+      *reinterpret_cast<uint4 *>(sdh + row * 128 + ((c ^ (row & 7)) << 4)) = v;
+    }
+    // input patches: thread t = voxel v0 + t, its 27 taps (stride-2 stem geometry)
+    {
+      const int64_t vo = v0 + t;
+      float *prow = sp + t * SW_PS;
+      if (vo < total) {
+        int64_t r = vo;
+        const int ow = (int)(r % g.Wo); r /= g.Wo;
+        const int oh = (int)(r % g.Ho); r /= g.Ho;
+        const int od = (int)(r % g.Do); r /= g.Do;
+        const int n = (int)r;
+        const float *xn = x + (int64_t)n * g.Di * g.Hi * g.Wi;
+#pragma unroll
+        for (int tap = 0; tap < 27; ++tap) {
+          const int id = od * g.s + tap / 9 - g.p, ih = oh * g.s + (tap / 3) % 3 - g.p, iw = ow * g.s + tap % 3 - g.p;
+          const bool ok = id >= 0 && id < g.Di && ih >= 0 && ih < g.Hi && iw >= 0 && iw < g.Wi;
+          prow[tap] = ok ? __ldg(xn + ((int64_t)id * g.Hi + ih) * g.Wi + iw) : 0.f;
+        }
+      } else {
+#pragma unroll
+        for (int tap = 0; tap < 27; ++tap) prow[tap] = 0.f;
+      }
+#pragma unroll
+      for (int tap = 27; tap < 32; ++tap) prow[tap] = 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int vb = (warp + 8 * ks) * 16;  // this warp's 16-voxel k-step
+      // A fragments (dh^T: rows co, cols v) via ldmatrix.trans from the [v][co] tile
+      uint32_t a[4][4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int q = lane >> 3, row = vb + (lane & 7) + ((q >> 1) << 3), c = m * 2 + (q & 1);
+        const uint32_t addr = (uint32_t)__cvta_generic_to_shared(sdh + row * 128 + ((c ^ (row & 7)) << 4));
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(a[m][0]), "=r"(a[m][1]), "=r"(a[m][2]), "=r"(a[m][3])
+                     : "r"(addr));
+      }
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {
+        const int col = n * 8 + gq;
+        const float p0 = sp[(vb + 2 * tq) * SW_PS + col], p1 = sp[(vb + 2 * tq + 1) * SW_PS + col];
+        const float p8 = sp[(vb + 2 * tq + 8) * SW_PS + col], p9 = sp[(vb + 2 * tq + 9) * SW_PS + col];
+        const float h0 = __bfloat162float(__float2bfloat16_rn(p0)), h1 = __bfloat162float(__float2bfloat16_rn(p1));
+        const float h8 = __bfloat162float(__float2bfloat16_rn(p8)), h9 = __bfloat162float(__float2bfloat16_rn(p9));
+        const uint32_t bh0 = pack_bf16x2(h0, h1), bh1 = pack_bf16x2(h8, h9);
+        const uint32_t bl0 = pack_bf16x2(p0 - h0, p1 - h1), bl1 = pack_bf16x2(p8 - h8, p9 - h9);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          mma_bf16_16816(acc[m][n], a[m], bh0, bh1);
+          mma_bf16_16816(acc[m][n], a[m], bl0, bl1);
+        }
+      }
+    }
+  }
+  // fixed-order reduction of the 8 warps' 64 x 32 accumulators through smem
+  __syncthreads();
+  float *red = reinterpret_cast<float *>(sm);  // [8 warps][64][32]
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int co = m * 16 + gq + ((r >> 1) << 3), tap = n * 8 + 2 * tq + (r & 1);
+        red[(warp * 64 + co) * 32 + tap] = acc[m][n][r];
+      }
+  __syncthreads();
+  for (int i = t; i < 64 * 27; i += 256) {
+    const int co = i / 27, tap = i % 27;
+    float sum = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sum += red[(w * 64 + co) * 32 + tap];
+    part[(int64_t)blockIdx.x * 64 * 27 + co * 27 + tap] = sum;
+  }
+}
+
 __global__ void stem_reduce_k(const float *__restrict__ part, int nblk, int n, float *__restrict__ dw) {
   pdl_begin();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -279,6 +413,19 @@ int stem_wgrad_blocks(const ConvGeom &g) {
 
 template <typename T, int CO>
 void stem_wgrad_launch(const ConvGeom &g, const float *x, const void *dh, float *dw, float *ws, cudaStream_t st) {
+  if (std::is_same<T, bf16>::value && CO == 64 && !getenv("RN_STEM_SIMT")) {
+    // tensor-core path (bf16 dh): 3 blocks per SM, partials reduced by stem_reduce_k
+    static bool attr = false;
+    if (!attr) {
+      CUDA_CHECK(cudaFuncSetAttribute(stem_wgrad_mma_k, cudaFuncAttributeMaxDynamicSharedMemorySize, SW_SMEM));
+      attr = true;
+    }
+    const int nb = std::min(stem_wgrad_blocks(g), 3 * 148);
+    launch_k(stem_wgrad_mma_k, nb, 256, SW_SMEM, st, g, x, (const bf16 *)dh, ws);
+    LAUNCH_CHECK();
+    launch_k(stem_reduce_k, (CO * 27 + 255) / 256, 256, 0, st, ws, nb, CO * 27, dw);
+    return;
+  }
   // (stem_wgrad_warp_k measured 466 us vs 331 us for the smem-staged kernel on
   // the r18 stem: latency-bound with 16 warps/SM; kept for reference)
   const int nb = stem_wgrad_blocks(g);

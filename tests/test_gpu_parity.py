@@ -244,3 +244,43 @@ def test_pipelined_host_steps_match_single_steps():
         outs.append((losses, plan.get_params()))
     assert outs[0][0] == outs[1][0]
     assert np.array_equal(outs[0][1], outs[1][1])
+
+
+_STEM_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import synthetic
+from paper_2104_05035_b200 import rn
+dims = (40, 48, 40)
+plan = rn.Plan(rn.net_desc(18, 64, dims), 2, rn.RN_BF16)
+arrays = synthetic.perturb_params(plan.tensors, synthetic.init_params(plan.tensors, seed=0))
+plan.set_params(np.concatenate([a.ravel() for a in arrays]).astype(np.float32))
+x, y = synthetic.make_batch(2, *dims, seed=1)
+plan.forward(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+plan.backward()
+np.save({out!r}, plan.get_grads())
+"""
+
+
+def test_stem_wgrad_tensor_cores_match_simt(tmp_path):
+    """The stem weight gradient on mma.sync (bf16 dh x split-bf16 fp32 input) vs
+    the fp32 SIMT kernel on the identical dh (everything upstream is
+    deterministic): equal to fp32 accumulation-order level; all other
+    gradients bitwise equal."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for simt in (0, 1):
+        out = str(tmp_path / f"g{simt}.npy")
+        env = dict(os.environ)
+        if simt:
+            env["RN_STEM_SIMT"] = "1"
+        else:
+            env.pop("RN_STEM_SIMT", None)
+        subprocess.run([sys.executable, "-c", _STEM_SCRIPT.format(root=root, out=out)], check=True, env=env)
+        outs.append(np.load(out))
+    n0 = 64 * 27  # the stem conv weight is the first canonical tensor
+    assert rel(outs[0][:n0], outs[1][:n0]) <= 1e-5
+    assert np.array_equal(outs[0][n0:], outs[1][n0:])
