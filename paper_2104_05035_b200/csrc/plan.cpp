@@ -250,6 +250,9 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
 Plan::~Plan() {
   drop_graphs();
   if (copy_stream) cudaStreamDestroy(copy_stream);
+  if (side) cudaStreamDestroy(side);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   for (int i = 0; i < 2; ++i) {
     if (ev_copied[i]) cudaEventDestroy(ev_copied[i]);
     if (ev_free[i]) cudaEventDestroy(ev_free[i]);
@@ -425,15 +428,33 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
   if (stats.bn) stats.bn->bP = parts;
   if (t) tk_end(e);
 }
+bool Plan::side_on() const {
+  auto it = opts.find("wgrad_stream");
+  const bool on = it == opts.end() || it->second != 0;
+  return on && !timing() && stream != nullptr && stream != cudaStreamLegacy && stream != cudaStreamPerThread;
+}
+
 void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32) {
   const bool t = timing();
   size_t e = t ? tk_begin(2, conv_flops(c.g)) : 0;
+  cudaStream_t ws = stream;
+  if (side_on()) {
+    if (!side) {
+      CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    CUDA_CHECK(cudaEventRecord(ev_fork, stream));  // dy (and x) ready
+    CUDA_CHECK(cudaStreamWaitEvent(side, ev_fork, 0));
+    ws = side;
+    side_used = true;
+  }
   if (x_f32 && stem_fast_supported(c.g))
-    stem_wgrad_fast(dt, c.g, (const float *)x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), stream);
+    stem_wgrad_fast(dt, c.g, (const float *)x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), ws);
   else if (!x_f32 && use_tc(c.g, false) && tc_wgrad_supported(c.g))
-    conv_wgrad_tc(c.g, (const bf16 *)x, (const bf16 *)dy, grad(c.w_idx), (float *)P(off_wgrad_ws), stream);
+    conv_wgrad_tc(c.g, (const bf16 *)x, (const bf16 *)dy, grad(c.w_idx), (float *)P(off_wgrad_ws), ws);
   else
-    conv_wgrad_simt(dt, x_f32, c.g, x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), stream);
+    conv_wgrad_simt(dt, x_f32, c.g, x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), ws);
   if (t) tk_end(e);
 }
 
@@ -804,6 +825,11 @@ void Plan::backward_body(const float *x_in) {
         nccl_send_bytes(pipe_comm, P(units[ui].send_dx), act_bytes(pu.cout, pu.out), unit_stage[ui - 1], stream);
       }
     }
+    if (side_used) {  // join the weight-gradient stream (per micro-batch: temporaries are reused)
+      CUDA_CHECK(cudaEventRecord(ev_join, side));
+      CUDA_CHECK(cudaStreamWaitEvent(stream, ev_join, 0));
+      side_used = false;
+    }
   }
 }
 
@@ -1040,7 +1066,7 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 
 rn_status Plan::set_option(const std::string &k, int64_t v) {
   if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv" && k != "fused_stats" &&
-      k != "pair_conv")
+      k != "pair_conv" && k != "wgrad_stream")
     return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;

@@ -169,6 +169,13 @@ struct Plan {
   // stream into a staging buffer while step i computes)
   size_t off_stage[2] = {0, 0};
   cudaStream_t copy_stream = nullptr;
+  // weight gradients run on a side stream (forked when their dy is ready, joined
+  // at the end of the backward): they are leaves of the backward graph, so they
+  // overlap the dgrad / BN chain and fill its tails (option "wgrad_stream")
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool side_used = false;
+  bool side_on() const;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   float *loss_pinned = nullptr;
   int loss_pinned_n = 0;

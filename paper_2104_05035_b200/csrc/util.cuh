@@ -62,10 +62,10 @@ __device__ __forceinline__ void store8(bf16 *p, const float *v) { store_vec(p, v
 // (no-op when launched without PDL), then allow the successor to launch.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_begin() {
-  pdl_wait();
-  pdl_trigger();
-}
+// (no early trigger: the dependent grid may launch when this one's blocks exit,
+// so its launch latency / prologue overlap this grid's teardown; an early
+// trigger measured slower — dependents squat on SMs the remaining waves need)
+__device__ __forceinline__ void pdl_begin() { pdl_wait(); }
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
