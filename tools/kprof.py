@@ -22,6 +22,8 @@ stream = torch.cuda.Stream()
 plan = rn.Plan(desc, batch, rn.RN_BF16, stream=stream)
 if os.environ.get("KPROF_NOGRAPH"):
     plan.set_option("graphs", 0)
+if os.environ.get("KPROF_NOSIDE"):
+    plan.set_option("wgrad_stream", 0)
 arrays = synthetic.init_params(plan.tensors, seed=0)
 plan.set_params(np.concatenate([a.ravel() for a in arrays]).astype(np.float32))
 x, y = synthetic.make_batch(batch, *dims, seed=1)
