@@ -1406,12 +1406,14 @@ constexpr int SGD_MAX_TENSORS = 512;
 __global__ void __launch_bounds__(256) sgd_repack_all_k(const ConvPack *__restrict__ tab, int n, int64_t total_tiles,
                                                         float *master, const float *__restrict__ grad, float lr) {
   pdl_begin();
-  __shared__ float tile[32][33];
+  __shared__ float tile[64][65];
   __shared__ int64_t t0s[SGD_MAX_TENSORS];  // tile0 of every tensor, searched in smem (not L2)
   const int tx = threadIdx.x, ty = threadIdx.y;
   for (int i = ty * 32 + tx; i < n; i += 256) t0s[i] = tab[i].tile0;
   __syncthreads();
-  // persistent: blocks stride over the 32x32 (co, ci) tiles of every tap of every conv tensor
+  // persistent: blocks stride over the 64x64 (co, ci) tiles of every tap of every conv tensor;
+  // a thread owns two consecutive ci of 8 rows: 128-B rows for the fp32 loads and
+  // for both bf16 copies (the transposed one through smem)
   for (int64_t b = blockIdx.x; b < total_tiles; b += gridDim.x) {
     int lo = 0, hi = n - 1;  // tensor of this tile: binary search on tile0 (uniform across the block)
     while (lo < hi) {
@@ -1421,40 +1423,76 @@ __global__ void __launch_bounds__(256) sgd_repack_all_k(const ConvPack *__restri
     }
     const ConvPack t = tab[lo];
     int64_t r = b - t.tile0;
-    const int nci = (t.Ci + 31) / 32, nco = (t.Co + 31) / 32;
+    const int nci = (t.Ci + 63) / 64, nco = (t.Co + 63) / 64;
     const int cit = (int)(r % nci); r /= nci;
     const int cot = (int)(r % nco); r /= nco;
     const int tap = (int)r;
-    const int ci0 = cit * 32, co0 = cot * 32;
+    const int ci0 = cit * 64, co0 = cot * 64;
     float *w = master + t.off;
     const float *g = grad ? grad + t.off : nullptr;
     bf16 *wf = (bf16 *)t.wf, *wd = (bf16 *)t.wd;
-    float v[4], gv[4];
-    int64_t idx[4];
-    bool ok[4];
+    const int ci = ci0 + 2 * tx;
+    const bool pair = ci + 1 < t.Ci && ((t.Ci & 1) == 0);  // float2 path (every r18 conv but the 1-channel stem)
+    float v[8][2], gv[8][2];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {  // all loads first
-      const int co = co0 + ty + 8 * q, ci = ci0 + tx;
-      ok[q] = co < t.Co && ci < t.Ci;
-      idx[q] = ((int64_t)co * t.taps + tap) * t.Ci + ci;
-      v[q] = ok[q] ? w[idx[q]] : 0.f;
-      gv[q] = ok[q] && g ? g[idx[q]] : 0.f;
+    for (int q = 0; q < 8; ++q) {  // all loads first
+      const int co = co0 + ty + 8 * q;
+      const int64_t i0 = ((int64_t)co * t.taps + tap) * t.Ci + ci;
+      v[q][0] = v[q][1] = gv[q][0] = gv[q][1] = 0.f;
+      if (co < t.Co && pair) {
+        const float2 a = *reinterpret_cast<const float2 *>(w + i0);
+        v[q][0] = a.x;
+        v[q][1] = a.y;
+        if (g) {
+          const float2 c = *reinterpret_cast<const float2 *>(g + i0);
+          gv[q][0] = c.x;
+          gv[q][1] = c.y;
+        }
+      } else if (co < t.Co) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (ci + e < t.Ci) {
+            v[q][e] = w[i0 + e];
+            if (g) gv[q][e] = g[i0 + e];
+          }
+      }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (g) v[q] -= lr * gv[q];
-      if (ok[q]) {
-        if (g) w[idx[q]] = v[q];
-        wf[idx[q]] = __float2bfloat16_rn(v[q]);
+    for (int q = 0; q < 8; ++q) {
+      const int co = co0 + ty + 8 * q;
+      const int64_t i0 = ((int64_t)co * t.taps + tap) * t.Ci + ci;
+      if (g) {
+        v[q][0] -= lr * gv[q][0];
+        v[q][1] -= lr * gv[q][1];
       }
-      tile[ty + 8 * q][tx] = v[q];
+      if (co < t.Co && pair) {
+        if (g) *reinterpret_cast<float2 *>(w + i0) = make_float2(v[q][0], v[q][1]);
+        *reinterpret_cast<__nv_bfloat162 *>(wf + i0) = __floats2bfloat162_rn(v[q][0], v[q][1]);
+      } else if (co < t.Co) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (ci + e < t.Ci) {
+            if (g) w[i0 + e] = v[q][e];
+            wf[i0 + e] = __float2bfloat16_rn(v[q][e]);
+          }
+      }
+      tile[ty + 8 * q][2 * tx] = v[q][0];
+      tile[ty + 8 * q][2 * tx + 1] = v[q][1];
     }
     __syncthreads();
+    const int co = co0 + 2 * tx;
+    const bool cpair = co + 1 < t.Co && ((t.Co & 1) == 0);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int ci = ci0 + ty + 8 * q, co = co0 + tx;
-      if (co < t.Co && ci < t.Ci)
-        wd[((int64_t)ci * t.taps + (t.taps - 1 - tap)) * t.Co + co] = __float2bfloat16_rn(tile[tx][ty + 8 * q]);
+    for (int q = 0; q < 8; ++q) {
+      const int cil = ty + 8 * q, cir = ci0 + cil;
+      if (cir >= t.Ci) continue;
+      bf16 *dst = wd + ((int64_t)cir * t.taps + (t.taps - 1 - tap)) * t.Co + co;
+      if (cpair) {
+        *reinterpret_cast<__nv_bfloat162 *>(dst) = __floats2bfloat162_rn(tile[2 * tx][cil], tile[2 * tx + 1][cil]);
+      } else {
+        if (co < t.Co) dst[0] = __float2bfloat16_rn(tile[2 * tx][cil]);
+        if (co + 1 < t.Co) dst[1] = __float2bfloat16_rn(tile[2 * tx + 1][cil]);
+      }
     }
     __syncthreads();
   }

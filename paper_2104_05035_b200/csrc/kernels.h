@@ -131,7 +131,7 @@ void sgd_update(float *w, const float *g, int64_t n, float lr, cudaStream_t st);
 // wf[co][tap][ci] = w, wd[ci][taps-1-tap][co] = w  (either may be null)
 void repack_conv(DType dt, const float *w, int Co, int taps, int Ci, void *wf, void *wd, cudaStream_t st);
 // One launch for every conv tensor of the plan: w -= lr * g (g may be null: repack only),
-// then the bf16 forward copy wf and the flipped transposed dgrad copy wd (32x32 tiles per tap).
+// then the bf16 forward copy wf and the flipped transposed dgrad copy wd (64x64 tiles per tap).
 struct ConvPack {
   int64_t off;    // offset of the tensor in the master / gradient arrays
   int64_t tile0;  // first tile index of this tensor in the launch

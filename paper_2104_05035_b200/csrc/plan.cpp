@@ -940,7 +940,7 @@ void Plan::bind(void *dev, size_t bytes) {
       c.pad = 0;
       c.wf = P(shadow_f[i]);
       c.wd = P(shadow_d[i]);
-      tiles += (int64_t)c.taps * ((c.Co + 31) / 32) * ((c.Ci + 31) / 32);
+      tiles += (int64_t)c.taps * ((c.Co + 63) / 64) * ((c.Ci + 63) / 64);  // 64x64 tiles (sgd_repack_all_k)
       packs.push_back(c);
     } else {
       if (!rg.empty() && rg.back() == t.canon_off) rg.back() = t.canon_off + t.numel;
