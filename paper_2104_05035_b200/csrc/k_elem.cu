@@ -987,6 +987,78 @@ __global__ void __launch_bounds__(NT) maxpool_bwd_k(const T *__restrict__ dy, co
   }
 }
 
+// bf16 gather-form adjoint with the pooled rows staged in smem: a block owns the
+// input rows ih = 2j, 2j+1 of one (n, id) plane; both need only pooled rows
+// oh = j, j+1 of od = id/2 (and (id+1)/2 for odd id), so <= 4 pooled rows of dy
+// and argmax codes are loaded once (coalesced 16-B vectors) and every candidate
+// window is then read from smem.  Same candidate order / arithmetic as maxpool_bwd_k.
+__global__ void __launch_bounds__(256) maxpool_bwd_stage_k(const bf16 *__restrict__ dy,
+                                                           const uint8_t *__restrict__ am, int N, int D, int H,
+                                                           int W, int C, int Do, int Ho, int Wo,
+                                                           bf16 *__restrict__ dx, int accumulate) {
+  extern __shared__ __align__(16) uint8_t smp[];
+  pdl_begin();
+  const int rowel = Wo * C;                  // elements of one pooled row
+  bf16 *sdy = reinterpret_cast<bf16 *>(smp);  // [4][Wo][C]
+  uint8_t *sam = smp + 4 * rowel * 2;         // [4][Wo][C]
+  const int Hj = (H + 1) / 2;
+  const int j = blockIdx.x % Hj, id = (blockIdx.x / Hj) % D, nn = blockIdx.x / (Hj * D);
+  const int od0 = id >> 1, od1 = (id & 1) && ((id + 1) >> 1) < Do ? (id + 1) >> 1 : -1;
+  // stage pooled rows slot = sd*2 + sh (od0/od1 x oh j/j+1)
+  const int vecs = rowel / 8;
+  for (int i = threadIdx.x; i < 4 * vecs; i += blockDim.x) {
+    const int slot = i / vecs, e = (i - slot * vecs) * 8;
+    const int od = (slot >> 1) ? od1 : od0, oh = j + (slot & 1);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    uint2 a = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // no code matches 255
+    if (od >= 0 && oh < Ho) {
+      const int64_t o = ((int64_t)(nn * Do + od) * Ho + oh) * rowel + e;
+      v = ld16(dy + o);
+      a = *reinterpret_cast<const uint2 *>(am + o);
+    }
+    *reinterpret_cast<uint4 *>(sdy + slot * rowel + e) = v;
+    *reinterpret_cast<uint2 *>(sam + slot * rowel + e) = a;
+  }
+  __syncthreads();
+  const int G = C / 8;
+  const int items = 2 * W * G;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int r = it / (W * G), rem = it - r * W * G, iw = rem / G, c0 = (rem - iw * G) * 8;
+    const int ih = 2 * j + r;
+    if (ih >= H) continue;
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int od = (q & 4) ? od1 : od0;
+      const int oh = (ih + (q >> 1 & 1)) >> 1, ow = (iw + (q & 1)) >> 1;
+      const bool ok = od >= 0 && oh < Ho && ow < Wo && (!(q & 4) || (id & 1)) && (!(q & 2) || (ih & 1)) &&
+                      (!(q & 1) || (iw & 1));
+      if (!ok) continue;
+      const int slot = ((q & 4) ? 2 : 0) + (oh - j);
+      const int tap = ((id - 2 * od + 1) * 3 + (ih - 2 * oh + 1)) * 3 + (iw - 2 * ow + 1);
+      const int e0 = slot * rowel + ow * C + c0;
+      float f[8];
+      load_vec(sdy + e0, f);
+      uint8_t code[8];
+      const uint2 a = *reinterpret_cast<const uint2 *>(sam + e0);
+      memcpy(code, &a, 8);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (code[e] == tap) acc[e] += f[e];
+    }
+    const int64_t o = (((int64_t)(nn * D + id) * H + ih) * W + iw) * C + c0;
+    if (accumulate) {
+      float pv[8];
+      load_vec(dx + o, pv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += pv[e];
+    }
+    store_vec(dx + o, acc);
+  }
+}
+
 template <typename T>
 __global__ void upsample_fwd_k(const T *__restrict__ x, int N, int Di, int Hi, int Wi, int C, T *__restrict__ y,
                                int Do, int Ho, int Wo, UpTables t) {
@@ -1348,6 +1420,13 @@ void maxpool_fwd(DType dt, const void *x, int N, int D, int H, int W, int C, con
 
 void maxpool_bwd(DType dt, const void *dy, const uint8_t *argmax, int N, int D, int H, int W, int C, int Do, int Ho,
                  int Wo, void *dx, bool accumulate, cudaStream_t st) {
+  const size_t smem = (size_t)4 * Wo * C * 3;
+  if (dt == DT_BF16 && C % 8 == 0 && smem <= 48 * 1024) {
+    launch_k(maxpool_bwd_stage_k, (unsigned)(N * D * ((H + 1) / 2)), 256, smem, st, (const bf16 *)dy, argmax, N, D, H,
+             W, C, Do, Ho, Wo, (bf16 *)dx, accumulate ? 1 : 0);
+    LAUNCH_CHECK();
+    return;
+  }
   DISPATCH(dt, launch_k(maxpool_bwd_k<T>, (unsigned)(N * D * H), NT, 0, st, 
                    (const T *)dy, argmax, N, D, H, W, C, Do, Ho, Wo, (T *)dx, accumulate ? 1 : 0));
   LAUNCH_CHECK();
