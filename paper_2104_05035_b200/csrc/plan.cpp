@@ -345,11 +345,15 @@ size_t Plan::tk_begin(int cls, double flops) {
   EvPair &e = ev_pool[ev_used];
   e.flops = flops;
   e.cls = cls;
+  e.kind = -1;
   CUDA_CHECK(cudaEventRecord(e.a, stream));
   return ev_used++;
 }
 
-void Plan::tk_end(size_t i) { CUDA_CHECK(cudaEventRecord(ev_pool[i].b, stream)); }
+void Plan::tk_end(size_t i, int kind) {
+  ev_pool[i].kind = kind;
+  CUDA_CHECK(cudaEventRecord(ev_pool[i].b, stream));
+}
 
 bool Plan::use_halo() const {
   auto it = opts.find("halo_conv");
@@ -384,20 +388,20 @@ void Plan::conv_fwd(const ConvL &c, const void *x, void *y, const float *bias, B
     es.part = (float *)P(stats->fpart);
     es.mode = 1;
   }
-  int parts = 0;
-  if (use_tc(c.g, false) && use_pair() && pair_conv_supported(c.g, false))
+  int parts = 0, kind = K_SIMT;
+  if (use_tc(c.g, false) && use_pair() && pair_conv_supported(c.g, false) && (kind = K_PAIR))
     parts = conv_pair(c.g, false, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, false,
                       nullptr, nullptr, stream, want ? &es : nullptr);
-  else if (use_tc(c.g, false) && use_halo() && halo_conv_supported(c.g, false))
+  else if (use_tc(c.g, false) && use_halo() && halo_conv_supported(c.g, false) && (kind = K_HALO))
     parts = conv_halo(c.g, false, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, false,
                       nullptr, nullptr, stream, want ? &es : nullptr);
-  else if (use_tc(c.g, false))
+  else if (use_tc(c.g, false) && (kind = K_TC))
     parts = conv_fprop_tc(c.g, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y,
                           (float *)P(off_conv_ws), conv_ws_floats, stream, want ? &es : nullptr);
   else
     conv_fprop_simt(dt, c.g, x, wfwd(c.w_idx), bias, y, stream);
   if (stats) stats->fP = parts;
-  if (t) tk_end(e);
+  if (t) tk_end(e, kind);
 }
 void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumulate, const void *res,
                          const void *res_mask, const StatsTarget &stats) {
@@ -412,21 +416,21 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
     es.h = (const bf16 *)stats.h;
     es.mean = stats.mean;
   }
-  int parts = 0;
-  if (use_tc(c.g, true) && use_pair() && pair_conv_supported(c.g, true))
+  int parts = 0, kind = K_SIMT;
+  if (use_tc(c.g, true) && use_pair() && pair_conv_supported(c.g, true) && (kind = K_PAIR))
     parts = conv_pair(c.g, true, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx,
                       accumulate, (const bf16 *)res, (const bf16 *)res_mask, stream, want ? &es : nullptr);
-  else if (use_tc(c.g, true) && use_halo() && halo_conv_supported(c.g, true))
+  else if (use_tc(c.g, true) && use_halo() && halo_conv_supported(c.g, true) && (kind = K_HALO))
     parts = conv_halo(c.g, true, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx,
                       accumulate, (const bf16 *)res, (const bf16 *)res_mask, stream, want ? &es : nullptr);
-  else if (use_tc(c.g, true))
+  else if (use_tc(c.g, true) && (kind = K_TC))
     parts = conv_dgrad_tc(c.g, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), (bf16 *)dx, accumulate,
                           (const bf16 *)res, (const bf16 *)res_mask, (float *)P(off_conv_ws), conv_ws_floats, stream,
                           want ? &es : nullptr);
   else
     conv_dgrad_simt(dt, c.g, dy, wfwd(c.w_idx), dx, accumulate, res, res_mask, stream);
   if (stats.bn) stats.bn->bP = parts;
-  if (t) tk_end(e);
+  if (t) tk_end(e, kind);
 }
 bool Plan::side_on() const {
   auto it = opts.find("wgrad_stream");
@@ -449,13 +453,17 @@ void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x
     ws = side;
     side_used = true;
   }
-  if (x_f32 && stem_fast_supported(c.g))
+  int kind = K_SIMT;
+  if (x_f32 && stem_fast_supported(c.g)) {
+    kind = K_STEM;
     stem_wgrad_fast(dt, c.g, (const float *)x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), ws);
-  else if (!x_f32 && use_tc(c.g, false) && tc_wgrad_supported(c.g))
+  } else if (!x_f32 && use_tc(c.g, false) && tc_wgrad_supported(c.g)) {
+    kind = K_WGRAD;
     conv_wgrad_tc(c.g, (const bf16 *)x, (const bf16 *)dy, grad(c.w_idx), (float *)P(off_wgrad_ws), ws);
-  else
+  } else {
     conv_wgrad_simt(dt, x_f32, c.g, x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), ws);
-  if (t) tk_end(e);
+  }
+  if (t) tk_end(e, kind);
 }
 
 float *Plan::bn_stat(const BNL &b, int k, int which) { return (float *)P(b.stat_off[k]) + which * b.C; }
@@ -596,7 +604,7 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
                                        P(L.stem_h[k]), stream, fuse ? (float *)P(L.stem_bn.fpart) : nullptr);
       else
         stem_conv_fprop(dt, L.stem_conv.g, (const float *)x, master(L.stem_conv.w_idx), P(L.stem_h[k]), stream);
-      if (t) tk_end(e);
+      if (t) tk_end(e, K_STEM);
     }
     if (u.pool && L.stem_bn.fP > 0) {
       // BN statistics fused into the stem conv; finalize + BN + ReLU + pool in one kernel
@@ -790,6 +798,7 @@ void Plan::step(float lr) {
 }
 
 void Plan::forward_body(const float *x_in, const int32_t *y) {
+  if (timing()) ev_used = 0;  // a step's conv events: this forward + its backward (eager launches)
   CUDA_CHECK(cudaMemsetAsync(P(off_loss), 0, sizeof(float), stream));
   const int nu = (int)net.units.size();
   for (int k = 0; k < Mb; ++k) {
@@ -1078,13 +1087,18 @@ rn_status Plan::query(const std::string &k, double *v) {
   if (k.rfind("conv_", 0) == 0) {
     // conv_ms / conv_flops / conv_launches, optionally suffixed _fprop/_dgrad/_wgrad
     CUDA_CHECK(cudaStreamSynchronize(stream));
-    int cls = -1;
+    int cls = -1, kind = -1;
     if (k.find("_fprop") != std::string::npos) cls = 0;
     if (k.find("_dgrad") != std::string::npos) cls = 1;
     if (k.find("_wgrad") != std::string::npos) cls = 2;
+    if (k.find("_pair") != std::string::npos) kind = K_PAIR;
+    if (k.find("_tcconv") != std::string::npos) kind = K_TC;
+    if (k.find("_tcwgrad") != std::string::npos) kind = K_WGRAD;
+    if (k.find("_stem") != std::string::npos) kind = K_STEM;
     double ms = 0, fl = 0, n = 0;
     for (size_t i = 0; i < ev_used; ++i) {
       if (cls >= 0 && ev_pool[i].cls != cls) continue;
+      if (kind >= 0 && ev_pool[i].kind != kind) continue;
       float e = 0.f;
       CUDA_CHECK(cudaEventElapsedTime(&e, ev_pool[i].a, ev_pool[i].b));
       ms += e;

@@ -212,13 +212,15 @@ struct Plan {
   struct EvPair {
     cudaEvent_t a, b;
     double flops;
-    int cls;  // 0 fprop, 1 dgrad, 2 wgrad
+    int cls;   // 0 fprop, 1 dgrad, 2 wgrad
+    int kind;  // kernel family (K_*)
   };
+  enum { K_SIMT = 0, K_PAIR = 1, K_TC = 2, K_HALO = 3, K_WGRAD = 4, K_STEM = 5 };
   std::vector<EvPair> ev_pool;
   size_t ev_used = 0;
   bool timing() const;
   size_t tk_begin(int cls, double flops);
-  void tk_end(size_t i);
+  void tk_end(size_t i, int kind);
 };
 
 }  // namespace rn
