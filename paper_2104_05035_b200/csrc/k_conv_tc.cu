@@ -369,14 +369,26 @@ int launch(const TcParams &p, cudaStream_t st) {
 }
 
 // split-K finish: out = sum_s part[s] (+bias) (+existing) (+res*(mask>0)), bf16 store through the view
-__global__ void splitk_finish_k(const float *__restrict__ part, int ks, int64_t nvv, int ych, int OW, int OH, int OD,
-                                bf16 *__restrict__ y, int64_t s_n, int64_t s_d, int64_t s_h, int64_t s_w,
-                                const float *__restrict__ bias, int accumulate, const bf16 *__restrict__ res,
-                                const bf16 *__restrict__ res_mask) {
+// split-K finish: out = sum_s part[s] (+bias) (+existing) (+res*(mask>0)), bf16 store
+// through the view; the partials of 8 splits are loaded per batch (summed in split
+// order).  With statistics (st.mode) each thread keeps a fixed 8-channel group (the
+// grid stride is a multiple of ych/8) and the block writes one BN-statistics
+// partial [2][ych] of the values it stored (fixed-order smem reduction).
+__global__ void __launch_bounds__(512) splitk_finish_k(const float *__restrict__ part, int ks, int64_t nvv, int ych,
+                                                       int OW, int OH, int OD, bf16 *__restrict__ y, int64_t s_n,
+                                                       int64_t s_d, int64_t s_h, int64_t s_w,
+                                                       const float *__restrict__ bias, int accumulate,
+                                                       const bf16 *__restrict__ res,
+                                                       const bf16 *__restrict__ res_mask, EpiStats st) {
+  extern __shared__ float fred[];  // [2][blockDim][8] when st.mode
   pdl_begin();
   const int G = ych / 8;
   const int64_t n = nvv * G;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  float a1[8], a2[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a1[j] = a2[j] = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const int c0 = (int)(i % G) * 8;
     const int64_t vidx = i / G;
     int64_t r = vidx;
@@ -387,12 +399,21 @@ __global__ void splitk_finish_k(const float *__restrict__ part, int ks, int64_t 
     float f[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) f[j] = 0.f;
-    for (int s = 0; s < ks; ++s) {
-      const float *src = part + ((int64_t)s * nvv + vidx) * ych + c0;
-      const float4 a = *reinterpret_cast<const float4 *>(src);
-      const float4 b = *reinterpret_cast<const float4 *>(src + 4);
-      f[0] += a.x; f[1] += a.y; f[2] += a.z; f[3] += a.w;
-      f[4] += b.x; f[5] += b.y; f[6] += b.z; f[7] += b.w;
+    for (int s0 = 0; s0 < ks; s0 += 8) {
+      float4 a[8], b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (s0 + u < ks) {
+          const float *src = part + ((int64_t)(s0 + u) * nvv + vidx) * ych + c0;
+          a[u] = *reinterpret_cast<const float4 *>(src);
+          b[u] = *reinterpret_cast<const float4 *>(src + 4);
+        }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (s0 + u < ks) {
+          f[0] += a[u].x; f[1] += a[u].y; f[2] += a[u].z; f[3] += a[u].w;
+          f[4] += b[u].x; f[5] += b[u].y; f[6] += b[u].z; f[7] += b[u].w;
+        }
     }
     if (bias)
 #pragma unroll
@@ -412,6 +433,42 @@ __global__ void splitk_finish_k(const float *__restrict__ part, int ks, int64_t 
       for (int j = 0; j < 8; ++j) f[j] += mv[j] > 0.f ? rv[j] : 0.f;
     }
     store_vec(y + o, f);
+    if (st.mode) {
+      float m[8], h[8];
+      if (st.mode == 2) {
+        load_vec(st.mask + o, m);
+        load_vec(st.h + o, h);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float q = __bfloat162float(__float2bfloat16_rn(f[j]));
+        if (st.mode == 1) {
+          a1[j] += q;
+          a2[j] = fmaf(q, q, a2[j]);
+        } else {
+          const float d = m[j] > 0.f ? q : 0.f;
+          a1[j] += d;
+          a2[j] = fmaf(d, h[j] - st.mean[c0 + j], a2[j]);
+        }
+      }
+    }
+  }
+  if (!st.mode) return;
+  const int nt = blockDim.x;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    fred[threadIdx.x * 8 + j] = a1[j];
+    fred[(nt + threadIdx.x) * 8 + j] = a2[j];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < ych; c += nt) {  // threads t == c/8 (mod G) own channel c: fixed order
+    float x1 = 0.f, x2 = 0.f;
+    for (int tt = c >> 3; tt < nt; tt += G) {
+      x1 += fred[tt * 8 + (c & 7)];
+      x2 += fred[(nt + tt) * 8 + (c & 7)];
+    }
+    st.part[(int64_t)blockIdx.x * 2 * ych + c] = x1;
+    st.part[(int64_t)blockIdx.x * 2 * ych + ych + c] = x2;
   }
 }
 
@@ -436,8 +493,10 @@ int run(TcParams &p, int BN, float *ws, size_t ws_floats, const EpiStats *est, c
   }
   if (!ws || (size_t)p.ksplit * p.n_view_vox * p.ych > ws_floats) p.ksplit = 1;
   p.part = ws;
-  // fused statistics need whole-K tiles (no split) covering every output channel
+  // fused statistics: whole-K tiles covering every output channel in the conv
+  // epilogue, or the split-K finish kernel (which sees whole rows)
   const bool stats = est && est->mode && p.ksplit == 1 && p.t_nblk == 1;
+  const bool fin_stats = est && est->mode && p.ksplit > 1;
   if (stats) p.st = *est;
   // The TMA ring must hold ~latency x bandwidth (measured ~1600 cycles x ~85 B/clk
   // per SM from L2): launches with more work items than SMs run two CTAs per SM
@@ -456,10 +515,15 @@ int run(TcParams &p, int BN, float *ws, size_t ws_floats, const EpiStats *est, c
   }
   if (p.ksplit > 1) {
     const int64_t n = p.n_view_vox * (p.ych / 8);
-    launch_k(splitk_finish_k, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st, 
-        ws, p.ksplit, p.n_view_vox, p.ych, p.OW, p.OH, p.OD, p.y, p.s_n, p.s_d, p.s_h, p.s_w, p.bias, p.accumulate,
-        p.res, p.res_mask);
+    // with statistics: <= 148 blocks (the partial count), stride a multiple of ych/8
+    const unsigned fg = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 511) / 512, fin_stats ? 148 : 148 * 8));
+    EpiStats fst;
+    if (fin_stats) fst = *est;
+    launch_k(splitk_finish_k, fg, 512, fin_stats ? (size_t)2 * 512 * 8 * sizeof(float) : 0, st, ws, p.ksplit,
+             p.n_view_vox, p.ych, p.OW, p.OH, p.OD, p.y, p.s_n, p.s_d, p.s_h, p.s_w, p.bias, p.accumulate, p.res,
+             p.res_mask, fst);
     LAUNCH_CHECK();
+    if (fin_stats) return (int)fg;
   }
   return stats ? grid : 0;
 }
