@@ -10,9 +10,12 @@
 //   A[m, (t,c)] = src[view_t](voxel(m) + offset_t)[c]   (TMA 5-D box, OOB -> 0)
 //   B[n, (t,c)] = W[n][kcoord_t + c]                      (TMA 2-D box)
 // fprop: src = x, W = W[co][tap][ci];  dgrad (stride 1): src = dy, W = flipped
-// W^T[ci][tap'][co];  dgrad stride 2: one launch per output parity class, each
-// with its subset of taps and a strided output view;  stride-2 fprop: the A
-// views are the 8 parity sub-lattices of x.
+// W^T[ci][tap'][co];  dgrad stride 2: ONE launch over the 8 output parity
+// classes ("classes": each a strided output view with its own subset of taps,
+// work items enumerated class after class, heaviest first), optionally with the
+// stage-entry 1x1x1 stride-2 projection's dgrad appended to class (0,0,0) as a
+// 28th tap from a second A/B tensor pair;  stride-2 fprop: the A views are the
+// 8 parity sub-lattices of x.
 //
 // Kernel: persistent, one CTA per SM, warp-specialised: warp 0 TMA producer,
 // warp 1 MMA issuer (one elected lane, tcgen05.mma M=128, N=BN, K=16), warps
@@ -42,14 +45,26 @@ namespace {
 
 constexpr int TC_THREADS = 192;
 
+constexpr int MAX_TAPS = 28;  // 27 taps + the appended projection tap (stride-2 dgrad)
+
 struct __align__(64) TcParams {
   CUtensorMap a_map[8];
-  CUtensorMap b_map;
+  CUtensorMap b_map, b_map2;
   int n_taps;
   int kblocks_per_tap;  // A channels / 64
-  int8_t tap_map[27];
-  int8_t tap_od[27], tap_oh[27], tap_ow[27];
-  int tap_kcoord[27];
+  int8_t tap_map[MAX_TAPS];   // A tensor map of the tap
+  int8_t tap_bsel[MAX_TAPS];  // 0: b_map, 1: b_map2
+  int8_t tap_od[MAX_TAPS], tap_oh[MAX_TAPS], tap_ow[MAX_TAPS];
+  int tap_kcoord[MAX_TAPS];
+  // classes of work items (1 for plain launches; the parity classes of a stride-2
+  // dgrad): items [cls_item0[c], cls_item0[c+1]) = tiles x cls_ks[c] splits of
+  // class c, whose taps are [cls_tap0[c], cls_tap0[c] + cls_ntaps[c])
+  int n_cls;
+  int64_t cls_item0[9];
+  int cls_ks[8], cls_tap0[8], cls_ntaps[8];
+  int cls_OW[8], cls_OH[8], cls_OD[8];  // valid extents of the class view
+  int64_t cls_yoff[8];                  // element offset of the class view in y / res / mask / h
+  int64_t cls_pbase[8];                 // split-K partial base (floats)
   // output tiling: view extents and box
   int OD, OH, OW, ON;
   int bw, bh, bd, bn;
@@ -63,11 +78,13 @@ struct __align__(64) TcParams {
   int accumulate;
   const bf16 *res;
   const bf16 *res_mask;
-  // split-K over the K blocks (layers with fewer tiles than SMs)
+  // split-K over the K blocks (layers with fewer tiles than SMs): ksplit of a
+  // one-class launch; use_part = the epilogue writes fp32 partials (finish kernel)
   int ksplit;
+  int use_part;
   float *part;
   int64_t n_view_vox;
-  EpiStats st;  // fused BN statistics of the stored output (needs ksplit == 1, t_nblk == 1)
+  EpiStats st;  // fused BN statistics of the stored output (needs !use_part, t_nblk == 1)
 };
 
 template <int BN, int STAGES>
@@ -79,6 +96,28 @@ struct Smem {
   static constexpr int BAR_OFF = RED_OFF + 4 * 2 * BN * 4;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
 };
+
+struct Item {
+  int c, split, nb, tw, th, td, tn, kb0, kb1;
+};
+__device__ __forceinline__ Item decode_item(const TcParams &p, int64_t item) {
+  Item it;
+  int c = 0;
+  while (c + 1 < p.n_cls && item >= p.cls_item0[c + 1]) ++c;
+  it.c = c;
+  int64_t r = item - p.cls_item0[c];
+  const int ks = p.cls_ks[c];
+  it.split = (int)(r % ks); r /= ks;
+  it.nb = (int)(r % p.t_nblk); r /= p.t_nblk;
+  it.tw = (int)(r % p.tw); r /= p.tw;
+  it.th = (int)(r % p.th); r /= p.th;
+  it.td = (int)(r % p.td); r /= p.td;
+  it.tn = (int)r;
+  const int nk = p.cls_ntaps[c] * p.kblocks_per_tap;
+  it.kb0 = it.split * nk / ks;
+  it.kb1 = (it.split + 1) * nk / ks;
+  return it;
+}
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_constant__ TcParams p) {
@@ -108,6 +147,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
     for (int i = 0; i < p.n_taps; ++i)
       if (i == 0 || p.tap_map[i] != p.tap_map[i - 1]) tc::tma_prefetch(&p.a_map[p.tap_map[i]]);
     tc::tma_prefetch(&p.b_map);
+    for (int i = 0; i < p.n_taps; ++i)
+      if (p.tap_bsel[i]) { tc::tma_prefetch(&p.b_map2); break; }
   }
   if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_slot);
   tc::tc_fence_before();
@@ -116,8 +157,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
   const uint32_t tmem_base = *tmem_slot;
   pdl_begin();  // prologue above overlaps the predecessor's tail
 
-  const int nk = p.n_taps * p.kblocks_per_tap;
-  const int64_t n_items = p.n_tiles * p.ksplit;
+  const int64_t n_items = p.cls_item0[p.n_cls];
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -125,24 +165,19 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-        int64_t r = item / p.ksplit;
-        const int split = (int)(item % p.ksplit);
-        const int nb = (int)(r % p.t_nblk); r /= p.t_nblk;
-        const int tw = (int)(r % p.tw); r /= p.tw;
-        const int th = (int)(r % p.th); r /= p.th;
-        const int td = (int)(r % p.td); r /= p.td;
-        const int tn = (int)r;
-        const int w0 = tw * p.bw, h0 = th * p.bh, d0 = td * p.bd, n0 = tn * p.bn;
-        const int kb0 = split * nk / p.ksplit, kb1 = (split + 1) * nk / p.ksplit;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          const int t = kb / p.kblocks_per_tap, cb = kb % p.kblocks_per_tap;
+        const Item it = decode_item(p, item);
+        const int w0 = it.tw * p.bw, h0 = it.th * p.bh, d0 = it.td * p.bd, n0 = it.tn * p.bn;
+        const int nb = it.nb;
+        for (int kb = it.kb0; kb < it.kb1; ++kb) {
+          const int t = p.cls_tap0[it.c] + kb / p.kblocks_per_tap, cb = kb % p.kblocks_per_tap;
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * S::STAGE;
           uint8_t *sb = sa + S::A_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], S::STAGE);
           tc::tma_load_5d(sa, &p.a_map[p.tap_map[t]], &full[stage], cb * 64, w0 + p.tap_ow[t], h0 + p.tap_oh[t],
                           d0 + p.tap_od[t], n0);
-          tc::tma_load_2d(sb, &p.b_map, &full[stage], p.tap_kcoord[t] + cb * 64, nb * BN);
+          tc::tma_load_2d(sb, p.tap_bsel[t] ? &p.b_map2 : &p.b_map, &full[stage], p.tap_kcoord[t] + cb * 64,
+                          nb * BN);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -158,8 +193,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
     uint32_t phase = 0;
     int local = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
-      const int split = (int)(item % p.ksplit);
-      const int kb0 = split * nk / p.ksplit, kb1 = (split + 1) * nk / p.ksplit;
+      const Item it = decode_item(p, item);
+      const int kb0 = it.kb0, kb1 = it.kb1;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -195,18 +230,14 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
               nz = row / (p.bw * p.bh * p.bd);
     int local = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
-      int64_t r = item / p.ksplit;
-      const int split = (int)(item % p.ksplit);
-      const int nb = (int)(r % p.t_nblk); r /= p.t_nblk;
-      const int tw = (int)(r % p.tw); r /= p.tw;
-      const int th = (int)(r % p.th); r /= p.th;
-      const int td = (int)(r % p.td); r /= p.td;
-      const int tn = (int)r;
-      const int ow = tw * p.bw + wx, oh = th * p.bh + hy, od = td * p.bd + dz, on = tn * p.bn + nz;
-      const bool valid = ow < p.OW && oh < p.OH && od < p.OD && on < p.ON;
+      const Item it = decode_item(p, item);
+      const int split = it.split, nb = it.nb, c = it.c;
+      const int ow = it.tw * p.bw + wx, oh = it.th * p.bh + hy, od = it.td * p.bd + dz, on = it.tn * p.bn + nz;
+      const bool valid = ow < p.cls_OW[c] && oh < p.cls_OH[c] && od < p.cls_OD[c] && on < p.ON;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
-      const int64_t obase = on * p.s_n + od * p.s_d + oh * p.s_h + ow * p.s_w + (int64_t)nb * BN;
+      const int64_t obase =
+          p.cls_yoff[c] + on * p.s_n + od * p.s_d + oh * p.s_h + ow * p.s_w + (int64_t)nb * BN;
       StatsPf pf_cur, pf_nxt;
       epi_stats_prefetch(p.st, valid, obase, pf_cur);  // before the accumulator wait
       tc::mbar_wait(&tfull[acc], acc_phase);
@@ -217,10 +248,10 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
         uint32_t v[32];
         tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
         tc::tmem_wait_ld();
-        if (valid && p.ksplit > 1) {
-          // split-K: raw fp32 partial [split][view voxel][Nout]; epilogue in conv_splitk_finish
+        if (valid && p.use_part) {
+          // split-K: raw fp32 partial [class][split][view voxel][Nout]; epilogue in the finish kernel
           const int64_t vidx = ((int64_t)(on * p.OD + od) * p.OH + oh) * p.OW + ow;
-          float *dst = p.part + ((int64_t)split * p.n_view_vox + vidx) * p.ych + nb * BN + c0;
+          float *dst = p.part + p.cls_pbase[c] + ((int64_t)split * p.n_view_vox + vidx) * p.ych + nb * BN + c0;
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
             *reinterpret_cast<float4 *>(dst + j) = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
@@ -362,7 +393,7 @@ int launch(const TcParams &p, cudaStream_t st) {
                                                              S::TOTAL));
     per_sm = std::max(1, std::min(per_sm, 512 / (2 * BN)));
   }
-  const int grid = (int)std::min<int64_t>(p.n_tiles * p.ksplit, (int64_t)sms * per_sm);
+  const int grid = (int)std::min<int64_t>(p.cls_item0[p.n_cls], (int64_t)sms * per_sm);
   launch_k(conv_tc_kernel<BN, STAGES>, grid, TC_THREADS, S::TOTAL, st, p);
   LAUNCH_CHECK();
   return grid;
@@ -472,6 +503,113 @@ __global__ void __launch_bounds__(512) splitk_finish_k(const float *__restrict__
   }
 }
 
+// finish of a stride-2 dgrad launched as parity classes: every voxel v of dx
+// (contiguous NDHWC) belongs to the class of its parity; its value is the sum of
+// that class's split partials at the coarse voxel (v / 2) (zero for a parity no
+// tap reaches), then accumulate / masked residual / statistics as splitk_finish_k
+struct ClsFin {
+  int slot[8];        // parity (pd*2+ph)*2+pw -> class index, -1: no tap reaches it
+  int ks[8];          // splits of the class
+  int64_t pbase[8];   // partial base of the class (floats)
+};
+__global__ void __launch_bounds__(512) splitk_finish_cls_k(const float *__restrict__ part, ClsFin cf, int64_t nvv,
+                                                           int ych, int OW, int OH, int OD, int Wi, int Hi, int Di,
+                                                           int64_t nvox, bf16 *__restrict__ y, int accumulate,
+                                                           const bf16 *__restrict__ res,
+                                                           const bf16 *__restrict__ res_mask, EpiStats st) {
+  extern __shared__ float fred[];  // [2][blockDim][8] when st.mode
+  pdl_begin();
+  const int G = ych / 8;
+  const int64_t n = nvox * G;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  float a1[8], a2[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a1[j] = a2[j] = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int c0 = (int)(i % G) * 8;
+    const int64_t v = i / G;
+    int64_t r = v;
+    const int w = (int)(r % Wi); r /= Wi;
+    const int h = (int)(r % Hi); r /= Hi;
+    const int d = (int)(r % Di); r /= Di;
+    const int nn = (int)r;
+    const int slot = cf.slot[((d & 1) * 2 + (h & 1)) * 2 + (w & 1)];
+    const int ks = slot < 0 ? 0 : cf.ks[slot];
+    const float *src0 = part + (slot < 0 ? 0 : cf.pbase[slot]) +
+                        ((((int64_t)nn * OD + (d >> 1)) * OH + (h >> 1)) * OW + (w >> 1)) * ych + c0;
+    float f[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = 0.f;
+    for (int s0 = 0; s0 < ks; s0 += 8) {
+      float4 a[8], b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (s0 + u < ks) {
+          const float *src = src0 + (int64_t)(s0 + u) * nvv * ych;
+          a[u] = *reinterpret_cast<const float4 *>(src);
+          b[u] = *reinterpret_cast<const float4 *>(src + 4);
+        }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (s0 + u < ks) {
+          f[0] += a[u].x; f[1] += a[u].y; f[2] += a[u].z; f[3] += a[u].w;
+          f[4] += b[u].x; f[5] += b[u].y; f[6] += b[u].z; f[7] += b[u].w;
+        }
+    }
+    const int64_t o = v * ych + c0;
+    if (accumulate) {
+      float e[8];
+      load_vec(y + o, e);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] += e[j];
+    }
+    if (res) {
+      float rv[8], mv[8];
+      load_vec(res + o, rv);
+      load_vec(res_mask + o, mv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] += mv[j] > 0.f ? rv[j] : 0.f;
+    }
+    store_vec(y + o, f);
+    if (st.mode) {
+      float m[8], hh[8];
+      if (st.mode == 2) {
+        load_vec(st.mask + o, m);
+        load_vec(st.h + o, hh);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float q = __bfloat162float(__float2bfloat16_rn(f[j]));
+        if (st.mode == 1) {
+          a1[j] += q;
+          a2[j] = fmaf(q, q, a2[j]);
+        } else {
+          const float dd = m[j] > 0.f ? q : 0.f;
+          a1[j] += dd;
+          a2[j] = fmaf(dd, hh[j] - st.mean[c0 + j], a2[j]);
+        }
+      }
+    }
+  }
+  if (!st.mode) return;
+  const int nt = blockDim.x;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    fred[threadIdx.x * 8 + j] = a1[j];
+    fred[(nt + threadIdx.x) * 8 + j] = a2[j];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < ych; c += nt) {  // threads t == c/8 (mod G) own channel c: fixed order
+    float x1 = 0.f, x2 = 0.f;
+    for (int tt = c >> 3; tt < nt; tt += G) {
+      x1 += fred[tt * 8 + (c & 7)];
+      x2 += fred[(nt + tt) * 8 + (c & 7)];
+    }
+    st.part[(int64_t)blockIdx.x * 2 * ych + c] = x1;
+    st.part[(int64_t)blockIdx.x * 2 * ych + ych + c] = x2;
+  }
+}
+
 // split-K factor for launches with fewer tiles than SMs: as many splits as fit
 // in ONE wave of 148 CTAs (rounding up leaves a few CTAs with two items and
 // doubles the launch time)
@@ -480,6 +618,31 @@ int choose_ksplit(int64_t n_tiles, int nk) {
   int ks = (int)(148 / std::max<int64_t>(n_tiles, 1));
   ks = std::min(ks, nk / 4);
   return std::max(ks, 1);
+}
+
+// one class covering the whole launch (every launch but the stride-2 dgrad)
+void one_class(TcParams &p) {
+  p.n_cls = 1;
+  p.cls_item0[0] = 0;
+  p.cls_item0[1] = p.n_tiles * p.ksplit;
+  p.cls_ks[0] = p.ksplit;
+  p.cls_tap0[0] = 0;
+  p.cls_ntaps[0] = p.n_taps;
+  p.cls_OW[0] = p.OW; p.cls_OH[0] = p.OH; p.cls_OD[0] = p.OD;
+  p.cls_yoff[0] = 0;
+  p.cls_pbase[0] = 0;
+  p.use_part = p.ksplit > 1;
+}
+
+// The TMA ring must hold ~latency x bandwidth (measured ~1600 cycles x ~85 B/clk
+// per SM from L2): launches with more work items than SMs run two CTAs per SM
+// (two rings of 96 KB); launches with at most one item per SM run one CTA with
+// a 192 KB ring (a 96 KB ring measured latency-bound: 29 us vs ~15 us)
+int launch_ring(const TcParams &p, int BN, cudaStream_t st) {
+  const bool one_wave = p.cls_item0[p.n_cls] <= 148;
+  if (BN == 64) return one_wave ? launch<64, 8>(p, st) : launch<64, 4>(p, st);
+  if (BN == 128) return one_wave ? launch<128, 6>(p, st) : launch<128, 3>(p, st);
+  return launch<256, 4>(p, st);
 }
 
 // returns the number of BN-statistics partials written (0: statistics not fused)
@@ -493,26 +656,13 @@ int run(TcParams &p, int BN, float *ws, size_t ws_floats, const EpiStats *est, c
   }
   if (!ws || (size_t)p.ksplit * p.n_view_vox * p.ych > ws_floats) p.ksplit = 1;
   p.part = ws;
+  one_class(p);
   // fused statistics: whole-K tiles covering every output channel in the conv
   // epilogue, or the split-K finish kernel (which sees whole rows)
   const bool stats = est && est->mode && p.ksplit == 1 && p.t_nblk == 1;
   const bool fin_stats = est && est->mode && p.ksplit > 1;
   if (stats) p.st = *est;
-  // The TMA ring must hold ~latency x bandwidth (measured ~1600 cycles x ~85 B/clk
-  // per SM from L2): launches with more work items than SMs run two CTAs per SM
-  // (two rings of 96 KB); launches with at most one item per SM run one CTA with
-  // a 192 KB ring (a 96 KB ring measured latency-bound: 29 us vs ~15 us)
-  const bool one_wave = p.n_tiles * p.ksplit <= 148;
-  int grid;
-  if (BN == 64) {
-    if (one_wave) grid = launch<64, 8>(p, st);
-    else grid = launch<64, 4>(p, st);
-  } else if (BN == 128) {
-    if (one_wave) grid = launch<128, 6>(p, st);
-    else grid = launch<128, 3>(p, st);
-  } else {
-    grid = launch<256, 4>(p, st);
-  }
+  const int grid = launch_ring(p, BN, st);
   if (p.ksplit > 1) {
     const int64_t n = p.n_view_vox * (p.ych / 8);
     // with statistics: <= 148 blocks (the partial count), stride a multiple of ych/8
@@ -530,14 +680,14 @@ int run(TcParams &p, int BN, float *ws, size_t ws_floats, const EpiStats *est, c
 
 // Largest N tile dividing nout, halved while the launch has fewer tiles than
 // SMs (small late-stage layers trade MMA width for parallelism before split-K).
-int pick_bn(int nout, int OW, int OH, int OD, int ON) {
+int pick_bn(int nout, int OW, int OH, int OD, int ON, int mult = 1) {
   int bw, bh, bd, bn;
   choose_box(OW, OH, OD, ON, bw, bh, bd, bn);
   const int64_t mt = (int64_t)((OW + bw - 1) / bw) * ((OH + bh - 1) / bh) * ((OD + bd - 1) / bd) * ((ON + bn - 1) / bn);
   int BN = nout % 256 == 0 ? 256 : nout % 128 == 0 ? 128 : 64;
   // halving BN for small layers measured slower overall (more A re-reads): only
   // when even split-K cannot fill the machine (fewer than 16 tiles)
-  while (BN > 64 && mt * (nout / BN) < 16) BN /= 2;
+  while (BN > 64 && mt * mult * (nout / BN) < 16) BN /= 2;
   return BN;
 }
 
@@ -621,11 +771,12 @@ int conv_fprop_tc(const ConvGeom &g, const bf16 *x, const bf16 *w, const float *
 
 // dgrad: dx[vi][ci] (=|+=) sum dy[vo][co] W[co][tap][ci]; wd = [ci][taps-1-tap][co]
 int conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, bool accumulate, const bf16 *res,
-                  const bf16 *res_mask, float *ws, size_t ws_floats, cudaStream_t st, const EpiStats *est) {
+                  const bf16 *res_mask, float *ws, size_t ws_floats, cudaStream_t st, const EpiStats *est,
+                  const bf16 *dy2, const bf16 *wd2) {
+  if (dy2 && !(g.s == 2 && g.k == 3)) throw Error(RN_ERR_ARG, "conv_dgrad_tc: projection merge needs a k3 s2 conv");
   const int taps = g.taps();
-  const int BN = g.s == 1 ? pick_bn(g.Ci, g.Wi, g.Hi, g.Di, g.N)
-                          : pick_bn(g.Ci, (g.Wi + 1) / 2, (g.Hi + 1) / 2, (g.Di + 1) / 2, g.N);
   if (g.s == 1) {
+    const int BN = pick_bn(g.Ci, g.Wi, g.Hi, g.Di, g.N);
     TcParams p;
     memset(&p, 0, sizeof p);
     fill_tiles(p, g.Wi, g.Hi, g.Di, g.N, g.Ci, BN);
@@ -655,57 +806,134 @@ int conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, b
   // stride 2: output parity classes (pd, ph, pw); input index i = 2a + par.
   // Contributions: i = 2o + k - p  =>  for k=3,p=1: par 0 <- (k=1, o=a); par 1 <- (k=2, o=a), (k=0, o=a+1)
   //                                    for k=1,p=0: par 0 <- (k=0, o=a); par 1 <- none
-  for (int pd = 0; pd < 2; ++pd)
-    for (int ph = 0; ph < 2; ++ph)
-      for (int pw = 0; pw < 2; ++pw) {
-        const int Wv = (g.Wi - pw + 1) / 2, Hv = (g.Hi - ph + 1) / 2, Dv = (g.Di - pd + 1) / 2;
-        if (Wv <= 0 || Hv <= 0 || Dv <= 0) continue;
-        TcParams p;
-        memset(&p, 0, sizeof p);
-        fill_tiles(p, Wv, Hv, Dv, g.N, g.Ci, BN);
-        p.kblocks_per_tap = g.Co / 64;
-        make_act_map(&p.a_map[0], dy, g.Co, g.Wo, g.Ho, g.Do, g.N, 1, g.Wo, (int64_t)g.Wo * g.Ho,
-                     (int64_t)g.Wo * g.Ho * g.Do, p.bw, p.bh, p.bd, p.bn);
-        int nt = 0;
-        for (int t = 0; t < taps; ++t) {
-          const int kk[3] = {t / (g.k * g.k), (t / g.k) % g.k, t % g.k};
-          const int par[3] = {pd, ph, pw};
-          int off[3];
-          bool ok = true;
-          for (int a = 0; a < 3; ++a) {
-            // need 2o + k - p = 2a' + par  ->  o = a' + (par + p - k)/2, integer
-            const int num = par[a] + g.p - kk[a];
-            if (num % 2 != 0) { ok = false; break; }
-            off[a] = num / 2;
-          }
-          if (!ok) continue;
-          p.tap_map[nt] = 0;
-          p.tap_od[nt] = off[0]; p.tap_oh[nt] = off[1]; p.tap_ow[nt] = off[2];
-          p.tap_kcoord[nt] = (taps - 1 - t) * g.Co;  // wd[ci][taps-1-t][co] == W[co][ci][t]
-          ++nt;
+  // All classes run in ONE launch over a common coarse tiling (extents of parity
+  // 0, the largest); with dy2/wd2 the 1x1x1 stride-2 projection's dgrad is an
+  // extra tap of class (0,0,0) reading A from dy2 and B from wd2.
+  struct Cls { int par, nt; int8_t map[MAX_TAPS], bsel[MAX_TAPS], od[MAX_TAPS], oh[MAX_TAPS], ow[MAX_TAPS];
+               int kc[MAX_TAPS]; };
+  std::vector<Cls> cls;
+  bool empty_class = false;
+  for (int par = 0; par < 8; ++par) {
+    const int pd = par >> 2, ph = (par >> 1) & 1, pw = par & 1;
+    Cls c;
+    memset(&c, 0, sizeof c);
+    c.par = par;
+    auto add_taps = [&](int k, int pad, int ntaps_w, int amap) {
+      for (int t = 0; t < ntaps_w; ++t) {
+        const int kk[3] = {t / (k * k), (t / k) % k, t % k};
+        const int pp[3] = {pd, ph, pw};
+        int off[3];
+        bool ok = true;
+        for (int q = 0; q < 3; ++q) {
+          // need 2o + k - p = 2a' + par  ->  o = a' + (par + p - k)/2, integer
+          const int num = pp[q] + pad - kk[q];
+          if (num % 2 != 0) { ok = false; break; }
+          off[q] = num / 2;
         }
-        if (nt == 0) {
-          // no tap reaches this parity class (1x1x1 stride 2): its dx is zero
-          if (!accumulate) throw Error(RN_ERR_STATE, "conv_dgrad_tc: empty parity class needs accumulate");
-          continue;
-        }
-        p.n_taps = nt;
-        make_w_map(&p.b_map, wd, g.Ci, (int64_t)taps * g.Co, BN);
-        // strided output view: voxel (a_d, a_h, a_w) -> (2a_d+pd, 2a_h+ph, 2a_w+pw)
-        p.y = dx + (((int64_t)pd * g.Hi + ph) * g.Wi + pw) * g.Ci;
-        p.ych = g.Ci;
-        p.s_w = 2LL * g.Ci;
-        p.s_h = 2LL * g.Wi * g.Ci;
-        p.s_d = 2LL * g.Hi * g.Wi * g.Ci;
-        p.s_n = (int64_t)g.Di * g.Hi * g.Wi * g.Ci;
-        p.accumulate = accumulate;
-        if (res) {
-          p.res = res + (((int64_t)pd * g.Hi + ph) * g.Wi + pw) * g.Ci;
-          p.res_mask = res_mask + (((int64_t)pd * g.Hi + ph) * g.Wi + pw) * g.Ci;
-        }
-        run(p, BN, ws, ws_floats, nullptr, st);  // stride-2 dgrad outputs never feed a BN directly
+        if (!ok) continue;
+        c.map[c.nt] = (int8_t)amap;
+        c.bsel[c.nt] = (int8_t)amap;
+        c.od[c.nt] = off[0]; c.oh[c.nt] = off[1]; c.ow[c.nt] = off[2];
+        c.kc[c.nt] = (ntaps_w - 1 - t) * g.Co;  // wd[ci][taps-1-t][co] == W[co][ci][t]
+        ++c.nt;
       }
-  return 0;
+    };
+    add_taps(g.k, g.p, taps, 0);
+    if (dy2) add_taps(1, 0, 1, 1);
+    if (c.nt == 0) { empty_class = true; continue; }
+    cls.push_back(c);
+  }
+  std::stable_sort(cls.begin(), cls.end(), [](const Cls &x, const Cls &y) { return x.nt > y.nt; });
+  const int Wv0 = (g.Wi + 1) / 2, Hv0 = (g.Hi + 1) / 2, Dv0 = (g.Di + 1) / 2;
+  const int BN = pick_bn(g.Ci, Wv0, Hv0, Dv0, g.N, (int)cls.size());
+  TcParams p;
+  memset(&p, 0, sizeof p);
+  fill_tiles(p, Wv0, Hv0, Dv0, g.N, g.Ci, BN);
+  p.kblocks_per_tap = g.Co / 64;
+  p.n_view_vox = (int64_t)p.ON * p.OD * p.OH * p.OW;
+  // split-K per class in proportion to its K (uniform item cost), one wave in total
+  const int ncls = (int)cls.size();
+  int64_t kwork = 0;
+  for (const Cls &c : cls) kwork += p.n_tiles * c.nt * p.kblocks_per_tap;
+  const bool split = p.n_tiles * ncls < 100;
+  const int64_t chunk = std::max<int64_t>(4, (kwork + 147) / 148);
+  p.n_cls = ncls;
+  p.n_taps = 0;
+  int64_t items = 0, pfl = 0;
+  for (int ci = 0; ci < ncls; ++ci) {
+    const Cls &c = cls[ci];
+    const int nk = c.nt * p.kblocks_per_tap;
+    const int ks = split ? (int)std::max<int64_t>(1, std::min<int64_t>(nk, nk / chunk)) : 1;
+    const int pd = c.par >> 2, ph = (c.par >> 1) & 1, pw = c.par & 1;
+    p.cls_item0[ci] = items;
+    p.cls_ks[ci] = ks;
+    p.cls_tap0[ci] = p.n_taps;
+    p.cls_ntaps[ci] = c.nt;
+    p.cls_OW[ci] = (g.Wi - pw + 1) / 2; p.cls_OH[ci] = (g.Hi - ph + 1) / 2; p.cls_OD[ci] = (g.Di - pd + 1) / 2;
+    p.cls_yoff[ci] = (((int64_t)pd * g.Hi + ph) * g.Wi + pw) * g.Ci;
+    p.cls_pbase[ci] = pfl;
+    for (int t = 0; t < c.nt; ++t) {
+      const int j = p.n_taps++;
+      p.tap_map[j] = c.map[t]; p.tap_bsel[j] = c.bsel[t];
+      p.tap_od[j] = c.od[t]; p.tap_oh[j] = c.oh[t]; p.tap_ow[j] = c.ow[t];
+      p.tap_kcoord[j] = c.kc[t];
+    }
+    items += p.n_tiles * ks;
+    pfl += (int64_t)ks * p.n_view_vox * g.Ci;
+  }
+  p.cls_item0[ncls] = items;
+  // partial mode (finish kernel): split launches, and launches with a parity no
+  // tap reaches (the finish writes every voxel of dx)
+  p.use_part = split || empty_class;
+  p.ych = g.Ci;
+  if (g_dry_need) {
+    if (p.use_part) *g_dry_need = std::max(*g_dry_need, (size_t)pfl);
+    return 0;
+  }
+  if (p.use_part && (!ws || (size_t)pfl > ws_floats))
+    throw Error(RN_ERR_STATE, "conv_dgrad_tc: stride-2 split-K workspace too small");
+  if (!p.use_part && empty_class && !accumulate)
+    throw Error(RN_ERR_STATE, "conv_dgrad_tc: empty parity class needs accumulate");
+  p.ksplit = p.use_part ? 2 : 1;
+  p.part = ws;
+  make_act_map(&p.a_map[0], dy, g.Co, g.Wo, g.Ho, g.Do, g.N, 1, g.Wo, (int64_t)g.Wo * g.Ho,
+               (int64_t)g.Wo * g.Ho * g.Do, p.bw, p.bh, p.bd, p.bn);
+  make_w_map(&p.b_map, wd, g.Ci, (int64_t)taps * g.Co, BN);
+  if (dy2) {
+    make_act_map(&p.a_map[1], dy2, g.Co, g.Wo, g.Ho, g.Do, g.N, 1, g.Wo, (int64_t)g.Wo * g.Ho,
+                 (int64_t)g.Wo * g.Ho * g.Do, p.bw, p.bh, p.bd, p.bn);
+    make_w_map(&p.b_map2, wd2, g.Ci, (int64_t)g.Co, BN);
+  }
+  // strided output views: class voxel (a_d, a_h, a_w) -> (2a_d+pd, 2a_h+ph, 2a_w+pw)
+  p.y = dx;
+  p.s_w = 2LL * g.Ci;
+  p.s_h = 2LL * g.Wi * g.Ci;
+  p.s_d = 2LL * g.Hi * g.Wi * g.Ci;
+  p.s_n = (int64_t)g.Di * g.Hi * g.Wi * g.Ci;
+  p.accumulate = accumulate;
+  p.res = res;
+  p.res_mask = res_mask;
+  const bool stats = est && est->mode && !p.use_part && p.t_nblk == 1;
+  const bool fin_stats = est && est->mode && p.use_part;
+  if (stats) p.st = *est;
+  const int grid = launch_ring(p, BN, st);
+  if (!p.use_part) return stats ? grid : 0;
+  ClsFin cf;
+  for (int q = 0; q < 8; ++q) cf.slot[q] = -1;
+  for (int ci = 0; ci < ncls; ++ci) {
+    cf.slot[cls[ci].par] = ci;
+    cf.ks[ci] = p.cls_ks[ci];
+    cf.pbase[ci] = p.cls_pbase[ci];
+  }
+  const int64_t nvox = (int64_t)g.N * g.Di * g.Hi * g.Wi;
+  const int64_t n = nvox * (g.Ci / 8);
+  const unsigned fg = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 511) / 512, fin_stats ? 148 : 148 * 8));
+  EpiStats fst;
+  if (fin_stats) fst = *est;
+  launch_k(splitk_finish_cls_k, fg, 512, fin_stats ? (size_t)2 * 512 * 8 * sizeof(float) : 0, st, ws, cf,
+           p.n_view_vox, g.Ci, p.OW, p.OH, p.OD, g.Wi, g.Hi, g.Di, nvox, dx, (int)accumulate, res, res_mask, fst);
+  LAUNCH_CHECK();
+  return fin_stats ? (int)fg : 0;
 }
 
 size_t tc_conv_ws_floats(const ConvGeom &g, bool dgrad) {
@@ -713,7 +941,14 @@ size_t tc_conv_ws_floats(const ConvGeom &g, bool dgrad) {
   g_dry_need = &need;
   try {
     if (!dgrad) conv_fprop_tc(g, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr);
-    else conv_dgrad_tc(g, nullptr, nullptr, nullptr, true, nullptr, nullptr, nullptr, 0, nullptr, nullptr);
+    else {
+      conv_dgrad_tc(g, nullptr, nullptr, nullptr, true, nullptr, nullptr, nullptr, 0, nullptr, nullptr);
+      // the k3 stride-2 dgrad may run with the projection merged (a different split)
+      static const bf16 dummy{};
+      if (g.s == 2 && g.k == 3)
+        conv_dgrad_tc(g, nullptr, nullptr, nullptr, true, nullptr, nullptr, nullptr, 0, nullptr, nullptr, &dummy,
+                      &dummy);
+    }
   } catch (...) {
     g_dry_need = nullptr;
     throw;

@@ -432,6 +432,34 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
   if (stats.bn) stats.bn->bP = parts;
   if (t) tk_end(e, kind);
 }
+void Plan::conv_bwd_data_proj(const ConvL &c1, const void *dy1, const ConvL &cp, const void *dyp, void *dx,
+                              bool accumulate, const StatsTarget &stats) {
+  auto it = opts.find("merge_proj");
+  const bool merge = (it == opts.end() || it->second != 0) && use_tc(c1.g, true) && use_tc(cp.g, true) &&
+                     c1.g.k == 3 && c1.g.s == 2 && cp.g.k == 1 && cp.g.s == 2 && cp.g.Ci == c1.g.Ci &&
+                     cp.g.Co == c1.g.Co;
+  if (!merge) {
+    conv_bwd_data(c1, dy1, dx, accumulate, nullptr, nullptr);
+    conv_bwd_data(cp, dyp, dx, true, nullptr, nullptr, stats);
+    return;
+  }
+  const bool t = timing();
+  size_t e = t ? tk_begin(1, conv_flops(c1.g) + conv_flops(cp.g)) : 0;
+  EpiStats es;
+  const bool want = stats.bn && fused_stats();
+  if (want) {
+    es.part = (float *)P(stats.bn->bpart);
+    es.mode = 2;
+    es.mask = (const bf16 *)stats.mask;
+    es.h = (const bf16 *)stats.h;
+    es.mean = stats.mean;
+  }
+  const int parts = conv_dgrad_tc(c1.g, (const bf16 *)dy1, (const bf16 *)P(shadow_d[c1.w_idx]), (bf16 *)dx,
+                                  accumulate, nullptr, nullptr, (float *)P(off_conv_ws), conv_ws_floats, stream,
+                                  want ? &es : nullptr, (const bf16 *)dyp, (const bf16 *)P(shadow_d[cp.w_idx]));
+  if (stats.bn) stats.bn->bP = parts;
+  if (t) tk_end(e, K_TC);
+}
 bool Plan::side_on() const {
   auto it = opts.find("wgrad_stream");
   const bool on = it == opts.end() || it->second != 0;
@@ -571,8 +599,7 @@ void Plan::block_bwd(BlockL &B, int k, const void *x, const void *dout, void *dx
   conv_bwd_weight(B.c1, x, P(B.dh1), false);
   if (dx) {
     if (B.proj) {
-      conv_bwd_data(B.c1, P(B.dh1), dx, accumulate, nullptr, nullptr);
-      conv_bwd_data(B.cp, P(B.dhp), dx, true, nullptr, nullptr, dx_stats);
+      conv_bwd_data_proj(B.c1, P(B.dh1), B.cp, P(B.dhp), dx, accumulate, dx_stats);
     } else {
       // identity skip: dx (+)= dgrad(dh1) + dout * (out > 0)
       conv_bwd_data(B.c1, P(B.dh1), dx, accumulate, dout, out, dx_stats);

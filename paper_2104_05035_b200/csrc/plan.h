@@ -145,6 +145,9 @@ struct Plan {
   void conv_fwd(const ConvL &c, const void *x, void *y, const float *bias = nullptr, BNL *stats = nullptr);
   void conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumulate, const void *res,
                      const void *res_mask, const StatsTarget &stats = StatsTarget());
+  // stage-entry block: dx (+)= dgrad(c1, dy1) + dgrad(cp, dyp); one launch when both run on tcgen05
+  void conv_bwd_data_proj(const ConvL &c1, const void *dy1, const ConvL &cp, const void *dyp, void *dx,
+                          bool accumulate, const StatsTarget &stats);
   bool fused_stats() const;
   BnFinal bn_final(const BNL &b, int k);
   StatsTarget dout_consumer(int ui, int k);

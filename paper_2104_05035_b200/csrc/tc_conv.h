@@ -18,10 +18,13 @@ size_t tc_conv_ws_floats(const ConvGeom &g, bool dgrad);
 // (split-K or multi-N-block launches, stride-2 dgrad)
 int conv_fprop_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, const float *bias,
                   __nv_bfloat16 *y, float *ws, size_t ws_floats, cudaStream_t st, const EpiStats *est = nullptr);
-// wd: [Ci][taps][Co] with the tap order flipped (repack_conv's wd)
+// wd: [Ci][taps][Co] with the tap order flipped (repack_conv's wd).  Stride 2 runs
+// the 8 output parity classes in one launch; dy2/wd2 (k3 stride-2 convs only) add
+// the stage-entry 1x1x1 stride-2 projection's dgrad (same Ci, Co, geometry) to it
 int conv_dgrad_tc(const ConvGeom &g, const __nv_bfloat16 *dy, const __nv_bfloat16 *wd, __nv_bfloat16 *dx,
                   bool accumulate, const __nv_bfloat16 *res, const __nv_bfloat16 *res_mask, float *ws,
-                  size_t ws_floats, cudaStream_t st, const EpiStats *est = nullptr);
+                  size_t ws_floats, cudaStream_t st, const EpiStats *est = nullptr,
+                  const __nv_bfloat16 *dy2 = nullptr, const __nv_bfloat16 *wd2 = nullptr);
 
 // haloed-A kernel for the 64 -> 64 channel stride-1 3x3x3 convs (k_conv_halo.cu)
 bool halo_conv_supported(const ConvGeom &g, bool dgrad);
