@@ -241,7 +241,11 @@ int64_t rn_kernel_launches(rn_plan_t plan);
 /* rn_set_option — runtime switches:
  *  "graphs"        : 1 capture forward/backward/step in CUDA graphs (default 1)
  *  "tc_conv"       : 1 use tcgen05 conv kernels in RN_BF16 (default 1)
- *  "time_kernels"  : 1 record CUDA events around the dominant conv launches      */
+ *  "time_kernels"  : 1 record CUDA events around the dominant conv launches
+ *  "halo_conv", "pair_conv", "fused_stats", "wgrad_stream" : kernel-variant switches (default 1)
+ *  "merge_proj"    : 1 stage-entry projection dgrad merged into the stride-2 dgrad launch (default 1)
+ *  "stem_bwd_fused": 1 fused stem backward (pool adjoint + mask + BN sums; BN apply in the wgrad) (default 1)
+ * Unknown keys: RN_ERR_ARG.  Every switch changes kernels only, not the result beyond fp32 rounding. */
 rn_status rn_set_option(rn_plan_t plan, const char *key, int64_t value);
 
 /* rn_query — named float64 statistics (e.g. "conv_ms", "conv_flops") collected

@@ -1059,6 +1059,173 @@ __global__ void __launch_bounds__(256) maxpool_bwd_stage_k(const bf16 *__restric
   }
 }
 
+// Stem backward, part 1 (bf16 path, pooled stem; PAPER.md:366 Conv block =
+// conv + BN + ReLU, reading X4 stem max-pool, X10 tie rule): one persistent
+// pass that computes, per stem voxel and channel,
+//   g  = pool adjoint (gathered from smem-staged pooled rows, as maxpool_bwd_stage_k), rounded to bf16
+//   d' = g * (h*scale + shift > 0)   (ReLU mask recomputed from the BN forward coefficients)
+// stores d' (bf16) and accumulates the BN-backward sums S1 = sum d', S2 = sum d' xhat
+// (xhat = (h - mean) invstd, the BwdOp convention) in registers (each thread keeps
+// one 8-channel group: blockDim is a multiple of C/8); per-block partials are
+// reduced in block order by the last block, which finalizes (BwdFin: dgamma,
+// dbeta, and the apply coefficients consumed by the stem weight gradient).
+// Replaces maxpool_bwd_stage_k + chan_reduce_fin_k<BwdOp> (one fewer 119 MB read).
+constexpr int SPB_PF = 3;  // staged 16-B vectors per thread (4 pooled rows x Wo x C / 8 <= 768)
+__global__ void __launch_bounds__(256, 3) stem_pool_bwd_k(const bf16 *__restrict__ dy, const uint8_t *__restrict__ am,
+                                                       const bf16 *__restrict__ h, int N, int D, int H, int W, int C,
+                                                       int Do, int Ho, int Wo, const float *__restrict__ scale,
+                                                       const float *__restrict__ shift, const float *__restrict__ mean,
+                                                       const float *__restrict__ invstd, bf16 *__restrict__ dprime,
+                                                       float *__restrict__ partial, unsigned *counter, BwdFin fin) {
+  extern __shared__ __align__(16) uint8_t smp[];
+  pdl_begin();
+  const int rowel = Wo * C;
+  bf16 *sdy = reinterpret_cast<bf16 *>(smp);  // [4][Wo][C]
+  uint8_t *sam = smp + 4 * rowel * 2;         // [4][Wo][C]
+  const int Hj = (H + 1) / 2;
+  const int G = C / 8;
+  const int vecs = rowel / 8;
+  const int cg = (threadIdx.x % G) * 8;  // this thread's channel group (items advance by blockDim)
+  __shared__ float coefs[4][256];           // scale, shift, mean, invstd per channel (C <= 256)
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    coefs[0][c] = scale[c];
+    coefs[1][c] = shift[c];
+    coefs[2][c] = mean[c];
+    coefs[3][c] = invstd[c];
+  }
+  float a1[8], a2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) a1[e] = a2[e] = 0.f;
+  const int units = N * D * Hj;
+  // the pooled rows of unit u are loaded into registers while unit u - gridDim.x
+  // is gathered (software pipeline: one global round trip per unit is hidden)
+  uint4 pv[SPB_PF];
+  uint2 pa[SPB_PF];
+  auto stage_load = [&](int u) {
+    const int j = u % Hj, id = (u / Hj) % D, nn = u / (Hj * D);
+    const int od0 = id >> 1, od1 = (id & 1) && ((id + 1) >> 1) < Do ? (id + 1) >> 1 : -1;
+#pragma unroll
+    for (int q = 0; q < SPB_PF; ++q) {
+      const int i = threadIdx.x + q * 256;
+      pv[q] = make_uint4(0, 0, 0, 0);
+      pa[q] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // no code matches 255
+      if (i < 4 * vecs) {
+        const int slot = i / vecs, e = (i - slot * vecs) * 8;
+        const int od = (slot >> 1) ? od1 : od0, oh = j + (slot & 1);
+        if (od >= 0 && oh < Ho) {
+          const int64_t o = ((int64_t)(nn * Do + od) * Ho + oh) * rowel + e;
+          pv[q] = ld16(dy + o);
+          pa[q] = *reinterpret_cast<const uint2 *>(am + o);
+        }
+      }
+    }
+  };
+  if (blockIdx.x < units) stage_load(blockIdx.x);
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int j = u % Hj, id = (u / Hj) % D, nn = u / (Hj * D);
+    const int od0 = id >> 1, od1 = (id & 1) && ((id + 1) >> 1) < Do ? (id + 1) >> 1 : -1;
+    __syncthreads();  // the previous unit's readers are done with the staged rows
+#pragma unroll
+    for (int q = 0; q < SPB_PF; ++q) {
+      const int i = threadIdx.x + q * 256;
+      if (i < 4 * vecs) {
+        const int slot = i / vecs, e = (i - slot * vecs) * 8;
+        *reinterpret_cast<uint4 *>(sdy + slot * rowel + e) = pv[q];
+        *reinterpret_cast<uint2 *>(sam + slot * rowel + e) = pa[q];
+      }
+    }
+    __syncthreads();
+    if (u + (int)gridDim.x < units) stage_load(u + gridDim.x);
+    const int items = 2 * W * G;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+      const int r = it / (W * G), rem = it - r * W * G, iw = rem / G;
+      const int ih = 2 * j + r;
+      if (ih >= H) continue;
+      const int64_t o = (((int64_t)(nn * D + id) * H + ih) * W + iw) * C + cg;
+      float hv[8];
+      load_vec(h + o, hv);  // issued before the gather: overlaps the smem work
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int od = (q & 4) ? od1 : od0;
+        const int oh = (ih + (q >> 1 & 1)) >> 1, ow = (iw + (q & 1)) >> 1;
+        const bool ok = od >= 0 && oh < Ho && ow < Wo && (!(q & 4) || (id & 1)) && (!(q & 2) || (ih & 1)) &&
+                        (!(q & 1) || (iw & 1));
+        if (!ok) continue;
+        const int slot = ((q & 4) ? 2 : 0) + (oh - j);
+        const int tap = ((id - 2 * od + 1) * 3 + (ih - 2 * oh + 1)) * 3 + (iw - 2 * ow + 1);
+        const int e0 = slot * rowel + ow * C + cg;
+        float f[8];
+        load_vec(sdy + e0, f);
+        uint8_t code[8];
+        const uint2 a = *reinterpret_cast<const uint2 *>(sam + e0);
+        memcpy(code, &a, 8);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (code[e] == tap) acc[e] += f[e];
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float g = __bfloat162float(__float2bfloat16_rn(acc[e]));  // the stored pool adjoint
+        const float d = fmaf(hv[e], coefs[0][cg + e], coefs[1][cg + e]) > 0.f ? g : 0.f;
+        acc[e] = d;
+        a1[e] += d;
+        a2[e] = fmaf(d, (hv[e] - coefs[2][cg + e]) * coefs[3][cg + e], a2[e]);
+      }
+      store_vec(dprime + o, acc);
+    }
+  }
+  // per-block partials: channel c = cg + e summed over the threads of group cg, in thread order
+  __syncthreads();
+  float *red = reinterpret_cast<float *>(smp);  // [2][blockDim][8] (<= the staging area)
+  const int nt = blockDim.x;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    red[threadIdx.x * 8 + e] = a1[e];
+    red[(nt + threadIdx.x) * 8 + e] = a2[e];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += nt) {
+    float x1 = 0.f, x2 = 0.f;
+    for (int tt = c >> 3; tt < nt; tt += G) {
+      x1 += red[tt * 8 + (c & 7)];
+      x2 += red[(nt + tt) * 8 + (c & 7)];
+    }
+    partial[(int64_t)blockIdx.x * 2 * C + c] = x1;
+    partial[(int64_t)blockIdx.x * 2 * C + C + c] = x2;
+  }
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  // last block: fixed-order fp64 reduction over the blocks, P threads per channel
+  double *dsm = reinterpret_cast<double *>(smp);
+  const int P = nt / C;  // C <= nt, nt % C == 0 (checked by the launcher)
+  const int c = threadIdx.x % C, s = threadIdx.x / C;
+  double A = 0.0, B = 0.0;
+  for (int k = s; k < (int)gridDim.x; k += P) {
+    A += (double)partial[(int64_t)k * 2 * C + c];
+    B += (double)partial[(int64_t)k * 2 * C + C + c];
+  }
+  dsm[s * C + c] = A;
+  dsm[nt + s * C + c] = B;
+  __syncthreads();
+  if (s == 0) {
+    double SA = 0.0, SB = 0.0;
+    for (int q = 0; q < P; ++q) {
+      SA += dsm[q * C + c];
+      SB += dsm[nt + q * C + c];
+    }
+    fin(c, SA, SB);
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
 template <typename T>
 __global__ void upsample_fwd_k(const T *__restrict__ x, int N, int Di, int Hi, int Wi, int C, T *__restrict__ y,
                                int Do, int Ho, int Wo, UpTables t) {
@@ -1429,6 +1596,23 @@ void maxpool_bwd(DType dt, const void *dy, const uint8_t *argmax, int N, int D, 
   }
   DISPATCH(dt, launch_k(maxpool_bwd_k<T>, (unsigned)(N * D * H), NT, 0, st, 
                    (const T *)dy, argmax, N, D, H, W, C, Do, Ho, Wo, (T *)dx, accumulate ? 1 : 0));
+  LAUNCH_CHECK();
+}
+
+int stem_pool_bwd_blocks() { return 148 * 3; }
+
+void stem_pool_bwd(const void *dy, const uint8_t *argmax, const void *h, int N, int D, int H, int W, int C, int Do,
+                   int Ho, int Wo, const float *scale, const float *shift, const float *mean, const float *invstd,
+                   const float *gamma, float *dgamma, float *dbeta, float *coef, void *dprime, float *partial,
+                   unsigned *counter, cudaStream_t st) {
+  const size_t smem = std::max((size_t)4 * Wo * C * 3, (size_t)2 * 256 * 8 * sizeof(float));
+  if (C % 8 != 0 || 256 % C != 0 || smem > 48 * 1024 || 4 * Wo * C / 8 > SPB_PF * 256)
+    throw Error(RN_ERR_ARG, "stem_pool_bwd: unsupported C / row");
+  const int units = N * D * ((H + 1) / 2);
+  const unsigned nb = (unsigned)std::min(units, stem_pool_bwd_blocks());
+  BwdFin fin{(int64_t)N * D * H * W, C, gamma, mean, invstd, dgamma, dbeta, coef};
+  launch_k(stem_pool_bwd_k, nb, 256, smem, st, (const bf16 *)dy, argmax, (const bf16 *)h, N, D, H, W, C, Do, Ho, Wo,
+           scale, shift, mean, invstd, (bf16 *)dprime, partial, counter, fin);
   LAUNCH_CHECK();
 }
 

@@ -41,60 +41,81 @@ __global__ void __launch_bounds__(128) stem_fprop_k(ConvGeom g, const float *__r
     const int co = i % CO, tap = i / CO;
     ws[i] = w[co * 27 + tap];
   }
-  // output staging: the block's 128 voxels x CO channels, stored back with
-  // consecutive threads on consecutive 16-B chunks (full L2 sectors)
-  __shared__ __align__(16) T so[128 * CO];
+  // Each thread computes VPT voxels (rows t, t + 128, ...): every weight vector
+  // read from smem (a warp-wide broadcast) feeds VPT x 8 FMAs (one voxel per
+  // thread measured smem-wavefront-bound at 68-79%).
+  constexpr int VPT = (int)(sizeof(T) * CO * 256 <= 32768 ? 2 : 1);
+  constexpr int ROWS = 128 * VPT;
+  // output staging: the block's ROWS voxels x CO channels, stored back with
+  // consecutive threads on consecutive 16-B chunks (full L2 sectors).  Row v's
+  // 16-B chunk q sits at chunk (q ^ (v & SWM)): the per-thread row writes (one
+  // row per thread, 128-B apart) would otherwise all hit the same 4 banks
+  __shared__ __align__(16) T so[ROWS * CO];
+  constexpr int VE = 16 / sizeof(T);   // elements per 16-B chunk
+  constexpr int NCH = CO / VE;         // chunks per row
+  constexpr int SWM = (NCH < 8 ? NCH : 8) - 1;
+  auto chunk_ptr = [&](int row, int q) { return so + (row * NCH + (q ^ (row & SWM))) * VE; };
   __syncthreads();
   const int64_t total = g.out_vox();
-  for (int64_t vb = blockIdx.x * (int64_t)blockDim.x; vb < total; vb += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t vo = vb + threadIdx.x;
-    const bool live = vo < total;
-    int64_t r = live ? vo : total - 1;
-    const int ow = (int)(r % g.Wo); r /= g.Wo;
-    const int oh = (int)(r % g.Ho); r /= g.Ho;
-    const int od = (int)(r % g.Do); r /= g.Do;
-    const int n = (int)r;
-    float xv[27];
+  for (int64_t vb = blockIdx.x * (int64_t)ROWS; vb < total; vb += (int64_t)gridDim.x * ROWS) {
+    float xv[VPT][27];
 #pragma unroll
-    for (int tap = 0; tap < 27; ++tap) {
-      const int id = od * g.s + tap / 9 - g.p, ih = oh * g.s + (tap / 3) % 3 - g.p, iw = ow * g.s + tap % 3 - g.p;
-      const bool ok = id >= 0 && id < g.Di && ih >= 0 && ih < g.Hi && iw >= 0 && iw < g.Wi;
-      xv[tap] = ok ? __ldg(&x[(((int64_t)n * g.Di + id) * g.Hi + ih) * g.Wi + iw]) : 0.f;
+    for (int u = 0; u < VPT; ++u) {
+      const int64_t vo = vb + threadIdx.x + 128 * u;
+      int64_t r = vo < total ? vo : total - 1;
+      const int ow = (int)(r % g.Wo); r /= g.Wo;
+      const int oh = (int)(r % g.Ho); r /= g.Ho;
+      const int od = (int)(r % g.Do); r /= g.Do;
+      const int n = (int)r;
+#pragma unroll
+      for (int tap = 0; tap < 27; ++tap) {
+        const int id = od * g.s + tap / 9 - g.p, ih = oh * g.s + (tap / 3) % 3 - g.p, iw = ow * g.s + tap % 3 - g.p;
+        const bool ok = id >= 0 && id < g.Di && ih >= 0 && ih < g.Hi && iw >= 0 && iw < g.Wi;
+        xv[u][tap] = ok ? __ldg(&x[(((int64_t)n * g.Di + id) * g.Hi + ih) * g.Wi + iw]) : 0.f;
+      }
     }
 #pragma unroll
     for (int c0 = 0; c0 < CO; c0 += 8) {
-      float acc[8];
+      float acc[VPT][8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+      for (int u = 0; u < VPT; ++u)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[u][j] = 0.f;
 #pragma unroll
       for (int tap = 0; tap < 27; ++tap) {
         const float4 a = *reinterpret_cast<const float4 *>(&ws[tap * CO + c0]);
         const float4 b = *reinterpret_cast<const float4 *>(&ws[tap * CO + c0 + 4]);
-        acc[0] = fmaf(xv[tap], a.x, acc[0]);
-        acc[1] = fmaf(xv[tap], a.y, acc[1]);
-        acc[2] = fmaf(xv[tap], a.z, acc[2]);
-        acc[3] = fmaf(xv[tap], a.w, acc[3]);
-        acc[4] = fmaf(xv[tap], b.x, acc[4]);
-        acc[5] = fmaf(xv[tap], b.y, acc[5]);
-        acc[6] = fmaf(xv[tap], b.z, acc[6]);
-        acc[7] = fmaf(xv[tap], b.w, acc[7]);
+#pragma unroll
+        for (int u = 0; u < VPT; ++u) {
+          const float xt = xv[u][tap];
+          acc[u][0] = fmaf(xt, a.x, acc[u][0]);
+          acc[u][1] = fmaf(xt, a.y, acc[u][1]);
+          acc[u][2] = fmaf(xt, a.z, acc[u][2]);
+          acc[u][3] = fmaf(xt, a.w, acc[u][3]);
+          acc[u][4] = fmaf(xt, b.x, acc[u][4]);
+          acc[u][5] = fmaf(xt, b.y, acc[u][5]);
+          acc[u][6] = fmaf(xt, b.z, acc[u][6]);
+          acc[u][7] = fmaf(xt, b.w, acc[u][7]);
+        }
       }
-      store8(so + threadIdx.x * CO + c0, acc);
+#pragma unroll
+      for (int u = 0; u < VPT; ++u)
+#pragma unroll
+        for (int h = 0; h < 8; h += VE) store_vec(chunk_ptr(threadIdx.x + 128 * u, (c0 + h) / VE), acc[u] + h);
     }
     __syncthreads();
-    constexpr int VE = 16 / sizeof(T);  // elements per 16-B chunk
-    const int64_t nvox = min((int64_t)blockDim.x, total - vb);
+    const int64_t nvox = min((int64_t)ROWS, total - vb);
     if (part) {  // statistics of the stored (rounded) values, channel t % CO
       const int c = threadIdx.x % CO;
       for (int v = threadIdx.x / CO; v < nvox; v += HG) {
-        const float f = to_f(so[v * CO + c]);
+        const float f = to_f(chunk_ptr(v, c / VE)[c % VE]);
         s1 += f;
         s2 = fmaf(f, f, s2);
       }
     }
     const int nchunk = (int)(nvox * CO / VE);
     for (int i = threadIdx.x; i < nchunk; i += blockDim.x)
-      reinterpret_cast<uint4 *>(y + vb * CO)[i] = reinterpret_cast<const uint4 *>(so)[i];
+      reinterpret_cast<uint4 *>(y + vb * CO)[i] = *reinterpret_cast<const uint4 *>(chunk_ptr(i / NCH, i % NCH));
     __syncthreads();
   }
   if (part) {
@@ -286,8 +307,158 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo_k, float hi_k) {
   return u;
 }
 
-__global__ void __launch_bounds__(256) stem_wgrad_mma_k(ConvGeom g, const float *__restrict__ x,
-                                                       const bf16 *__restrict__ dh, float *__restrict__ part) {
+// fprop on the legacy warp tensor cores (bf16 path, C0 = 64): per warp a tile of
+// 16 consecutive output voxels is the GEMM  Y[16 x 64] = P[16 x 32] W[32 x 64]
+// (P = the 27-tap input patches, padded to K = 32).  Both fp32 operands are split
+// into bf16 pairs (v = v_hi + v_lo, |v - v_hi - v_lo| <= 2^-17 |v|) and the three
+// significant products hi*hi + hi*lo + lo*hi go through mma.m16n8k16 with fp32
+// accumulation: each output is the fp32-input convolution to ~2^-16 relative,
+// far below the bf16 rounding of the stored output (the SIMT kernel it replaces
+// issued one smem weight load per 8 FMAs and was smem-pipe-bound at 150 us).
+// W fragments (hi and lo) stay in registers for the whole kernel.  The tile goes
+// through a per-warp smem staging tile (16-B chunks XOR-swizzled by row) so the
+// global stores are full 16-B vectors; BN statistics (sum, sum of squares of
+// the stored bf16 values) accumulate in registers and are reduced once per block.
+constexpr int SF_WARPS = 4;
+__global__ void __launch_bounds__(SF_WARPS * 32) stem_fprop_mma_k(ConvGeom g, const float *__restrict__ x,
+                                                               const float *__restrict__ w, bf16 *__restrict__ y,
+                                                               float *__restrict__ part) {
+  __shared__ __align__(16) uint32_t stile[SF_WARPS][16 * 32];  // [voxel][64 ch] bf16, swizzled 16-B chunks
+  __shared__ float sred[SF_WARPS][2][64];
+  pdl_begin();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tq = lane & 3;
+  // B fragments: k = tap (rows), n = channel (cols); b0 = (k 2tq, 2tq+1), b1 = (k 2tq+8, 2tq+9) + 16 ks
+  uint32_t bh[2][8][2], bl[2][8][2];
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int t0 = 16 * ks + 2 * tq + 8 * r, co = n * 8 + gq;
+        const float w0 = t0 < 27 ? w[co * 27 + t0] : 0.f, w1 = t0 + 1 < 27 ? w[co * 27 + t0 + 1] : 0.f;
+        const float h0 = __bfloat162float(__float2bfloat16_rn(w0)), h1 = __bfloat162float(__float2bfloat16_rn(w1));
+        bh[ks][n][r] = pack_bf16x2(h0, h1);
+        bl[ks][n][r] = pack_bf16x2(w0 - h0, w1 - h1);
+      }
+  float s1[16], s2[16];  // channels n*8 + 2tq + e  (index n*2 + e)
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s1[i] = s2[i] = 0.f;
+  const int64_t total = g.out_vox();
+  const int64_t ntiles = (total + 15) / 16;
+  uint32_t *st = stile[warp];
+  for (int64_t tile = (int64_t)blockIdx.x * SF_WARPS + warp; tile < ntiles; tile += (int64_t)gridDim.x * SF_WARPS) {
+    const int64_t v0 = tile * 16;
+    // A fragments: rows gq, gq + 8 (voxels), cols 2tq, 2tq+1, 2tq+8, 2tq+9 (+16 ks) (taps)
+    float xv[2][2][4];  // [voxel half][ks][j]: tap = 16 ks + 2tq + (j & 1) + 8 (j >> 1)
+#pragma unroll
+    for (int hv = 0; hv < 2; ++hv) {
+      const int64_t vo = v0 + gq + 8 * hv;
+      const bool live = vo < total;
+      int64_t r = live ? vo : 0;
+      const int ow = (int)(r % g.Wo); r /= g.Wo;
+      const int oh = (int)(r % g.Ho); r /= g.Ho;
+      const int od = (int)(r % g.Do); r /= g.Do;
+      const int nn = (int)r;
+      const float *xn = x + (int64_t)nn * g.Di * g.Hi * g.Wi;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int tap = 16 * ks + 2 * tq + (j & 1) + 8 * (j >> 1);
+          const int kd = tap / 9, kh = (tap / 3) % 3, kw = tap % 3;
+          const int id = od * g.s + kd - g.p, ih = oh * g.s + kh - g.p, iw = ow * g.s + kw - g.p;
+          const bool ok = live && tap < 27 && id >= 0 && id < g.Di && ih >= 0 && ih < g.Hi && iw >= 0 && iw < g.Wi;
+          xv[hv][ks][j] = ok ? __ldg(xn + ((int64_t)id * g.Hi + ih) * g.Wi + iw) : 0.f;
+        }
+    }
+    float acc[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[n][q] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      uint32_t ah[4], al[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        // a_q: q=0 (row gq, k 2tq..), 1 (row gq+8), 2 (row gq, k +8), 3 (row gq+8, k +8)
+        const int hv = q & 1, jj = (q >> 1) * 2;
+        const float p0 = xv[hv][ks][jj], p1 = xv[hv][ks][jj + 1];
+        const float h0 = __bfloat162float(__float2bfloat16_rn(p0)), h1 = __bfloat162float(__float2bfloat16_rn(p1));
+        ah[q] = pack_bf16x2(h0, h1);
+        al[q] = pack_bf16x2(p0 - h0, p1 - h1);
+      }
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        mma_bf16_16816(acc[n], al, bh[ks][n][0], bh[ks][n][1]);
+        mma_bf16_16816(acc[n], ah, bl[ks][n][0], bl[ks][n][1]);
+        mma_bf16_16816(acc[n], ah, bh[ks][n][0], bh[ks][n][1]);
+      }
+    }
+    // round, statistics of the stored values, stage: row (voxel) v, 16-B chunk n at (n ^ (v & 7))
+    __syncwarp();
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int hv = 0; hv < 2; ++hv) {
+        const int v = gq + 8 * hv;
+        const bool live = v0 + v < total;
+        const __nv_bfloat162 b = __floats2bfloat162_rn(acc[n][2 * hv], acc[n][2 * hv + 1]);
+        const float2 f = __bfloat1622float2(b);
+        if (live) {
+          s1[2 * n] += f.x;
+          s2[2 * n] = fmaf(f.x, f.x, s2[2 * n]);
+          s1[2 * n + 1] += f.y;
+          s2[2 * n + 1] = fmaf(f.y, f.y, s2[2 * n + 1]);
+        }
+        uint32_t u;
+        memcpy(&u, &b, 4);
+        st[v * 32 + ((n ^ (v & 7)) << 2) + tq] = u;
+      }
+    __syncwarp();
+    // 16 voxels x 128 B = 128 chunks of 16 B: lane takes chunks lane, lane+32, ...
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = lane + 32 * q, v = c >> 3, n = c & 7;
+      if (v0 + v < total) {
+        const uint4 val = *reinterpret_cast<const uint4 *>(st + v * 32 + ((n ^ (v & 7)) << 2));
+        *reinterpret_cast<uint4 *>(y + (v0 + v) * 64 + n * 8) = val;
+      }
+    }
+  }
+  if (!part) return;
+  // statistics: lanes with the same tq hold the same channels -> butterfly over gq (fixed order)
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      s1[i] += __shfl_xor_sync(0xffffffffu, s1[i], off);
+      s2[i] += __shfl_xor_sync(0xffffffffu, s2[i], off);
+    }
+  if (gq == 0)
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        sred[warp][0][n * 8 + 2 * tq + e] = s1[2 * n + e];
+        sred[warp][1][n * 8 + 2 * tq + e] = s2[2 * n + e];
+      }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) {
+    const int k = i >> 6, c = i & 63;
+    float a = 0.f;
+#pragma unroll
+    for (int q = 0; q < SF_WARPS; ++q) a += sred[q][k][c];
+    part[(int64_t)blockIdx.x * 128 + k * 64 + c] = a;
+  }
+}
+
+// hx/coef (optional): the BN-backward apply fused into the staging, dh = bf16(A d' + B h + Cc)
+// with dh holding d' (bn_bwd_apply_k's arithmetic, coef = [A | B | Cc] per channel)
+__global__ void __launch_bounds__(256, 2) stem_wgrad_mma_k(ConvGeom g, const float *__restrict__ x,
+                                                       const bf16 *__restrict__ dh, float *__restrict__ part,
+                                                       const bf16 *__restrict__ hx, const float *__restrict__ coef) {
   extern __shared__ __align__(16) uint8_t sm[];
   pdl_begin();
   uint8_t *sdh = sm;                                  // [256][128 B], chunk c of row v at ((c ^ (v & 7)) * 16)
@@ -301,15 +472,59 @@ __global__ void __launch_bounds__(256) stem_wgrad_mma_k(ConvGeom g, const float 
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc[m][n][r] = 0.f;
   const int64_t total = g.out_vox();
+  // fused apply: this thread's staging chunk is always channel group (t & 7)
+  float cA[8], cB[8], cC[8];
+  if (coef) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = (t & 7) * 8 + e;
+      cA[e] = coef[c];
+      cB[e] = coef[64 + c];
+      cC[e] = coef[128 + c];
+    }
+  }
   for (int64_t v0 = (int64_t)blockIdx.x * SW_CH; v0 < total; v0 += (int64_t)gridDim.x * SW_CH) {
     __syncthreads();
     // dh tile: 256 rows x 8 chunks of 16 B
+    if (coef) {
+      uint4 dv[8], hv[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int i = t + 256 * j, row = i >> 3, c = i & 7;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (v0 + row < total) v = __ldg(reinterpret_cast<const uint4 *>(dh + (v0 + row) * 64) + c);
-      *reinterpret_cast<uint4 *>(sdh + row * 128 + ((c ^ (row & 7)) << 4)) = v;
+      for (int j = 0; j < 8; ++j) {
+        const int i = t + 256 * j, row = i >> 3, c = i & 7;
+        dv[j] = hv[j] = make_uint4(0, 0, 0, 0);
+        if (v0 + row < total) {
+          dv[j] = __ldg(reinterpret_cast<const uint4 *>(dh + (v0 + row) * 64) + c);
+          hv[j] = __ldg(reinterpret_cast<const uint4 *>(hx + (v0 + row) * 64) + c);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = t + 256 * j, row = i >> 3, c = i & 7;
+        float d[8], hh[8], o[8];
+        const __nv_bfloat162 *pd = reinterpret_cast<const __nv_bfloat162 *>(&dv[j]);
+        const __nv_bfloat162 *ph = reinterpret_cast<const __nv_bfloat162 *>(&hv[j]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 a = __bfloat1622float2(pd[q]), b = __bfloat1622float2(ph[q]);
+          d[2 * q] = a.x; d[2 * q + 1] = a.y;
+          hh[2 * q] = b.x; hh[2 * q + 1] = b.y;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = v0 + row < total ? fmaf(cA[e], d[e], fmaf(cB[e], hh[e], cC[e])) : 0.f;
+        uint4 v;
+        __nv_bfloat162 *pv = reinterpret_cast<__nv_bfloat162 *>(&v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pv[q] = __floats2bfloat162_rn(o[2 * q], o[2 * q + 1]);
+        *reinterpret_cast<uint4 *>(sdh + row * 128 + ((c ^ (row & 7)) << 4)) = v;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = t + 256 * j, row = i >> 3, c = i & 7;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (v0 + row < total) v = __ldg(reinterpret_cast<const uint4 *>(dh + (v0 + row) * 64) + c);
+        *reinterpret_cast<uint4 *>(sdh + row * 128 + ((c ^ (row & 7)) << 4)) = v;
+      }
     }
     // input patches: thread t = voxel v0 + t, its 27 taps (stride-2 stem geometry)
     {
@@ -400,6 +615,17 @@ __global__ void stem_reduce_k(const float *__restrict__ part, int nblk, int n, f
 template <typename T, int CO>
 int stem_fprop_launch(const ConvGeom &g, const float *x, const float *w, void *y, float *part, cudaStream_t st) {
   const int64_t total = g.out_vox();
+  if (std::is_same<T, bf16>::value && CO == 64 && !getenv("RN_STEM_FPROP_SIMT")) {
+    // tensor-core path; the grid is the statistics-partial count (<= 4 per SM)
+    static int per_sm = 0;
+    if (!per_sm) {
+      CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stem_fprop_mma_k, SF_WARPS * 32, 0));
+      per_sm = std::max(1, std::min(per_sm, 4));
+    }
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((total + 63) / 64, per_sm * 148));
+    launch_k(stem_fprop_mma_k, blocks, SF_WARPS * 32, 0, st, g, x, w, (bf16 *)y, part);
+    return part ? (int)blocks : 0;
+  }
   // with fused statistics the grid is the partial count: 4 blocks per SM
   const unsigned blocks = (unsigned)std::min<int64_t>((total + 127) / 128, part ? 4 * 148 : 148 * 16);
   launch_k(stem_fprop_k<T, CO>, blocks, 128, 0, st, g, x, w, (T *)y, part);
@@ -412,7 +638,8 @@ int stem_wgrad_blocks(const ConvGeom &g) {
 }
 
 template <typename T, int CO>
-void stem_wgrad_launch(const ConvGeom &g, const float *x, const void *dh, float *dw, float *ws, cudaStream_t st) {
+void stem_wgrad_launch(const ConvGeom &g, const float *x, const void *dh, float *dw, float *ws, cudaStream_t st,
+                       const void *hx = nullptr, const float *coef = nullptr) {
   if (std::is_same<T, bf16>::value && CO == 64 && !getenv("RN_STEM_SIMT")) {
     // tensor-core path (bf16 dh): 3 blocks per SM, partials reduced by stem_reduce_k
     static bool attr = false;
@@ -420,12 +647,13 @@ void stem_wgrad_launch(const ConvGeom &g, const float *x, const void *dh, float 
       CUDA_CHECK(cudaFuncSetAttribute(stem_wgrad_mma_k, cudaFuncAttributeMaxDynamicSharedMemorySize, SW_SMEM));
       attr = true;
     }
-    const int nb = std::min(stem_wgrad_blocks(g), 3 * 148);
-    launch_k(stem_wgrad_mma_k, nb, 256, SW_SMEM, st, g, x, (const bf16 *)dh, ws);
+    const int nb = std::min(stem_wgrad_blocks(g), 2 * 148);
+    launch_k(stem_wgrad_mma_k, nb, 256, SW_SMEM, st, g, x, (const bf16 *)dh, ws, (const bf16 *)hx, coef);
     LAUNCH_CHECK();
     launch_k(stem_reduce_k, (CO * 27 + 255) / 256, 256, 0, st, ws, nb, CO * 27, dw);
     return;
   }
+  if (coef) throw Error(RN_ERR_ARG, "stem_wgrad: the fused BN apply needs the bf16 64-channel tensor-core path");
   // (stem_wgrad_warp_k measured 466 us vs 331 us for the smem-staged kernel on
   // the r18 stem: latency-bound with 16 warps/SM; kept for reference)
   const int nb = stem_wgrad_blocks(g);
@@ -455,6 +683,13 @@ int stem_fprop_fast(DType dt, const ConvGeom &g, const float *x, const float *w,
 #undef STEM_F
   LAUNCH_CHECK();
   return P;
+}
+
+void stem_wgrad_fused_apply(const ConvGeom &g, const float *x, const void *dprime, const void *h, const float *coef,
+                            float *dw, float *ws, cudaStream_t st) {
+  if (g.Co != 64 || getenv("RN_STEM_SIMT")) throw Error(RN_ERR_ARG, "stem_wgrad_fused_apply: needs Co = 64");
+  stem_wgrad_launch<bf16, 64>(g, x, dprime, dw, ws, st, h, coef);
+  LAUNCH_CHECK();
 }
 
 void stem_wgrad_fast(DType dt, const ConvGeom &g, const float *x, const void *dh, float *dw, float *ws,

@@ -466,7 +466,8 @@ bool Plan::side_on() const {
   return on && !timing() && stream != nullptr && stream != cudaStreamLegacy && stream != cudaStreamPerThread;
 }
 
-void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32) {
+void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32, const void *h_fused,
+                           const float *coef_fused) {
   const bool t = timing();
   size_t e = t ? tk_begin(2, conv_flops(c.g)) : 0;
   cudaStream_t ws = stream;
@@ -482,7 +483,11 @@ void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x
     side_used = true;
   }
   int kind = K_SIMT;
-  if (x_f32 && stem_fast_supported(c.g)) {
+  if (coef_fused) {
+    kind = K_STEM;
+    stem_wgrad_fused_apply(c.g, (const float *)x, dy, h_fused, coef_fused, grad(c.w_idx), (float *)P(off_wgrad_ws),
+                           ws);
+  } else if (x_f32 && stem_fast_supported(c.g)) {
     kind = K_STEM;
     stem_wgrad_fast(dt, c.g, (const float *)x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), ws);
   } else if (!x_f32 && use_tc(c.g, false) && tc_wgrad_supported(c.g)) {
@@ -699,6 +704,21 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
     const void *dy;
     int mode;
     const void *mt = nullptr;
+    auto it = opts.find("stem_bwd_fused");
+    const bool fuse = (it == opts.end() || it->second != 0) && u.pool && dt == DT_BF16 && u.cout == 64 &&
+                      stem_fast_supported(L.stem_conv.g) && !getenv("RN_STEM_SIMT");
+    if (fuse) {
+      // pool adjoint + ReLU mask + BN-backward sums/finalize in one pass (d' -> tmp0), the
+      // BN-backward apply inside the stem weight gradient (no dh tensor)
+      const BNL &b = L.stem_bn;
+      float *coef = (float *)P(off_coef);
+      stem_pool_bwd(P(L.dout), (const uint8_t *)P(L.am[k]), P(L.stem_h[k]), mb, u.conv.d, u.conv.h, u.conv.w, u.cout,
+                    u.out.d, u.out.h, u.out.w, bn_stat(b, k, 2), bn_stat(b, k, 3), bn_stat(b, k, 0), bn_stat(b, k, 1),
+                    master(b.gamma_idx), grad(b.gamma_idx), grad(b.gamma_idx + 1), coef, P(L.tmp0),
+                    (float *)P(off_partial), counter(), stream);
+      conv_bwd_weight(L.stem_conv, x, P(L.tmp0), true, P(L.stem_h[k]), coef);
+      return;
+    }
     if (u.pool) {
       maxpool_bwd(dt, P(L.dout), (const uint8_t *)P(L.am[k]), mb, u.conv.d, u.conv.h, u.conv.w, u.cout, u.out.d,
                   u.out.h, u.out.w, P(L.tmp0), false, stream);
@@ -1102,7 +1122,7 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 
 rn_status Plan::set_option(const std::string &k, int64_t v) {
   if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv" && k != "fused_stats" &&
-      k != "pair_conv" && k != "wgrad_stream")
+      k != "pair_conv" && k != "wgrad_stream" && k != "merge_proj" && k != "stem_bwd_fused")
     return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;

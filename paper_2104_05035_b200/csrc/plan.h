@@ -151,7 +151,10 @@ struct Plan {
   bool fused_stats() const;
   BnFinal bn_final(const BNL &b, int k);
   StatsTarget dout_consumer(int ui, int k);
-  void conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32);
+  // h_fused / coef_fused: stem only (bf16, 64 channels): dy holds d' and the BN-backward apply
+  // dh = A d' + B h + Cc is formed inside the weight-gradient kernel
+  void conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32, const void *h_fused = nullptr,
+                       const float *coef_fused = nullptr);
   void bn_forward_stats(const BNL &b, int k, const void *h);
   void bn_fwd(const BNL &b, int k, const void *h, const void *res, const float *rscale, const float *rshift, bool relu,
               void *y);
