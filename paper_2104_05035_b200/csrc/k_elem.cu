@@ -1071,8 +1071,9 @@ __global__ void __launch_bounds__(256) maxpool_bwd_stage_k(const bf16 *__restric
 // dbeta, and the apply coefficients consumed by the stem weight gradient).
 // Replaces maxpool_bwd_stage_k + chan_reduce_fin_k<BwdOp> (one fewer 119 MB read).
 constexpr int SPB_PF = 3;  // staged 16-B vectors per thread (4 pooled rows x Wo x C / 8 <= 768)
+template <int C>  // channels (compile-time: the index math is shifts)
 __global__ void __launch_bounds__(256, 3) stem_pool_bwd_k(const bf16 *__restrict__ dy, const uint8_t *__restrict__ am,
-                                                       const bf16 *__restrict__ h, int N, int D, int H, int W, int C,
+                                                       const bf16 *__restrict__ h, int N, int D, int H, int W, int,
                                                        int Do, int Ho, int Wo, const float *__restrict__ scale,
                                                        const float *__restrict__ shift, const float *__restrict__ mean,
                                                        const float *__restrict__ invstd, bf16 *__restrict__ dprime,
@@ -1083,10 +1084,11 @@ __global__ void __launch_bounds__(256, 3) stem_pool_bwd_k(const bf16 *__restrict
   bf16 *sdy = reinterpret_cast<bf16 *>(smp);  // [4][Wo][C]
   uint8_t *sam = smp + 4 * rowel * 2;         // [4][Wo][C]
   const int Hj = (H + 1) / 2;
-  const int G = C / 8;
+  constexpr int G = C / 8;
   const int vecs = rowel / 8;
   const int cg = (threadIdx.x % G) * 8;  // this thread's channel group (items advance by blockDim)
-  __shared__ float coefs[4][256];           // scale, shift, mean, invstd per channel (C <= 256)
+  const int WG = W * G;
+  __shared__ float coefs[4][C];             // scale, shift, mean, invstd per channel
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     coefs[0][c] = scale[c];
     coefs[1][c] = shift[c];
@@ -1137,13 +1139,26 @@ __global__ void __launch_bounds__(256, 3) stem_pool_bwd_k(const bf16 *__restrict
     __syncthreads();
     if (u + (int)gridDim.x < units) stage_load(u + gridDim.x);
     const int items = 2 * W * G;
-    for (int it = threadIdx.x; it < items; it += blockDim.x) {
-      const int r = it / (W * G), rem = it - r * W * G, iw = rem / G;
+    // h of all this thread's items of the unit, loaded up front (one exposed
+    // round trip per unit instead of one per item)
+    uint4 hq[SPB_PF];
+#pragma unroll
+    for (int q = 0; q < SPB_PF; ++q) {
+      const int it = threadIdx.x + q * 256;
+      const int r = it >= WG, iw = (it - (r ? WG : 0)) / G;
+      const int ih = 2 * j + r;
+      if (it < items && ih < H) hq[q] = ld16(h + (((int64_t)(nn * D + id) * H + ih) * W + iw) * C + cg);
+    }
+#pragma unroll
+    for (int q = 0; q < SPB_PF; ++q) {
+      const int it = threadIdx.x + q * 256;
+      if (it >= items) break;
+      const int r = it >= WG, iw = (it - (r ? WG : 0)) / G;
       const int ih = 2 * j + r;
       if (ih >= H) continue;
       const int64_t o = (((int64_t)(nn * D + id) * H + ih) * W + iw) * C + cg;
       float hv[8];
-      load_vec(h + o, hv);  // issued before the gather: overlaps the smem work
+      unpack16(hq[q], hv, h);
       float acc[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] = 0.f;
@@ -1606,12 +1621,13 @@ void stem_pool_bwd(const void *dy, const uint8_t *argmax, const void *h, int N, 
                    const float *gamma, float *dgamma, float *dbeta, float *coef, void *dprime, float *partial,
                    unsigned *counter, cudaStream_t st) {
   const size_t smem = std::max((size_t)4 * Wo * C * 3, (size_t)2 * 256 * 8 * sizeof(float));
-  if (C % 8 != 0 || 256 % C != 0 || smem > 48 * 1024 || 4 * Wo * C / 8 > SPB_PF * 256)
+  if (C % 8 != 0 || 256 % C != 0 || smem > 48 * 1024 || 4 * Wo * C / 8 > SPB_PF * 256 || 2 * W * C / 8 > SPB_PF * 256)
     throw Error(RN_ERR_ARG, "stem_pool_bwd: unsupported C / row");
   const int units = N * D * ((H + 1) / 2);
   const unsigned nb = (unsigned)std::min(units, stem_pool_bwd_blocks());
   BwdFin fin{(int64_t)N * D * H * W, C, gamma, mean, invstd, dgamma, dbeta, coef};
-  launch_k(stem_pool_bwd_k, nb, 256, smem, st, (const bf16 *)dy, argmax, (const bf16 *)h, N, D, H, W, C, Do, Ho, Wo,
+  if (C != 64) throw Error(RN_ERR_ARG, "stem_pool_bwd: instantiated for 64 channels");
+  launch_k(stem_pool_bwd_k<64>, nb, 256, smem, st, (const bf16 *)dy, argmax, (const bf16 *)h, N, D, H, W, C, Do, Ho, Wo,
            scale, shift, mean, invstd, (bf16 *)dprime, partial, counter, fin);
   LAUNCH_CHECK();
 }

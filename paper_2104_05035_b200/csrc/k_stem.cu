@@ -347,31 +347,64 @@ __global__ void __launch_bounds__(SF_WARPS * 32) stem_fprop_mma_k(ConvGeom g, co
   const int64_t total = g.out_vox();
   const int64_t ntiles = (total + 15) / 16;
   uint32_t *st = stile[warp];
-  for (int64_t tile = (int64_t)blockIdx.x * SF_WARPS + warp; tile < ntiles; tile += (int64_t)gridDim.x * SF_WARPS) {
-    const int64_t v0 = tile * 16;
-    // A fragments: rows gq, gq + 8 (voxels), cols 2tq, 2tq+1, 2tq+8, 2tq+9 (+16 ks) (taps)
-    float xv[2][2][4];  // [voxel half][ks][j]: tap = 16 ks + 2tq + (j & 1) + 8 (j >> 1)
+  // the next tile's patch values are loaded while the current tile computes
+  // (software pipeline: one L1/L2 round trip per tile is hidden)
+  float xv[2][2][4], xn_[2][2][4];  // [voxel half][ks][j]: tap = 16 ks + 2tq + (j & 1) + 8 (j >> 1)
+  // this thread's 8 taps (fixed by tq): element offset and (kd, kh, kw) bits
+  int toff[2][4], tbits[2][4];
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int tap = 16 * ks + 2 * tq + (j & 1) + 8 * (j >> 1);
+      const int kd = tap / 9, kh = (tap / 3) % 3, kw = tap % 3;
+      toff[ks][j] = (kd * g.Hi + kh) * g.Wi + kw;
+      tbits[ks][j] = tap < 27 ? (1 << kd) | (8 << kh) | (64 << kw) : 0;  // all-zero: padding tap
+    }
+  const int HWi = g.Hi * g.Wi;
+  // voxel index < 2^31 (checked by the launcher): 32-bit coordinate decode
+  auto load_patch = [&](int64_t tile, float (&dst)[2][2][4]) {
 #pragma unroll
     for (int hv = 0; hv < 2; ++hv) {
-      const int64_t vo = v0 + gq + 8 * hv;
-      const bool live = vo < total;
-      int64_t r = live ? vo : 0;
-      const int ow = (int)(r % g.Wo); r /= g.Wo;
-      const int oh = (int)(r % g.Ho); r /= g.Ho;
-      const int od = (int)(r % g.Do); r /= g.Do;
-      const int nn = (int)r;
-      const float *xn = x + (int64_t)nn * g.Di * g.Hi * g.Wi;
+      const int vo = (int)(tile * 16) + gq + 8 * hv;
+      const bool live = tile < ntiles && vo < (int)total;
+      int r = live ? vo : 0;
+      const int ow = r % g.Wo; r /= g.Wo;
+      const int oh = r % g.Ho; r /= g.Ho;
+      const int od = r % g.Do;
+      const int nn = r / g.Do;
+      const int id0 = od * g.s - g.p, ih0 = oh * g.s - g.p, iw0 = ow * g.s - g.p;
+      // valid-offset masks: bit kd (d), 3 + kh (h), 6 + kw (w)
+      int vm = 0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        vm |= (id0 + k >= 0 && id0 + k < g.Di) ? (1 << k) : 0;
+        vm |= (ih0 + k >= 0 && ih0 + k < g.Hi) ? (8 << k) : 0;
+        vm |= (iw0 + k >= 0 && iw0 + k < g.Wi) ? (64 << k) : 0;
+      }
+      if (!live) vm = 0;
+      const float *xb = x + (int64_t)nn * g.Di * HWi + ((int64_t)id0 * g.Hi + ih0) * g.Wi + iw0;
 #pragma unroll
       for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int tap = 16 * ks + 2 * tq + (j & 1) + 8 * (j >> 1);
-          const int kd = tap / 9, kh = (tap / 3) % 3, kw = tap % 3;
-          const int id = od * g.s + kd - g.p, ih = oh * g.s + kh - g.p, iw = ow * g.s + kw - g.p;
-          const bool ok = live && tap < 27 && id >= 0 && id < g.Di && ih >= 0 && ih < g.Hi && iw >= 0 && iw < g.Wi;
-          xv[hv][ks][j] = ok ? __ldg(xn + ((int64_t)id * g.Hi + ih) * g.Wi + iw) : 0.f;
+          const int tb = tbits[ks][j];
+          const bool ok = tb != 0 && (tb & vm) == tb;
+          dst[hv][ks][j] = ok ? __ldg(xb + toff[ks][j]) : 0.f;
         }
     }
+  };
+  const int64_t tstride = (int64_t)gridDim.x * SF_WARPS;
+  load_patch((int64_t)blockIdx.x * SF_WARPS + warp, xn_);
+  for (int64_t tile = (int64_t)blockIdx.x * SF_WARPS + warp; tile < ntiles; tile += tstride) {
+    const int64_t v0 = tile * 16;
+#pragma unroll
+    for (int hv = 0; hv < 2; ++hv)
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) xv[hv][ks][j] = xn_[hv][ks][j];
+    load_patch(tile + tstride, xn_);
     float acc[8][4];
 #pragma unroll
     for (int n = 0; n < 8; ++n)
@@ -531,11 +564,11 @@ __global__ void __launch_bounds__(256, 2) stem_wgrad_mma_k(ConvGeom g, const flo
       const int64_t vo = v0 + t;
       float *prow = sp + t * SW_PS;
       if (vo < total) {
-        int64_t r = vo;
-        const int ow = (int)(r % g.Wo); r /= g.Wo;
-        const int oh = (int)(r % g.Ho); r /= g.Ho;
-        const int od = (int)(r % g.Do); r /= g.Do;
-        const int n = (int)r;
+        int r = (int)vo;  // < 2^31 (checked by the launcher): 32-bit decode
+        const int ow = r % g.Wo; r /= g.Wo;
+        const int oh = r % g.Ho; r /= g.Ho;
+        const int od = r % g.Do;
+        const int n = r / g.Do;
         const float *xn = x + (int64_t)n * g.Di * g.Hi * g.Wi;
 #pragma unroll
         for (int tap = 0; tap < 27; ++tap) {
@@ -615,7 +648,7 @@ __global__ void stem_reduce_k(const float *__restrict__ part, int nblk, int n, f
 template <typename T, int CO>
 int stem_fprop_launch(const ConvGeom &g, const float *x, const float *w, void *y, float *part, cudaStream_t st) {
   const int64_t total = g.out_vox();
-  if (std::is_same<T, bf16>::value && CO == 64 && !getenv("RN_STEM_FPROP_SIMT")) {
+  if (std::is_same<T, bf16>::value && CO == 64 && !getenv("RN_STEM_FPROP_SIMT") && total + 64 < (1LL << 31)) {
     // tensor-core path; the grid is the statistics-partial count (<= 4 per SM)
     static int per_sm = 0;
     if (!per_sm) {
@@ -640,7 +673,7 @@ int stem_wgrad_blocks(const ConvGeom &g) {
 template <typename T, int CO>
 void stem_wgrad_launch(const ConvGeom &g, const float *x, const void *dh, float *dw, float *ws, cudaStream_t st,
                        const void *hx = nullptr, const float *coef = nullptr) {
-  if (std::is_same<T, bf16>::value && CO == 64 && !getenv("RN_STEM_SIMT")) {
+  if (std::is_same<T, bf16>::value && CO == 64 && !getenv("RN_STEM_SIMT") && g.out_vox() < (1LL << 31)) {
     // tensor-core path (bf16 dh): 3 blocks per SM, partials reduced by stem_reduce_k
     static bool attr = false;
     if (!attr) {
