@@ -1070,9 +1070,42 @@ __global__ void __launch_bounds__(256) maxpool_bwd_stage_k(const bf16 *__restric
 // reduced in block order by the last block, which finalizes (BwdFin: dgamma,
 // dbeta, and the apply coefficients consumed by the stem weight gradient).
 // Replaces maxpool_bwd_stage_k + chan_reduce_fin_k<BwdOp> (one fewer 119 MB read).
+// Pool-adjoint gather for one stem voxel x 8 channels, specialised on the voxel's
+// parity (PD, PH, PW): a coordinate i is covered by window o = i >> 1 (tap 1) when
+// even, by o = i >> 1 (tap 2) and o + 1 (tap 0) when odd.  Slots / taps are
+// compile-time; out-of-range pooled rows were staged with code 255 (never
+// matches), only the w-neighbour needs a bound check.  Candidates are visited
+// in (d, h, w) order (the summation order of maxpool_bwd_stage_k).
+template <int C, int PD, int PH, int PW>
+__device__ __forceinline__ void pool_gather(const bf16 *sdy, const uint8_t *sam, int rowel, int ow0, int Wo, int cg,
+                                            float (&acc)[8]) {
+#pragma unroll
+  for (int a = 0; a <= PD; ++a)
+#pragma unroll
+    for (int b = 0; b <= PH; ++b)
+#pragma unroll
+      for (int c = 0; c <= PW; ++c) {
+        const int kd = PD ? (a ? 0 : 2) : 1, kh = PH ? (b ? 0 : 2) : 1, kw = PW ? (c ? 0 : 2) : 1;
+        const uint32_t tap4 = (uint32_t)((kd * 3 + kh) * 3 + kw) * 0x01010101u;
+        const int ow = ow0 + c;
+        if (c == 1 && ow >= Wo) continue;
+        const int e0 = (a * 2 + b) * rowel + ow * C + cg;
+        const uint4 v = *reinterpret_cast<const uint4 *>(sdy + e0);
+        const uint2 code = *reinterpret_cast<const uint2 *>(sam + e0);
+        const uint32_t m0 = __vcmpeq4(code.x, tap4), m1 = __vcmpeq4(code.y, tap4);
+        const uint32_t w4[4] = {v.x & __byte_perm(m0, 0, 0x1100), v.y & __byte_perm(m0, 0, 0x3322),
+                                v.z & __byte_perm(m1, 0, 0x1100), v.w & __byte_perm(m1, 0, 0x3322)};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          acc[2 * k] += __uint_as_float(w4[k] << 16);
+          acc[2 * k + 1] += __uint_as_float(w4[k] & 0xFFFF0000u);
+        }
+      }
+}
+
 constexpr int SPB_PF = 3;  // staged 16-B vectors per thread (4 pooled rows x Wo x C / 8 <= 768)
 template <int C>  // channels (compile-time: the index math is shifts)
-__global__ void __launch_bounds__(256, 3) stem_pool_bwd_k(const bf16 *__restrict__ dy, const uint8_t *__restrict__ am,
+__global__ void __launch_bounds__(256, 2) stem_pool_bwd_k(const bf16 *__restrict__ dy, const uint8_t *__restrict__ am,
                                                        const bf16 *__restrict__ h, int N, int D, int H, int W, int,
                                                        int Do, int Ho, int Wo, const float *__restrict__ scale,
                                                        const float *__restrict__ shift, const float *__restrict__ mean,
@@ -1139,13 +1172,23 @@ __global__ void __launch_bounds__(256, 3) stem_pool_bwd_k(const bf16 *__restrict
     __syncthreads();
     if (u + (int)gridDim.x < units) stage_load(u + gridDim.x);
     const int items = 2 * W * G;
+    // item -> (ih parity r, iw): voxels v < We have even iw = 2v, the rest odd iw, so
+    // that a warp's 4 voxels share their parity class (specialised gather below)
+    const int We = (W + 1) / 2;
+    auto item_iw = [&](int it, int &r) {
+      const int v = it / G;
+      r = v >= W;
+      const int vv = v - (r ? W : 0);
+      return vv < We ? 2 * vv : 2 * (vv - We) + 1;
+    };
     // h of all this thread's items of the unit, loaded up front (one exposed
     // round trip per unit instead of one per item)
     uint4 hq[SPB_PF];
 #pragma unroll
     for (int q = 0; q < SPB_PF; ++q) {
       const int it = threadIdx.x + q * 256;
-      const int r = it >= WG, iw = (it - (r ? WG : 0)) / G;
+      int r;
+      const int iw = item_iw(it, r);
       const int ih = 2 * j + r;
       if (it < items && ih < H) hq[q] = ld16(h + (((int64_t)(nn * D + id) * H + ih) * W + iw) * C + cg);
     }
@@ -1153,7 +1196,8 @@ __global__ void __launch_bounds__(256, 3) stem_pool_bwd_k(const bf16 *__restrict
     for (int q = 0; q < SPB_PF; ++q) {
       const int it = threadIdx.x + q * 256;
       if (it >= items) break;
-      const int r = it >= WG, iw = (it - (r ? WG : 0)) / G;
+      int r;
+      const int iw = item_iw(it, r);
       const int ih = 2 * j + r;
       if (ih >= H) continue;
       const int64_t o = (((int64_t)(nn * D + id) * H + ih) * W + iw) * C + cg;
@@ -1162,24 +1206,16 @@ __global__ void __launch_bounds__(256, 3) stem_pool_bwd_k(const bf16 *__restrict
       float acc[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int od = (q & 4) ? od1 : od0;
-        const int oh = (ih + (q >> 1 & 1)) >> 1, ow = (iw + (q & 1)) >> 1;
-        const bool ok = od >= 0 && oh < Ho && ow < Wo && (!(q & 4) || (id & 1)) && (!(q & 2) || (ih & 1)) &&
-                        (!(q & 1) || (iw & 1));
-        if (!ok) continue;
-        const int slot = ((q & 4) ? 2 : 0) + (oh - j);
-        const int tap = ((id - 2 * od + 1) * 3 + (ih - 2 * oh + 1)) * 3 + (iw - 2 * ow + 1);
-        const int e0 = slot * rowel + ow * C + cg;
-        float f[8];
-        load_vec(sdy + e0, f);
-        uint8_t code[8];
-        const uint2 a = *reinterpret_cast<const uint2 *>(sam + e0);
-        memcpy(code, &a, 8);
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if (code[e] == tap) acc[e] += f[e];
+      const int ow0 = iw >> 1;
+      switch (((id & 1) << 2) | (r << 1) | (iw & 1)) {
+        case 0: pool_gather<C, 0, 0, 0>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
+        case 1: pool_gather<C, 0, 0, 1>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
+        case 2: pool_gather<C, 0, 1, 0>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
+        case 3: pool_gather<C, 0, 1, 1>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
+        case 4: pool_gather<C, 1, 0, 0>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
+        case 5: pool_gather<C, 1, 0, 1>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
+        case 6: pool_gather<C, 1, 1, 0>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
+        default: pool_gather<C, 1, 1, 1>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
       }
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -1614,7 +1650,7 @@ void maxpool_bwd(DType dt, const void *dy, const uint8_t *argmax, int N, int D, 
   LAUNCH_CHECK();
 }
 
-int stem_pool_bwd_blocks() { return 148 * 3; }
+int stem_pool_bwd_blocks() { return 148 * 2; }
 
 void stem_pool_bwd(const void *dy, const uint8_t *argmax, const void *h, int N, int D, int H, int W, int C, int Do,
                    int Ho, int Wo, const float *scale, const float *shift, const float *mean, const float *invstd,
