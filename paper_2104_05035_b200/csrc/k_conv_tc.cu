@@ -94,11 +94,19 @@ struct Smem {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int RED_OFF = STAGES * STAGE;   // [4 warps][2][BN] fp32 BN-statistics accumulators
   static constexpr int BAR_OFF = RED_OFF + 4 * 2 * BN * 4;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
+  static constexpr int TAB_OFF = BAR_OFF + 256;       // per-tap TMA table (the producer's hot loop)
+  static constexpr int TOTAL = TAB_OFF + MAX_TAPS * 16 + 1024;  // + alignment slack
 };
 
 struct Item {
   int c, split, nb, tw, th, td, tn, kb0, kb1;
+};
+// one tap's TMA coordinates, staged in smem (indexed kernel-parameter loads in
+// the producer loop measured as a visible stall)
+struct __align__(16) TapEnt {
+  const CUtensorMap *amap, *bmap;
+  int16_t od, oh, ow, pad;
+  int kcoord;
 };
 __device__ __forceinline__ Item decode_item(const TcParams &p, int64_t item) {
   Item it;
@@ -119,8 +127,10 @@ __device__ __forceinline__ Item decode_item(const TcParams &p, int64_t item) {
   return it;
 }
 
+// deep-ring variants (one CTA per SM by smem) get the whole register file: no spills
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_constant__ TcParams p) {
+__global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE > 110 * 1024) ? 1 : 2)
+    conv_tc_kernel(const __grid_constant__ TcParams p) {
   using S = Smem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -129,8 +139,17 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+  TapEnt *tab = (TapEnt *)(smem + S::TAB_OFF);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane < p.n_taps) {
+    TapEnt e;
+    e.amap = &p.a_map[p.tap_map[lane]];
+    e.bmap = p.tap_bsel[lane] ? &p.b_map2 : &p.b_map;
+    e.od = p.tap_od[lane]; e.oh = p.tap_oh[lane]; e.ow = p.tap_ow[lane]; e.pad = 0;
+    e.kcoord = p.tap_kcoord[lane];
+    tab[lane] = e;
+  }
   constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                   : (2 * BN <= 256) ? 256 : 512;
 
@@ -168,16 +187,17 @@ __global__ void __launch_bounds__(TC_THREADS, 2) conv_tc_kernel(const __grid_con
         const Item it = decode_item(p, item);
         const int w0 = it.tw * p.bw, h0 = it.th * p.bh, d0 = it.td * p.bd, n0 = it.tn * p.bn;
         const int nb = it.nb;
+        const int tap0 = p.cls_tap0[it.c], kpt = p.kblocks_per_tap;
+        int t = tap0 + it.kb0 / kpt, cb = it.kb0 % kpt;
         for (int kb = it.kb0; kb < it.kb1; ++kb) {
-          const int t = p.cls_tap0[it.c] + kb / p.kblocks_per_tap, cb = kb % p.kblocks_per_tap;
+          const TapEnt e = tab[t];
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * S::STAGE;
           uint8_t *sb = sa + S::A_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], S::STAGE);
-          tc::tma_load_5d(sa, &p.a_map[p.tap_map[t]], &full[stage], cb * 64, w0 + p.tap_ow[t], h0 + p.tap_oh[t],
-                          d0 + p.tap_od[t], n0);
-          tc::tma_load_2d(sb, p.tap_bsel[t] ? &p.b_map2 : &p.b_map, &full[stage], p.tap_kcoord[t] + cb * 64,
-                          nb * BN);
+          tc::tma_load_5d(sa, e.amap, &full[stage], cb * 64, w0 + e.ow, h0 + e.oh, d0 + e.od, n0);
+          tc::tma_load_2d(sb, e.bmap, &full[stage], e.kcoord + cb * 64, nb * BN);
+          if (++cb == kpt) { cb = 0; ++t; }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
