@@ -40,6 +40,7 @@ namespace {
 
 constexpr int WG_THREADS = 192;
 constexpr int MAX_ATOMS = 128;  // M-tiles per problem (2 atoms each)
+constexpr int ATAB_MAX = 32;    // x atoms staged per CTA (per-tap mode: 2 G)
 
 struct __align__(64) WgParams {
   CUtensorMap x_map[8];
@@ -74,6 +75,14 @@ struct WgSmem {
   static constexpr int X_MAX = 110 * 1024 - DY_BYTES;  // x bytes per stage (haloed region or atoms)
 };
 
+// one x atom's TMA coordinates, staged in smem for the producer (indexed
+// kernel-parameter loads stall the single issuing thread)
+struct __align__(16) AtomEnt {
+  const CUtensorMap *map;
+  int c;
+  int8_t od, oh, ow, pad;
+};
+
 template <int BN, int STAGES, int XBYTES>
 __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_constant__ WgParams p) {
   constexpr int DYB = (BN / 64) * 16384;
@@ -84,6 +93,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
   uint64_t *empty = full + STAGES;
   uint64_t *done = empty + STAGES;
   uint32_t *tmem_slot = (uint32_t *)(done + 1);
+  AtomEnt *atab = (AtomEnt *)(smem + STAGES * STAGE + 256);  // [2 * G]
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
   // CTA -> (m-group, co block, split)
@@ -96,6 +106,15 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
   const int64_t vt0 = (int64_t)split * p.vt_per_split;
   const int64_t vt1 = min(p.n_vtiles, vt0 + p.vt_per_split);
 
+  if (warp == 0 && !p.haloed)
+    for (int a = lane; a < 2 * G; a += 32) {
+      const int at = 2 * mt0 + a;
+      AtomEnt e;
+      e.map = &p.x_map[p.atom_map[at]];
+      e.c = p.atom_cb[at] * 64;
+      e.od = p.atom_od[at]; e.oh = p.atom_oh[at]; e.ow = p.atom_ow[at]; e.pad = 0;
+      atab[a] = e;
+    }
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) {
       tc::mbar_init(&full[i], 1);
@@ -135,9 +154,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
           tc::tma_load_5d(sx, &p.x_map[0], &full[stage], 0, w0 - 1, h0 - 1, d0 - 1, n0);
         } else {
           for (int a = 0; a < 2 * G; ++a) {
-            const int at = 2 * mt0 + a;
-            tc::tma_load_5d(sx + a * 16384, &p.x_map[p.atom_map[at]], &full[stage], p.atom_cb[at] * 64,
-                            w0 + p.atom_ow[at], h0 + p.atom_oh[at], d0 + p.atom_od[at], n0);
+            const AtomEnt e = atab[a];
+            tc::tma_load_5d(sx + a * 16384, e.map, &full[stage], e.c, w0 + e.ow, h0 + e.oh, d0 + e.od, n0);
           }
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -279,7 +297,7 @@ __global__ void wg_reduce_add(const float *__restrict__ part, int splits, int64_
 template <int BN, int STAGES, int XBYTES>
 void wg_launch(const WgParams &p, int grid, cudaStream_t st) {
   constexpr int STAGE = (BN / 64) * 16384 + XBYTES;
-  constexpr int SMEM = STAGES * STAGE + 256 + 1024;
+  constexpr int SMEM = STAGES * STAGE + 256 + ATAB_MAX * 16 + 1024;
   static bool attr = false;
   if (!attr) {
     CUDA_CHECK(cudaFuncSetAttribute(wgrad_tc_kernel<BN, STAGES, XBYTES>,
@@ -382,6 +400,7 @@ void conv_wgrad_tc(const ConvGeom &g, const bf16 *x, const bf16 *dy, float *dw, 
   memset(&p, 0, sizeof p);
   p.haloed = s.haloed;
   p.G = s.G;
+  if (!s.haloed && 2 * s.G > ATAB_MAX) throw Error(RN_ERR_STATE, "conv_wgrad_tc: atom table overflow");
   p.n_mgroups = s.n_mgroups;
   p.n_cob = s.n_cob;
   p.splits = s.splits;
