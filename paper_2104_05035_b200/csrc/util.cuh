@@ -73,4 +73,9 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+
+// pull one line into L2 ahead of use (no register, no completion tracking)
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 }  // namespace rn

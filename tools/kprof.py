@@ -24,6 +24,9 @@ if os.environ.get("KPROF_NOGRAPH"):
     plan.set_option("graphs", 0)
 if os.environ.get("KPROF_NOSIDE"):
     plan.set_option("wgrad_stream", 0)
+for kv in filter(None, os.environ.get("KPROF_OPTS", "").split(",")):  # e.g. KPROF_OPTS=fused_stats=0
+    k, v = kv.split("=")
+    plan.set_option(k, int(v))
 arrays = synthetic.init_params(plan.tensors, seed=0)
 plan.set_params(np.concatenate([a.ravel() for a in arrays]).astype(np.float32))
 x, y = synthetic.make_batch(batch, *dims, seed=1)
