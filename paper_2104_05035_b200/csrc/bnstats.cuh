@@ -17,9 +17,13 @@ namespace rn {
 struct EpiStats {
   float *part = nullptr;       // [gridDim.x][2][C]
   const bf16 *mask = nullptr;  // mode 2
-  const bf16 *h = nullptr;     // mode 2
-  const float *mean = nullptr; // mode 2: the consumer BN's batch mean per channel
-  int mode = 0;                // 0 off, 1 forward, 2 backward
+  const bf16 *h = nullptr;     // modes 2, 3
+  const float *mean = nullptr; // modes 2, 3: the consumer BN's batch mean per channel
+  // mode 3: the consumer's ReLU mask recomputed from h, (h*mscale + mshift > 0) — the
+  // forward apply's own fp32 pre-activation (scale/shift as it stored them), so one
+  // tensor stream less than mode 2 (valid for a BN + ReLU without residual)
+  const float *mscale = nullptr, *mshift = nullptr;
+  int mode = 0;                // 0 off, 1 forward, 2 backward (mask tensor), 3 backward (recomputed mask)
 };
 
 // x[j] (channel j of this lane's row) summed over the 32 lanes; lane l returns
@@ -44,10 +48,10 @@ struct StatsPf {
   uint4 m[4], h[4];
 };
 __device__ __forceinline__ void epi_stats_prefetch(const EpiStats &st, bool valid, int64_t eo, StatsPf &pf) {
-  if (st.mode != 2 || !valid) return;
+  if (st.mode < 2 || !valid) return;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    pf.m[i] = __ldg(reinterpret_cast<const uint4 *>(st.mask + eo) + i);
+    if (st.mode == 2) pf.m[i] = __ldg(reinterpret_cast<const uint4 *>(st.mask + eo) + i);
     pf.h[i] = __ldg(reinterpret_cast<const uint4 *>(st.h + eo) + i);
   }
 }
@@ -79,9 +83,19 @@ __device__ __forceinline__ void epi_stats_add(const EpiStats &st, const float *f
     float m[32], h[32];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      unpack_bf16x8(pf.m[i], m + 8 * i);
       unpack_bf16x8(pf.h[i], h + 8 * i);
+      if (st.mode == 2) unpack_bf16x8(pf.m[i], m + 8 * i);
     }
+    if (st.mode == 3)
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        const float4 a = __ldg(reinterpret_cast<const float4 *>(st.mscale + c0 + j));
+        const float4 b = __ldg(reinterpret_cast<const float4 *>(st.mshift + c0 + j));
+        m[j] = fmaf(h[j], a.x, b.x);
+        m[j + 1] = fmaf(h[j + 1], a.y, b.y);
+        m[j + 2] = fmaf(h[j + 2], a.z, b.z);
+        m[j + 3] = fmaf(h[j + 3], a.w, b.w);
+      }
 #pragma unroll
     for (int j = 0; j < 32; j += 4) {
       const float4 mu = __ldg(reinterpret_cast<const float4 *>(st.mean + c0 + j));

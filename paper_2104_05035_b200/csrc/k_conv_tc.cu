@@ -486,9 +486,12 @@ __global__ void __launch_bounds__(512) splitk_finish_k(const float *__restrict__
     store_vec(y + o, f);
     if (st.mode) {
       float m[8], h[8];
-      if (st.mode == 2) {
-        load_vec(st.mask + o, m);
+      if (st.mode >= 2) {
         load_vec(st.h + o, h);
+        if (st.mode == 2) load_vec(st.mask + o, m);
+        else
+#pragma unroll
+          for (int j = 0; j < 8; ++j) m[j] = fmaf(h[j], st.mscale[c0 + j], st.mshift[c0 + j]);
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -593,9 +596,12 @@ __global__ void __launch_bounds__(512) splitk_finish_cls_k(const float *__restri
     store_vec(y + o, f);
     if (st.mode) {
       float m[8], hh[8];
-      if (st.mode == 2) {
-        load_vec(st.mask + o, m);
+      if (st.mode >= 2) {
         load_vec(st.h + o, hh);
+        if (st.mode == 2) load_vec(st.mask + o, m);
+        else
+#pragma unroll
+          for (int j = 0; j < 8; ++j) m[j] = fmaf(hh[j], st.mscale[c0 + j], st.mshift[c0 + j]);
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {

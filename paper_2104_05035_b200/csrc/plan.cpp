@@ -360,6 +360,11 @@ bool Plan::use_halo() const {
   return it == opts.end() || it->second != 0;
 }
 
+bool Plan::recompute_mask() const {
+  auto it = opts.find("recompute_mask");
+  return it == opts.end() || it->second != 0;
+}
+
 bool Plan::use_pair() const {
   auto it = opts.find("pair_conv");
   return it == opts.end() || it->second != 0;
@@ -411,10 +416,12 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
   const bool want = stats.bn && fused_stats();
   if (want) {
     es.part = (float *)P(stats.bn->bpart);
-    es.mode = 2;
+    es.mode = stats.mscale && recompute_mask() ? 3 : 2;
     es.mask = (const bf16 *)stats.mask;
     es.h = (const bf16 *)stats.h;
     es.mean = stats.mean;
+    es.mscale = stats.mscale;
+    es.mshift = stats.mshift;
   }
   int parts = 0, kind = K_SIMT;
   if (use_tc(c.g, true) && use_pair() && pair_conv_supported(c.g, true) && (kind = K_PAIR))
@@ -449,10 +456,12 @@ void Plan::conv_bwd_data_proj(const ConvL &c1, const void *dy1, const ConvL &cp,
   const bool want = stats.bn && fused_stats();
   if (want) {
     es.part = (float *)P(stats.bn->bpart);
-    es.mode = 2;
+    es.mode = stats.mscale && recompute_mask() ? 3 : 2;
     es.mask = (const bf16 *)stats.mask;
     es.h = (const bf16 *)stats.h;
     es.mean = stats.mean;
+    es.mscale = stats.mscale;
+    es.mshift = stats.mshift;
   }
   const int parts = conv_dgrad_tc(c1.g, (const bf16 *)dy1, (const bf16 *)P(shadow_d[c1.w_idx]), (bf16 *)dx,
                                   accumulate, nullptr, nullptr, (float *)P(off_conv_ws), conv_ws_floats, stream,
@@ -599,6 +608,8 @@ void Plan::block_bwd(BlockL &B, int k, const void *x, const void *dout, void *dx
   t1.mask = P(B.a1[k]);
   t1.h = P(B.h1[k]);
   t1.mean = bn_stat(B.b1, k, 0);
+  t1.mscale = bn_stat(B.b1, k, 2);
+  t1.mshift = bn_stat(B.b1, k, 3);
   conv_bwd_data(B.c2, P(B.dh2), P(B.da1), false, nullptr, nullptr, t1);
   bn_backward(B.b1, k, P(B.da1), P(B.h1[k]), MASK_TENSOR, P(B.a1[k]), P(B.dh1), 0);
   conv_bwd_weight(B.c1, x, P(B.dh1), false);
@@ -745,6 +756,8 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
     tm.mask = P(L.r[k]);
     tm.h = P(L.mh[k]);
     tm.mean = bn_stat(L.mbn, k, 0);
+    tm.mscale = bn_stat(L.mbn, k, 2);
+    tm.mshift = bn_stat(L.mbn, k, 3);
     conv_bwd_data(L.mc2, P(L.dm), P(L.dr), false, nullptr, nullptr, tm);
     bn_backward(L.mbn, k, P(L.dr), P(L.mh[k]), MASK_TENSOR, P(L.r[k]), P(L.dmh), 0);
     conv_bwd_weight(L.mc1, P(L.up[k]), P(L.dmh), false);
@@ -1122,7 +1135,8 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 
 rn_status Plan::set_option(const std::string &k, int64_t v) {
   if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv" && k != "fused_stats" &&
-      k != "pair_conv" && k != "wgrad_stream" && k != "merge_proj" && k != "stem_bwd_fused")
+      k != "pair_conv" && k != "wgrad_stream" && k != "merge_proj" && k != "stem_bwd_fused" &&
+      k != "recompute_mask")
     return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;

@@ -36,6 +36,9 @@ struct StatsTarget {
   const void *mask = nullptr;   // backward: the consumer's ReLU output
   const void *h = nullptr;      // backward: the consumer's BN input
   const float *mean = nullptr;  // backward: the consumer's batch mean
+  // backward, optional: the consumer's BN scale/shift — its ReLU mask is then
+  // recomputed from h (BN + ReLU without residual), the mask tensor is not read
+  const float *mscale = nullptr, *mshift = nullptr;
 };
 
 struct ConvL {
@@ -142,6 +145,7 @@ struct Plan {
   bool use_tc(const ConvGeom &g, bool dgrad) const;
   bool use_halo() const;
   bool use_pair() const;
+  bool recompute_mask() const;
   void conv_fwd(const ConvL &c, const void *x, void *y, const float *bias = nullptr, BNL *stats = nullptr);
   void conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumulate, const void *res,
                      const void *res_mask, const StatsTarget &stats = StatsTarget());

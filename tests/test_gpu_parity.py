@@ -252,6 +252,25 @@ def test_fused_stem_backward_matches_separate_kernels():
         assert rel(g1[idx[name]], g0[idx[name]]) <= 1e-4, name
 
 
+def test_recomputed_relu_mask_matches_mask_tensor():
+    """Backward BN sums fused into the dgrad epilogues with the consumer's ReLU
+    mask recomputed from h (h*scale + shift > 0, the forward apply's own fp32
+    pre-activation) select exactly the voxels the stored mask tensor selects:
+    every gradient is bitwise identical to the mask-tensor path."""
+    dims = (91, 109, 91)
+    grads = []
+    for rec in (1, 0):
+        plan = rn.Plan(rn.net_desc(18, 64, dims), 2, rn.RN_BF16)
+        plan.set_option("recompute_mask", rec)
+        arrays = synthetic.perturb_params(plan.tensors, synthetic.init_params(plan.tensors, seed=0))
+        plan.set_params(np.concatenate([a.ravel() for a in arrays]).astype(np.float32))
+        x, y = synthetic.make_batch(2, *dims, seed=1)
+        plan.forward(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+        plan.backward()
+        grads.append(plan.get_grads())
+    assert np.array_equal(grads[0], grads[1])
+
+
 def test_pipelined_host_steps_match_single_steps():
     """rn_train_steps_host (step i+1's H2D overlapped with step i) computes
     exactly what the same number of rn_train_step_host calls computes."""
