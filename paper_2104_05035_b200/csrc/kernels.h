@@ -124,6 +124,10 @@ struct UpTables {  // device pointers
 };
 void upsample_fwd(DType dt, const void *x, int N, int Di, int Hi, int Wi, int C, void *y, int Do, int Ho, int Wo,
                   const UpTables &t, cudaStream_t st);
+// separable trilinear adjoint (bf16): three passes w, h, d with fp32 intermediates in ws
+size_t upsample_bwd_ws_floats(int N, int Di, int Hi, int Wi, int C, int Do, int Ho, int Wo);
+void upsample_bwd_sep(const void *dy, int N, int Di, int Hi, int Wi, int C, void *dx, int Do, int Ho, int Wo,
+                      const UpTables &t, float *ws, cudaStream_t st);
 void upsample_bwd(DType dt, const void *dy, int N, int Di, int Hi, int Wi, int C, void *dx, int Do, int Ho, int Wo,
                   const UpTables &t, cudaStream_t st);
 // out = (1 + sigmoid(m)) * T

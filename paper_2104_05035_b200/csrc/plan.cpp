@@ -238,6 +238,14 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
   off_counter = alloc(256);  // last-block tickets of the fused reduce+finalize kernels (zeroed at bind)
   off_wgrad_ws = alloc(sizeof(float) * (wgrad_ws_floats ? wgrad_ws_floats : 1));
   off_conv_ws = alloc(sizeof(float) * (conv_ws_floats ? conv_ws_floats : 1));
+  size_t up_floats = 1;
+  for (int ui = 0; ui < (int)net.units.size(); ++ui) {
+    const Unit &u = net.units[ui];
+    if (u.kind == U_ATT && local[ui])
+      up_floats = std::max(up_floats, upsample_bwd_ws_floats(mb, u.mask.d, u.mask.h, u.mask.w, u.cout, u.in.d,
+                                                             u.in.h, u.in.w));
+  }
+  off_up_ws = alloc(sizeof(float) * up_floats);
 
   // --- communicators ---
   if (world > 1) {
@@ -762,7 +770,13 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
     bn_backward(L.mbn, k, P(L.dr), P(L.mh[k]), MASK_TENSOR, P(L.r[k]), P(L.dmh), 0);
     conv_bwd_weight(L.mc1, P(L.up[k]), P(L.dmh), false);
     conv_bwd_data(L.mc1, P(L.dmh), P(L.dup), false, nullptr, nullptr);
-    upsample_bwd(dt, P(L.dup), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.dum), u.in.d, u.in.h, u.in.w, L.tab, stream);
+    auto itu = opts.find("up_bwd_sep");
+    if (dt == DT_BF16 && (itu == opts.end() || itu->second != 0))
+      upsample_bwd_sep(P(L.dup), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.dum), u.in.d, u.in.h, u.in.w, L.tab,
+                       (float *)P(off_up_ws), stream);
+    else
+      upsample_bwd(dt, P(L.dup), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.dum), u.in.d, u.in.h, u.in.w, L.tab,
+                   stream);
     block_bwd(L.mask, k, P(L.u0[k]), P(L.dum), P(L.du0), false);
     maxpool_bwd(dt, P(L.du0), (const uint8_t *)P(L.am[k]), mb, u.in.d, u.in.h, u.in.w, C, u.mask.d, u.mask.h,
                 u.mask.w, dx, false, stream);
@@ -1136,7 +1150,7 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 rn_status Plan::set_option(const std::string &k, int64_t v) {
   if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv" && k != "fused_stats" &&
       k != "pair_conv" && k != "wgrad_stream" && k != "merge_proj" && k != "stem_bwd_fused" &&
-      k != "recompute_mask")
+      k != "recompute_mask" && k != "up_bwd_sep")
     return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;

@@ -108,7 +108,7 @@ struct Plan {
   size_t off_counter = 0;
   unsigned *counter() { return (unsigned *)P(off_counter); }
   size_t off_partial = 0, off_coef = 0, off_wgrad_ws = 0, off_x = 0, off_y = 0;
-  size_t wgrad_ws_floats = 0, conv_ws_floats = 0, off_conv_ws = 0;
+  size_t wgrad_ws_floats = 0, conv_ws_floats = 0, off_conv_ws = 0, off_up_ws = 0;
   size_t off_pack = 0, off_sgdrg = 0;
   int n_pack = 0, n_sgdrg = 0, max_pack = 0, max_sgdrg = 0;
   int64_t pack_tiles = 0;
