@@ -246,6 +246,8 @@ int64_t rn_kernel_launches(rn_plan_t plan);
  *  "merge_proj"    : 1 stage-entry projection dgrad merged into the stride-2 dgrad launch (default 1)
  *  "stem_bwd_fused": 1 fused stem backward (pool adjoint + mask + BN sums; BN apply in the wgrad) (default 1)
  *  "recompute_mask": 1 dgrad-epilogue BN sums recompute the consumer's ReLU mask from h (default 1)
+ *  "pair_bwd_stats": 1 fuse the backward BN sums into the CTA-pair dgrad epilogue (default 0: standalone pass)
+ *  "up_bwd_sep"    : 1 separable trilinear adjoint (default 1)
  * Unknown keys: RN_ERR_ARG.  Every switch changes kernels only, not the result beyond fp32 rounding. */
 rn_status rn_set_option(rn_plan_t plan, const char *key, int64_t value);
 

@@ -432,9 +432,15 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
     es.mshift = stats.mshift;
   }
   int parts = 0, kind = K_SIMT;
+  // the CTA-pair dgrad's epilogue is the kernel's bottleneck: its backward BN sums
+  // cost more fused (~14 us per stage-1 launch) than the standalone partials pass
+  // (~8 us), so by default they are left to bn_backward (option pair_bwd_stats)
+  auto itp = opts.find("pair_bwd_stats");
+  const bool pair_stats = itp != opts.end() && itp->second != 0;
   if (use_tc(c.g, true) && use_pair() && pair_conv_supported(c.g, true) && (kind = K_PAIR))
     parts = conv_pair(c.g, true, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx,
-                      accumulate, (const bf16 *)res, (const bf16 *)res_mask, stream, want ? &es : nullptr);
+                      accumulate, (const bf16 *)res, (const bf16 *)res_mask, stream,
+                      want && pair_stats ? &es : nullptr);
   else if (use_tc(c.g, true) && use_halo() && halo_conv_supported(c.g, true) && (kind = K_HALO))
     parts = conv_halo(c.g, true, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx,
                       accumulate, (const bf16 *)res, (const bf16 *)res_mask, stream, want ? &es : nullptr);
@@ -1150,7 +1156,7 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 rn_status Plan::set_option(const std::string &k, int64_t v) {
   if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv" && k != "fused_stats" &&
       k != "pair_conv" && k != "wgrad_stream" && k != "merge_proj" && k != "stem_bwd_fused" &&
-      k != "recompute_mask" && k != "up_bwd_sep")
+      k != "recompute_mask" && k != "up_bwd_sep" && k != "pair_bwd_stats")
     return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;
