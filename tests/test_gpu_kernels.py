@@ -83,3 +83,36 @@ def test_conv_wgrad(cv, impl):
     _, dw_ref = O.conv3d_backward(xn, np.zeros((Co, Ci, k, k, k)), dyn, s, p, need_dx=False)
     got = dw.cpu().numpy().reshape(Co, k, k, k, Ci).transpose(0, 4, 1, 2, 3)
     assert rel(got, dw_ref) < 1e-4
+
+
+@pytest.mark.parametrize("cv", CONVS, ids=[c[0] for c in CONVS])
+def test_conv_bench_batch(cv):
+    """The launch configuration bench.py times: batch 8 (BASELINE configs[1]) and
+    the plan's own dispatch (impl 0: CTA pair for 64->64 stride 1, tcgen05 with its
+    batch-8 tiling / ring depth / split-K / parity classes otherwise) for fprop,
+    dgrad and wgrad, against the float64 oracle on the same bf16 values."""
+    name, Di, Hi, Wi, Ci, Co, k, s, p = cv
+    N = 8
+    Do, Ho, Wo = (O.conv_out(v, k, s, p) for v in (Di, Hi, Wi))
+    rng = np.random.default_rng(2)
+    x = bf16_vals((N, Di, Hi, Wi, Ci), rng)
+    w = bf16_vals((Co, k * k * k, Ci), rng, scale=(2.0 / (Co * k ** 3)) ** 0.5)
+    dy = bf16_vals((N, Do, Ho, Wo, Co), rng)
+    geom = [N, Di, Hi, Wi, Ci, Do, Ho, Wo, Co, k, s, p]
+    y = torch.empty((N, Do, Ho, Wo, Co), dtype=torch.bfloat16, device="cuda")
+    dx = torch.empty((N, Di, Hi, Wi, Ci), dtype=torch.bfloat16, device="cuda")
+    dw = torch.empty((Co, k ** 3, Ci), dtype=torch.float32, device="cuda")
+    xd, wd, dyd = x.cuda(), w.cuda(), dy.cuda()
+    rn.op_conv3d(rn.RN_BF16, 0, geom, xd, wd, y, 0)
+    rn.op_conv3d(rn.RN_BF16, 1, geom, dyd, wd, dx, 0)
+    rn.op_conv3d(rn.RN_BF16, 2, geom, xd, dyd, dw, 0)
+    torch.cuda.synchronize()
+    wc = w.float().numpy().astype(np.float64).reshape(Co, k, k, k, Ci).transpose(0, 4, 1, 2, 3)
+    xn = x.float().numpy().astype(np.float64)
+    dyn = dy.float().numpy().astype(np.float64)
+    y_ref = O.conv3d(xn, wc, s, p)
+    dx_ref, dw_ref = O.conv3d_backward(xn, wc, dyn, s, p)
+    assert rel(y.float().cpu().numpy(), y_ref) < 4e-3
+    assert rel(dx.float().cpu().numpy(), dx_ref) < 4e-3
+    got = dw.cpu().numpy().reshape(Co, k, k, k, Ci).transpose(0, 4, 1, 2, 3)
+    assert rel(got, dw_ref) < 1e-4

@@ -133,6 +133,44 @@ def test_bf16_step(depth, w, dims, N):
     assert rel(res["g"], ref["grad"]) <= max(2e-2, 3 * floor["_global"])
 
 
+def test_bf16_step_bench_config():
+    """The whole step in the configuration bench.py times (r18, batch 8, full
+    91x109x91 volumes, bf16, default options: CUDA graphs, side stream, fused
+    kernels): loss within 2e-2 of the float64 oracle and 1e-2 of the
+    bf16-storage oracle (X23), every gradient tensor and the global gradient
+    within max(2e-2, 3 x the chaos floor) of the bf16-storage oracle — the
+    criterion of test_bf16_step, here at the bench's batch."""
+    dims, N = (91, 109, 91), 8
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        plan = rn.Plan(rn.net_desc(18, 64, dims), N, rn.RN_BF16, stream=st)
+        net = O.Net(18, 64, dims, store="bf16")
+        arrays = synthetic.perturb_params(net.tensors, synthetic.init_params(net.tensors, seed=0))
+        plan.set_params(np.concatenate([a.ravel() for a in arrays]).astype(np.float32))
+        x, y = synthetic.make_batch(N, *dims, seed=1)
+        xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        for _ in range(2):  # second step replays the captured graphs; parameters restored in between
+            plan.set_params(np.concatenate([a.ravel() for a in arrays]).astype(np.float32))
+            loss = plan.forward(xd, yd)
+            plan.backward()
+            g = plan.get_grads()
+        st.synchronize()
+    ref = net.train_step(arrays, x, y, LR)
+    ref64 = O.Net(18, 64, dims).train_step(arrays, x, y, LR)
+    assert abs(loss - ref64["loss"]) <= 2e-2 * abs(ref64["loss"]), (loss, ref64["loss"])
+    assert abs(loss - ref["loss"]) <= 1e-2 * abs(ref["loss"]), (loss, ref["loss"])
+    floor = bf16_noise_floor(net, arrays, x, y, ref)
+    off, bad = 0, []
+    for name, shape, kind in net.tensors:
+        n = int(np.prod(shape))
+        e = rel(g[off:off + n], ref["grad"][off:off + n])
+        if e > max(2e-2, 3 * floor[name]):
+            bad.append((name, e, floor[name]))
+        off += n
+    assert not bad, bad[:8]
+    assert rel(g, ref["grad"]) <= max(2e-2, 3 * floor["_global"]), (rel(g, ref["grad"]), floor["_global"])
+
+
 def test_gpu_deterministic():
     a = run_both(0, 8, (16, 16, 16), 2, rn.RN_F32)
     b = run_both(0, 8, (16, 16, 16), 2, rn.RN_F32)
