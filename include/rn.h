@@ -76,6 +76,13 @@ typedef struct {
   int32_t init_attempts;     /* random draws per initial chromosome (64; G19)         */
   int32_t require_all_used;  /* 1: "each GPU runs at least one partition" (G7) */
   int32_t early_stop_at_ub;  /* 1: stop when f(Z*) == sum_i max_j c_ij (G18)   */
+  int32_t objective;         /* 0: Eq. 3 profit sum_i p_i/d_{g_i} (the paper, default);
+                              * 1: bottleneck f = lb / max_j(L_j/d_j), lb = max(sum p/sum d,
+                              *    max p/max d) — SURVEY §8(f) f2, not in the paper: the GA
+                              *    then minimises the slowest GPU's normalised load (the
+                              *    pipeline step time), which Eq. 3 cannot see on identical
+                              *    GPUs (its value is the same for every feasible placement);
+                              *    early stop at f = 1.  profit_out reports f.               */
 } rn_ga_params;
 
 /* Fill *gp with the defaults above (seed 7). */

@@ -129,12 +129,46 @@ def profit_matrix(p, d):
     return [[float(pi) / float(dj) for dj in d] for pi in p]
 
 
-def fitness(genes, c):
+def profit_fitness(genes, c):
     """Fitness equation (reading G9): f = sum_i c[i][gene_i], left to right."""
     f = 0.0
     for i, g in enumerate(genes):
         f = f + c[i][g]
     return f
+
+
+fitness = profit_fitness
+
+
+def bottleneck_bound(p, d):
+    """SURVEY §8(f) f2 (not in the paper): lower bound of the bottleneck load
+    ratio max_j L_j / d_j over all placements — max(sum p / sum d, max p / max d)
+    (the work must fit the total capacity; the largest partition sits somewhere)."""
+    sp, sd = 0, 0
+    for v in p:
+        sp += v
+    for v in d:
+        sd += v
+    a = float(sp) / float(sd)
+    b = float(max(p)) / float(max(d))
+    return a if a > b else b
+
+
+def bottleneck_fitness(genes, p, d, lb):
+    """f2 objective: f = lb / max_j (L_j / d_j) in (0, 1] (1 = the bound is met);
+    the GA maximises it, i.e. minimises the slowest GPU's normalised load — the
+    pipeline step time on identical GPUs, where Eq. 3's profit is flat
+    (finding 3).  max over j ascending with strict >; f = 1 when every load is 0."""
+    m = len(d)
+    load = gpu_loads(genes, p, m)
+    mr = 0.0
+    for j in range(m):
+        r = float(load[j]) / float(d[j])
+        if r > mr:
+            mr = r
+    if mr == 0.0:
+        return 1.0
+    return lb / mr
 
 
 def gpu_loads(genes, p, m):
@@ -193,7 +227,8 @@ def repair(genes, p, d, require_all_used=False):
 # ----------------------------------------------------------------------------
 
 DEFAULT_PARAMS = dict(pop_size=50, t_max=500, p_cross=0.8, p_mut=0.1, seed=7,
-                      dup_retries=20, init_attempts=64, require_all_used=0, early_stop_at_ub=1)
+                      dup_retries=20, init_attempts=64, require_all_used=0, early_stop_at_ub=1,
+                      objective=0)
 
 
 def gabra(p, d, **kw):
@@ -209,6 +244,15 @@ def gabra(p, d, **kw):
         raise ValueError("bad sizes")
     rng = Xoshiro256ss(prm["seed"])
     c = profit_matrix(p, d)                                   # Algorithm 1 line 1
+    obj = int(prm["objective"])
+    if obj not in (0, 1):
+        raise ValueError("objective must be 0 (Eq. 3) or 1 (bottleneck, SURVEY f2)")
+    lb = bottleneck_bound(p, d) if obj == 1 else 0.0
+
+    def fitness(genes, c):                                    # objective 0: Eq. 3 profit
+        if obj == 1:
+            return bottleneck_fitness(genes, p, d, lb)
+        return profit_fitness(genes, c)
 
     # initial population (Algorithm 2; reading G19)
     pop = []
@@ -231,6 +275,8 @@ def gabra(p, d, **kw):
     ub = 0.0
     for i in range(n):
         ub = ub + max(c[i])
+    if obj == 1:
+        ub = 1.0                                              # the bottleneck bound is met
     if E and best_val == ub:                                  # P:277 "optimal profit obtained"
         return best, best_val, gpu_loads(best, p, m)
 
@@ -282,13 +328,18 @@ def gabra(p, d, **kw):
     return best, best_val, gpu_loads(best, p, m)
 
 
-def brute_force(p, d, require_all_used=False, limit=10 ** 7):
-    """Exhaustive Eq. 5 maximiser over all m^n assignments (gene 0 most
-    significant); ties -> lexicographically smallest (first found, strict >)."""
+def brute_force(p, d, require_all_used=False, limit=10 ** 7, objective=0):
+    """Exhaustive Eq. 5 maximiser (objective 0) or bottleneck maximiser
+    (objective 1, f2) over all m^n assignments (gene 0 most significant);
+    ties -> lexicographically smallest (first found, strict >)."""
     n, m = len(p), len(d)
     if m ** n > limit:
         raise OverflowError("instance too large")
     c = profit_matrix(p, d)
+    lb = bottleneck_bound(p, d)
+
+    def fitness(genes, c):
+        return bottleneck_fitness(genes, p, d, lb) if objective == 1 else profit_fitness(genes, c)
     best, best_val = None, None
     genes = [0] * n
     for code in range(m ** n):

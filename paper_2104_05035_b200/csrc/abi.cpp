@@ -81,6 +81,7 @@ void rn_ga_default(rn_ga_params *gp) {
   gp->init_attempts = 64;
   gp->require_all_used = 0;
   gp->early_stop_at_ub = 1;
+  gp->objective = 0;
 }
 
 rn_status rn_gabra_place(int32_t n, const int64_t *loads, int32_t m, const int64_t *caps, const rn_ga_params *gp,
@@ -95,7 +96,7 @@ rn_status rn_gabra_place(int32_t n, const int64_t *loads, int32_t m, const int64
   rn_ga_default(&d);
   const rn_ga_params &g = gp ? *gp : d;
   if (g.pop_size < 2 || g.t_max < 0 || g.dup_retries < 1 || g.init_attempts < 1 || g.p_cross < 0 || g.p_cross > 1 ||
-      g.p_mut < 0 || g.p_mut > 1)
+      g.p_mut < 0 || g.p_mut > 1 || (g.objective != 0 && g.objective != 1))
     return set_error(RN_ERR_ARG, "rn_gabra_place: bad GA parameters");
   return gabra_place(n, loads, m, caps, g, genes_out, profit_out, gpu_load_out);
   GUARD_END

@@ -53,8 +53,22 @@ struct Problem {
   bool U;
   std::vector<double> c;  // c[i*m + j] = p_i / d_j  (Eq. 3, reading G5)
 
-  double fit(const std::vector<int> &g) const {  // fitness, left-to-right (G9)
-    double f = 0.0;
+  int objective = 0;  // 0: Eq. 3 profit (the paper); 1: bottleneck
+  double lb = 0.0;    // objective 1: max(sum p / sum d, max p / max d)
+
+  double fit(const std::vector<int> &g) const {
+    if (objective == 1) {
+      // f2: lb / max_j (L_j / d_j) in (0, 1]; max over j ascending, strict >; 1 when all loads are 0
+      std::vector<int64_t> L;
+      loads(g, L);
+      double mr = 0.0;
+      for (int j = 0; j < m; ++j) {
+        const double r = (double)L[j] / (double)d[j];
+        if (r > mr) mr = r;
+      }
+      return mr == 0.0 ? 1.0 : lb / mr;
+    }
+    double f = 0.0;  // fitness, left-to-right (G9)
     for (int i = 0; i < n; ++i) f = f + c[(size_t)i * m + g[i]];
     return f;
   }
@@ -126,6 +140,20 @@ rn_status gabra_place(int32_t n, const int64_t *loads, int32_t m, const int64_t 
   pr.p = loads;
   pr.d = caps;
   pr.U = gp.require_all_used != 0;
+  pr.objective = gp.objective;
+  {
+    int64_t sp = 0, sd = 0, mp = loads[0], md = caps[0];
+    for (int i = 0; i < n; ++i) {
+      sp += loads[i];
+      if (loads[i] > mp) mp = loads[i];
+    }
+    for (int j = 0; j < m; ++j) {
+      sd += caps[j];
+      if (caps[j] > md) md = caps[j];
+    }
+    const double a = (double)sp / (double)sd, b = (double)mp / (double)md;
+    pr.lb = a > b ? a : b;
+  }
   pr.c.resize((size_t)n * m);
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < m; ++j) pr.c[(size_t)i * m + j] = (double)loads[i] / (double)caps[j];
@@ -160,6 +188,7 @@ rn_status gabra_place(int32_t n, const int64_t *loads, int32_t m, const int64_t 
       if (pr.c[(size_t)i * m + j] > mx) mx = pr.c[(size_t)i * m + j];
     ub = ub + mx;
   }
+  if (pr.objective == 1) ub = 1.0;  // the bottleneck bound is met
 
   auto roulette = [&]() -> const std::vector<int> & {
     double tot = 0.0;

@@ -31,7 +31,7 @@ class RnError(RuntimeError):
 class GaParams(C.Structure):
     _fields_ = [("pop_size", C.c_int32), ("t_max", C.c_int32), ("p_cross", C.c_double), ("p_mut", C.c_double),
                 ("seed", C.c_uint64), ("dup_retries", C.c_int32), ("init_attempts", C.c_int32),
-                ("require_all_used", C.c_int32), ("early_stop_at_ub", C.c_int32)]
+                ("require_all_used", C.c_int32), ("early_stop_at_ub", C.c_int32), ("objective", C.c_int32)]
 
 
 class NetDesc(C.Structure):

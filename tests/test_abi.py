@@ -56,6 +56,35 @@ def test_gabra_bit_exact_vs_oracle():
         pairs += 1
 
 
+def test_gabra_bottleneck_bit_exact_vs_oracle():
+    """objective = 1: C++ == Python over 1000 (instance, seed) pairs."""
+    r = random.Random(5)
+    pairs = 0
+    while pairs < 1000:
+        n = r.randint(1, 12)
+        m = r.randint(1, 5)
+        p = [r.randint(0, 200) for _ in range(n)]
+        if r.random() < 0.5:
+            d = [r.randint(max(max(p), 1), max(max(p), 1) + sum(p) // m + 30) for _ in range(m)]
+        else:
+            d = G.default_capacities([max(v, 1) for v in p], m)
+        kw = dict(seed=r.randint(0, 2 ** 63), pop_size=r.choice([2, 10, 50]), t_max=r.choice([0, 5, 60]),
+                  require_all_used=int(r.random() < 0.2), early_stop_at_ub=int(r.random() < 0.7), objective=1)
+        try:
+            ref = G.gabra(p, d, **kw)
+        except G.Infeasible:
+            with pytest.raises(rn.RnError) as e:
+                rn.gabra_place(p, d, **kw)
+            assert e.value.status == 3
+            continue
+        got = rn.gabra_place(p, d, **kw)
+        assert got[0] == ref[0] and got[1] == ref[1] and got[2] == ref[2], (p, d, kw)
+        pairs += 1
+    with pytest.raises(rn.RnError) as e:
+        rn.gabra_place([1, 2], [4, 4], objective=2)
+    assert e.value.status == 1
+
+
 def test_gabra_worked_example_and_errors():
     assert rn.gabra_place([5, 4, 3], [8, 7]) == ([0, 1, 1], 1.625, [5, 7])
     with pytest.raises(rn.RnError) as e:

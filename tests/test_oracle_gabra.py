@@ -139,3 +139,60 @@ def test_require_all_used():
     assert len(set(g)) == 2
     bg, bv, _ = G.brute_force(p, d, require_all_used=True)
     assert len(set(bg)) == 2
+
+
+# ----------------------------------------------------------------------------
+# bottleneck objective (objective=1; not in the paper)
+# ----------------------------------------------------------------------------
+
+def test_bottleneck_worked_instance_by_hand():
+    """p = [5, 4, 3], d = [8, 7]: the feasible placements, enumerated by hand,
+    with their bottleneck ratios max_j L_j / d_j: (0,1,1) -> max(5/8, 7/7) = 1;
+    (1,0,0) -> max(7/8, 5/7) = 7/8; (0,0,1) -> 9/8 > 1 infeasible; (1,1,0) ->
+    L = (3, 9): 9 > 7 infeasible; (0,1,0) -> L = (8, 4): max(1, 4/7) = 1;
+    (1,0,1) -> L = (4, 8): 8 > 7 infeasible.  Bound lb = max(12/15, 5/8) = 0.8.
+    Optimum (1,0,0) with f = 0.8 / (7/8) = 32/35."""
+    lb = G.bottleneck_bound([5, 4, 3], [8, 7])
+    assert lb == 0.8
+    assert G.bottleneck_fitness([0, 1, 1], [5, 4, 3], [8, 7], lb) == 0.8
+    assert G.bottleneck_fitness([1, 0, 0], [5, 4, 3], [8, 7], lb) == 0.8 / (7 / 8)
+    g, v, loads = G.brute_force([5, 4, 3], [8, 7], objective=1)
+    assert g == [1, 0, 0] and loads == [7, 5] and abs(v - 32 / 35) < 1e-15
+    g2, v2, _ = G.gabra([5, 4, 3], [8, 7], objective=1)
+    assert g2 == [1, 0, 0] and v2 == v
+
+
+def test_bottleneck_identical_gpus_closed_forms():
+    """Identical GPUs: n = m equal partitions -> one per GPU, f = 1 (the bound
+    sum p / sum d is met); the tiny network's 4 units on 2 GPUs (configs[0]):
+    the bound max p / d is met by isolating the attention module
+    (983040 + 14385152 + 32788 = 15400980 <= 16908288), f = 1.  Eq. 3's profit
+    is the same for every feasible placement there (finding 3)."""
+    p = [100] * 4
+    d = G.default_capacities(p, 4)
+    g, v, loads = G.gabra(p, d, objective=1)
+    assert v == 1.0 and sorted(g) == [0, 1, 2, 3] and loads == [100] * 4
+    p = [983040, 14385152, 16908288, 32788]
+    d = [18599117, 18599117]
+    g, v, loads = G.gabra(p, d, objective=1)
+    assert v == 1.0 and sorted(loads) == [15400980, 16908288]
+    assert g[2] != g[0] and g[0] == g[1] == g[3]
+
+
+def test_bottleneck_gabra_vs_bruteforce():
+    """The GA under the bottleneck objective: feasible, never above the brute-force
+    optimum, and >= 0.95 x optimum on >= 90 of 100 random heterogeneous instances."""
+    r = random.Random(77)
+    good = total = 0
+    for t in range(100):
+        p, d = random_instance(r)
+        try:
+            bg, bv, _ = G.brute_force(p, d, objective=1)
+            g, v, l = G.gabra(p, d, seed=t, objective=1)
+        except G.Infeasible:
+            continue
+        total += 1
+        assert G.feasible(g, p, d)
+        assert v <= bv + 1e-12
+        good += v >= 0.95 * bv
+    assert total >= 90 and good >= 0.9 * total
