@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--stages", type=int, default=1, help="pipeline stages per replica (hybrid)")
     ap.add_argument("--micro-batches", type=int, default=1)
+    ap.add_argument("--ga-objective", type=int, default=0, choices=[0, 1],
+                    help="GABRA objective for --stages > 1: 0 = the paper's Eq. 3, 1 = bottleneck (SURVEY f2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     return ap.parse_args()
@@ -161,7 +163,7 @@ def main():
     if S > 1:
         loads = rn.net_units(desc)[2]
         caps = [int(np.ceil(1.10 * max(max(loads), -(-sum(loads) // S))))] * S
-        genes = rn.gabra_place(loads, caps, seed=7, require_all_used=1)[0]
+        genes = rn.gabra_place(loads, caps, seed=7, require_all_used=1, objective=a.ga_objective)[0]
     nid = None
     if world > 1:
         obj = [rn.nccl_unique_id() if rank == 0 else None]
