@@ -205,6 +205,18 @@ rn_status rn_get_bn_running(rn_plan_t plan, float *mean_host, float *var_host, i
  * Errors: RN_ERR_ARG (unit not local / out of range), RN_ERR_SIZE. */
 rn_status rn_get_activation(rn_plan_t plan, int32_t unit, int32_t micro_batch, float *host, int64_t count);
 
+/* rn_gradcam — Grad-CAM of class `cls` (0/1) for the batch of the last rn_forward
+ * ("explainable block"), at the last convolutional
+ * layer: the head is GAP + FC, so dy_c/dA_k = W[c,k]/V at every voxel and
+ * alpha_k = W[c,k]/V; map = trilinear(ReLU(sum_k alpha_k A_k)) to the input grid
+ * (align_corners = False, reading X11).
+ *  map_dev : float32 [b][D][H][W] on the device (the input volume grid), written on the
+ *            plan's stream (stream-ordered; no synchronisation)
+ *  count   : must equal b * D * H * W
+ * Errors: RN_ERR_STATE (no forward yet), RN_ERR_SIZE (count), RN_ERR_ARG (cls, null map,
+ * head / last conv unit not on this rank). */
+rn_status rn_gradcam(rn_plan_t plan, int32_t cls, float *map_dev, int64_t count);
+
 /* rn_forward — forward pass of this replica's local batch.
  *  x_dev : float32 [b][D][H][W] input volumes (device), y_dev: int32 [b] labels in {0,1}
  *          (only read on the stages that need them: stage of the first / last partition)

@@ -452,6 +452,28 @@ def unit_backward(P, ui, u, dout, c, G):
     raise ValueError(u.kind)
 
 
+def gradcam_last(A, W, cls, out_dims):
+    """Grad-CAM ("explainable block") at the last
+    convolutional layer, written as its definition (Selvaraju et al.):
+      dy_c/dA_k  — the gradient of the class score y_c = FC(GAP(A))_c; the head is
+                   GAP + FC, so its backward gives W[c, k] / V at every voxel
+      alpha_k    = mean over voxels of dy_c / dA_k
+      cam        = ReLU(sum_k alpha_k A_k)
+      map        = trilinear(cam, out_dims), align_corners=False (reading X11)
+    A: (N, d, h, w, C) float64 (NDHWC, as the rest of the oracle); W: (2, C);
+    cls: int or per-sample ints.  Returns (N, D, H, W) float64."""
+    N, C = A.shape[0], A.shape[4]
+    V = A.shape[1] * A.shape[2] * A.shape[3]
+    cls = np.broadcast_to(np.asarray(cls), (N,))
+    out = []
+    for n in range(N):
+        grad = np.broadcast_to(W[cls[n]] / V, A.shape[1:])          # GAP + FC backward, every voxel
+        alpha = grad.reshape(-1, C).mean(axis=0)
+        cam = relu(A[n] @ alpha)                                     # (d, h, w)
+        out.append(upsample_trilinear(cam[None, :, :, :, None], out_dims)[0, :, :, :, 0])
+    return np.stack(out)
+
+
 def softmax_ce(z, y):
     """Mean softmax cross-entropy over the batch (reading X12) and dL/dz."""
     zmax = z.max(axis=1, keepdims=True)

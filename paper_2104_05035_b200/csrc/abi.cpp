@@ -283,6 +283,18 @@ rn_status rn_get_activation(rn_plan_t plan, int32_t unit, int32_t micro_batch, f
   GUARD_END
 }
 
+rn_status rn_gradcam(rn_plan_t plan, int32_t cls, float *map_dev, int64_t count) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  Plan *p = plan->p;
+  if (!map_dev) return set_error(RN_ERR_ARG, "rn_gradcam: null map");
+  if (!p->fwd_ever) return set_error(RN_ERR_STATE, "rn_gradcam before rn_forward");
+  if (count != (int64_t)p->b * p->net.units[0].in.vol()) return set_error(RN_ERR_SIZE, "rn_gradcam: count mismatch");
+  p->gradcam(cls, map_dev);
+  return RN_OK;
+  GUARD_END
+}
+
 static rn_status finish_loss(Plan *p, float *loss_host) {
   if (!loss_host) return RN_OK;
   float l = p->read_loss();

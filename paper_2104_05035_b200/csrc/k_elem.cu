@@ -1668,6 +1668,66 @@ void stem_pool_bwd(const void *dy, const uint8_t *argmax, const void *h, int N, 
   LAUNCH_CHECK();
 }
 
+// Grad-CAM at the last conv layer (oracle gradcam_last):
+// alpha_k = W[c, k] / V (the GAP + FC head's gradient, averaged over voxels),
+// coarse[v] = ReLU(sum_k alpha_k A[v][k]) — one warp per voxel, fixed-order
+// lane sums + butterfly; then a 1-channel fp32 trilinear upsample to the input grid.
+template <typename T>
+__global__ void cam_k(const T *__restrict__ A, const float *__restrict__ wrow, float invV, int C, int64_t nvox,
+                      float *__restrict__ coarse) {
+  pdl_begin();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nvox; v += nw) {
+    float s = 0.f;
+    for (int c = lane; c < C; c += 32) s = fmaf(to_f(A[v * C + c]), wrow[c] * invV, s);
+    s = warp_sum(s);
+    if (lane == 0) coarse[v] = s > 0.f ? s : 0.f;
+  }
+}
+__global__ void up1_k(const float *__restrict__ in, int N, int d, int h, int w, float *__restrict__ out, int D,
+                      int H, int W, UpTables t) {
+  pdl_begin();
+  const int64_t n = (int64_t)N * D * H * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i;
+    const int ow = (int)(r % W); r /= W;
+    const int oh = (int)(r % H); r /= H;
+    const int od = (int)(r % D); r /= D;
+    const int nn = (int)r;
+    const float *src = in + (int64_t)nn * d * h * w;
+    float acc = 0.f;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int id = t.fw_idx[0][2 * od + a];
+      const float wd = t.fw_w[0][2 * od + a];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int ih = t.fw_idx[1][2 * oh + b];
+        const float wh = wd * t.fw_w[1][2 * oh + b];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int iw = t.fw_idx[2][2 * ow + c];
+          acc = fmaf(wh * t.fw_w[2][2 * ow + c], src[((int64_t)id * h + ih) * w + iw], acc);
+        }
+      }
+    }
+    out[i] = acc;
+  }
+}
+
+void gradcam_last(DType dt, const void *A, const float *wrow, int N, int d, int h, int w, int C, float *coarse,
+                  float *map, int D, int H, int W, const UpTables &t, cudaStream_t st) {
+  const int64_t nvox = (int64_t)N * d * h * w;
+  const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nvox * 32 + 255) / 256, 148 * 8));
+  DISPATCH(dt, launch_k(cam_k<T>, gb, 256, 0, st, (const T *)A, wrow, 1.0f / (float)(d * h * w), C, nvox, coarse));
+  LAUNCH_CHECK();
+  const int64_t nout = (int64_t)N * D * H * W;
+  launch_k(up1_k, (unsigned)std::max<int64_t>(1, std::min<int64_t>((nout + 255) / 256, 148 * 16)), 256, 0, st,
+           (const float *)coarse, N, d, h, w, map, D, H, W, t);
+  LAUNCH_CHECK();
+}
+
 void upsample_fwd(DType dt, const void *x, int N, int Di, int Hi, int Wi, int C, void *y, int Do, int Ho, int Wo,
                   const UpTables &t, cudaStream_t st) {
   DISPATCH(dt, launch_k(upsample_fwd_k<T>, grid_for((int64_t)N * Do * Ho * Wo * C / Vec<T>::N), NT, 0, st, 

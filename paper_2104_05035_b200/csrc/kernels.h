@@ -122,6 +122,9 @@ struct UpTables {  // device pointers
   const int *bw_o[3];      // [nnz]
   const float *bw_w[3];    // [nnz]
 };
+// Grad-CAM at the last conv layer: map[n][D][H][W] = trilinear(ReLU(sum_k W[c,k]/V A[n][v][k]))
+void gradcam_last(DType dt, const void *A, const float *wrow, int N, int d, int h, int w, int C, float *coarse,
+                  float *map, int D, int H, int W, const UpTables &t, cudaStream_t st);
 void upsample_fwd(DType dt, const void *x, int N, int Di, int Hi, int Wi, int C, void *y, int Do, int Ho, int Wo,
                   const UpTables &t, cudaStream_t st);
 // separable trilinear adjoint (bf16): three passes w, h, d with fp32 intermediates in ws

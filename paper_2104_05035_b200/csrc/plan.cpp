@@ -212,7 +212,7 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
       L.dum = alloc(am_);
       L.du0 = alloc(am_);
       // trilinear tables (reading X11), mask dims -> unit dims
-      build_up_tables(L, u.mask, u.in);
+      build_up_tables(L.tab, u.mask, u.in);
     } else {
       L.g = per_mb(sizeof(float) * mb * u.cin);
       L.dz = per_mb(sizeof(float) * mb * 2);
@@ -276,7 +276,7 @@ Plan::~Plan() {
   nccl_destroy(world_comm);
 }
 
-void Plan::build_up_tables(UnitL &L, Dims in, Dims out) {
+void Plan::build_up_tables(UpTables &tab, Dims in, Dims out) {
   // 1-D linear maps per dim: src = max((o+1/2)*in/out - 1/2, 0), i0 = floor(src),
   // i1 = min(i0+1, in-1), weights (1-lambda, lambda); adjoint as CSR per input index.
   int ins[3] = {in.d, in.h, in.w}, outs[3] = {out.d, out.h, out.w};
@@ -321,11 +321,11 @@ void Plan::build_up_tables(UnitL &L, Dims in, Dims out) {
       up_dev.push_back(d);
       return d;
     };
-    L.tab.fw_idx[a] = (const int *)up(fidx.data(), fidx.size() * 4);
-    L.tab.fw_w[a] = (const float *)up(fw.data(), fw.size() * 4);
-    L.tab.bw_start[a] = (const int *)up(start.data(), start.size() * 4);
-    L.tab.bw_o[a] = (const int *)up(bo.data(), bo.size() * 4);
-    L.tab.bw_w[a] = (const float *)up(bw.data(), bw.size() * 4);
+    tab.fw_idx[a] = (const int *)up(fidx.data(), fidx.size() * 4);
+    tab.fw_w[a] = (const float *)up(fw.data(), fw.size() * 4);
+    tab.bw_start[a] = (const int *)up(start.data(), start.size() * 4);
+    tab.bw_o[a] = (const int *)up(bo.data(), bo.size() * 4);
+    tab.bw_w[a] = (const float *)up(bw.data(), bw.size() * 4);
   }
 }
 
@@ -483,6 +483,26 @@ void Plan::conv_bwd_data_proj(const ConvL &c1, const void *dy1, const ConvL &cp,
   if (stats.bn) stats.bn->bP = parts;
   if (t) tk_end(e, K_TC);
 }
+void Plan::gradcam(int cls, float *map_dev) {
+  const int hi = (int)net.units.size() - 1;
+  const Unit &hu = net.units[hi];
+  if (hu.kind != U_HEAD || hi < 1 || !local[hi] || !local[hi - 1])
+    throw Error(RN_ERR_ARG, "rn_gradcam: the head and the last conv unit must be on this rank");
+  if (cls < 0 || cls > 1) throw Error(RN_ERR_ARG, "rn_gradcam: class must be 0 or 1");
+  const Unit &lu = net.units[hi - 1];
+  const Dims in = net.units[0].in;
+  if (!cam_tab_built) {
+    build_up_tables(cam_tab, lu.out, in);
+    cam_tab_built = true;
+  }
+  const int64_t coarse_n = (int64_t)mb * lu.out.vol();
+  if (coarse_n > (int64_t)nblk_max * 2 * 512) throw Error(RN_ERR_SIZE, "rn_gradcam: scratch too small");
+  const float *wrow = master(net.unit_param_begin[hi]) + (int64_t)cls * hu.cin;
+  for (int k = 0; k < Mb; ++k)
+    gradcam_last(dt, P(units[hi - 1].out[k]), wrow, mb, lu.out.d, lu.out.h, lu.out.w, lu.cout,
+                 (float *)P(off_partial), map_dev + (int64_t)k * mb * in.vol(), in.d, in.h, in.w, cam_tab, stream);
+}
+
 bool Plan::side_on() const {
   auto it = opts.find("wgrad_stream");
   const bool on = it == opts.end() || it->second != 0;
@@ -861,6 +881,7 @@ void Plan::run_phase(int ph, const std::function<void()> &body) {
 void Plan::forward(const float *x_in, const int32_t *y) {
   run_phase(0, [&] { forward_body(x_in, y); });
   fwd_done = true;
+  fwd_ever = true;
 }
 
 void Plan::backward(const float *x_in) {

@@ -118,7 +118,7 @@ struct Plan {
   std::vector<UnitL> units;
   std::vector<void *> up_dev;
   NcclComm *world_comm = nullptr, *pipe_comm = nullptr, *dp_comm = nullptr;
-  bool params_set = false, fwd_done = false;
+  bool params_set = false, fwd_done = false, fwd_ever = false;
   const float *last_x = nullptr;
 
   Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int dtype, cudaStream_t st);
@@ -133,7 +133,11 @@ struct Plan {
   void make_conv(ConvL &c, int w_idx, int Ci, int Co, int k, int s, int p, Dims in, Dims out);
   void make_block(BlockL &b, int pidx, int cin, int cout, int stride, Dims in);
   int block_param_count(int cin, int cout, int stride) const;
-  void build_up_tables(UnitL &L, Dims in, Dims out);
+  void build_up_tables(UpTables &t, Dims in, Dims out);
+  // Grad-CAM at the last conv layer for class cls over the last forward's batch
+  void gradcam(int cls, float *map_dev);
+  UpTables cam_tab{};
+  bool cam_tab_built = false;
 
   // params
   float *master(int idx);

@@ -18,7 +18,7 @@ STATUS = {0: "RN_OK", 1: "RN_ERR_ARG", 2: "RN_ERR_SCHEMA", 3: "RN_ERR_INFEASIBLE
 EXPORTS = ["rn_ga_default", "rn_gabra_place", "rn_net_units", "rn_net_param_count", "rn_net_param_info",
            "rn_nccl_unique_id", "rn_plan", "rn_plan_describe", "rn_plan_bind", "rn_set_params", "rn_get_params", "rn_get_grads",
            "rn_get_bn_running", "rn_get_activation", "rn_forward", "rn_backward", "rn_step", "rn_train_step_host",
-           "rn_train_steps_host",
+           "rn_train_steps_host", "rn_gradcam",
            "rn_kernel_launches", "rn_set_option", "rn_query", "rn_op_conv3d", "rn_plan_destroy", "rn_last_error"]
 
 
@@ -194,6 +194,10 @@ class Plan:
         _check(lib().rn_get_activation(self.h, unit, micro_batch, a.ctypes.data_as(C.POINTER(C.c_float)),
                                        C.c_int64(n)))
         return a.reshape(shape)
+
+    def gradcam(self, cls: int, map_dev):
+        """rn_gradcam into a float32 device tensor of b x D x H x W (stream-ordered)."""
+        _check(lib().rn_gradcam(self.h, C.c_int32(cls), C.c_void_p(map_dev.data_ptr()), C.c_int64(map_dev.numel())))
 
     # --- step ---
     def forward(self, x_dev, y_dev, want_loss=True):

@@ -374,3 +374,32 @@ def test_stem_wgrad_tensor_cores_match_simt(tmp_path):
     n1 = n0 + 2 * 64
     assert rel(outs[0][n0:n1], outs[1][n0:n1]) <= 1e-5
     assert np.array_equal(outs[0][n1:], outs[1][n1:])
+
+
+@pytest.mark.parametrize("depth,w,dims,dtype", [(18, 64, (40, 48, 40), rn.RN_BF16), (0, 8, (16, 16, 16), rn.RN_F32)])
+def test_gradcam_matches_oracle(depth, w, dims, dtype):
+    """rn_gradcam against the oracle's Grad-CAM definition on the
+    same last-conv activations (read back through rn_get_activation) and the same
+    FC weights: the GPU forms alpha = W[c]/V, the channel dot product, ReLU and the
+    trilinear upsample in fp32 -> 1e-5 relative."""
+    N = 2
+    plan = rn.Plan(rn.net_desc(depth, w, dims), N, dtype)
+    arrays = synthetic.perturb_params(plan.tensors, synthetic.init_params(plan.tensors, seed=0))
+    flat = np.concatenate([a.ravel() for a in arrays]).astype(np.float32)
+    plan.set_params(flat)
+    x, y = synthetic.make_batch(N, *dims, seed=1)
+    plan.forward(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+    net = O.Net(depth, w, dims)
+    last = net.units[-2]
+    A = plan.get_activation(len(net.units) - 2, 0, (N,) + tuple(last.out_dims) + (last.cout,))
+    W = arrays[-2].astype(np.float32).astype(np.float64)  # head FC weight [2][C]
+    peak = 0.0
+    for cls in (0, 1):
+        m = torch.empty((N,) + dims, dtype=torch.float32, device="cuda")
+        plan.gradcam(cls, m)
+        torch.cuda.synchronize()
+        ref = O.gradcam_last(A.astype(np.float64), W, cls, dims)
+        got = m.cpu().numpy()
+        assert np.abs(got - ref).max() <= 1e-5 * max(np.abs(ref).max(), 1e-30) + 1e-12
+        peak = max(peak, float(ref.max()))
+    assert peak > 0.0  # at least one class has positive evidence somewhere (non-trivial maps)

@@ -153,3 +153,33 @@ def test_attention_and_ce_special_cases():
     assert abs(loss - 0.6931471805599453) < 1e-15
     np.testing.assert_allclose(dz.sum(axis=1), 0, atol=1e-16)
     np.testing.assert_allclose(dz, np.array([[-0.5, 0.5], [0.5, -0.5], [0.5, -0.5]]) / 3)
+
+
+def test_gradcam_last_pins():
+    """Grad-CAM at the last conv layer: (a) the gradient it uses
+    matches central finite differences of the class score y_c = FC(GAP(A))_c;
+    (b) a constant activation gives a constant map ReLU(sum_k alpha_k a_k);
+    (c) a negative evidence map is zeroed (ReLU)."""
+    rng = np.random.default_rng(3)
+    N, d, h, w, C = 2, 3, 4, 3, 5
+    A = rng.standard_normal((N, d, h, w, C))
+    W = rng.standard_normal((2, C))
+    V = d * h * w
+
+    def score(Ax, c):  # y_c for one sample
+        return float(Ax.reshape(-1, C).mean(axis=0) @ W[c])
+    eps = 1e-6
+    for c in (0, 1):
+        k, vox = 2, (1, 2, 0)
+        Ap, Am = A[0].copy(), A[0].copy()
+        Ap[vox + (k,)] += eps
+        Am[vox + (k,)] -= eps
+        fd = (score(Ap, c) - score(Am, c)) / (2 * eps)
+        assert abs(fd - W[c, k] / V) < 1e-8
+    const = np.ones((1, d, h, w, C)) * 0.7
+    m = O.gradcam_last(const, W, 1, (7, 9, 5))
+    ref = max(0.0, float(0.7 * W[1].sum() / V))
+    np.testing.assert_allclose(m, ref, rtol=1e-12, atol=1e-15)
+    neg = -np.abs(np.ones((1, d, h, w, C)))
+    Wp = np.abs(W)
+    assert np.all(O.gradcam_last(neg, Wp, 0, (5, 5, 5)) == 0.0)
