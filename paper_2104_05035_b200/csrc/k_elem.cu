@@ -1688,14 +1688,14 @@ __global__ void cam_k(const T *__restrict__ A, const float *__restrict__ wrow, f
 __global__ void up1_k(const float *__restrict__ in, int N, int d, int h, int w, float *__restrict__ out, int D,
                       int H, int W, UpTables t) {
   pdl_begin();
-  const int64_t n = (int64_t)N * D * H * W;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i;
-    const int ow = (int)(r % W); r /= W;
-    const int oh = (int)(r % H); r /= H;
-    const int od = (int)(r % D); r /= D;
-    const int nn = (int)r;
-    const float *src = in + (int64_t)nn * d * h * w;
+  const int n = N * D * H * W;  // < 2^31 (checked by the launcher): 32-bit index math
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int r = i;
+    const int ow = r % W; r /= W;
+    const int oh = r % H; r /= H;
+    const int od = r % D;
+    const int nn = r / D;
+    const float *src = in + nn * d * h * w;
     float acc = 0.f;
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
@@ -1708,7 +1708,7 @@ __global__ void up1_k(const float *__restrict__ in, int N, int d, int h, int w, 
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const int iw = t.fw_idx[2][2 * ow + c];
-          acc = fmaf(wh * t.fw_w[2][2 * ow + c], src[((int64_t)id * h + ih) * w + iw], acc);
+          acc = fmaf(wh * t.fw_w[2][2 * ow + c], src[(id * h + ih) * w + iw], acc);
         }
       }
     }
@@ -1723,6 +1723,7 @@ void gradcam_last(DType dt, const void *A, const float *wrow, int N, int d, int 
   DISPATCH(dt, launch_k(cam_k<T>, gb, 256, 0, st, (const T *)A, wrow, 1.0f / (float)(d * h * w), C, nvox, coarse));
   LAUNCH_CHECK();
   const int64_t nout = (int64_t)N * D * H * W;
+  if (nout >= (1LL << 31)) throw Error(RN_ERR_SIZE, "gradcam_last: map too large");
   launch_k(up1_k, (unsigned)std::max<int64_t>(1, std::min<int64_t>((nout + 255) / 256, 148 * 16)), 256, 0, st,
            (const float *)coarse, N, d, h, w, map, D, H, W, t);
   LAUNCH_CHECK();
