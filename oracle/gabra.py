@@ -264,6 +264,21 @@ def gabra(p, d, **kw):
                 accepted = g
                 break
         if accepted is None:
+            # reading G19b: the deterministic worst-fit-decreasing chromosome
+            # (partitions by (p desc, i asc), each to the GPU with the most
+            # remaining capacity, lowest index on ties); no random numbers
+            g = [0] * n
+            rem = list(d)
+            for i in sorted(range(n), key=lambda i: (-p[i], i)):
+                k = 0
+                for j in range(1, m):
+                    if rem[j] > rem[k]:
+                        k = j
+                g[i] = k
+                rem[k] -= p[i]
+            if feasible(g, p, d, U):
+                accepted = g
+        if accepted is None:
             raise Infeasible("no capacity-respecting placement found")
         pop.append(accepted)
     f = [fitness(g, c) for g in pop]                          # evaluate P(t)

@@ -171,6 +171,25 @@ rn_status gabra_place(int32_t n, const int64_t *loads, int32_t m, const int64_t 
       for (int i = 0; i < n; ++i) g[i] = rng.randint(m);
       if (pr.feasible(g) || pr.repair(g)) ok = true;
     }
+    if (!ok) {
+      // reading G19b: A random draws + repair found nothing (tight capacities, or
+      // require_all_used with n close to m) -> the deterministic worst-fit-decreasing
+      // chromosome (partitions by (p desc, i asc), each to the GPU with the most
+      // remaining capacity, lowest index on ties); consumes no random numbers
+      std::vector<int> order(n);
+      for (int i = 0; i < n; ++i) order[i] = i;
+      for (int a = 1; a < n; ++a)  // insertion sort: stable, (p desc, i asc)
+        for (int b = a; b > 0 && loads[order[b]] > loads[order[b - 1]]; --b) std::swap(order[b], order[b - 1]);
+      std::vector<int64_t> rem(caps, caps + m);
+      for (int a = 0; a < n; ++a) {
+        int k = 0;
+        for (int j = 1; j < m; ++j)
+          if (rem[j] > rem[k]) k = j;
+        g[order[a]] = k;
+        rem[k] -= loads[order[a]];
+      }
+      ok = pr.feasible(g);
+    }
     if (!ok) return set_error(RN_ERR_INFEASIBLE, "GABRA: no capacity-respecting placement found");
     pop[q] = g;
   }

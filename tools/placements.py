@@ -13,7 +13,7 @@ from paper_2104_05035_b200 import rn  # noqa: E402
 
 seeds = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "7,8,9,10,11").split(",")]
 dims = (91, 109, 91)
-cases = [("r18 (configs[3])", 18, 0, [2]), ("r34 (configs[4])", 34, -1, [2, 4, 8])]
+cases = [("r18 (configs[3])", 18, 0, [2, 4, 8]), ("r34 (configs[4])", 34, -1, [2, 4, 8])]
 for name, depth, cap, ms in cases:
     units, first, loads = rn.net_units(rn.net_desc(depth, 64, dims))
     if cap < 0:  # r34: cap merged light partitions at the heaviest singleton
