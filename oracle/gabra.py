@@ -226,6 +226,22 @@ def repair(genes, p, d, require_all_used=False):
 # GABRA (Algorithm 1), pinned step by step
 # ----------------------------------------------------------------------------
 
+def wfd_chromosome(p, d):
+    """Reading G19b: worst-fit decreasing — partitions by (p desc, i asc), each to
+    the GPU with the most remaining capacity (lowest index on ties)."""
+    n, m = len(p), len(d)
+    g = [0] * n
+    rem = list(d)
+    for i in sorted(range(n), key=lambda i: (-p[i], i)):
+        k = 0
+        for j in range(1, m):
+            if rem[j] > rem[k]:
+                k = j
+        g[i] = k
+        rem[k] -= p[i]
+    return g
+
+
 DEFAULT_PARAMS = dict(pop_size=50, t_max=500, p_cross=0.8, p_mut=0.1, seed=7,
                       dup_retries=20, init_attempts=64, require_all_used=0, early_stop_at_ub=1,
                       objective=0)
@@ -267,15 +283,7 @@ def gabra(p, d, **kw):
             # reading G19b: the deterministic worst-fit-decreasing chromosome
             # (partitions by (p desc, i asc), each to the GPU with the most
             # remaining capacity, lowest index on ties); no random numbers
-            g = [0] * n
-            rem = list(d)
-            for i in sorted(range(n), key=lambda i: (-p[i], i)):
-                k = 0
-                for j in range(1, m):
-                    if rem[j] > rem[k]:
-                        k = j
-                g[i] = k
-                rem[k] -= p[i]
+            g = wfd_chromosome(p, d)
             if feasible(g, p, d, U):
                 accepted = g
         if accepted is None:

@@ -196,3 +196,20 @@ def test_bottleneck_gabra_vs_bruteforce():
         assert v <= bv + 1e-12
         good += v >= 0.95 * bv
     assert total >= 90 and good >= 0.9 * total
+
+
+def test_init_fallback_worst_fit_decreasing():
+    """Reading G19b: with a single random draw per chromosome (init_attempts=1) on
+    identical GPUs that only admit permutations (p = [5, 4, 3, 2], d = 5 each,
+    require_all_used), the chromosomes that neither the draw nor the repair makes
+    feasible are the worst-fit-decreasing one, derived by hand: 5 -> GPU 0 (all
+    have 5 free, lowest index), 4 -> GPU 1, 3 -> GPU 2, 2 -> GPU 3."""
+    p, d = [5, 4, 3, 2], [5, 5, 5, 5]
+    assert G.wfd_chromosome(p, d) == [0, 1, 2, 3]
+    # heterogeneous, by hand: 3 (i=0) -> GPU 1 (6 free); 3 (i=1) -> GPU 0 (4 free); 2 -> GPU 1 (3 free)
+    assert G.wfd_chromosome([3, 3, 2], [4, 6]) == [1, 0, 1]
+    g, v, loads = G.gabra(p, d, require_all_used=1, init_attempts=1, seed=3, early_stop_at_ub=0, t_max=3)
+    assert sorted(g) == [0, 1, 2, 3] and sorted(loads) == [2, 3, 4, 5]
+    # a capacity that no placement satisfies is still reported infeasible
+    with pytest.raises(G.Infeasible):
+        G.gabra([6, 1], [5, 5], init_attempts=2)
