@@ -183,6 +183,8 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
         __syncwarp();
       }
     }
+    // every MMA of the pair is issued: the dependent grid may start launching
+    if (lane == 0) pdl_trigger();
   } else {
     // ---------------- epilogue (warps 2..5, both CTAs) ----------------
     const int q = warp & 3;

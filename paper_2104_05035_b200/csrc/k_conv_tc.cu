@@ -44,6 +44,7 @@ namespace rn {
 namespace {
 
 constexpr int TC_THREADS = 192;
+constexpr bool kPdlLate = true;  // explicit late PDL trigger (after the last MMA issue)
 
 constexpr int MAX_TAPS = 28;  // 27 taps + the appended projection tap (stride-2 dgrad)
 
@@ -236,6 +237,9 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
+    // every MMA of this CTA is issued: the dependent grid may start launching
+    // (persistent grid: no later wave of this kernel to be displaced)
+    if (kPdlLate) pdl_trigger();
   } else {
     // ---------------- epilogue (warps 2..5) ----------------
     const int q = warp & 3;  // TMEM lane quarter this warp may access
