@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${TAG}_build.log 2>&1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${TAG}_gpu.txt 2>&1
 timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
-KPROF_NOSIDE=1 KPROF_NOGRAPH=1 timeout 300 python tools/kprof.py 5 8 gpurun_out/${TAG}_kprof.txt > /dev/null 2>&1
+RN_PDL=0 KPROF_NOSIDE=1 KPROF_NOGRAPH=1 timeout 300 python tools/kprof.py 5 8 gpurun_out/${TAG}_kprof.txt > /dev/null 2>&1  # PDL off: CUPTI durations would include the griddepcontrol.wait of early-launched kernels
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
   python tools/profile_step.py 2 > gpurun_out/${TAG}_launches.log 2>&1
 python tools/launch_summary.py gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_launches_summary.txt 2>&1
