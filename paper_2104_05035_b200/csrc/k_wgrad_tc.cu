@@ -279,12 +279,6 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
   }
 }
 
-__global__ void zero_rows_k(float *part, int64_t n) {
-  pdl_begin();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    part[i] = 0.f;
-}
-
 __global__ void wg_reduce_add(const float *__restrict__ part, int splits, int64_t n, float *__restrict__ out) {
   pdl_begin();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {

@@ -402,13 +402,13 @@ void Plan::conv_fwd(const ConvL &c, const void *x, void *y, const float *bias, B
     es.mode = 1;
   }
   int parts = 0, kind = K_SIMT;
-  if (use_tc(c.g, false) && use_pair() && pair_conv_supported(c.g, false) && (kind = K_PAIR))
+  if (use_tc(c.g, false) && use_pair() && pair_conv_supported(c.g, false) && ((kind = K_PAIR) != 0))
     parts = conv_pair(c.g, false, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, false,
                       nullptr, nullptr, stream, want ? &es : nullptr);
-  else if (use_tc(c.g, false) && use_halo() && halo_conv_supported(c.g, false) && (kind = K_HALO))
+  else if (use_tc(c.g, false) && use_halo() && halo_conv_supported(c.g, false) && ((kind = K_HALO) != 0))
     parts = conv_halo(c.g, false, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, false,
                       nullptr, nullptr, stream, want ? &es : nullptr);
-  else if (use_tc(c.g, false) && (kind = K_TC))
+  else if (use_tc(c.g, false) && ((kind = K_TC) != 0))
     parts = conv_fprop_tc(c.g, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y,
                           (float *)P(off_conv_ws), conv_ws_floats, stream, want ? &es : nullptr);
   else
@@ -437,14 +437,14 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
   // (~8 us), so by default they are left to bn_backward (option pair_bwd_stats)
   auto itp = opts.find("pair_bwd_stats");
   const bool pair_stats = itp != opts.end() && itp->second != 0;
-  if (use_tc(c.g, true) && use_pair() && pair_conv_supported(c.g, true) && (kind = K_PAIR))
+  if (use_tc(c.g, true) && use_pair() && pair_conv_supported(c.g, true) && ((kind = K_PAIR) != 0))
     parts = conv_pair(c.g, true, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx,
                       accumulate, (const bf16 *)res, (const bf16 *)res_mask, stream,
                       want && pair_stats ? &es : nullptr);
-  else if (use_tc(c.g, true) && use_halo() && halo_conv_supported(c.g, true) && (kind = K_HALO))
+  else if (use_tc(c.g, true) && use_halo() && halo_conv_supported(c.g, true) && ((kind = K_HALO) != 0))
     parts = conv_halo(c.g, true, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx,
                       accumulate, (const bf16 *)res, (const bf16 *)res_mask, stream, want ? &es : nullptr);
-  else if (use_tc(c.g, true) && (kind = K_TC))
+  else if (use_tc(c.g, true) && ((kind = K_TC) != 0))
     parts = conv_dgrad_tc(c.g, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), (bf16 *)dx, accumulate,
                           (const bf16 *)res, (const bf16 *)res_mask, (float *)P(off_conv_ws), conv_ws_floats, stream,
                           want ? &es : nullptr);
