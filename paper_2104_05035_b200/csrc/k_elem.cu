@@ -1120,7 +1120,6 @@ __global__ void __launch_bounds__(256, 2) stem_pool_bwd_k(const bf16 *__restrict
   constexpr int G = C / 8;
   const int vecs = rowel / 8;
   const int cg = (threadIdx.x % G) * 8;  // this thread's channel group (items advance by blockDim)
-  const int WG = W * G;
   __shared__ float coefs[4][C];             // scale, shift, mean, invstd per channel
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     coefs[0][c] = scale[c];
@@ -1158,7 +1157,6 @@ __global__ void __launch_bounds__(256, 2) stem_pool_bwd_k(const bf16 *__restrict
   if (blockIdx.x < units) stage_load(blockIdx.x);
   for (int u = blockIdx.x; u < units; u += gridDim.x) {
     const int j = u % Hj, id = (u / Hj) % D, nn = u / (Hj * D);
-    const int od0 = id >> 1, od1 = (id & 1) && ((id + 1) >> 1) < Do ? (id + 1) >> 1 : -1;
     __syncthreads();  // the previous unit's readers are done with the staged rows
 #pragma unroll
     for (int q = 0; q < SPB_PF; ++q) {
