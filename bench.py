@@ -222,6 +222,12 @@ def main():
         conv_ms, conv_fl = plan.query("conv_ms"), plan.query("conv_flops")
         pair_ms, pair_fl = plan.query("conv_ms_pair"), plan.query("conv_flops_pair")
         pair_n = plan.query("conv_launches_pair")
+        # per conv class / kernel family ("reported per layer class")
+        classes = {}
+        for key in ("fprop", "dgrad", "wgrad", "pair", "tcconv", "tcwgrad", "stem"):
+            cms, cfl = plan.query("conv_ms_" + key), plan.query("conv_flops_" + key)
+            classes[key] = {"ms_per_step": cms, "tflops": (cfl / (cms / 1000.0) / 1e12) if cms > 0 else None,
+                            "launches": plan.query("conv_launches_" + key)}
         plan.set_option("time_kernels", 0)
         torch.cuda.synchronize(dev)
         # end-to-end through the public C ABI with pinned host buffers
@@ -263,7 +269,8 @@ def main():
             "flops_per_launch": pair_fl / pair_n if pair_n else None,
             "all_convs": {"achieved": conv_tf, "frac": (conv_tf / peak_tf) if peak_tf else None,
                           "ms_per_step": conv_ms, "share_of_step": conv_ms / step_ms,
-                          "note": "every fprop/dgrad/wgrad launch, algorithmic 2*M*N*K FLOPs"},
+                          "note": "every fprop/dgrad/wgrad launch, algorithmic 2*M*N*K FLOPs",
+                          "by_class": classes},
             "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)"
             if "_fallback" not in pk else "fallback"}
     if rank == 0:
