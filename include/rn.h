@@ -205,6 +205,34 @@ rn_status rn_get_bn_running(rn_plan_t plan, float *mean_host, float *var_host, i
  * Errors: RN_ERR_ARG (unit not local / out of range), RN_ERR_SIZE. */
 rn_status rn_get_activation(rn_plan_t plan, int32_t unit, int32_t micro_batch, float *host, int64_t count);
 
+/* rn_get_unit_grad — copy dl/d(output of top-level unit `unit`), the gradient the
+ * chain rule hands to that unit's backward, of the LAST micro-batch of the
+ * last rn_backward, to host as float32 NDHWC [mb][D][H][W][C] (the same shape as
+ * rn_get_activation).  Not defined for the head (its incoming gradient is dz of
+ * the loss).  Used for teacher-forced per-unit parity: unit u's backward maps
+ * rn_get_unit_grad(u) to rn_get_unit_grad(u-1).  Only for units placed on this rank.
+ * Errors: RN_ERR_ARG (head / not local / out of range), RN_ERR_SIZE,
+ * RN_ERR_STATE (no rn_backward yet). */
+rn_status rn_get_unit_grad(rn_plan_t plan, int32_t unit, float *host, int64_t count);
+
+/* rn_get_saved — copy one tensor the step keeps (forward tensors saved for the
+ * backward, per micro-batch) or leaves behind (backward temporaries and BN
+ * statistics: the LAST micro-batch's) of top-level unit `unit` to host as float32
+ * (bf16 / uint8 values converted exactly).  Test/diagnostic access for op-level
+ * parity; names (NDHWC activation layouts [mb][D][H][W][C] unless stated):
+ *   stem : "h" conv output (pre-BN, conv dims), "am" max-pool argmax 0..26 (pooled
+ *          dims), "d1" pool adjoint x ReLU mask (fused bf16 stem backward), "bn.stats"
+ *   block: "h1" "a1" "h2" ["hp"] "out" (forward), "dh2" "da1" "dh1" ["dhp"]
+ *          (backward), "bn1.stats" "bn2.stats" ["projbn.stats"]
+ *   att  : "trunk.<block name>", "mask.<block name>", "u0" "am" (mask-branch
+ *          max-pool), "up" "mh" "r" "m" "mbn.stats", "dT" "dm" "dr" "dmh" "dup" "dum" "du0"
+ *   head : "dz" [mb][2] fp32 (dl/dlogits, scaled by 1/(batch * replicas))
+ * "*.stats" = [4][C] fp32: batch mean, 1/sqrt(var + eps), scale = gamma*invstd,
+ * shift = beta - mean*scale.  count must equal the tensor's size.
+ * Errors: RN_ERR_ARG (bad unit / micro-batch / unknown name), RN_ERR_SIZE. */
+rn_status rn_get_saved(rn_plan_t plan, int32_t unit, const char *name, int32_t micro_batch, float *host,
+                       int64_t count);
+
 /* rn_gradcam — Grad-CAM of class `cls` (0/1) for the batch of the last rn_forward
  * ("explainable block"), at the last convolutional
  * layer: the head is GAP + FC, so dy_c/dA_k = W[c,k]/V at every voxel and

@@ -531,6 +531,34 @@ class Net:
                 bnstate.update(name, cache)
         return loss, G, h
 
+    def unit_step(self, P: Params, ui: int, x, dout=None, y=None):
+        """Teacher-forced single unit (test infrastructure for per-unit parity):
+        unit ui's forward from the given input x (NDHWC; the stem takes the raw
+        [N,D,H,W] volume) and its backward from the given output gradient dout —
+        the same unit_forward / unit_backward the whole step chains, in
+        this Net's storage mode.  For the head, dout is None and y the labels:
+        its incoming gradient is dz of the cross-entropy; dout None for
+        any other unit runs the forward only.
+        Returns dict(out, dx, G, bns, cache, loss)."""
+        global Q, QW
+        Q = QW = (_bf16_round if self.store == "bf16" else _identity)
+        try:
+            u = self.units[ui]
+            h = np.asarray(x, dtype=np.float64)
+            if u.kind == "stem":
+                h = h[..., None]
+            bns = []
+            out, c = unit_forward(P, ui, u, h, bns)
+            loss = None
+            if u.kind == "head":
+                loss, dout = softmax_ce(out, np.asarray(y))
+            G, dx = {}, None
+            if dout is not None:             # dout None (not the head): forward only
+                dx = unit_backward(P, ui, u, np.asarray(dout, dtype=np.float64), c, G)
+            return dict(out=out, dx=dx, G=G, bns=bns, cache=c, loss=loss)
+        finally:
+            Q = QW = _identity
+
     def flat(self, G) -> np.ndarray:
         return np.concatenate([np.asarray(G[n], dtype=np.float64).ravel() for n, _, _ in self.tensors])
 

@@ -287,6 +287,63 @@ rn_status rn_get_activation(rn_plan_t plan, int32_t unit, int32_t micro_batch, f
   GUARD_END
 }
 
+rn_status rn_get_unit_grad(rn_plan_t plan, int32_t unit, float *host, int64_t count) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  Plan *p = plan->p;
+  if (!host || unit < 0 || unit >= (int)p->net.units.size() || !p->local[unit] ||
+      p->net.units[unit].kind == U_HEAD)
+    return set_error(RN_ERR_ARG, "rn_get_unit_grad: bad unit (head, not local or out of range)");
+  if (!p->bwd_ever) return set_error(RN_ERR_STATE, "rn_get_unit_grad before rn_backward");
+  const Unit &u = p->net.units[unit];
+  const int64_t n = (int64_t)p->mb * u.out.vol() * u.cout;
+  if (count != n) return set_error(RN_ERR_SIZE, "rn_get_unit_grad: count mismatch");
+  CUDA_CHECK(cudaStreamSynchronize(p->stream));
+  const void *src = p->P(p->units[unit].dout);
+  if (p->dt == DT_F32) {
+    CUDA_CHECK(cudaMemcpy(host, src, 4 * n, cudaMemcpyDeviceToHost));
+  } else {
+    std::vector<uint16_t> tmp(n);
+    CUDA_CHECK(cudaMemcpy(tmp.data(), src, 2 * n, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i) {
+      uint32_t b = (uint32_t)tmp[i] << 16;
+      memcpy(&host[i], &b, 4);
+    }
+  }
+  return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_get_saved(rn_plan_t plan, int32_t unit, const char *name, int32_t micro_batch, float *host,
+                       int64_t count) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  Plan *p = plan->p;
+  if (!host || !name || unit < 0 || unit >= (int)p->net.units.size() || !p->local[unit] || micro_batch < 0 ||
+      micro_batch >= p->Mb)
+    return set_error(RN_ERR_ARG, "rn_get_saved: bad unit / micro-batch");
+  SavedRef r;
+  if (!p->saved(unit, micro_batch, name, r)) return set_error(RN_ERR_ARG, "rn_get_saved: unknown tensor name");
+  if (count != r.n) return set_error(RN_ERR_SIZE, "rn_get_saved: count mismatch");
+  CUDA_CHECK(cudaStreamSynchronize(p->stream));
+  if (r.type == 1 || (r.type == 0 && p->dt == DT_F32)) {
+    CUDA_CHECK(cudaMemcpy(host, r.ptr, 4 * r.n, cudaMemcpyDeviceToHost));
+  } else if (r.type == 2) {
+    std::vector<uint8_t> tmp(r.n);
+    CUDA_CHECK(cudaMemcpy(tmp.data(), r.ptr, r.n, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < r.n; ++i) host[i] = (float)tmp[i];
+  } else {
+    std::vector<uint16_t> tmp(r.n);
+    CUDA_CHECK(cudaMemcpy(tmp.data(), r.ptr, 2 * r.n, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < r.n; ++i) {
+      uint32_t b = (uint32_t)tmp[i] << 16;
+      memcpy(&host[i], &b, 4);
+    }
+  }
+  return RN_OK;
+  GUARD_END
+}
+
 rn_status rn_gradcam(rn_plan_t plan, int32_t cls, float *map_dev, int64_t count) {
   GUARD_BEGIN
   NEED_BOUND(plan);

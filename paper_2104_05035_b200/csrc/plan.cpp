@@ -40,8 +40,10 @@ void Plan::make_bn(BNL &b, int gamma_idx, int C, int64_t V) {
   b.stat_off.resize(Mb);
   for (int k = 0; k < Mb; ++k) b.stat_off[k] = alloc(4 * sizeof(float) * C);
   if (dt == DT_BF16) {  // up to 2 CTAs per SM in the producing conv
-    b.fpart = alloc(sizeof(float) * 4 * 148 * 2 * C);  // up to 4 producer blocks per SM (stem)
-    b.bpart = alloc(sizeof(float) * 2 * 148 * 2 * C);
+    // one [2][C] partial per producing CTA: convolution grids are sized from the
+    // device's SM count (<= 2 CTAs per SM), the stem's from up to 4 blocks per SM
+    b.fpart = alloc(sizeof(float) * 4 * nsm * 2 * C);
+    b.bpart = alloc(sizeof(float) * 2 * nsm * 2 * C);
   }
 }
 
@@ -104,6 +106,13 @@ int Plan::block_param_count(int cin, int cout, int stride) const {
 Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int dtype, cudaStream_t st)
     : net(build_net(nd)), stream(st) {
   dt = dtype == RN_BF16 ? DT_BF16 : DT_F32;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    nsm = std::max(nsm, 148);  // scratch sized for at least a B200's 148 SMs
+  }
   rank = dd.rank;
   world = dd.world;
   S = dd.n_stages;
@@ -232,7 +241,7 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
     }
   }
   // scratch
-  nblk_max = 4 * 148;
+  nblk_max = 4 * nsm;
   off_partial = alloc(sizeof(float) * nblk_max * 2 * 512);
   off_coef = alloc(sizeof(float) * 3 * 512 * 2);
   off_counter = alloc(256);  // last-block tickets of the fused reduce+finalize kernels (zeroed at bind)
@@ -573,6 +582,7 @@ void Plan::bn_fwd(const BNL &b, int k, const void *h, const void *res, const flo
     BNL &m = const_cast<BNL &>(b);
     if (m.fP <= 0) m.fP = bn_stats_partials(dt, h, b.V, b.C, (float *)P(b.fpart), stream);
     bn_apply_fused(dt, h, b.V, b.C, bn_final(b, k), nullptr, res, relu, y, stream);
+    m.fP = 0;  // consumed: the next producer decides again (never reuse stale partials)
     return;
   }
   float *part = (float *)P(off_partial);
@@ -619,6 +629,7 @@ void Plan::block_fwd(BlockL &B, int k, const void *x) {
       if (B.bp.fP <= 0) B.bp.fP = bn_stats_partials(dt, P(B.hp[k]), B.bp.V, B.bp.C, (float *)P(B.bp.fpart), stream);
       const BnFinal fp = bn_final(B.bp, k);
       bn_apply_fused(dt, P(B.h2[k]), B.b2.V, B.b2.C, bn_final(B.b2, k), &fp, P(B.hp[k]), true, P(B.out_[k]), stream);
+      B.b2.fP = B.bp.fP = 0;
     } else {
       bn_forward_stats(B.bp, k, P(B.hp[k]));
       bn_fwd(B.b2, k, P(B.h2[k]), P(B.hp[k]), bn_stat(B.bp, k, 2), bn_stat(B.bp, k, 3), true, P(B.out_[k]));
@@ -679,8 +690,10 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
       if (stem_fast_supported(L.stem_conv.g))
         L.stem_bn.fP = stem_fprop_fast(dt, L.stem_conv.g, (const float *)x, master(L.stem_conv.w_idx),
                                        P(L.stem_h[k]), stream, fuse ? (float *)P(L.stem_bn.fpart) : nullptr);
-      else
+      else {
         stem_conv_fprop(dt, L.stem_conv.g, (const float *)x, master(L.stem_conv.w_idx), P(L.stem_h[k]), stream);
+        L.stem_bn.fP = 0;  // no fused statistics: the BN below reduces h itself
+      }
       if (t) tk_end(e, K_STEM);
     }
     if (u.pool && L.stem_bn.fP > 0) {
@@ -815,6 +828,89 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
 }
 
 // ---------------------------------------------------------------------------
+// saved tensors by name (rn_get_saved: op-level teacher-forced parity)
+// ---------------------------------------------------------------------------
+bool Plan::saved(int ui, int k, const std::string &name, SavedRef &r) {
+  const Unit &u = net.units[ui];
+  UnitL &L = units[ui];
+  auto act = [&](size_t off, int C, Dims d) {
+    r.ptr = P(off);
+    r.n = (int64_t)mb * d.vol() * C;
+    r.type = 0;
+    return true;
+  };
+  auto stats = [&](const BNL &b) {
+    r.ptr = P(b.stat_off[k]);
+    r.n = 4 * (int64_t)b.C;
+    r.type = 1;
+    return true;
+  };
+  auto block = [&](BlockL &B, const std::string &n) {
+    const int C = B.cout;
+    if (n == "h1") return act(B.h1[k], C, B.out);
+    if (n == "a1") return act(B.a1[k], C, B.out);
+    if (n == "h2") return act(B.h2[k], C, B.out);
+    if (n == "out") return act(B.out_[k], C, B.out);
+    if (n == "dh2") return act(B.dh2, C, B.out);
+    if (n == "da1") return act(B.da1, C, B.out);
+    if (n == "dh1") return act(B.dh1, C, B.out);
+    if (n == "bn1.stats") return stats(B.b1);
+    if (n == "bn2.stats") return stats(B.b2);
+    if (B.proj) {
+      if (n == "hp") return act(B.hp[k], C, B.out);
+      if (n == "dhp") return act(B.dhp, C, B.out);
+      if (n == "projbn.stats") return stats(B.bp);
+    }
+    return false;
+  };
+  if (u.kind == U_STEM) {
+    if (name == "h") return act(L.stem_h[k], u.cout, u.conv);
+    if (name == "bn.stats") return stats(L.stem_bn);
+    if (name == "d1") return act(L.tmp0, u.cout, u.conv);
+    if (name == "am" && u.pool) {
+      r.ptr = P(L.am[k]);
+      r.n = (int64_t)mb * u.out.vol() * u.cout;
+      r.type = 2;
+      return true;
+    }
+    return false;
+  }
+  if (u.kind == U_BLOCK) return block(L.blk, name);
+  if (u.kind == U_ATT) {
+    const int C = u.cout;
+    if (name.rfind("trunk.", 0) == 0) return block(L.trunk, name.substr(6));
+    if (name.rfind("mask.", 0) == 0) return block(L.mask, name.substr(5));
+    if (name == "u0") return act(L.u0[k], C, u.mask);
+    if (name == "am") {
+      r.ptr = P(L.am[k]);
+      r.n = (int64_t)mb * u.mask.vol() * C;
+      r.type = 2;
+      return true;
+    }
+    if (name == "up") return act(L.up[k], C, u.in);
+    if (name == "mh") return act(L.mh[k], C, u.in);
+    if (name == "r") return act(L.r[k], C, u.in);
+    if (name == "m") return act(L.m[k], C, u.in);
+    if (name == "mbn.stats") return stats(L.mbn);
+    if (name == "dT") return act(L.dT, C, u.in);
+    if (name == "dm") return act(L.dm, C, u.in);
+    if (name == "dr") return act(L.dr, C, u.in);
+    if (name == "dmh") return act(L.dmh, C, u.in);
+    if (name == "dup") return act(L.dup, C, u.in);
+    if (name == "dum") return act(L.dum, C, u.mask);
+    if (name == "du0") return act(L.du0, C, u.mask);
+    return false;
+  }
+  if (name == "dz") {
+    r.ptr = P(L.dz[k]);
+    r.n = (int64_t)mb * 2;
+    r.type = 1;
+    return true;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------------------
 // step phases
 // ---------------------------------------------------------------------------
 // CUDA graphs: each phase is captured once (after one eager warm-up run that
@@ -886,6 +982,7 @@ void Plan::forward(const float *x_in, const int32_t *y) {
 
 void Plan::backward(const float *x_in) {
   run_phase(1, [&] { backward_body(x_in); });
+  bwd_ever = true;
 }
 
 void Plan::step(float lr) {

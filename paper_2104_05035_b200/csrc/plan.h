@@ -95,10 +95,17 @@ struct Schedule {
 Schedule make_schedule(const NetModel &net, const rn_dist_desc &dd, int local_batch, DType dt);
 std::vector<std::pair<int64_t, int64_t>> local_param_ranges(const NetModel &net, const std::vector<char> &local);
 
+struct SavedRef {
+  const void *ptr = nullptr;
+  int64_t n = 0;
+  int type = 0;  // 0 activation dtype, 1 fp32, 2 uint8
+};
+
 struct Plan {
   NetModel net;
   DType dt;
   cudaStream_t stream;
+  int nsm = 148;  // SM count of the plan's device (sizes the per-CTA statistics partials)
   int rank = 0, world = 1, S = 1, Mb = 1, b = 1, mb = 1, replicas = 1, stage = 0, replica = 0;
   std::vector<int> genes, unit_stage;
   std::vector<char> local;
@@ -118,7 +125,7 @@ struct Plan {
   std::vector<UnitL> units;
   std::vector<void *> up_dev;
   NcclComm *world_comm = nullptr, *pipe_comm = nullptr, *dp_comm = nullptr;
-  bool params_set = false, fwd_done = false, fwd_ever = false;
+  bool params_set = false, fwd_done = false, fwd_ever = false, bwd_ever = false;
   const float *last_x = nullptr;
 
   Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int dtype, cudaStream_t st);
@@ -175,6 +182,9 @@ struct Plan {
   void *unit_dx_target(int ui);
   void unit_fwd(int ui, int k, const float *x_in, const int32_t *y);
   void unit_bwd(int ui, int k, const float *x_in);
+
+  // a saved forward tensor / backward temporary of unit ui by name (rn_get_saved)
+  bool saved(int ui, int k, const std::string &name, SavedRef &r);
 
   // phases
   void bind(void *dev, size_t bytes);

@@ -17,7 +17,7 @@ STATUS = {0: "RN_OK", 1: "RN_ERR_ARG", 2: "RN_ERR_SCHEMA", 3: "RN_ERR_INFEASIBLE
           5: "RN_ERR_CUDA", 6: "RN_ERR_NCCL", 7: "RN_ERR_STATE", 8: "RN_ERR_SIZE"}
 EXPORTS = ["rn_ga_default", "rn_gabra_place", "rn_net_units", "rn_net_param_count", "rn_net_param_info",
            "rn_nccl_unique_id", "rn_plan", "rn_plan_describe", "rn_plan_bind", "rn_set_params", "rn_get_params", "rn_get_grads",
-           "rn_get_bn_running", "rn_get_activation", "rn_forward", "rn_backward", "rn_step", "rn_train_step_host",
+           "rn_get_bn_running", "rn_get_activation", "rn_get_unit_grad", "rn_get_saved", "rn_forward", "rn_backward", "rn_step", "rn_train_step_host",
            "rn_train_steps_host", "rn_gradcam",
            "rn_kernel_launches", "rn_set_option", "rn_query", "rn_op_conv3d", "rn_plan_destroy", "rn_last_error"]
 
@@ -193,6 +193,21 @@ class Plan:
         a = np.empty(n, dtype=np.float32)
         _check(lib().rn_get_activation(self.h, unit, micro_batch, a.ctypes.data_as(C.POINTER(C.c_float)),
                                        C.c_int64(n)))
+        return a.reshape(shape)
+
+    def get_unit_grad(self, unit: int, shape) -> np.ndarray:
+        """dl/d(output of `unit`) of the last micro-batch of the last backward."""
+        n = int(np.prod(shape))
+        a = np.empty(n, dtype=np.float32)
+        _check(lib().rn_get_unit_grad(self.h, unit, a.ctypes.data_as(C.POINTER(C.c_float)), C.c_int64(n)))
+        return a.reshape(shape)
+
+    def get_saved(self, unit: int, name: str, shape, micro_batch: int = 0) -> np.ndarray:
+        """A saved forward tensor / backward temporary / BN statistics of `unit` (rn_get_saved)."""
+        n = int(np.prod(shape))
+        a = np.empty(n, dtype=np.float32)
+        _check(lib().rn_get_saved(self.h, unit, name.encode(), micro_batch, a.ctypes.data_as(C.POINTER(C.c_float)),
+                                  C.c_int64(n)))
         return a.reshape(shape)
 
     def gradcam(self, cls: int, map_dev):

@@ -170,3 +170,97 @@ def test_bf16_storage_gap():
     v = np.random.default_rng(0).standard_normal(1000) * 100
     t = torch.tensor(v, dtype=torch.float32).to(torch.bfloat16).to(torch.float64).numpy()
     np.testing.assert_array_equal(O._bf16_round(v), t)
+
+
+@pytest.mark.parametrize("depth", [18, 34])
+def test_deep_step_vs_torch_autograd(depth):
+    """Pins the r18 / r34 COMPOSITION of the oracle: stride-2
+    stage-entry blocks with the 1x1x1 projection branch (block_backward's dz ->
+    projection BN backward -> dxp path), the stem max-pool and its adjoint, three
+    attention modules at three resolutions, and r34's 3/4/6/3 block counts —
+    against the independently written torch float64 autograd model.  Width 4 and a
+    40x48x40 volume keep it CPU-cheap while every stage keeps >= 2x2x2 voxels."""
+    dims = (40, 48, 40)
+    net = O.Net(depth, 4, dims)
+    kinds = [u.kind for u in net.units]
+    assert kinds.count("att") == 3 and sum(1 for u in net.units if u.kind == "block" and u.stride == 2) == 3
+    arrays = synthetic.perturb_params(net.tensors, synthetic.init_params(net.tensors, seed=0))
+    x, y = synthetic.make_batch(2, *dims, seed=1)
+    res = net.train_step(arrays, x, y, lr=1e-4)
+    running = {}
+    loss_t, P = torch_resattnet_loss(net, arrays, x, y, running)
+    loss_t.backward()
+    assert abs(res["loss"] - loss_t.item()) < 1e-11 * abs(loss_t.item())
+    off = 0
+    for name, shape, _ in net.tensors:
+        n = int(np.prod(shape))
+        gt = P[name].grad.numpy().ravel()
+        np.testing.assert_allclose(res["grad"][off:off + n], gt, rtol=1e-7, atol=1e-9 * np.abs(gt).max() + 1e-300,
+                                   err_msg=name)
+        off += n
+    st = res["bn_state"]
+    for name in net.bn_names:
+        np.testing.assert_allclose(st.mean[name], running[name][0].numpy(), rtol=1e-9, atol=1e-13)
+        np.testing.assert_allclose(st.var[name], running[name][1].numpy(), rtol=1e-9)
+
+
+def test_deep_finite_differences_proj_and_stem():
+    """Central finite differences of the r18 oracle's own loss at coordinates of
+    the stem conv (pool adjoint on the path), a stage-entry projection conv and its
+    BN, and the stage-3 attention mask conv — the branches only the deep network
+    has (SPEC S:365-373 kink rule)."""
+    dims = (24, 28, 24)
+    net = O.Net(18, 4, dims)
+    arrays = synthetic.perturb_params(net.tensors, synthetic.init_params(net.tensors, seed=0))
+    x, y = synthetic.make_batch(2, *dims, seed=1)
+    _, G, _ = net.forward_backward(O.Params(net.tensors, arrays), x, y)
+    names = [t[0] for t in net.tensors]
+    r = np.random.default_rng(11)
+    checked = ok = 0
+    for tname in ("u0.conv", "u4.proj", "u4.projbn.gamma", "u7.proj", "u9.mconv1"):
+        ti = names.index(tname)
+        for _ in range(6):
+            j = int(r.integers(arrays[ti].size))
+            vals = []
+            for e in (1e-6, 0.0, -1e-6):
+                arr = [a.copy() for a in arrays]
+                arr[ti] = arr[ti].astype(np.float64)
+                arr[ti].reshape(-1)[j] += e
+                vals.append(net.forward_backward(O.Params(net.tensors, arr), x, y)[0])
+            lp, l0, lm = vals
+            fwd, bwd = (lp - l0) / 1e-6, (l0 - lm) / 1e-6
+            if abs(fwd - bwd) > 1e-3 * max(abs(fwd), abs(bwd), 1e-6):
+                continue
+            fd = (lp - lm) / 2e-6
+            g = np.asarray(G[tname]).reshape(-1)[j]
+            checked += 1
+            ok += abs(fd - g) <= 1e-5 * max(abs(fd), 1e-3)
+    assert checked >= 15 and ok >= checked - 1, (checked, ok)
+
+
+def test_unit_step_composes_to_whole_step():
+    """Net.unit_step (teacher-forced single unit, used by the per-unit GPU parity
+    test) chained over all units with the oracle's own outputs reproduces
+    forward_backward exactly (r18 composition, both storage modes)."""
+    dims = (24, 28, 24)
+    for store in ("f64", "bf16"):
+        net = O.Net(18, 4, dims, store=store)
+        arrays = synthetic.perturb_params(net.tensors, synthetic.init_params(net.tensors, seed=0))
+        x, y = synthetic.make_batch(2, *dims, seed=1)
+        P = O.Params(net.tensors, arrays)
+        loss, Gw, _ = net.forward_backward(P, x, y)
+        outs, h = [], x
+        for ui in range(len(net.units)):
+            r = net.unit_step(P, ui, h, None, y)
+            outs.append(r)
+            h = r["out"]
+        assert outs[-1]["loss"] == loss
+        g = None
+        G = {}
+        for ui in reversed(range(len(net.units))):
+            xin = x if ui == 0 else outs[ui - 1]["out"]
+            r = net.unit_step(P, ui, xin, g, y)
+            G.update(r["G"])
+            g = r["dx"]
+        for n, _, _ in net.tensors:
+            assert np.array_equal(np.asarray(G[n]), np.asarray(Gw[n])), n
