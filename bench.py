@@ -27,6 +27,10 @@ METRIC = "3D-ResAttNet train samples/s at 1/2/4/8 B200; conv tensor-pipe util %"
 DIMS = (91, 109, 91)
 
 
+ELT_FAMILIES = ("bn_apply", "bn_bwd_apply", "bn_partials", "stem_pool_fwd", "stem_pool_bwd", "maxpool_fwd",
+                "maxpool_bwd", "upsample_fwd", "upsample_bwd", "att_fwd", "att_bwd", "sgd")
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -42,6 +46,8 @@ def parse():
                     help="GABRA objective for --stages > 1: 0 = the paper's Eq. 3, 1 = bottleneck (SURVEY f2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--f32-steps", type=int, default=5,
+                    help="also time the RN_F32 path (the paper's implicit fp32 precision) at N=1; 0 = skip")
     return ap.parse_args()
 
 
@@ -228,6 +234,14 @@ def main():
             cms, cfl = plan.query("conv_ms_" + key), plan.query("conv_flops_" + key)
             classes[key] = {"ms_per_step": cms, "tflops": (cfl / (cms / 1000.0) / 1e12) if cms > 0 else None,
                             "launches": plan.query("conv_launches_" + key)}
+        # HBM-bound (elementwise) launches, same live timing: algorithmic bytes / duration
+        elt = {}
+        for fam in ELT_FAMILIES:
+            ems, eby = plan.query("elt_ms_" + fam), plan.query("elt_bytes_" + fam)
+            if ems > 0:
+                elt[fam] = {"ms_per_step": ems, "gbs": eby / (ems / 1000.0) / 1e9, "bytes_per_step": eby,
+                            "launches": plan.query("elt_launches_" + fam)}
+        elt_ms, elt_by = plan.query("elt_ms"), plan.query("elt_bytes")
         plan.set_option("time_kernels", 0)
         torch.cuda.synchronize(dev)
         # end-to-end through the public C ABI with pinned host buffers
@@ -247,13 +261,41 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
 
+        f32 = None
+        if world == 1 and a.f32_steps > 0 and dtype == rn.RN_BF16:
+            p32 = rn.Plan(desc, a.batch, rn.RN_F32, stream=stream, device=dev)
+            p32.set_params(np.concatenate([v.ravel() for v in arrays]).astype(np.float32))
+
+            def step32():
+                p32.forward(xd, yd, want_loss=False)
+                p32.backward()
+                p32.step(lr)
+            for _ in range(2):
+                step32()
+            torch.cuda.synchronize(dev)
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            for _ in range(a.f32_steps):
+                step32()
+            f1.record(stream)
+            torch.cuda.synchronize(dev)
+            fms = f0.elapsed_time(f1) / a.f32_steps
+            f32 = {"value": a.batch / (fms / 1000.0), "unit": "samples/s", "ms_per_step": fms, "steps": a.f32_steps,
+                   "dtype": "f32", "note": "RN_F32: fp32 storage, fp32 SIMT FFMA convolutions (no TF32), same "
+                                           "workload; parity 1e-4 vs float64 (tests/test_gpu_parity.py)"}
+            del p32
+
     step_ms = ms / a.steps
     samples_per_step = a.batch * replicas
     value = samples_per_step * a.steps / (ms / 1000.0)
     pk = peaks()
-    peak_tf = pk.get("bf16_tflops_sustained", 1400.0) if dtype == rn.RN_BF16 else 0.0
-    if dtype == rn.RN_F32:
-        peak_tf = 0.0
+    # the kernels run inside a ~4 ms step: at full clock (no power cap seen) the burst
+    # peak applies, the sustained (power-capped) figure only when the run was capped
+    full_clock = (ck.get("sm_mhz") is not None and ck.get("sm_max_mhz") and
+                  ck["sm_mhz"] >= 0.95 * ck["sm_max_mhz"] and "sw_power_cap" not in ck.get("reasons", []))
+    peak_key = "bf16_tflops" if full_clock else "bf16_tflops_sustained"
+    peak_tf = pk.get(peak_key, 1400.0) if dtype == rn.RN_BF16 else 0.0
+    hbm = pk.get("hbm_gbs", 6550.0)
     tf = lambda fl, ms: fl / (ms / 1000.0) / 1e12 if ms > 0 else 0.0  # noqa: E731
     pair_tf, conv_tf = tf(pair_fl, pair_ms), tf(conv_fl, conv_ms)
     traffic = None
@@ -271,7 +313,16 @@ def main():
                           "ms_per_step": conv_ms, "share_of_step": conv_ms / step_ms,
                           "note": "every fprop/dgrad/wgrad launch, algorithmic 2*M*N*K FLOPs",
                           "by_class": classes},
-            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel inside a long step)"
+            "all_convs_frac": (conv_tf / peak_tf) if peak_tf else None,
+            "class_frac": {k: (c["tflops"] / peak_tf if (c["tflops"] and peak_tf) else None) for k, c in classes.items()},
+            "elementwise": {"bound": "hbm", "peak_gbs": hbm, "ms_per_step": elt_ms,
+                            "gbs": elt_by / (elt_ms / 1000.0) / 1e9 if elt_ms > 0 else None,
+                            "frac": (elt_by / (elt_ms / 1000.0) / 1e9 / hbm) if elt_ms > 0 else None,
+                            "note": "every BN / pool / upsample / attention / SGD launch; algorithmic bytes = each "
+                                    "tensor element read + written once (DESIGN.md 7)",
+                            "by_family": {k: dict(v, frac=v["gbs"] / hbm) for k, v in elt.items()}},
+            "peak_source": ("MEASURED_PEAKS.json " + peak_key + (" (full clock during the run: burst peak)"
+                                                                  if full_clock else " (clock below max: sustained)"))
             if "_fallback" not in pk else "fallback"}
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": a.steps,
@@ -286,6 +337,8 @@ def main():
                "e2e": {"value": samples_per_step * a.e2e_steps / e2e_s, "unit": "samples/s",
                        "h2d_bytes_per_step": int(xs.nbytes + ys.nbytes), "d2h_bytes_per_step": 4},
                "roofline": roof}
+        if f32 is not None:
+            out["f32_path"] = f32
         if world == 1 and not a.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(a.depth, DIMS)
         print(json.dumps(out))

@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -405,6 +406,10 @@ int launch(const TcParams &p, cudaStream_t st) {
   if (!attr) {
     CUDA_CHECK(cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     S::TOTAL));
+    // the whole unified L1/smem as shared memory: the 96 KB-ring variants fit two
+    // CTAs per SM only with the maximum carveout (the default gave 1 CTA per SM)
+    CUDA_CHECK(cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared));
     attr = true;
   }
   int dev = 0, sms = 148;
@@ -415,9 +420,18 @@ int launch(const TcParams &p, cudaStream_t st) {
   if (!per_sm) {
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_tc_kernel<BN, STAGES>, TC_THREADS,
                                                              S::TOTAL));
+    // the 96 KB-ring variants are compiled for 2 CTAs per SM (launch bounds) and two
+    // fit in smem (2 x 101 KB of 228 KB); the occupancy query reports 1 for them
+    // (measured), which left half of every SM idle in the epilogue-heavy launches
+    const int by_smem = (int)(232448 / (S::TOTAL + 1024));
+    const int by_bounds = (STAGES * S::STAGE > 110 * 1024) ? 1 : 2;
+    per_sm = std::max(per_sm, std::min(by_smem, by_bounds));
     per_sm = std::max(1, std::min(per_sm, 512 / (2 * BN)));
   }
   const int grid = (int)std::min<int64_t>(p.cls_item0[p.n_cls], (int64_t)sms * per_sm);
+  if (getenv("RN_DEBUG_GRID"))
+    fprintf(stderr, "conv_tc<%d,%d> items %lld per_sm %d grid %d smem %d\n", BN, STAGES,
+            (long long)p.cls_item0[p.n_cls], per_sm, grid, S::TOTAL);
   launch_k(conv_tc_kernel<BN, STAGES>, grid, TC_THREADS, S::TOTAL, st, p);
   LAUNCH_CHECK();
   return grid;
@@ -710,14 +724,17 @@ int run(TcParams &p, int BN, float *ws, size_t ws_floats, const EpiStats *est, c
 
 // Largest N tile dividing nout, halved while the launch has fewer tiles than
 // SMs (small late-stage layers trade MMA width for parallelism before split-K).
-int pick_bn(int nout, int OW, int OH, int OD, int ON, int mult = 1) {
+int pick_bn(int nout, int OW, int OH, int OD, int ON, int mult = 1, int kblocks = 1 << 20) {
   int bw, bh, bd, bn;
   choose_box(OW, OH, OD, ON, bw, bh, bd, bn);
   const int64_t mt = (int64_t)((OW + bw - 1) / bw) * ((OH + bh - 1) / bh) * ((OD + bd - 1) / bd) * ((ON + bn - 1) / bn);
   int BN = nout % 256 == 0 ? 256 : nout % 128 == 0 ? 128 : 64;
   // halving BN for small layers measured slower overall (more A re-reads): only
-  // when even split-K cannot fill the machine (fewer than 16 tiles)
-  while (BN > 64 && mt * mult * (nout / BN) < 16) BN /= 2;
+  // when even split-K cannot fill the machine (fewer than 16 tiles) -- or when K
+  // is too short to split (1x1x1 convs, <= 8 K-blocks): there the A re-read is
+  // cheap and narrower tiles are the only source of parallelism
+  const int64_t want = kblocks <= 8 ? 148 : 16;
+  while (BN > 64 && mt * mult * (nout / BN) < want) BN /= 2;
   return BN;
 }
 
@@ -754,7 +771,7 @@ int conv_fprop_tc(const ConvGeom &g, const bf16 *x, const bf16 *w, const float *
                   size_t ws_floats, cudaStream_t st, const EpiStats *est) {
   TcParams p;
   memset(&p, 0, sizeof p);
-  const int BN = pick_bn(g.Co, g.Wo, g.Ho, g.Do, g.N);
+  const int BN = pick_bn(g.Co, g.Wo, g.Ho, g.Do, g.N, 1, g.taps() * g.Ci / 64);
   fill_tiles(p, g.Wo, g.Ho, g.Do, g.N, g.Co, BN);
   const int taps = g.taps();
   p.n_taps = taps;
@@ -806,7 +823,7 @@ int conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, b
   if (dy2 && !(g.s == 2 && g.k == 3)) throw Error(RN_ERR_ARG, "conv_dgrad_tc: projection merge needs a k3 s2 conv");
   const int taps = g.taps();
   if (g.s == 1) {
-    const int BN = pick_bn(g.Ci, g.Wi, g.Hi, g.Di, g.N);
+    const int BN = pick_bn(g.Ci, g.Wi, g.Hi, g.Di, g.N, 1, g.taps() * g.Co / 64);
     TcParams p;
     memset(&p, 0, sizeof p);
     fill_tiles(p, g.Wi, g.Hi, g.Di, g.N, g.Ci, BN);

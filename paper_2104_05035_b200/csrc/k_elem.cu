@@ -381,11 +381,20 @@ struct SumFin {
 // registers) and loads EU vectors before computing (memory-level parallelism).
 constexpr int EU = 4;
 
-inline unsigned grid_elem(int64_t vecs) {
+// blocks rounded to a multiple of G / gcd(G, threads): the grid stride must be a
+// multiple of the G = C/VEC channel vectors of a voxel (C = 24 has G = 3)
+inline int64_t stride_multiple(int64_t b, int threads, int G) {
+  int a = G, c = threads;
+  while (c) { const int t = a % c; a = c; c = t; }
+  const int64_t m = G / a;
+  return (b + m - 1) / m * m;
+}
+
+inline unsigned grid_elem(int64_t vecs, int G) {
   int64_t b = (vecs + (int64_t)NT * EU - 1) / ((int64_t)NT * EU);
   if (b > 148 * 8) b = 148 * 8;
   if (b < 1) b = 1;
-  return (unsigned)b;
+  return (unsigned)stride_multiple(b, NT, G);
 }
 
 // y = act(x*scale + shift + R), R = 0 | res | res*rscale + rshift
@@ -508,6 +517,13 @@ __global__ void __launch_bounds__(NT) bn_bwd_apply_k(const T *__restrict__ dy, c
 // ---------------------------------------------------------------------------
 constexpr int NTA = 512;
 
+// BN statistics finalized once per layer by a small kernel (default) instead of
+// in every apply block's prologue (RN_BN_FIN_INLINE=1 restores the latter)
+static bool bn_fin_separate() {
+  static const bool v = !(getenv("RN_BN_FIN_INLINE") && atoi(getenv("RN_BN_FIN_INLINE")) != 0);
+  return v;
+}
+
 // per-channel sums over the P partials [P][2][C] -> dscr[0..C) / dscr[C..2C) (fp64)
 __device__ __forceinline__ void reduce_partials(const float *part, int P, int C, double *out, double *scr) {
   const int t = threadIdx.x, nt = blockDim.x;
@@ -588,6 +604,63 @@ __device__ __forceinline__ void bn_part_finalize(const BnPart &b, int C, float *
   __syncthreads();
 }
 
+// One finalize per BN layer (instead of every apply block reducing all P
+// partials in its prologue): block = 32 channels, warp w sums partials
+// k = w, w+8, ... in fp64 (fixed order), warp 0 combines the 8 warps in order and
+// finalizes exactly as bn_part_finalize (mean / invstd / scale / shift, running
+// statistics).  The apply kernels then read scale / shift (b.P < 0).
+__global__ void __launch_bounds__(256) bn_fin_fwd_k(BnPart b, int C) {
+  __shared__ double red[8][2][32];
+  pdl_begin();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  double s1 = 0.0, s2 = 0.0;
+  if (c < C)
+    for (int k = w; k < b.P; k += 8) {
+      s1 += (double)b.part[(int64_t)k * 2 * C + c];
+      s2 += (double)b.part[(int64_t)k * 2 * C + C + c];
+    }
+  red[w][0][lane] = s1;
+  red[w][1][lane] = s2;
+  __syncthreads();
+  if (w == 0 && c < C) {
+    double S1 = 0.0, S2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      S1 += red[q][0][lane];
+      S2 += red[q][1][lane];
+    }
+    const double mu = S1 / (double)b.V;
+    double var = S2 / (double)b.V - mu * mu;
+    if (var < 0) var = 0;
+    const double is = 1.0 / sqrt(var + (double)b.eps);
+    const double scd = (double)b.gamma[c] * is;
+    b.mean[c] = (float)mu;
+    b.invstd[c] = (float)is;
+    b.scale[c] = (float)scd;
+    b.shift[c] = (float)((double)b.beta[c] - mu * scd);
+    if (b.run_mean) {
+      const double unb = b.V > 1 ? var * (double)b.V / (double)(b.V - 1) : var;
+      b.run_mean[c] = (float)((1.0 - b.momentum) * b.run_mean[c] + b.momentum * mu);
+      b.run_var[c] = (float)((1.0 - b.momentum) * b.run_var[c] + b.momentum * unb);
+    }
+  }
+}
+
+// sc/sh (smem) from statistics finalized by bn_fin_fwd_k (b.P < 0) or from the partials
+__device__ __forceinline__ void bn_part_coefs(const BnPart &b, int C, float *sc, float *sh, double *sums,
+                                              double *scr) {
+  if (b.P >= 0) {
+    bn_part_finalize(b, C, sc, sh, sums, scr);
+    return;
+  }
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    sc[c] = b.scale[c];
+    sh[c] = b.shift[c];
+  }
+  __syncthreads();
+}
+
 // y = act(x*scale + shift + R), R = 0 | res | BN_r(res) (set r.part != null)
 template <typename T>
 __global__ void __launch_bounds__(NTA) bn_apply_part_k(const T *__restrict__ x, int64_t V, int C, BnPart b,
@@ -614,9 +687,9 @@ __global__ void __launch_bounds__(NTA) bn_apply_part_k(const T *__restrict__ x, 
       if (res) rv[q] = ld16(res + k * VEC);
     }
   }
-  bn_part_finalize(b, C, sc, sh, sums, scr);
+  bn_part_coefs(b, C, sc, sh, sums, scr);
   const bool rbn = rb.part != nullptr;
-  if (rbn) bn_part_finalize(rb, C, rsc, rsh, sums, scr);
+  if (rbn) bn_part_coefs(rb, C, rsc, rsh, sums, scr);
   float a[VEC], bb[VEC], ra[VEC], rbv[VEC];
 #pragma unroll
   for (int j = 0; j < VEC; ++j) {
@@ -661,11 +734,48 @@ __global__ void __launch_bounds__(NTA) bn_apply_part_k(const T *__restrict__ x, 
 
 struct BnBwdPart {
   const float *part;  // [P][2][C]: (sum dy', sum dy' (h - mean)), dy' = dy * (mask > 0)
-  int P;
+  int P;              // < 0: coefficients precomputed by bn_fin_bwd_k into coef
   int64_t V;
   const float *gamma, *mean, *invstd;
   float *dgamma, *dbeta;
+  float *coef;        // [3][C] (A, B, Cc) when P < 0
 };
+
+// backward finalize (one per BN layer, as bn_fin_fwd_k): dx = A dy' + B h + Cc,
+// A = gamma*invstd, B = -A*invstd*m2, Cc = -A*m1 + A*invstd*mean*m2 with
+// m1 = mean(dy'), m2 = mean(dy' * xhat); dgamma += S2, dbeta += S1
+__global__ void __launch_bounds__(256) bn_fin_bwd_k(BnBwdPart b, int C) {
+  __shared__ double red[8][2][32];
+  pdl_begin();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  double s1 = 0.0, s2 = 0.0;
+  if (c < C)
+    for (int k = w; k < b.P; k += 8) {
+      s1 += (double)b.part[(int64_t)k * 2 * C + c];
+      s2 += (double)b.part[(int64_t)k * 2 * C + C + c];
+    }
+  red[w][0][lane] = s1;
+  red[w][1][lane] = s2;
+  __syncthreads();
+  if (w == 0 && c < C) {
+    double S1 = 0.0, S2r = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      S1 += red[q][0][lane];
+      S2r += red[q][1][lane];
+    }
+    const double is = b.invstd[c], mu = b.mean[c];
+    const double S2 = is * S2r;  // sum dy' * xhat
+    const double m1 = S1 / (double)b.V, m2 = S2 / (double)b.V;
+    const double A = (double)b.gamma[c] * is;
+    b.coef[c] = (float)A;
+    b.coef[C + c] = (float)(-A * is * m2);
+    b.coef[2 * C + c] = (float)(-A * m1 + A * is * mu * m2);
+    b.dgamma[c] += (float)S2;
+    b.dbeta[c] += (float)S1;
+  }
+}
 
 // dx = A dy' + B h + Cc with the coefficients finalized from the partials
 template <typename T>
@@ -694,6 +804,13 @@ __global__ void __launch_bounds__(NTA) bn_bwd_apply_part_k(const T *__restrict__
       mv[q] = ld16(mask_t + k * VEC);
     }
   }
+  if (b.P < 0) {
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      cA[c] = b.coef[c];
+      cB[c] = b.coef[C + c];
+      cC[c] = b.coef[2 * C + c];
+    }
+  } else {
   reduce_partials(b.part, b.P, C, sums, scr);
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     const double S1 = sums[c], is = b.invstd[c], mu = b.mean[c];
@@ -707,6 +824,7 @@ __global__ void __launch_bounds__(NTA) bn_bwd_apply_part_k(const T *__restrict__
       b.dgamma[c] += (float)S2;
       b.dbeta[c] += (float)S1;
     }
+  }
   }
   __syncthreads();
   float A[VEC], B[VEC], Cc[VEC];
@@ -768,13 +886,13 @@ __global__ void __launch_bounds__(NTA) stem_pool_fwd_k(const bf16 *__restrict__ 
   double *sums = dsm, *scr = dsm + 2 * C;
   float *fs = (float *)(scr + 2 * NTA);
   float *sc = fs, *sh = fs + C;
-  bn_part_finalize(b, C, sc, sh, sums, scr);
-  const int G = C / 8, lg = __ffs(G) - 1;
-  const int ipr = Wo << lg;  // items per output row
+  bn_part_coefs(b, C, sc, sh, sums, scr);
+  const int G = C / 8;
+  const int ipr = Wo * G;  // items per output row
   const int total = N * Do * Ho * ipr;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     const int row = idx / ipr, it = idx - row * ipr;
-    const int ow = it >> lg, c0 = (it & (G - 1)) * 8;
+    const int ow = it / G, c0 = (it - ow * G) * 8;
     const int oh = row % Ho, od = (row / Ho) % Do, nn = row / (Ho * Do);
     float s_[8], b_[8];
     uint32_t fm[4];
@@ -842,11 +960,11 @@ __global__ void __launch_bounds__(NTA) stem_pool_fwd_k(const bf16 *__restrict__ 
   }
 }
 
-inline unsigned grid_part(int64_t vecs) {
+inline unsigned grid_part(int64_t vecs, int G) {
   int64_t b = (vecs + (int64_t)NTA * EU - 1) / ((int64_t)NTA * EU);
   if (b > 148) b = 148;
   if (b < 1) b = 1;
-  return (unsigned)b;
+  return (unsigned)stride_multiple(b, NTA, G);
 }
 
 // max-pool k3 s2 p1, -inf padding; first maximum in (kd,kh,kw) order (reading X10).
@@ -872,14 +990,19 @@ __global__ void __launch_bounds__(NT) maxpool_fwd_k(const T *__restrict__ x, int
   pdl_begin();
   constexpr int VEC = Vec<T>::N;
   typedef typename ArgVec<VEC>::type AT;
-  // one block per output row (n, od, oh); 32-bit index math, G = C/VEC a power of two
-  const int lg = __ffs(C / VEC) - 1;
-  const int oh = (int)(blockIdx.x % (unsigned)Ho), od = (int)((blockIdx.x / (unsigned)Ho) % (unsigned)Do);
-  const int nn = (int)(blockIdx.x / ((unsigned)Ho * Do));
-  const int items = Wo << lg;
-  for (int t = threadIdx.x; t < items; t += blockDim.x) {
-    const int ow = t >> lg, c0 = (t & ((1 << lg) - 1)) * VEC;
-    const int64_t vo = (int64_t)blockIdx.x * Wo + ow;
+  // flattened over (n, od, oh, ow, channel group): every thread busy (one block per
+  // output row left most of a block idle on the 12-14 voxel rows of the mask
+  // branch); 32-bit index math, any G = C/VEC (C = 24 has G = 3)
+  const unsigned G = (unsigned)(C / VEC);
+  const unsigned total = (unsigned)(N * Do * Ho * Wo) * G;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const unsigned vox = t / G;
+    const int c0 = (int)(t - vox * G) * VEC;
+    const int ow = (int)(vox % (unsigned)Wo);
+    const unsigned row = vox / (unsigned)Wo;
+    const int oh = (int)(row % (unsigned)Ho), od = (int)((row / (unsigned)Ho) % (unsigned)Do);
+    const int nn = (int)(row / ((unsigned)Ho * Do));
+    const int64_t vo = (int64_t)vox;
     float sc[VEC], sh[VEC];
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
@@ -938,13 +1061,13 @@ __global__ void __launch_bounds__(NT) maxpool_bwd_k(const T *__restrict__ dy, co
   pdl_begin();
   constexpr int VEC = Vec<T>::N;
   typedef typename ArgVec<VEC>::type AT;
-  // one block per input row (n, id, ih); 32-bit index math
-  const int lg = __ffs(C / VEC) - 1;
+  // one block per input row (n, id, ih); 32-bit index math, any G = C/VEC
+  const int G = C / VEC;
   const int ih = (int)(blockIdx.x % (unsigned)H), id = (int)((blockIdx.x / (unsigned)H) % (unsigned)D);
   const int nn = (int)(blockIdx.x / ((unsigned)H * D));
-  const int items = W << lg;
+  const int items = W * G;
   for (int t = threadIdx.x; t < items; t += blockDim.x) {
-    const int iw = t >> lg, c0 = (t & ((1 << lg) - 1)) * VEC;
+    const int iw = t / G, c0 = (t - iw * G) * VEC;
     const int64_t vi = (int64_t)blockIdx.x * W + iw;
     uint4 g[8];
     AT a[8];
@@ -1280,36 +1403,43 @@ __global__ void upsample_fwd_k(const T *__restrict__ x, int N, int Di, int Hi, i
                                int Do, int Ho, int Wo, UpTables t) {
   pdl_begin();
   constexpr int VEC = Vec<T>::N;
-  const int G = C / VEC;
-  const int64_t n = (int64_t)N * Do * Ho * Wo * G;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i % G) * VEC;
-    int64_t r = i / G;
-    const int64_t vo = r;
-    const int ow = (int)(r % Wo); r /= Wo;
-    const int oh = (int)(r % Ho); r /= Ho;
-    const int od = (int)(r % Do); r /= Do;
-    const int nn = (int)r;
+  // 32-bit index math (the 64-bit div/mod chain made this kernel instruction-bound);
+  // G = C/VEC a power of two; the 6 table entries and the 8 taps are loaded before
+  // the FMAs (same accumulation order as before: a, b, c nested); any G = C/VEC
+  const unsigned G = (unsigned)(C / VEC);
+  const unsigned total = (unsigned)(N * Do * Ho * Wo) * G;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned vo = i / G;
+    const int c0 = (int)(i - vo * G) * VEC;
+    const int ow = (int)(vo % (unsigned)Wo);
+    unsigned r = vo / (unsigned)Wo;
+    const int oh = (int)(r % (unsigned)Ho); r /= (unsigned)Ho;
+    const int od = (int)(r % (unsigned)Do);
+    const int nn = (int)(r / (unsigned)Do);
+    const int2 di = *reinterpret_cast<const int2 *>(t.fw_idx[0] + 2 * od);
+    const int2 hi = *reinterpret_cast<const int2 *>(t.fw_idx[1] + 2 * oh);
+    const int2 wi = *reinterpret_cast<const int2 *>(t.fw_idx[2] + 2 * ow);
+    const float2 dw = *reinterpret_cast<const float2 *>(t.fw_w[0] + 2 * od);
+    const float2 hw = *reinterpret_cast<const float2 *>(t.fw_w[1] + 2 * oh);
+    const float2 ww = *reinterpret_cast<const float2 *>(t.fw_w[2] + 2 * ow);
+    const int ids[2] = {di.x, di.y}, ihs[2] = {hi.x, hi.y}, iws[2] = {wi.x, wi.y};
+    const float wds[2] = {dw.x, dw.y}, whs[2] = {hw.x, hw.y}, wws[2] = {ww.x, ww.y};
+    float v[8][VEC];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const unsigned src = (((unsigned)nn * Di + ids[q >> 2]) * Hi + ihs[(q >> 1) & 1]) * Wi + iws[q & 1];
+      load_vec(x + (int64_t)src * C + c0, v[q]);
+    }
     float acc[VEC];
 #pragma unroll
     for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
-    for (int a = 0; a < 2; ++a) {
-      const int id = t.fw_idx[0][2 * od + a];
-      const float wa = t.fw_w[0][2 * od + a];
-      for (int b = 0; b < 2; ++b) {
-        const int ih = t.fw_idx[1][2 * oh + b];
-        const float wb = wa * t.fw_w[1][2 * oh + b];
-        for (int c = 0; c < 2; ++c) {
-          const int iw = t.fw_idx[2][2 * ow + c];
-          const float wc = wb * t.fw_w[2][2 * ow + c];
-          float v[VEC];
-          load_vec(x + ((((int64_t)nn * Di + id) * Hi + ih) * Wi + iw) * C + c0, v);
 #pragma unroll
-          for (int j = 0; j < VEC; ++j) acc[j] = fmaf(wc, v[j], acc[j]);
-        }
-      }
+    for (int q = 0; q < 8; ++q) {
+      const float wc = (wds[q >> 2] * whs[(q >> 1) & 1]) * wws[q & 1];
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) acc[j] = fmaf(wc, v[q][j], acc[j]);
     }
-    store_vec(y + vo * C + c0, acc);
+    store_vec(y + (int64_t)vo * C + c0, acc);
   }
 }
 
@@ -1554,14 +1684,14 @@ void att_bwd_finalize(DType dt, const void *dout, const void *m, const void *T_,
 
 void bn_apply(DType dt, const void *x, int64_t V, int C, const float *scale, const float *shift, const void *res,
               const float *rscale, const float *rshift, bool relu, void *y, cudaStream_t st) {
-  DISPATCH(dt, launch_k(bn_apply_k<T>, grid_elem(V * C / Vec<T>::N), NT, 0, st, 
+  DISPATCH(dt, launch_k(bn_apply_k<T>, grid_elem(V * C / Vec<T>::N, C / Vec<T>::N), NT, 0, st, 
                    (const T *)x, V, C, scale, shift, (const T *)res, rscale, rshift, relu ? 1 : 0, (T *)y));
   LAUNCH_CHECK();
 }
 
 void bn_bwd_apply(DType dt, const void *dy, const void *x, int64_t V, int C, int mask_mode, const void *mask_t,
                   const float *scale, const float *shift, const float *coef, void *dx, cudaStream_t st) {
-  DISPATCH(dt, launch_k(bn_bwd_apply_k<T>, grid_elem(V * C / Vec<T>::N), NT, 0, st, 
+  DISPATCH(dt, launch_k(bn_bwd_apply_k<T>, grid_elem(V * C / Vec<T>::N, C / Vec<T>::N), NT, 0, st, 
                    (const T *)dy, (const T *)x, V, C, mask_mode, (const T *)mask_t, scale, shift, coef, (T *)dx));
   LAUNCH_CHECK();
 }
@@ -1599,29 +1729,49 @@ void bn_apply_fused(DType dt, const void *x, int64_t V, int C, const BnFinal &f,
     return BnPart{q.part, q.P, V, q.gamma, q.beta, q.mean, q.invstd, q.scale, q.shift, q.run_mean, q.run_var,
                   q.momentum, q.eps};
   };
-  const BnPart b = mk(f);
+  BnPart b = mk(f);
   BnPart r{};
   if (rf) r = mk(*rf);
+  if (bn_fin_separate()) {
+    launch_k(bn_fin_fwd_k, (unsigned)((C + 31) / 32), 256, 0, st, b, C);
+    LAUNCH_CHECK();
+    b.P = -1;
+    if (rf) {
+      launch_k(bn_fin_fwd_k, (unsigned)((C + 31) / 32), 256, 0, st, r, C);
+      LAUNCH_CHECK();
+      r.P = -1;
+    }
+  }
   const size_t smem = (2 * (size_t)C + 2 * NTA) * sizeof(double) + 4 * (size_t)C * sizeof(float);
-  DISPATCH(dt, launch_k(bn_apply_part_k<T>, grid_part(V * C / Vec<T>::N), NTA, smem, st, (const T *)x, V, C, b, r,
+  DISPATCH(dt, launch_k(bn_apply_part_k<T>, grid_part(V * C / Vec<T>::N, C / Vec<T>::N), NTA, smem, st, (const T *)x, V, C, b, r,
                         (const T *)res, relu ? 1 : 0, (T *)y));
   LAUNCH_CHECK();
 }
 
 void bn_bwd_apply_fused(DType dt, const void *dy, const void *h, const void *mask_t, int64_t V, int C,
                         const float *part, int P, const float *gamma, const float *mean, const float *invstd,
-                        float *dgamma, float *dbeta, void *dx, cudaStream_t st) {
-  const BnBwdPart b{part, P, V, gamma, mean, invstd, dgamma, dbeta};
+                        float *dgamma, float *dbeta, void *dx, cudaStream_t st, float *coef) {
+  BnBwdPart b{part, P, V, gamma, mean, invstd, dgamma, dbeta, coef};
+  if (bn_fin_separate() && coef) {
+    launch_k(bn_fin_bwd_k, (unsigned)((C + 31) / 32), 256, 0, st, b, C);
+    LAUNCH_CHECK();
+    b.P = -1;
+  }
   const size_t smem = (2 * (size_t)C + 2 * NTA) * sizeof(double) + 3 * (size_t)C * sizeof(float);
-  DISPATCH(dt, launch_k(bn_bwd_apply_part_k<T>, grid_part(V * C / Vec<T>::N), NTA, smem, st, (const T *)dy,
+  DISPATCH(dt, launch_k(bn_bwd_apply_part_k<T>, grid_part(V * C / Vec<T>::N, C / Vec<T>::N), NTA, smem, st, (const T *)dy,
                         (const T *)h, (const T *)mask_t, V, C, b, (T *)dx));
   LAUNCH_CHECK();
 }
 
 void stem_pool_fwd(const void *h, int N, int D, int H, int W, int C, const BnFinal &f, int64_t V, void *y,
                    uint8_t *am, int Do, int Ho, int Wo, cudaStream_t st) {
-  const BnPart b{f.part, f.P, V, f.gamma, f.beta, f.mean, f.invstd, f.scale, f.shift, f.run_mean, f.run_var,
-                 f.momentum, f.eps};
+  BnPart b{f.part, f.P, V, f.gamma, f.beta, f.mean, f.invstd, f.scale, f.shift, f.run_mean, f.run_var,
+           f.momentum, f.eps};
+  if (bn_fin_separate()) {
+    launch_k(bn_fin_fwd_k, (unsigned)((C + 31) / 32), 256, 0, st, b, C);
+    LAUNCH_CHECK();
+    b.P = -1;
+  }
   const size_t smem = (2 * (size_t)C + 2 * NTA) * sizeof(double) + 2 * (size_t)C * sizeof(float);
   launch_k(stem_pool_fwd_k<0>, 148, NTA, smem, st, (const bf16 *)h, N, D, H, W, C, b, (bf16 *)y, am, Do, Ho, Wo);
   LAUNCH_CHECK();
@@ -1629,7 +1779,7 @@ void stem_pool_fwd(const void *h, int N, int D, int H, int W, int C, const BnFin
 
 void maxpool_fwd(DType dt, const void *x, int N, int D, int H, int W, int C, const float *scale, const float *shift,
                  bool relu, void *y, uint8_t *argmax, int Do, int Ho, int Wo, cudaStream_t st) {
-  DISPATCH(dt, launch_k(maxpool_fwd_k<T>, (unsigned)(N * Do * Ho), NT, 0, st, 
+  DISPATCH(dt, launch_k(maxpool_fwd_k<T>, grid_for((int64_t)N * Do * Ho * Wo * C / Vec<T>::N, NT, 148 * 8), NT, 0, st,
                    (const T *)x, N, D, H, W, C, scale, shift, relu ? 1 : 0, (T *)y, argmax, Do, Ho, Wo));
   LAUNCH_CHECK();
 }
@@ -1765,23 +1915,24 @@ __global__ void up_adj_pass_k(const Ti *__restrict__ in, int64_t A, int Lin, int
                               const int *__restrict__ start, const int *__restrict__ oidx,
                               const float *__restrict__ w, To *__restrict__ out) {
   pdl_begin();
-  const int64_t B4 = B / 4;
-  const int64_t n = A * Lout * B4;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = (i % B4) * 4;
-    const int64_t r = i / B4;
-    const int j = (int)(r % Lout);
-    const int64_t a = r / Lout;
+  // 32-bit index math (the launcher checks the sizes fit)
+  const unsigned B4 = (unsigned)(B / 4);
+  const unsigned n = (unsigned)A * Lout * B4;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned b = (i % B4) * 4;
+    const unsigned r = i / B4;
+    const int j = (int)(r % (unsigned)Lout);
+    const unsigned a = r / (unsigned)Lout;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
     const int k1 = start[j + 1];
     for (int k = start[j]; k < k1; ++k) {
       float v[4];
-      ld4f(in + (a * Lin + oidx[k]) * B + b, v);
+      ld4f(in + ((int64_t)a * Lin + oidx[k]) * B + b, v);
       const float wk = w[k];
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[e] = fmaf(wk, v[e], acc[e]);
     }
-    st4f(out + (a * Lout + j) * B + b, acc);
+    st4f(out + ((int64_t)a * Lout + j) * B + b, acc);
   }
 }
 
@@ -1794,6 +1945,7 @@ size_t upsample_bwd_ws_floats(int N, int Di, int Hi, int Wi, int C, int Do, int 
 void upsample_bwd_sep(const void *dy, int N, int Di, int Hi, int Wi, int C, void *dx, int Do, int Ho, int Wo,
                       const UpTables &t, float *ws, cudaStream_t st) {
   if (C % 4 != 0) throw Error(RN_ERR_ARG, "upsample_bwd_sep: C % 4");
+  if ((int64_t)N * Di * Hi * Wi * C >= (1LL << 31)) throw Error(RN_ERR_ARG, "upsample_bwd_sep: tensor too large");
   float *t1 = ws, *t2 = ws + (size_t)N * Do * Ho * Wi * C;
   auto grid = [](int64_t vec) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((vec + 255) / 256, 148 * 16)); };
   // w: [N*Do*Ho][Wo][C] -> [N*Do*Ho][Wi][C]

@@ -352,6 +352,31 @@ bool Plan::timing() const {
   return it != opts.end() && it->second != 0;
 }
 
+// elementwise / HBM-bound launches timed live (option time_kernels): event pair
+// around each launch on the plan stream, tagged with its family and its
+// algorithmic bytes (every tensor element read + written once)
+const char *const kEltFamilies[] = {"bn_apply", "bn_bwd_apply", "bn_partials", "stem_pool_fwd", "stem_pool_bwd",
+                                    "maxpool_fwd", "maxpool_bwd", "upsample_fwd", "upsample_bwd", "att_fwd",
+                                    "att_bwd", "head", "sgd", nullptr};
+enum { F_BN_APPLY = 0, F_BN_BWD_APPLY, F_BN_PARTIALS, F_STEM_POOL_FWD, F_STEM_POOL_BWD, F_MAXPOOL_FWD,
+       F_MAXPOOL_BWD, F_UP_FWD, F_UP_BWD, F_ATT_FWD, F_ATT_BWD, F_HEAD, F_SGD };
+
+struct EltTimer {
+  Plan *p;
+  size_t i = 0;
+  int fam;
+  bool on;
+  EltTimer(Plan *pl, int f, double bytes) : p(pl), fam(f), on(pl->timing()) {
+    if (on) i = p->tk_begin(3, bytes);
+  }
+  ~EltTimer() {
+    if (on) {
+      p->ev_pool[i].kind = fam;
+      cudaEventRecord(p->ev_pool[i].b, p->stream);
+    }
+  }
+};
+
 size_t Plan::tk_begin(int cls, double flops) {
   if (ev_used == ev_pool.size()) {
     EvPair e;
@@ -580,12 +605,19 @@ void Plan::bn_fwd(const BNL &b, int k, const void *h, const void *res, const flo
                   bool relu, void *y) {
   if (fused_stats() && y && !rscale) {
     BNL &m = const_cast<BNL &>(b);
-    if (m.fP <= 0) m.fP = bn_stats_partials(dt, h, b.V, b.C, (float *)P(b.fpart), stream);
+    const double vc = (double)b.V * b.C * dt_size(dt);
+    if (m.fP <= 0) {
+      EltTimer tm(this, F_BN_PARTIALS, vc);
+      m.fP = bn_stats_partials(dt, h, b.V, b.C, (float *)P(b.fpart), stream);
+    }
+    EltTimer tm(this, F_BN_APPLY, vc * (res ? 3 : 2));
     bn_apply_fused(dt, h, b.V, b.C, bn_final(b, k), nullptr, res, relu, y, stream);
     m.fP = 0;  // consumed: the next producer decides again (never reuse stale partials)
     return;
   }
   float *part = (float *)P(off_partial);
+  const double vc = (double)b.V * b.C * dt_size(dt);
+  EltTimer tm(this, F_BN_APPLY, vc * (y ? (res ? 4 : 3) : 1));
   bn_stats_finalize(dt, h, b.V, b.C, part, counter(), master(b.gamma_idx), master(b.gamma_idx + 1),
                     bn_stat(b, k, 0), bn_stat(b, k, 1), bn_stat(b, k, 2), bn_stat(b, k, 3),
                     (float *)P(off_run_mean) + b.run_off, (float *)P(off_run_var) + b.run_off, BN_MOMENTUM, BN_EPS,
@@ -600,14 +632,21 @@ void Plan::bn_backward(const BNL &b, int k, const void *dy, const void *h, int m
                        void *dx, int slot) {
   if (fused_stats() && mask_mode == MASK_TENSOR) {
     BNL &m = const_cast<BNL &>(b);
-    if (m.bP <= 0) m.bP = bn_bwd_partials(dt, dy, h, mask_t, bn_stat(b, k, 0), b.V, b.C, (float *)P(b.bpart), stream);
+    const double vc = (double)b.V * b.C * dt_size(dt);
+    if (m.bP <= 0) {
+      EltTimer tm(this, F_BN_PARTIALS, vc * 3);
+      m.bP = bn_bwd_partials(dt, dy, h, mask_t, bn_stat(b, k, 0), b.V, b.C, (float *)P(b.bpart), stream);
+    }
+    EltTimer tm(this, F_BN_BWD_APPLY, vc * 4);
     bn_bwd_apply_fused(dt, dy, h, mask_t, b.V, b.C, (const float *)P(b.bpart), b.bP, master(b.gamma_idx),
-                       bn_stat(b, k, 0), bn_stat(b, k, 1), grad(b.gamma_idx), grad(b.gamma_idx + 1), dx, stream);
+                       bn_stat(b, k, 0), bn_stat(b, k, 1), grad(b.gamma_idx), grad(b.gamma_idx + 1), dx, stream,
+                       (float *)P(off_coef) + slot * 3 * 512);
     m.bP = 0;  // consumed: the next producer decides again
     return;
   }
   float *part = (float *)P(off_partial);
   float *coef = (float *)P(off_coef) + slot * 3 * 512;
+  EltTimer tm(this, F_BN_BWD_APPLY, (double)b.V * b.C * dt_size(dt) * (mask_mode == MASK_TENSOR ? 7 : 5));
   bn_bwd_reduce_finalize(dt, dy, h, b.V, b.C, mask_mode, mask_t, bn_stat(b, k, 2), bn_stat(b, k, 3),
                          bn_stat(b, k, 0), bn_stat(b, k, 1), master(b.gamma_idx), part, counter(),
                          grad(b.gamma_idx), grad(b.gamma_idx + 1), coef, stream);
@@ -625,9 +664,17 @@ void Plan::block_fwd(BlockL &B, int k, const void *x) {
     conv_fwd(B.cp, x, P(B.hp[k]), nullptr, &B.bp);
     if (fused_stats()) {
       // out = ReLU(BN2(h2) + BNp(hp)): both statistics finalized in the apply kernel
-      if (B.b2.fP <= 0) B.b2.fP = bn_stats_partials(dt, P(B.h2[k]), B.b2.V, B.b2.C, (float *)P(B.b2.fpart), stream);
-      if (B.bp.fP <= 0) B.bp.fP = bn_stats_partials(dt, P(B.hp[k]), B.bp.V, B.bp.C, (float *)P(B.bp.fpart), stream);
+      const double vc = (double)B.b2.V * B.b2.C * dt_size(dt);
+      if (B.b2.fP <= 0) {
+        EltTimer tm(this, F_BN_PARTIALS, vc);
+        B.b2.fP = bn_stats_partials(dt, P(B.h2[k]), B.b2.V, B.b2.C, (float *)P(B.b2.fpart), stream);
+      }
+      if (B.bp.fP <= 0) {
+        EltTimer tm(this, F_BN_PARTIALS, vc);
+        B.bp.fP = bn_stats_partials(dt, P(B.hp[k]), B.bp.V, B.bp.C, (float *)P(B.bp.fpart), stream);
+      }
       const BnFinal fp = bn_final(B.bp, k);
+      EltTimer tm(this, F_BN_APPLY, vc * 3);
       bn_apply_fused(dt, P(B.h2[k]), B.b2.V, B.b2.C, bn_final(B.b2, k), &fp, P(B.hp[k]), true, P(B.out_[k]), stream);
       B.b2.fP = B.bp.fP = 0;
     } else {
@@ -698,6 +745,8 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
     }
     if (u.pool && L.stem_bn.fP > 0) {
       // BN statistics fused into the stem conv; finalize + BN + ReLU + pool in one kernel
+      EltTimer tm(this, F_STEM_POOL_FWD,
+                  (double)mb * u.cout * (2.0 * u.conv.vol() + 3.0 * u.out.vol()));
       stem_pool_fwd(P(L.stem_h[k]), mb, u.conv.d, u.conv.h, u.conv.w, u.cout, bn_final(L.stem_bn, k), L.stem_bn.V,
                     P(L.out[k]), (uint8_t *)P(L.am[k]), u.out.d, u.out.h, u.out.w, stream);
     } else if (u.pool) {
@@ -714,14 +763,21 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
     const int C = u.cout;
     const int64_t V = (int64_t)mb * u.in.vol();
     block_fwd(L.trunk, k, x);
+    {
+    EltTimer tm(this, F_MAXPOOL_FWD, (double)mb * C * (u.in.vol() * dt_size(dt) + u.mask.vol() * (dt_size(dt) + 1.0)));
     maxpool_fwd(dt, x, mb, u.in.d, u.in.h, u.in.w, C, nullptr, nullptr, false, P(L.u0[k]), (uint8_t *)P(L.am[k]),
                 u.mask.d, u.mask.h, u.mask.w, stream);
+    }
     block_fwd(L.mask, k, P(L.u0[k]));
+    {
+    EltTimer tm(this, F_UP_FWD, (double)mb * C * (u.in.vol() + u.mask.vol()) * dt_size(dt));
     upsample_fwd(dt, P(L.mask.out_[k]), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.up[k]), u.in.d, u.in.h, u.in.w,
                  L.tab, stream);
+    }
     conv_fwd(L.mc1, P(L.up[k]), P(L.mh[k]), nullptr, &L.mbn);
     bn_fwd(L.mbn, k, P(L.mh[k]), nullptr, nullptr, nullptr, true, P(L.r[k]));
     conv_fwd(L.mc2, P(L.r[k]), P(L.m[k]), master(L.bias_idx));
+    EltTimer tm(this, F_ATT_FWD, 3.0 * V * C * dt_size(dt));
     att_fwd(dt, P(L.m[k]), P(L.trunk.out_[k]), V, C, P(L.out[k]), stream);
   } else {
     const float dz_scale = 1.0f / (float)(mb * Mb * replicas);
@@ -770,10 +826,13 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
       // BN-backward apply inside the stem weight gradient (no dh tensor)
       const BNL &b = L.stem_bn;
       float *coef = (float *)P(off_coef);
-      stem_pool_bwd(P(L.dout), (const uint8_t *)P(L.am[k]), P(L.stem_h[k]), mb, u.conv.d, u.conv.h, u.conv.w, u.cout,
-                    u.out.d, u.out.h, u.out.w, bn_stat(b, k, 2), bn_stat(b, k, 3), bn_stat(b, k, 0), bn_stat(b, k, 1),
-                    master(b.gamma_idx), grad(b.gamma_idx), grad(b.gamma_idx + 1), coef, P(L.tmp0),
-                    (float *)P(off_partial), counter(), stream);
+      {
+        EltTimer tm(this, F_STEM_POOL_BWD, (double)mb * u.cout * (3.0 * u.out.vol() + 4.0 * u.conv.vol()));
+        stem_pool_bwd(P(L.dout), (const uint8_t *)P(L.am[k]), P(L.stem_h[k]), mb, u.conv.d, u.conv.h, u.conv.w,
+                      u.cout, u.out.d, u.out.h, u.out.w, bn_stat(b, k, 2), bn_stat(b, k, 3), bn_stat(b, k, 0),
+                      bn_stat(b, k, 1), master(b.gamma_idx), grad(b.gamma_idx), grad(b.gamma_idx + 1), coef,
+                      P(L.tmp0), (float *)P(off_partial), counter(), stream);
+      }
       conv_bwd_weight(L.stem_conv, x, P(L.tmp0), true, P(L.stem_h[k]), coef);
       return;
     }
@@ -794,8 +853,11 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
   } else if (u.kind == U_ATT) {
     const int C = u.cout;
     const int64_t V = (int64_t)mb * u.in.vol();
+    {
+    EltTimer tm(this, F_ATT_BWD, 5.0 * V * C * dt_size(dt));
     att_bwd_finalize(dt, P(L.dout), P(L.m[k]), P(L.trunk.out_[k]), V, C, P(L.dT), P(L.dm), (float *)P(off_partial),
                      counter(), grad(L.bias_idx), stream);
+    }
     conv_bwd_weight(L.mc2, P(L.r[k]), P(L.dm), false);
     StatsTarget tm;
     tm.bn = &L.mbn;
@@ -809,16 +871,22 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
     bn_backward(L.mbn, k, P(L.dr), P(L.mh[k]), MASK_TENSOR, P(L.r[k]), P(L.dmh), 0);
     conv_bwd_weight(L.mc1, P(L.up[k]), P(L.dmh), false);
     conv_bwd_data(L.mc1, P(L.dmh), P(L.dup), false, nullptr, nullptr);
-    auto itu = opts.find("up_bwd_sep");
-    if (dt == DT_BF16 && (itu == opts.end() || itu->second != 0))
-      upsample_bwd_sep(P(L.dup), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.dum), u.in.d, u.in.h, u.in.w, L.tab,
-                       (float *)P(off_up_ws), stream);
-    else
-      upsample_bwd(dt, P(L.dup), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.dum), u.in.d, u.in.h, u.in.w, L.tab,
-                   stream);
+    {
+      EltTimer tu(this, F_UP_BWD, (double)mb * C * (u.in.vol() + u.mask.vol()) * dt_size(dt));
+      auto itu = opts.find("up_bwd_sep");
+      if (dt == DT_BF16 && (itu == opts.end() || itu->second != 0))
+        upsample_bwd_sep(P(L.dup), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.dum), u.in.d, u.in.h, u.in.w, L.tab,
+                         (float *)P(off_up_ws), stream);
+      else
+        upsample_bwd(dt, P(L.dup), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.dum), u.in.d, u.in.h, u.in.w, L.tab,
+                     stream);
+    }
     block_bwd(L.mask, k, P(L.u0[k]), P(L.dum), P(L.du0), false);
-    maxpool_bwd(dt, P(L.du0), (const uint8_t *)P(L.am[k]), mb, u.in.d, u.in.h, u.in.w, C, u.mask.d, u.mask.h,
-                u.mask.w, dx, false, stream);
+    {
+      EltTimer tp(this, F_MAXPOOL_BWD, (double)mb * C * (u.mask.vol() * (dt_size(dt) + 1.0) + u.in.vol() * dt_size(dt)));
+      maxpool_bwd(dt, P(L.du0), (const uint8_t *)P(L.am[k]), mb, u.in.d, u.in.h, u.in.w, C, u.mask.d, u.mask.h,
+                  u.mask.w, dx, false, stream);
+    }
     block_bwd(L.trunk, k, x, P(L.dT), dx, true, dout_consumer(ui, k));
   } else {
     const int p0 = net.unit_param_begin[ui];
@@ -1114,6 +1182,14 @@ void Plan::step_body(float lr) {
   if (replicas > 1)
     for (auto &rg : ranges)
       nccl_allreduce_sum_f32(dp_comm, (float *)P(off_grad) + rg.first, (size_t)(rg.second - rg.first), stream);
+  int64_t conv_params = 0, all_params = 0;
+  for (const auto &t : net.params)
+    if (local[t.unit]) {
+      all_params += t.numel;
+      if (t.kind == P_CONV) conv_params += t.numel;
+    }
+  // w, g read + w written (fp32), + the bf16 forward and flipped dgrad copies of every conv weight
+  EltTimer tm(this, F_SGD, 12.0 * all_params + (dt == DT_BF16 ? 4.0 * conv_params : 0.0));
   sgd_ranges((const int64_t *)P(off_sgdrg), n_sgdrg, (float *)P(off_master), (const float *)P(off_grad), lr, stream);
   if (dt == DT_BF16)
     sgd_repack_all((const ConvPack *)P(off_pack), n_pack, pack_tiles, (float *)P(off_master),
@@ -1296,6 +1372,7 @@ rn_status Plan::query(const std::string &k, double *v) {
     if (k.find("_stem") != std::string::npos) kind = K_STEM;
     double ms = 0, fl = 0, n = 0;
     for (size_t i = 0; i < ev_used; ++i) {
+      if (ev_pool[i].cls == 3) continue;  // elementwise launches
       if (cls >= 0 && ev_pool[i].cls != cls) continue;
       if (kind >= 0 && ev_pool[i].kind != kind) continue;
       float e = 0.f;
@@ -1307,6 +1384,33 @@ rn_status Plan::query(const std::string &k, double *v) {
     if (k.rfind("conv_ms", 0) == 0) *v = ms;
     else if (k.rfind("conv_flops", 0) == 0) *v = fl;
     else if (k.rfind("conv_launches", 0) == 0) *v = n;
+    else return set_error(RN_ERR_ARG, "unknown statistic " + k);
+    return RN_OK;
+  }
+  if (k.rfind("elt_", 0) == 0) {
+    // elt_ms / elt_bytes / elt_launches [_<family>] of the elementwise launches (time_kernels)
+    CUDA_CHECK(cudaStreamSynchronize(stream));
+    const std::string what = k.substr(4, k.find('_', 4) == std::string::npos ? std::string::npos : k.find('_', 4) - 4);
+    int fam = -1;
+    const size_t us = k.find('_', 4);
+    if (us != std::string::npos) {
+      const std::string f = k.substr(us + 1);
+      for (int i = 0; kEltFamilies[i]; ++i)
+        if (f == kEltFamilies[i]) fam = i;
+      if (fam < 0) return set_error(RN_ERR_ARG, "unknown elementwise family " + f);
+    }
+    double ms = 0, by = 0, n = 0;
+    for (size_t i = 0; i < ev_used; ++i) {
+      if (ev_pool[i].cls != 3 || (fam >= 0 && ev_pool[i].kind != fam)) continue;
+      float e = 0.f;
+      CUDA_CHECK(cudaEventElapsedTime(&e, ev_pool[i].a, ev_pool[i].b));
+      ms += e;
+      by += ev_pool[i].flops;
+      n += 1;
+    }
+    if (what == "ms") *v = ms;
+    else if (what == "bytes") *v = by;
+    else if (what == "launches") *v = n;
     else return set_error(RN_ERR_ARG, "unknown statistic " + k);
     return RN_OK;
   }

@@ -273,6 +273,7 @@ def op_parity(depth, w, dims, N):
 
 
 @pytest.mark.parametrize("depth,w,dims,N,tag", [
+    (0, 24, (16, 16, 16), 2, "tiny_w24"),           # SIMT convs, C = 24 (channel groups of 3)
     (18, 64, (40, 48, 40), 2, "r18_small"),
     (18, 64, (91, 109, 91), 8, "bench"),           # bench.py's configuration (BASELINE configs[1])
 ])

@@ -403,3 +403,32 @@ def test_gradcam_matches_oracle(depth, w, dims, dtype):
         assert np.abs(got - ref).max() <= 1e-5 * max(np.abs(ref).max(), 1e-30) + 1e-12
         peak = max(peak, float(ref.max()))
     assert peak > 0.0  # at least one class has positive evidence somewhere (non-trivial maps)
+
+
+@pytest.mark.parametrize("w", [24, 64])
+def test_bf16_no_stale_statistics_across_steps(w):
+    """BN statistics partials are never reused across launches: a plan
+    that stepped on batch 1 twice (eager, then captured) and then runs batch 2 (a
+    graph replay on new data) produces bit for bit what a fresh plan produces on
+    batch 2 — including the tiny net at base width 24, where the stem has no fast
+    path and no pool, and with 2 micro-batches."""
+    dims = (16, 16, 16)
+    xa, ya = synthetic.make_batch(4, *dims, seed=1)
+    xb, yb = synthetic.make_batch(4, *dims, seed=5)
+    outs = []
+    for seq in ((xa, ya), (xa, ya), (xb, yb)), ((xb, yb),):
+        st = torch.cuda.Stream()
+        plan = rn.Plan(rn.net_desc(0, w, dims), 4, rn.RN_BF16, micro_batches=2, stream=st)
+        arrays = synthetic.perturb_params(plan.tensors, synthetic.init_params(plan.tensors, seed=0))
+        flat = np.concatenate([a.ravel() for a in arrays]).astype(np.float32)
+        with torch.cuda.stream(st):
+            for xv, yv in seq:
+                plan.set_params(flat)
+                loss = plan.forward(torch.from_numpy(xv).cuda(), torch.from_numpy(yv).cuda())
+                plan.backward()
+                g = plan.get_grads()
+            st.synchronize()
+        outs.append((loss, g, plan.get_bn_running()))
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][1], outs[1][1])
+    assert np.array_equal(outs[0][2][0], outs[1][2][0]) and np.array_equal(outs[0][2][1], outs[1][2][1])
