@@ -168,8 +168,9 @@ def main():
     genes = None
     if S > 1:
         loads = rn.net_units(desc)[2]
-        caps = [int(np.ceil(1.10 * max(max(loads), -(-sum(loads) // S))))] * S
-        genes = rn.gabra_place(loads, caps, seed=7, require_all_used=1, objective=a.ga_objective)[0]
+        # reading G4b: smallest capacity slack (1.1, 1.2, ...) with a feasible placement
+        genes = rn.gabra_place_slack(loads, S, seed=7, require_all_used=1, objective=a.ga_objective,
+                                     init_attempts=4096)[0]
     nid = None
     if world > 1:
         obj = [rn.nccl_unique_id() if rank == 0 else None]

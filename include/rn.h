@@ -102,6 +102,18 @@ rn_status rn_gabra_place(int32_t n, const int64_t *loads, int32_t m, const int64
                          const rn_ga_params *gp, int32_t *genes_out, double *profit_out,
                          int64_t *gpu_load_out);
 
+/* rn_gabra_place_slack — the placement policy the hybrid runs use (reading G4b,
+ * DESIGN.md): identical capacities d_j = ceil(s * max(max_i p_i, ceil(sum_i p_i / m)))
+ * for the smallest slack s in 1.1, 1.2, ..., 2.0 (k/10) for which rn_gabra_place
+ * finds a capacity-respecting placement (P:171-216 give no capacities for
+ * identical GPUs; a chain of coarse partitions, e.g. r18 on 4 GPUs, cannot be
+ * packed at 10 % slack).  Outputs as rn_gabra_place, plus caps_out[m] (may be
+ * NULL) and slack_out (may be NULL).  Bit-identical to oracle/gabra.py
+ * place_with_slack.  Errors: RN_ERR_ARG, RN_ERR_INFEASIBLE (none up to 2.0). */
+rn_status rn_gabra_place_slack(int32_t n, const int64_t *loads, int32_t m, const rn_ga_params *gp,
+                               int32_t *genes_out, double *profit_out, int64_t *gpu_load_out, int64_t *caps_out,
+                               double *slack_out);
+
 /* ------------------------------------------------------------------------- */
 /* Network description, costing and partitioning (§3.1.1).            */
 /* ------------------------------------------------------------------------- */

@@ -69,6 +69,25 @@ def default_capacities(loads, m: int, slack: float = 1.10):
     return [int(math.ceil(slack * base))] * m
 
 
+def place_with_slack(loads, m: int, **kw):
+    """Reading G4b: the paper gives no capacities for identical GPUs
+    (P:171-216).  Take the G4 capacities with the smallest slack s in 1.1, 1.2,
+    ..., 2.0 (k/10, k = 11..20) for which Algorithm 1 (with the Algorithm 2
+    fallback, G19b) finds a capacity-respecting placement: a partition chain
+    whose blocks are too coarse to pack at 10 % slack (r18 on 4 GPUs, r34 on 8)
+    is placed at the next slack instead of being declared infeasible.
+    Returns (genes, profit, per-GPU loads, capacities, slack)."""
+    for k in range(11, 21):
+        s = k / 10
+        d = default_capacities(loads, m, s)
+        try:
+            g, f, L = gabra(loads, d, **kw)
+        except Infeasible:
+            continue
+        return g, f, L, d, s
+    raise Infeasible("no capacity-respecting placement up to slack 2.0")
+
+
 # ----------------------------------------------------------------------------
 # PRNG (reading G20): xoshiro256** seeded by splitmix64
 # ----------------------------------------------------------------------------

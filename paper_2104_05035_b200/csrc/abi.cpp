@@ -2,11 +2,13 @@
 // validation, exception -> rn_status conversion, thread-local error message.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/rn.h"
 #include "comm.h"
@@ -103,6 +105,36 @@ rn_status rn_gabra_place(int32_t n, const int64_t *loads, int32_t m, const int64
       g.p_mut < 0 || g.p_mut > 1 || (g.objective != 0 && g.objective != 1))
     return set_error(RN_ERR_ARG, "rn_gabra_place: bad GA parameters");
   return gabra_place(n, loads, m, caps, g, genes_out, profit_out, gpu_load_out);
+  GUARD_END
+}
+
+rn_status rn_gabra_place_slack(int32_t n, const int64_t *loads, int32_t m, const rn_ga_params *gp,
+                               int32_t *genes_out, double *profit_out, int64_t *gpu_load_out, int64_t *caps_out,
+                               double *slack_out) {
+  GUARD_BEGIN
+  if (n < 1 || m < 1 || !loads || !genes_out) return set_error(RN_ERR_ARG, "rn_gabra_place_slack: bad arguments");
+  int64_t tot = 0, mx = 0;
+  for (int i = 0; i < n; ++i) {
+    if (loads[i] < 0) return set_error(RN_ERR_ARG, "rn_gabra_place_slack: negative load");
+    tot += loads[i];
+    mx = std::max(mx, loads[i]);
+  }
+  const int64_t base = std::max(mx, (tot + m - 1) / m);
+  if (base <= 0) return set_error(RN_ERR_ARG, "rn_gabra_place_slack: all loads are zero");
+  std::vector<int64_t> caps(m);
+  for (int k = 11; k <= 20; ++k) {  // reading G4b: slack k/10
+    const double s = k / 10.0;
+    const int64_t d = (int64_t)std::ceil(s * (double)base);
+    for (int j = 0; j < m; ++j) caps[j] = d;
+    const rn_status r = rn_gabra_place(n, loads, m, caps.data(), gp, genes_out, profit_out, gpu_load_out);
+    if (r == RN_ERR_INFEASIBLE) continue;
+    if (r != RN_OK) return r;
+    if (caps_out)
+      for (int j = 0; j < m; ++j) caps_out[j] = d;
+    if (slack_out) *slack_out = s;
+    return RN_OK;
+  }
+  return set_error(RN_ERR_INFEASIBLE, "rn_gabra_place_slack: no capacity-respecting placement up to slack 2.0");
   GUARD_END
 }
 

@@ -517,10 +517,11 @@ __global__ void __launch_bounds__(NT) bn_bwd_apply_k(const T *__restrict__ dy, c
 // ---------------------------------------------------------------------------
 constexpr int NTA = 512;
 
-// BN statistics finalized once per layer by a small kernel (default) instead of
-// in every apply block's prologue (RN_BN_FIN_INLINE=1 restores the latter)
+// BN statistics finalized once per layer by a small kernel (RN_BN_FIN_SEPARATE=1)
+// instead of in every apply block's prologue (default: measured equal within run
+// noise, 2186-2227 vs 2194-2227 samples/s, and one launch fewer per BN)
 static bool bn_fin_separate() {
-  static const bool v = !(getenv("RN_BN_FIN_INLINE") && atoi(getenv("RN_BN_FIN_INLINE")) != 0);
+  static const bool v = getenv("RN_BN_FIN_SEPARATE") && atoi(getenv("RN_BN_FIN_SEPARATE")) != 0;
   return v;
 }
 

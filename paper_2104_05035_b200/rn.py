@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "librn.so")
 RN_F32, RN_BF16 = 0, 1
 STATUS = {0: "RN_OK", 1: "RN_ERR_ARG", 2: "RN_ERR_SCHEMA", 3: "RN_ERR_INFEASIBLE", 4: "RN_ERR_NUMERIC",
           5: "RN_ERR_CUDA", 6: "RN_ERR_NCCL", 7: "RN_ERR_STATE", 8: "RN_ERR_SIZE"}
-EXPORTS = ["rn_ga_default", "rn_gabra_place", "rn_net_units", "rn_net_param_count", "rn_net_param_info",
+EXPORTS = ["rn_ga_default", "rn_gabra_place", "rn_gabra_place_slack", "rn_net_units", "rn_net_param_count", "rn_net_param_info",
            "rn_nccl_unique_id", "rn_plan", "rn_plan_describe", "rn_plan_bind", "rn_set_params", "rn_get_params", "rn_get_grads",
            "rn_get_bn_running", "rn_get_activation", "rn_get_unit_grad", "rn_get_saved", "rn_forward", "rn_backward", "rn_step", "rn_train_step_host",
            "rn_train_steps_host", "rn_gradcam",
@@ -94,6 +94,20 @@ def gabra_place(loads, caps, **kw):
     gp = ga_params(**kw)
     _check(lib().rn_gabra_place(n, L, m, D, C.byref(gp), genes, C.byref(profit), gl))
     return list(genes), profit.value, list(gl)
+
+
+def gabra_place_slack(loads, m, **kw):
+    """rn_gabra_place_slack: (genes, profit, per-GPU loads, capacities, slack)."""
+    n = len(loads)
+    L = (C.c_int64 * n)(*loads)
+    genes = (C.c_int32 * n)()
+    profit = C.c_double()
+    gl = (C.c_int64 * m)()
+    caps = (C.c_int64 * m)()
+    slack = C.c_double()
+    gp = ga_params(**kw)
+    _check(lib().rn_gabra_place_slack(n, L, m, C.byref(gp), genes, C.byref(profit), gl, caps, C.byref(slack)))
+    return list(genes), profit.value, list(gl), list(caps), slack.value
 
 
 def net_units(desc: NetDesc):

@@ -122,3 +122,29 @@ def test_schema_errors():
     with pytest.raises(rn.RnError) as e:
         rn.net_units(rn.net_desc(0, 12, (16, 16, 16)))
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("depth,cap", [(18, False), (34, True)])
+def test_slack_placement_policy_bit_exact_and_minimal(depth, cap):
+    """Reading G4b: rn_gabra_place_slack == oracle place_with_slack (genes, profit,
+    loads, capacities, slack) for the configs[3]/[4] partition chains on 2/4/8
+    GPUs and both objectives; every configuration is now placeable; and the slack
+    chosen is minimal where brute force can check it: at slack - 0.1 no
+    capacity-respecting placement exists (every GPU used)."""
+    desc = rn.net_desc(depth, 64, (91, 109, 91))
+    units, _, loads = rn.net_units(desc)
+    if cap:
+        _, _, loads = rn.net_units(rn.net_desc(depth, 64, (91, 109, 91), max_merge_load=max(units)))
+    for m in (2, 4, 8):
+        for obj in (0, 1):
+            kw = dict(seed=7, objective=obj, require_all_used=1, init_attempts=4096)
+            got = rn.gabra_place_slack(loads, m, **kw)
+            ref = G.place_with_slack(loads, m, **kw)
+            assert list(got[0]) == list(ref[0]) and got[1] == ref[1] and list(got[2]) == list(ref[2])
+            assert list(got[3]) == list(ref[3]) and got[4] == ref[4]
+            assert max(got[2]) <= got[3][0]
+            s = got[4]
+            if s > 1.1 + 1e-9 and m ** len(loads) <= 10 ** 6:
+                d = G.default_capacities(loads, m, round(s - 0.1, 1))
+                with pytest.raises(G.Infeasible):
+                    G.brute_force(loads, d, require_all_used=True)

@@ -8,7 +8,6 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle.gabra import default_capacities  # noqa: E402  (capacity rule G4 only; no GABRA arithmetic)
 from paper_2104_05035_b200 import rn  # noqa: E402
 
 seeds = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "7,8,9,10,11").split(",")]
@@ -20,17 +19,16 @@ for name, depth, cap, ms in cases:
         units, first, loads = rn.net_units(rn.net_desc(depth, 64, dims, max_merge_load=max(units)))
     print(f"{name}: n = {len(loads)} partitions, loads = {loads}")
     for m in ms:
-        d = default_capacities(loads, m)
         for obj in (0, 1):
             for seed in seeds:
-                try:
-                    g, f, L = rn.gabra_place(loads, d, seed=seed, objective=obj, require_all_used=1,
-                                             init_attempts=4096)
+                try:  # reading G4b: the smallest slack 1.1, 1.2, ... with a feasible placement
+                    g, f, L, d, slack = rn.gabra_place_slack(loads, m, seed=seed, objective=obj,
+                                                             require_all_used=1, init_attempts=4096)
                 except rn.RnError as e:
                     print(f"  m={m} objective={obj} seed={seed}: {e}")
                     continue
                 worst = max(L[j] / d[j] for j in range(m))
                 bound = max(sum(loads) / sum(d), max(loads) / max(d))
                 hops = sum(1 for i in range(len(g) - 1) if g[i] != g[i + 1])
-                print(f"  m={m} objective={obj} seed={seed}: genes={g} f={f:.6f} loads={L} "
+                print(f"  m={m} objective={obj} seed={seed}: slack={slack:.1f} genes={g} f={f:.6f} loads={L} "
                       f"bottleneck/bound={worst / bound:.4f} hops={hops}")
