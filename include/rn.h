@@ -161,7 +161,13 @@ typedef struct {
                                NULL allowed when n_stages == 1                               */
   int32_t micro_batches;    /* M_b micro-batches per replica step (reading X18; >= 1)       */
   uint8_t nccl_id[128];     /* ncclUniqueId from rn_nccl_unique_id on rank 0, broadcast by
-                               the caller; ignored when world == 1                            */
+                               the caller; ignored when world == 1.  An id whose first 8
+                               bytes are "RNLOCAL" + NUL selects the in-process transport
+                               instead: the ranks are plans of THIS process (one host thread
+                               each, any device), exchanging by device-to-device copies
+                               (send/recv), rank-order sums (all-reduce) and copies
+                               (broadcast) -- the multi-rank executor's CUDA path tested on
+                               one GPU; CUDA graphs are off on that transport.           */
 } rn_dist_desc;
 
 typedef struct rn_plan_s *rn_plan_t;

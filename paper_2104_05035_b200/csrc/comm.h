@@ -20,6 +20,11 @@ NcclComm *nccl_init(const uint8_t id[128], int nranks, int rank);
 NcclComm *nccl_split(NcclComm *parent, int color, int key);
 void nccl_destroy(NcclComm *c);
 int nccl_size(NcclComm *c);
+// in-process transport (ranks = plans of this process on one device; id prefix "RNLOCAL\0")
+bool nccl_is_local(NcclComm *c);
+// ncclGroupStart/End (no-ops on the in-process transport)
+void nccl_group_start(NcclComm *c);
+void nccl_group_end(NcclComm *c);
 void nccl_allreduce_sum_f32(NcclComm *c, float *buf, size_t count, cudaStream_t st);
 void nccl_send_bytes(NcclComm *c, const void *buf, size_t bytes, int peer, cudaStream_t st);
 void nccl_recv_bytes(NcclComm *c, void *buf, size_t bytes, int peer, cudaStream_t st);

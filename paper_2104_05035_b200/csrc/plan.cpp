@@ -988,7 +988,9 @@ bool Plan::saved(int ui, int k, const std::string &name, SavedRef &r) {
 bool Plan::graphs_on() const {
   auto it = opts.find("graphs");
   const bool on = it == opts.end() ? true : it->second != 0;
-  return on && stream != nullptr && stream != cudaStreamLegacy && stream != cudaStreamPerThread && !timing();
+  // the in-process transport's host rendezvous cannot be captured into a graph
+  return on && stream != nullptr && stream != cudaStreamLegacy && stream != cudaStreamPerThread && !timing() &&
+         !nccl_is_local(world_comm);
 }
 
 void Plan::drop_graphs() {

@@ -136,6 +136,12 @@ def net_params(desc: NetDesc):
     return out, n.value, nb.value
 
 
+def local_transport_id() -> bytes:
+    """An id selecting the in-process transport (include/rn.h rn_dist_desc):
+    ranks = plans of this process on one device, one host thread per rank."""
+    return b"RNLOCAL\0" + os.urandom(120)
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(lib().rn_nccl_unique_id(buf))
