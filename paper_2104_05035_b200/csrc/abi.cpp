@@ -34,11 +34,14 @@ void add_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed
 void set_capturing(bool c) { g_capturing = c; }
 int64_t launch_count() { return g_launches.load(); }
 // Programmatic Dependent Launch for every kernel (launch.h): on by default
-// (RN_PDL=0 turns it off).  With the implicit trigger (no launch_dependents: a
-// dependent grid launches when the predecessor's blocks have exited) and every
-// kernel's griddepcontrol.wait placed after its smem / TMEM / barrier prologue,
-// the r18 step measured 3.917 -> 3.636 ms (2042 -> 2200 samples/s, two runs each);
-// an early trigger at kernel entry measured slower (dependents squat on SMs).
+// (RN_PDL=0 turns it off).  Every kernel's griddepcontrol.wait sits after its
+// smem / TMEM / barrier prologue; the trigger is implicit (a dependent grid
+// launches when the predecessor's blocks exit) except in the persistent
+// tensor-core convolutions, which issue griddepcontrol.launch_dependents after
+// their last MMA (kPdlLate in k_conv_tc.cu / k_conv_pair.cu: the grid is fully
+// resident, so no later wave can be displaced).  Measured: 3.917 -> 3.636 ms per
+// r18 step (implicit trigger), 2198 -> 2203 samples/s (late explicit trigger); a
+// trigger at kernel entry measured slower (dependents squat on SMs).
 bool pdl_enabled() {
   static const bool on = [] {
     const char *e = getenv("RN_PDL");

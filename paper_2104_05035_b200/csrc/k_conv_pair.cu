@@ -300,11 +300,10 @@ int conv_pair(const ConvGeom &g, bool dgrad, const bf16 *src, const bf16 *w, con
   p.res = res;
   p.res_mask = res_mask;
   if (est && est->mode) p.st = *est;
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_devs = 0;  // kernel attributes are per device
+  if (!once_on_device(attr_devs)) {
     CUDA_CHECK(cudaFuncSetAttribute(conv_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-    attr = true;
-  }
+      }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -402,16 +402,15 @@ void choose_box(int W, int H, int D, int N, int &bw, int &bh, int &bd, int &bn) 
 template <int BN, int STAGES>
 int launch(const TcParams &p, cudaStream_t st) {
   using S = Smem<BN, STAGES>;
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_devs = 0;  // kernel attributes are per device
+  if (!once_on_device(attr_devs)) {
     CUDA_CHECK(cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     S::TOTAL));
     // the whole unified L1/smem as shared memory: the 96 KB-ring variants fit two
     // CTAs per SM only with the maximum carveout (the default gave 1 CTA per SM)
     CUDA_CHECK(cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                     cudaSharedmemCarveoutMaxShared));
-    attr = true;
-  }
+      }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

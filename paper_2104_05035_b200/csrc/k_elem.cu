@@ -2101,10 +2101,13 @@ __global__ void __launch_bounds__(256) sgd_repack_all_k(const ConvPack *__restri
   }
 }
 
+// w <- w - lr g over the ranges: blockIdx.y = range, blockIdx.x strides within it
+// (one range can hold every parameter of the fp32 path: spread it over the SMs)
 __global__ void sgd_ranges_k(const int64_t *__restrict__ rg, float *master, const float *__restrict__ grad, float lr) {
   pdl_begin();
-  const int64_t a = rg[2 * blockIdx.x], e = rg[2 * blockIdx.x + 1];
-  for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) master[i] -= lr * grad[i];
+  const int64_t a = rg[2 * blockIdx.y], e = rg[2 * blockIdx.y + 1];
+  for (int64_t i = a + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x)
+    master[i] -= lr * grad[i];
 }
 
 template <typename T>
@@ -2130,7 +2133,8 @@ void sgd_repack_all(const ConvPack *table_dev, int n, int64_t total_tiles, float
 
 void sgd_ranges(const int64_t *ranges_dev, int n, float *master, const float *grad, float lr, cudaStream_t st) {
   if (n <= 0) return;
-  launch_k(sgd_ranges_k, n, 256, 0, st, ranges_dev, master, grad, lr);
+  launch_k(sgd_ranges_k, dim3((unsigned)std::max(1, 148 * 4 / n), (unsigned)n), 256, 0, st, ranges_dev, master, grad,
+           lr);
   LAUNCH_CHECK();
 }
 

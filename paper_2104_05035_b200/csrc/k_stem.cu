@@ -840,11 +840,10 @@ void stem_wgrad_launch(const ConvGeom &g, const float *x, const void *dh, float 
                        const void *hx = nullptr, const float *coef = nullptr) {
   if (std::is_same<T, bf16>::value && CO == 64 && !getenv("RN_STEM_SIMT") && g.out_vox() < (1LL << 31)) {
     // tensor-core path (bf16 dh): 3 blocks per SM, partials reduced by stem_reduce_k
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr_devs = 0;  // kernel attributes are per device
+    if (!once_on_device(attr_devs)) {
       CUDA_CHECK(cudaFuncSetAttribute(stem_wgrad_mma_k, cudaFuncAttributeMaxDynamicSharedMemorySize, SW_SMEM));
-      attr = true;
-    }
+          }
     const int nb = std::min(stem_wgrad_blocks(g), 2 * 148);
     launch_k(stem_wgrad_mma_k, nb, 256, SW_SMEM, st, g, x, (const bf16 *)dh, ws, (const bf16 *)hx, coef);
     LAUNCH_CHECK();
@@ -887,11 +886,10 @@ void stem_wgrad_fused_apply(const ConvGeom &g, const float *x, const void *dprim
                             float *dw, float *ws, cudaStream_t st) {
   if (g.Co != 64 || getenv("RN_STEM_SIMT")) throw Error(RN_ERR_ARG, "stem_wgrad_fused_apply: needs Co = 64");
   if (!getenv("RN_STEM_WG_2PHASE") && g.out_vox() < (1LL << 31)) {
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr_devs = 0;  // kernel attributes are per device
+    if (!once_on_device(attr_devs)) {
       CUDA_CHECK(cudaFuncSetAttribute(stem_wgrad_pipe_k, cudaFuncAttributeMaxDynamicSharedMemorySize, SWP_SMEM));
-      attr = true;
-    }
+          }
     const int nb = std::min(stem_wgrad_blocks(g), 148);  // one CTA per SM (196 KB)
     launch_k(stem_wgrad_pipe_k, nb, 256, SWP_SMEM, st, g, x, (const bf16 *)dprime, (const bf16 *)h, coef, ws);
     LAUNCH_CHECK();

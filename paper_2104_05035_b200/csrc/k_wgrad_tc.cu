@@ -292,12 +292,11 @@ template <int BN, int STAGES, int XBYTES>
 void wg_launch(const WgParams &p, int grid, cudaStream_t st) {
   constexpr int STAGE = (BN / 64) * 16384 + XBYTES;
   constexpr int SMEM = STAGES * STAGE + 256 + ATAB_MAX * 16 + 1024;
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t attr_devs = 0;  // kernel attributes are per device
+  if (!once_on_device(attr_devs)) {
     CUDA_CHECK(cudaFuncSetAttribute(wgrad_tc_kernel<BN, STAGES, XBYTES>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-    attr = true;
-  }
+      }
   launch_k(wgrad_tc_kernel<BN, STAGES, XBYTES>, grid, WG_THREADS, SMEM, st, p);
   LAUNCH_CHECK();
 }

@@ -9,6 +9,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <utility>
 
 #include "error.h"
@@ -16,6 +17,18 @@
 namespace rn {
 
 bool pdl_enabled();
+
+// true if this call site already ran on the current device (bit per device
+// ordinal in *mask), else marks it: function attributes such as the dynamic-smem
+// limit are per device, so a process that drives a second GPU sets them again
+inline bool once_on_device(uint64_t &mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (mask & bit) return true;
+  mask |= bit;
+  return false;
+}
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

@@ -262,12 +262,57 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
     pipe_comm = nccl_split(world_comm, replica, stage);
     dp_comm = nccl_split(world_comm, stage, replica);
   }
+  // all-reduce buckets: runs of consecutive local units, in backward order
+  if (replicas > 1) {
+    const int64_t target = 2 * 1024 * 1024;  // floats (8 MB) per bucket
+    for (int ui = nu - 1; ui >= 0; --ui) {
+      if (!local[ui]) continue;
+      const int a = net.unit_param_begin[ui], e = net.unit_param_end[ui];
+      if (a == e) continue;
+      const int64_t b0 = net.params[a].canon_off, e0 = net.params[e - 1].canon_off + net.params[e - 1].numel;
+      if (!buckets.empty() && buckets.back().ulo == ui + 1 && buckets.back().b == e0 &&
+          buckets.back().e - buckets.back().b < target) {
+        buckets.back().ulo = ui;
+        buckets.back().b = b0;
+      } else {
+        buckets.push_back({ui, ui, b0, e0});
+      }
+    }
+  }
+}
+
+bool Plan::overlap_ar() const {
+  auto it = opts.find("overlap_allreduce");
+  return replicas > 1 && (it == opts.end() || it->second != 0) && stream != nullptr && stream != cudaStreamLegacy &&
+         stream != cudaStreamPerThread;
+}
+
+// enqueue bucket bi's all-reduce on the comm stream after everything that writes
+// its gradients: the main stream's backward of its units and the weight-gradient
+// side stream's work enqueued so far
+void Plan::launch_bucket(size_t bi) {
+  if (!comm_st) CUDA_CHECK(cudaStreamCreateWithFlags(&comm_st, cudaStreamNonBlocking));
+  while (ar_ev.size() < 2 * buckets.size() + 1) {
+    cudaEvent_t e;
+    CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ar_ev.push_back(e);
+  }
+  CUDA_CHECK(cudaEventRecord(ar_ev[2 * bi], stream));
+  CUDA_CHECK(cudaStreamWaitEvent(comm_st, ar_ev[2 * bi], 0));
+  if (side_used) {
+    CUDA_CHECK(cudaEventRecord(ar_ev[2 * bi + 1], side));
+    CUDA_CHECK(cudaStreamWaitEvent(comm_st, ar_ev[2 * bi + 1], 0));
+  }
+  const Bucket &bk = buckets[bi];
+  nccl_allreduce_sum_f32(dp_comm, (float *)P(off_grad) + bk.b, (size_t)(bk.e - bk.b), comm_st);
 }
 
 Plan::~Plan() {
   drop_graphs();
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (side) cudaStreamDestroy(side);
+  if (comm_st) cudaStreamDestroy(comm_st);
+  for (auto e : ar_ev) cudaEventDestroy(e);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
   for (int i = 0; i < 2; ++i) {
@@ -1089,6 +1134,8 @@ void Plan::forward_body(const float *x_in, const int32_t *y) {
 void Plan::backward_body(const float *x_in) {
   CUDA_CHECK(cudaMemsetAsync(P(off_grad), 0, sizeof(float) * net.n_params, stream));
   const int nu = (int)net.units.size();
+  const bool ov = overlap_ar();
+  size_t bi = 0;
   for (int k = 0; k < Mb; ++k) {
     for (int ui = nu - 1; ui >= 0; --ui) {
       if (!local[ui]) continue;
@@ -1101,12 +1148,19 @@ void Plan::backward_body(const float *x_in) {
         const Unit &pu = net.units[ui - 1];
         nccl_send_bytes(pipe_comm, P(units[ui].send_dx), act_bytes(pu.cout, pu.out), unit_stage[ui - 1], stream);
       }
+      // last micro-batch: a bucket whose units are all done is reduced while the
+      // backward of the earlier units continues (P:284 ring all-reduce, Eq. 11)
+      if (ov && k == Mb - 1 && bi < buckets.size() && ui == buckets[bi].ulo) launch_bucket(bi++);
     }
     if (side_used) {  // join the weight-gradient stream (per micro-batch: temporaries are reused)
       CUDA_CHECK(cudaEventRecord(ev_join, side));
       CUDA_CHECK(cudaStreamWaitEvent(stream, ev_join, 0));
       side_used = false;
     }
+  }
+  if (ov && comm_st) {  // the averaged gradient is complete when the backward is
+    CUDA_CHECK(cudaEventRecord(ar_ev.back(), comm_st));
+    CUDA_CHECK(cudaStreamWaitEvent(stream, ar_ev.back(), 0));
   }
 }
 
@@ -1181,7 +1235,7 @@ std::vector<std::pair<int64_t, int64_t>> local_param_ranges(const NetModel &net,
 // (bf16 path) updated and repacked into its two bf16 copies in one more launch.
 void Plan::step_body(float lr) {
   auto ranges = local_ranges();
-  if (replicas > 1)
+  if (replicas > 1 && !overlap_ar())  // else reduced during the backward (launch_bucket)
     for (auto &rg : ranges)
       nccl_allreduce_sum_f32(dp_comm, (float *)P(off_grad) + rg.first, (size_t)(rg.second - rg.first), stream);
   int64_t conv_params = 0, all_params = 0;
@@ -1352,7 +1406,7 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 rn_status Plan::set_option(const std::string &k, int64_t v) {
   if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv" && k != "fused_stats" &&
       k != "pair_conv" && k != "wgrad_stream" && k != "merge_proj" && k != "stem_bwd_fused" &&
-      k != "recompute_mask" && k != "up_bwd_sep" && k != "pair_bwd_stats")
+      k != "recompute_mask" && k != "up_bwd_sep" && k != "pair_bwd_stats" && k != "overlap_allreduce")
     return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;

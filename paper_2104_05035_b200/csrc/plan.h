@@ -199,6 +199,19 @@ struct Plan {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool side_used = false;
+  // data-parallel gradient all-reduce bucketed and overlapped with the backward
+  // (option overlap_allreduce, default on when replicas > 1): bucket = a run of
+  // consecutive local units (>= ~8 MB of fp32 gradients), reduced on comm_st as
+  // soon as its last unit's backward (and weight gradients) are enqueued
+  struct Bucket {
+    int ulo, uhi;
+    int64_t b, e;
+  };
+  std::vector<Bucket> buckets;  // backward order (units descending)
+  cudaStream_t comm_st = nullptr;
+  std::vector<cudaEvent_t> ar_ev;
+  bool overlap_ar() const;
+  void launch_bucket(size_t bi);
   bool side_on() const;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   float *loss_pinned = nullptr;

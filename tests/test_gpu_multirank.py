@@ -49,10 +49,12 @@ def run_ranks(world, fn, timeout=600):
     return out
 
 
-def step_rank(desc, b, dtype, r, world, S, genes, Mb, nid, flat, x, y):
+def step_rank(desc, b, dtype, r, world, S, genes, Mb, nid, flat, x, y, opts=None):
     st = torch.cuda.Stream()
     plan = rn.Plan(desc, b, dtype, rank=r, world=world, n_stages=S, genes=genes, micro_batches=Mb, nccl_id=nid,
                    stream=st)
+    for k, v in (opts or {}).items():
+        plan.set_option(k, v)
     plan.set_params(flat)
     rep = r // S
     with torch.cuda.stream(st):
@@ -193,3 +195,25 @@ def test_hybrid_bf16_2x2_matches_data_parallel():
             tol = 5e-2 if (".mask." in name or ".mbn." in name or ".mconv" in name) else 2e-2  # X23b
             assert rel(g[off:off + n], dp[rep]["g"][off:off + n]) <= tol, name
             off += n
+
+
+def test_overlapped_bucketed_allreduce_matches_after_backward_allreduce():
+    """The gradient all-reduce bucketed and overlapped with the backward (default)
+    computes exactly what one all-reduce after the backward computes (same
+    rank-order sums on this transport): DP 2 replicas and hybrid 2x2, bf16."""
+    dims = (40, 48, 40)
+    desc = rn.net_desc(18, 64, dims)
+    loads = rn.net_units(desc)[2]
+    genes = rn.gabra_place_slack(loads, 2, seed=7, require_all_used=1)[0]
+    tensors = rn.net_params(desc)[0]
+    arrays = synthetic.init_params(tensors, seed=0)
+    flat = np.concatenate([a.ravel() for a in arrays]).astype(np.float32)
+    x, y = synthetic.make_batch(4, *dims, seed=1)
+    for world, S, g in ((2, 1, None), (4, 2, genes)):
+        outs = []
+        for ov in (1, 0):
+            nid = rn.local_transport_id()
+            outs.append(run_ranks(world, lambda r: step_rank(desc, 2, rn.RN_BF16, r, world, S, g, 1, nid, flat, x, y,
+                                                             {"overlap_allreduce": ov})))
+        for r in range(world):
+            assert np.array_equal(outs[0][r]["w"], outs[1][r]["w"])
