@@ -313,11 +313,20 @@ int64_t rn_kernel_launches(rn_plan_t plan);
  *  "recompute_mask": 1 dgrad-epilogue BN sums recompute the consumer's ReLU mask from h (default 1)
  *  "pair_bwd_stats": 1 fuse the backward BN sums into the CTA-pair dgrad epilogue (default 0: standalone pass)
  *  "up_bwd_sep"    : 1 separable trilinear adjoint (default 1)
+ *  "overlap_allreduce": 1 reduce the gradient over the stage's data-parallel group in
+ *                    ~8 MB buckets during rn_backward, on a comm stream, as soon as a
+ *                    bucket's units are done (default 1 when replicas > 1; rn_get_grads
+ *                    after rn_backward then returns the replica average G of Eq. 11);
+ *                    0: one all-reduce per range inside rn_step
  * Unknown keys: RN_ERR_ARG.  Every switch changes kernels only, not the result beyond fp32 rounding. */
 rn_status rn_set_option(rn_plan_t plan, const char *key, int64_t value);
 
 /* rn_query — named float64 statistics (e.g. "conv_ms", "conv_flops") collected
- * when time_kernels is on; reset by rn_set_option("time_kernels", 1). */
+ * when time_kernels is on; reset by rn_set_option("time_kernels", 1).
+ * "conv_ms|conv_flops|conv_launches[_fprop|_dgrad|_wgrad|_pair|_tcconv|_tcwgrad|_stem]",
+ * "elt_ms|elt_bytes|elt_launches[_<family>]" (HBM-bound launches: bn_apply,
+ * bn_bwd_apply, bn_partials, stem_pool_fwd, stem_pool_bwd, maxpool_fwd, maxpool_bwd,
+ * upsample_fwd, upsample_bwd, att_fwd, att_bwd, sgd; bytes = algorithmic). */
 rn_status rn_query(rn_plan_t plan, const char *key, double *value);
 
 /* rn_op_conv3d — ONE convolution of the step as a stand-alone launch, for the
