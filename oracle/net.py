@@ -594,6 +594,73 @@ class Net:
                     bn_state=states[0], losses=losses)
 
 
+def delayed_pipeline_train(net, arrays, batches, lr, unit_stage):
+    """Delayed-gradient pipelined training (PAPER.md:156
+    "all partitions are computed simultaneously", Eqs. 1-2; reading F1 in
+    DESIGN.md).  unit_stage[u] = pipeline stage (0..S-1) of unit u, non-decreasing
+    along the chain; stage s is S-1-s iterations from the loss.  Iteration t
+    (batches[t] = (x, y)):
+      1. forward of batch t through every stage with its CURRENT weights, saving
+         each stage's forward state and a copy of the weights it used (w^{(t)});
+         loss of batch t and dl/dz at the head;
+      2. every stage s backpropagates batch b = t - (S-1-s) (if b >= 0): the last
+         stage the batch just forwarded (delay 0), stage s < S-1 the gradient of
+         its output that stage s+1 produced in iteration t-1 -- through its saved
+         forward state and the weights of that forward (Eq. 1: the Jacobian at
+         w^{t-i+1}, the version that produced a^{t-i+1}), giving its weight
+         gradient and the gradient of its input (sent to stage s-1, used there in
+         iteration t+1);
+      3. every stage that backpropagated updates its CURRENT weights,
+         w <- w - lr * g (Eq. 2 with the delayed gradient).
+    S = 1 is plain SGD.  Returns dict(losses, params (flat, float64), bn_state)."""
+    global Q, QW
+    Q = QW = (_bf16_round if net.store == "bf16" else _identity)
+    try:
+        S = max(unit_stage) + 1
+        assert all(unit_stage[i] <= unit_stage[i + 1] for i in range(len(unit_stage) - 1))
+        P = Params(net.tensors, [np.asarray(a, dtype=np.float64).copy() for a in arrays])
+        st = BNState(net.bn_names, net.bn_channels)
+        stage_units = [[u for u in range(len(net.units)) if unit_stage[u] == s] for s in range(S)]
+        saved = {}      # (stage, batch) -> (weights dict used, [(ui, cache)], input of the stage)
+        pending = {}    # (stage, batch) -> gradient of the stage's output
+        losses = []
+        for t, (x, y) in enumerate(batches):
+            h = np.asarray(x, dtype=np.float64)[..., None]
+            for s in range(S):                                  # 1. forward of batch t
+                used = Params(net.tensors, [P[n].copy() for n in P.names])
+                caches = []
+                bns = []
+                for ui in stage_units[s]:
+                    h, c = unit_forward(used, ui, net.units[ui], h, bns)
+                    caches.append((ui, c))
+                for name, cache in bns:
+                    st.update(name, cache)
+                saved[(s, t)] = (used, caches)
+            loss, dz = softmax_ce(h, np.asarray(y))
+            losses.append(loss)
+            pending[(S - 1, t)] = dz
+            updates = []
+            for s in reversed(range(S)):                        # 2. delayed backward
+                b = t - (S - 1 - s)
+                if b < 0:
+                    continue
+                used, caches = saved.pop((s, b))
+                g = pending.pop((s, b))
+                G = {}
+                for ui, c in reversed(caches):
+                    g = unit_backward(used, ui, net.units[ui], g, c, G)
+                if s > 0:
+                    pending[(s - 1, b)] = g
+                updates.append(G)
+            for G in updates:                                   # 3. update current weights
+                for n, v in G.items():
+                    P.d[n] = P.d[n] - lr * np.asarray(v, dtype=np.float64)
+        flat = np.concatenate([P[n].ravel() for n in P.names])
+        return dict(losses=losses, params=flat, bn_state=st)
+    finally:
+        Q = QW = _identity
+
+
 def unit_costs(units) -> list:
     """Per-sample MAC cost of each top-level unit (a1; P:366 conv complexity
     O(Co*Ci*T*H*W*Kt*Kh*Kw); light-layer constants BN 2, ReLU/pool/add/mul/
