@@ -184,6 +184,30 @@ rn_status rn_nccl_unique_id(uint8_t out[128]);
 rn_status rn_plan(const rn_net_desc *net, const rn_dist_desc *dist, int32_t local_batch,
                   int32_t dtype, void *cuda_stream, rn_plan_t *out, size_t *workspace_bytes);
 
+/* rn_plan_delayed — rn_plan for the delayed-gradient pipeline (
+ * P:156 "all partitions are computed simultaneously", Eqs. 1-2; reading
+ * F1 in DESIGN.md): the genes must place the partitions on contiguous stages in
+ * chain order (non-decreasing genes); micro_batches must be 1.  Every rank keeps
+ * S slots of saved forward state and of the weights those forwards used (the
+ * Jacobian of Eq. 1 is taken at the forward's weights).  Drive it with
+ * rn_delayed_step only (rn_forward / rn_backward / rn_step are not used).
+ * Errors: as rn_plan, plus RN_ERR_ARG for non-contiguous genes or M_b != 1. */
+rn_status rn_plan_delayed(const rn_net_desc *net, const rn_dist_desc *dist, int32_t local_batch, int32_t dtype,
+                          void *cuda_stream, rn_plan_t *out, size_t *workspace_bytes);
+
+/* rn_delayed_step — iteration t of the delayed-gradient pipeline on this rank
+ * (stage s, delay d = S-1-s): forward of batch t (x_dev on stage 0, y_dev on the
+ * last stage; both may be NULL elsewhere) with the current weights; backward of
+ * batch t-d (its output gradient came from stage s+1 in iteration t-1; the last
+ * stage's is the batch-t loss gradient) through the saved state and the weights
+ * of that forward; SGD w <- w - lr * g on the current weights (all-reduced over
+ * replicas when world > S).  Exchanges are grouped (ncclGroupStart/End) pairwise
+ * with the neighbour stages, so they cannot deadlock.  loss_host (may be NULL):
+ * the batch-t loss, broadcast from the last stage.  Collective over all ranks.
+ * S = 1 is plain SGD.  Errors: RN_ERR_STATE (not a delayed plan, no parameters),
+ * RN_ERR_NUMERIC (non-finite loss), RN_ERR_CUDA / RN_ERR_NCCL. */
+rn_status rn_delayed_step(rn_plan_t plan, const void *x_dev, const int32_t *y_dev, float lr, float *loss_host);
+
 /* rn_plan_describe — the schedule rn_plan builds for this rank, computed on the
  * host only (no GPU, no communicators): which units run here and, in forward
  * order, the partition-boundary exchanges of P:156.

@@ -215,6 +215,25 @@ rn_status rn_plan(const rn_net_desc *net, const rn_dist_desc *dist, int32_t loca
   GUARD_END
 }
 
+rn_status rn_plan_delayed(const rn_net_desc *net, const rn_dist_desc *dist, int32_t local_batch, int32_t dtype,
+                          void *cuda_stream, rn_plan_t *out, size_t *workspace_bytes) {
+  GUARD_BEGIN
+  if (!net || !out || !workspace_bytes) return set_error(RN_ERR_ARG, "rn_plan_delayed: null argument");
+  if (dtype != RN_F32 && dtype != RN_BF16) return set_error(RN_ERR_ARG, "rn_plan_delayed: bad dtype");
+  rn_dist_desc d;
+  memset(&d, 0, sizeof d);
+  d.world = 1;
+  d.n_stages = 1;
+  d.micro_batches = 1;
+  if (dist) d = *dist;
+  Plan *p = new Plan(*net, d, local_batch, dtype, (cudaStream_t)cuda_stream, true);
+  *out = new rn_plan_s{p};
+  *workspace_bytes = p->ws_bytes;
+  return RN_OK;
+  GUARD_END
+}
+
+
 rn_status rn_plan_describe(const rn_net_desc *net, const rn_dist_desc *dist, int32_t local_batch, int32_t dtype,
                            int32_t *local_units, int32_t cap, int32_t *n_xfer, int64_t *xfer, int32_t *n_ranges,
                            int64_t *ranges) {
@@ -426,6 +445,17 @@ rn_status rn_step(rn_plan_t plan, float lr) {
   NEED_BOUND(plan);
   plan->p->step(lr);
   return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_delayed_step(rn_plan_t plan, const void *x_dev, const int32_t *y_dev, float lr, float *loss_host) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  Plan *p = plan->p;
+  if (!p->delayed) return set_error(RN_ERR_STATE, "rn_delayed_step: plan not created by rn_plan_delayed");
+  if (!p->params_set) return set_error(RN_ERR_STATE, "rn_set_params must precede rn_delayed_step");
+  p->delayed_step((const float *)x_dev, y_dev, lr);
+  return finish_loss(p, loss_host);
   GUARD_END
 }
 

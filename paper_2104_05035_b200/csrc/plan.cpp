@@ -37,8 +37,8 @@ void Plan::make_bn(BNL &b, int gamma_idx, int C, int64_t V) {
   b.C = C;
   b.V = V;
   b.run_off = bn_run_off[gamma_idx];
-  b.stat_off.resize(Mb);
-  for (int k = 0; k < Mb; ++k) b.stat_off[k] = alloc(4 * sizeof(float) * C);
+  b.stat_off.resize(std::max(Mb, slots));
+  for (int k = 0; k < std::max(Mb, slots); ++k) b.stat_off[k] = alloc(4 * sizeof(float) * C);
   if (dt == DT_BF16) {  // up to 2 CTAs per SM in the producing conv
     // one [2][C] partial per producing CTA: convolution grids are sized from the
     // device's SM count (<= 2 CTAs per SM), the stem's from up to 4 blocks per SM
@@ -66,8 +66,10 @@ void Plan::make_conv(ConvL &c, int w_idx, int Ci, int Co, int k, int s, int p, D
 size_t Plan::act_bytes(int C, Dims d) const { return (size_t)mb * d.vol() * C * dt_size(dt); }
 
 std::vector<size_t> Plan::per_mb(size_t bytes) {
-  std::vector<size_t> v(Mb);
-  for (int k = 0; k < Mb; ++k) v[k] = alloc(bytes);
+  // one buffer per micro-batch, or per delayed-pipeline slot
+  const int n = std::max(Mb, slots);
+  std::vector<size_t> v(n);
+  for (int k = 0; k < n; ++k) v[k] = alloc(bytes);
   return v;
 }
 
@@ -103,8 +105,8 @@ int Plan::block_param_count(int cin, int cout, int stride) const {
 }
 
 // ---------------------------------------------------------------------------
-Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int dtype, cudaStream_t st)
-    : net(build_net(nd)), stream(st) {
+Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int dtype, cudaStream_t st, bool dl)
+    : net(build_net(nd)), stream(st), delayed(dl) {
   dt = dtype == RN_BF16 ? DT_BF16 : DT_F32;
   {
     int dev = 0;
@@ -133,6 +135,21 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
     local = sc.local;
   }
   const int nu = (int)net.units.size();
+  if (delayed) {
+    // reading F1: every rank holds one contiguous stage of the chain, stages in
+    // chain order; S slots of saved forward state, one batch per iteration
+    if (Mb != 1) throw Error(RN_ERR_ARG, "delayed pipeline: micro_batches must be 1");
+    for (int ui = 0; ui + 1 < nu; ++ui)
+      if (unit_stage[ui] > unit_stage[ui + 1])
+        throw Error(RN_ERR_ARG, "delayed pipeline: genes must be non-decreasing along the chain (contiguous stages)");
+    slots = S;
+    for (int ui = 0; ui < nu; ++ui)
+      if (local[ui]) {
+        if (entry_unit < 0) entry_unit = ui;
+        exit_unit = ui;
+      }
+    if (entry_unit < 0) throw Error(RN_ERR_ARG, "delayed pipeline: a stage without units");
+  }
 
   // --- parameters (full model on every rank; only local ranges are used) ---
   const int np = (int)net.params.size();
@@ -159,6 +176,15 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
       shadow_d[i] = alloc(2 * t.numel);
     }
   }
+  if (delayed) {  // the weights each in-flight forward used (Eq. 1: the Jacobian at w^{t-i+1})
+    stash_master.resize(slots);
+    stash_shadow_d.assign(slots, std::vector<size_t>(np, 0));
+    for (int sl = 0; sl < slots; ++sl) {
+      stash_master[sl] = alloc(sizeof(float) * net.n_params);
+      for (int i = 0; i < np; ++i)
+        if (shadow_d[i]) stash_shadow_d[sl][i] = alloc(2 * net.params[i].numel);
+    }
+  }
   off_loss = alloc(64);
   off_flag = alloc(64);
   max_pack = 0;
@@ -170,8 +196,8 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
   }
   off_pack = alloc(sizeof(ConvPack) * (max_pack + 1));
   off_sgdrg = alloc(2 * sizeof(int64_t) * (max_sgdrg + 1));
-  off_x = alloc(sizeof(float) * (size_t)b * net.units[0].in.vol());
-  off_y = alloc(sizeof(int32_t) * (size_t)b);
+  off_x = alloc(sizeof(float) * (size_t)b * net.units[0].in.vol() * slots);  // per slot (delayed pipeline)
+  off_y = alloc(sizeof(int32_t) * (size_t)b * slots);
   for (int i = 0; i < 2; ++i)  // staging slots of the pipelined host-input loop: x then y
     off_stage[i] = alloc(sizeof(float) * (size_t)b * net.units[0].in.vol() + 256 + sizeof(int32_t) * (size_t)b);
 
@@ -1035,7 +1061,7 @@ bool Plan::graphs_on() const {
   const bool on = it == opts.end() ? true : it->second != 0;
   // the in-process transport's host rendezvous cannot be captured into a graph
   return on && stream != nullptr && stream != cudaStreamLegacy && stream != cudaStreamPerThread && !timing() &&
-         !nccl_is_local(world_comm);
+         !nccl_is_local(world_comm) && !delayed;
 }
 
 void Plan::drop_graphs() {
@@ -1110,47 +1136,48 @@ void Plan::step(float lr) {
   run_phase(2, [&] { step_body(lr); });
 }
 
-void Plan::forward_body(const float *x_in, const int32_t *y) {
+void Plan::forward_body(const float *x_in, const int32_t *y, int k_only) {
   if (timing()) ev_used = 0;  // a step's conv events: this forward + its backward (eager launches)
   CUDA_CHECK(cudaMemsetAsync(P(off_loss), 0, sizeof(float), stream));
   const int nu = (int)net.units.size();
-  for (int k = 0; k < Mb; ++k) {
+  for (int k = k_only < 0 ? 0 : k_only; k < (k_only < 0 ? Mb : k_only + 1); ++k) {
     for (int ui = 0; ui < nu; ++ui) {
       if (!local[ui]) continue;
-      if (ui > 0 && !local[ui - 1]) {
+      if (ui > 0 && !local[ui - 1] && !xfer_external) {
         const Unit &pu = net.units[ui - 1];
         nccl_recv_bytes(pipe_comm, P(units[ui].recv_in[k]), act_bytes(pu.cout, pu.out), unit_stage[ui - 1], stream);
       }
       unit_fwd(ui, k, x_in, y);
-      if (ui + 1 < nu && !local[ui + 1]) {
+      if (ui + 1 < nu && !local[ui + 1] && !xfer_external) {
         const Unit &u = net.units[ui];
         nccl_send_bytes(pipe_comm, P(units[ui].out[k]), act_bytes(u.cout, u.out), unit_stage[ui + 1], stream);
       }
     }
   }
-  if (S > 1) nccl_bcast_f32(pipe_comm, (float *)P(off_loss), 1, unit_stage[nu - 1], stream);
+  if (S > 1 && !xfer_external) nccl_bcast_f32(pipe_comm, (float *)P(off_loss), 1, unit_stage[nu - 1], stream);
 }
 
-void Plan::backward_body(const float *x_in) {
+void Plan::backward_body(const float *x_in, int k_only) {
   CUDA_CHECK(cudaMemsetAsync(P(off_grad), 0, sizeof(float) * net.n_params, stream));
   const int nu = (int)net.units.size();
   const bool ov = overlap_ar();
   size_t bi = 0;
-  for (int k = 0; k < Mb; ++k) {
+  const int k0 = k_only < 0 ? 0 : k_only, k1 = k_only < 0 ? Mb : k_only + 1;
+  for (int k = k0; k < k1; ++k) {
     for (int ui = nu - 1; ui >= 0; --ui) {
       if (!local[ui]) continue;
-      if (ui + 1 < nu && !local[ui + 1]) {
+      if (ui + 1 < nu && !local[ui + 1] && !xfer_external) {
         const Unit &u = net.units[ui];
         nccl_recv_bytes(pipe_comm, P(units[ui].dout), act_bytes(u.cout, u.out), unit_stage[ui + 1], stream);
       }
       unit_bwd(ui, k, x_in);
-      if (ui > 0 && !local[ui - 1]) {
+      if (ui > 0 && !local[ui - 1] && !xfer_external) {
         const Unit &pu = net.units[ui - 1];
         nccl_send_bytes(pipe_comm, P(units[ui].send_dx), act_bytes(pu.cout, pu.out), unit_stage[ui - 1], stream);
       }
       // last micro-batch: a bucket whose units are all done is reduced while the
       // backward of the earlier units continues (P:284 ring all-reduce, Eq. 11)
-      if (ov && k == Mb - 1 && bi < buckets.size() && ui == buckets[bi].ulo) launch_bucket(bi++);
+      if (ov && k == k1 - 1 && bi < buckets.size() && ui == buckets[bi].ulo) launch_bucket(bi++);
     }
     if (side_used) {  // join the weight-gradient stream (per micro-batch: temporaries are reused)
       CUDA_CHECK(cudaEventRecord(ev_join, side));
@@ -1250,6 +1277,90 @@ void Plan::step_body(float lr) {
   if (dt == DT_BF16)
     sgd_repack_all((const ConvPack *)P(off_pack), n_pack, pack_tiles, (float *)P(off_master),
                    (const float *)P(off_grad), lr, stream);
+}
+
+// One iteration t of the delayed-gradient pipeline (reading F1; Eqs.
+// 1-2 P:158-166) on this rank's stage s (delay d = S-1-s):
+//   1. group{ recv the batch-t input from stage s-1 ; send it the input gradient
+//      this stage produced in iteration t-1 }
+//   2. forward of batch t into slot t mod S with the current weights; stash them
+//   3. group{ send the batch-t output to stage s+1 ; receive the gradient of this
+//      stage's output for batch t-d (stage s+1 produced it in iteration t-1) }
+//   4. loss of batch t broadcast from the last stage
+//   5. backward of batch t-d (slot (t-d) mod S) with the weights its forward used
+//   6. SGD on the current weights (+ data-parallel all-reduce over replicas)
+// The two-sided groups pair neighbour stages (stage s's step 3 with stage s+1's
+// step 1), so the exchanges cannot deadlock under NCCL's rendezvous sends.
+void Plan::delayed_step(const float *x_dev, const int32_t *y_dev, float lr) {
+  const int nu = (int)net.units.size();
+  const int slot = (int)(iter % slots);
+  const int d = S - 1 - stage;
+  const int64_t bb = iter - d;
+  const size_t xv = (size_t)b * net.units[0].in.vol();
+  if (local[0] && x_dev)
+    CUDA_CHECK(cudaMemcpyAsync((float *)P(off_x) + slot * xv, x_dev, sizeof(float) * xv, cudaMemcpyDeviceToDevice,
+                               stream));
+  if (local[nu - 1] && y_dev)
+    CUDA_CHECK(cudaMemcpyAsync((int32_t *)P(off_y) + (size_t)slot * b, y_dev, sizeof(int32_t) * b,
+                               cudaMemcpyDeviceToDevice, stream));
+  xfer_external = true;
+  const Unit *eu = &net.units[entry_unit];
+  const Unit *pu = entry_unit > 0 ? &net.units[entry_unit - 1] : nullptr;
+  // 1.
+  if (entry_unit > 0) {
+    nccl_group_start(pipe_comm);
+    nccl_recv_bytes(pipe_comm, P(units[entry_unit].recv_in[slot]), act_bytes(pu->cout, pu->out),
+                    unit_stage[entry_unit - 1], stream);
+    if (dx_pending)
+      nccl_send_bytes(pipe_comm, P(units[entry_unit].send_dx), act_bytes(pu->cout, pu->out),
+                      unit_stage[entry_unit - 1], stream);
+    nccl_group_end(pipe_comm);
+  }
+  dx_pending = false;
+  (void)eu;
+  // 2.
+  forward_body((const float *)P(off_x), (const int32_t *)P(off_y), slot);
+  CUDA_CHECK(cudaMemcpyAsync(P(stash_master[slot]), P(off_master), sizeof(float) * net.n_params,
+                             cudaMemcpyDeviceToDevice, stream));
+  for (size_t i = 0; i < shadow_d.size(); ++i)
+    if (shadow_d[i])
+      CUDA_CHECK(cudaMemcpyAsync(P(stash_shadow_d[slot][i]), P(shadow_d[i]), 2 * net.params[i].numel,
+                                 cudaMemcpyDeviceToDevice, stream));
+  // 3.
+  if (exit_unit + 1 < nu) {
+    const Unit &xu = net.units[exit_unit];
+    nccl_group_start(pipe_comm);
+    nccl_send_bytes(pipe_comm, P(units[exit_unit].out[slot]), act_bytes(xu.cout, xu.out), unit_stage[exit_unit + 1],
+                    stream);
+    if (bb >= 0)
+      nccl_recv_bytes(pipe_comm, P(units[exit_unit].dout), act_bytes(xu.cout, xu.out), unit_stage[exit_unit + 1],
+                      stream);
+    nccl_group_end(pipe_comm);
+  }
+  // 4.
+  if (S > 1) nccl_bcast_f32(pipe_comm, (float *)P(off_loss), 1, unit_stage[nu - 1], stream);
+  // 5.-6.
+  if (bb >= 0) {
+    const int bs = (int)(bb % slots);
+    std::swap(off_master, stash_master[bs]);  // the weights of batch bb's forward
+    std::swap(shadow_d, stash_shadow_d[bs]);
+    try {
+      backward_body((const float *)P(off_x), bs);
+    } catch (...) {
+      std::swap(off_master, stash_master[bs]);
+      std::swap(shadow_d, stash_shadow_d[bs]);
+      xfer_external = false;
+      throw;
+    }
+    std::swap(off_master, stash_master[bs]);
+    std::swap(shadow_d, stash_shadow_d[bs]);
+    dx_pending = entry_unit > 0;
+    step_body(lr);
+  }
+  xfer_external = false;
+  ++iter;
+  fwd_ever = true;
+  bwd_ever = bwd_ever || bb >= 0;
 }
 
 void Plan::refresh_shadows() {

@@ -128,7 +128,22 @@ struct Plan {
   bool params_set = false, fwd_done = false, fwd_ever = false, bwd_ever = false;
   const float *last_x = nullptr;
 
-  Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int dtype, cudaStream_t st);
+  Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int dtype, cudaStream_t st,
+       bool delayed = false);
+
+  // --- delayed-gradient pipeline (Eqs. 1-2; reading F1) ---
+  // slots = S saved forward states per rank (ring indexed by batch mod S), the
+  // weights each forward used stashed per slot (master fp32 + the bf16 dgrad
+  // copies), iteration counter; exchanges done by delayed_step itself
+  bool delayed = false;
+  int slots = 1;
+  int64_t iter = 0;
+  std::vector<size_t> stash_master;
+  std::vector<std::vector<size_t>> stash_shadow_d;
+  int entry_unit = -1, exit_unit = -1;  // first / last unit of this rank's (contiguous) stage
+  bool dx_pending = false;              // input gradient of last iteration's backward not yet sent
+  bool xfer_external = false;           // forward_body / backward_body skip their exchanges
+  void delayed_step(const float *x_dev, const int32_t *y_dev, float lr);
   ~Plan();
 
   // workspace
@@ -220,8 +235,8 @@ struct Plan {
   void forward(const float *x_in, const int32_t *y);
   void backward(const float *x_in);
   void step(float lr);
-  void forward_body(const float *x_in, const int32_t *y);
-  void backward_body(const float *x_in);
+  void forward_body(const float *x_in, const int32_t *y, int k_only = -1);
+  void backward_body(const float *x_in, int k_only = -1);
   void step_body(float lr);
   // CUDA graphs per phase (0 forward, 1 backward, 2 step)
   cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};

@@ -16,7 +16,7 @@ RN_F32, RN_BF16 = 0, 1
 STATUS = {0: "RN_OK", 1: "RN_ERR_ARG", 2: "RN_ERR_SCHEMA", 3: "RN_ERR_INFEASIBLE", 4: "RN_ERR_NUMERIC",
           5: "RN_ERR_CUDA", 6: "RN_ERR_NCCL", 7: "RN_ERR_STATE", 8: "RN_ERR_SIZE"}
 EXPORTS = ["rn_ga_default", "rn_gabra_place", "rn_gabra_place_slack", "rn_net_units", "rn_net_param_count", "rn_net_param_info",
-           "rn_nccl_unique_id", "rn_plan", "rn_plan_describe", "rn_plan_bind", "rn_set_params", "rn_get_params", "rn_get_grads",
+           "rn_nccl_unique_id", "rn_plan", "rn_plan_delayed", "rn_delayed_step", "rn_plan_describe", "rn_plan_bind", "rn_set_params", "rn_get_params", "rn_get_grads",
            "rn_get_bn_running", "rn_get_activation", "rn_get_unit_grad", "rn_get_saved", "rn_forward", "rn_backward", "rn_step", "rn_train_step_host",
            "rn_train_steps_host", "rn_gradcam",
            "rn_kernel_launches", "rn_set_option", "rn_query", "rn_op_conv3d", "rn_plan_destroy", "rn_last_error"]
@@ -152,7 +152,7 @@ class Plan:
     """One rank's plan.  torch provides the workspace and the stream."""
 
     def __init__(self, desc: NetDesc, local_batch: int, dtype=RN_F32, rank=0, world=1, n_stages=1, genes=None,
-                 micro_batches=1, nccl_id: bytes | None = None, stream=None, device=None):
+                 micro_batches=1, nccl_id: bytes | None = None, stream=None, device=None, delayed=False):
         import torch
         self.torch = torch
         self.desc = desc
@@ -168,8 +168,9 @@ class Plan:
             C.memmove(dd.nccl_id, nccl_id, 128)
         self.h = C.c_void_p()
         ws = C.c_size_t()
-        _check(lib().rn_plan(C.byref(desc), C.byref(dd), local_batch, dtype, C.c_void_p(self.stream.cuda_stream),
-                             C.byref(self.h), C.byref(ws)))
+        make = lib().rn_plan_delayed if delayed else lib().rn_plan
+        _check(make(C.byref(desc), C.byref(dd), local_batch, dtype, C.c_void_p(self.stream.cuda_stream),
+                    C.byref(self.h), C.byref(ws)))
         self.ws_bytes = ws.value
         self.workspace = torch.empty(self.ws_bytes + 256, dtype=torch.uint8, device=self.device)
         ptr = self.workspace.data_ptr()
@@ -235,6 +236,14 @@ class Plan:
         _check(lib().rn_gradcam(self.h, C.c_int32(cls), C.c_void_p(map_dev.data_ptr()), C.c_int64(map_dev.numel())))
 
     # --- step ---
+    def delayed_step(self, x_dev, y_dev, lr: float, want_loss=True):
+        """rn_delayed_step (x_dev / y_dev may be None on stages that do not read them)."""
+        loss = C.c_float()
+        _check(lib().rn_delayed_step(self.h, C.c_void_p(x_dev.data_ptr() if x_dev is not None else 0),
+                                     C.c_void_p(y_dev.data_ptr() if y_dev is not None else 0), C.c_float(lr),
+                                     C.byref(loss) if want_loss else None))
+        return loss.value if want_loss else None
+
     def forward(self, x_dev, y_dev, want_loss=True):
         loss = C.c_float()
         _check(lib().rn_forward(self.h, C.c_void_p(x_dev.data_ptr()), C.c_void_p(y_dev.data_ptr()),
