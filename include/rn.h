@@ -115,6 +115,42 @@ rn_status rn_gabra_place_slack(int32_t n, const int64_t *loads, int32_t m, const
                                double *slack_out);
 
 /* ------------------------------------------------------------------------- */
+/* Placement quality on real hardware.                      */
+/* ------------------------------------------------------------------------- */
+
+/* Step-time model of the hybrid schedule (reading F2, ring
+ * all-reduce P:284 / Fig. 3).  Per micro-batch, stage s computes
+ * C_s = sum of part_time[i] over its partitions and pays 2 (alpha + cut/beta) for
+ * every chain cut i|i+1 that crosses stages (activation forward, gradient back,
+ * P:156), charged to both stages: T_s = C_s + P_s.  Pipeline: schedule 0
+ * (synchronous, M_b micro-batches) (M_b + S - 1) max T_s; schedule 1 (delayed
+ * gradients, f1) M_b max T_s.  All-reduce: max over stages of the ring time
+ * 2 (R-1) (g_s/R)/beta + 2 (R-1) alpha.  Step: pipeline + all-reduce, or their max
+ * when overlap != 0.  part_time: seconds (measured on the B200 with rn_query
+ * "unit_ms_fwd_<u>" + "unit_ms_bwd_<u>"); cut_bytes[n-1], param_bytes[n]: bytes. */
+typedef struct {
+  int32_t n, n_stages, replicas, micro_batches, schedule, overlap;
+  double alpha, beta;        /* s per message, bytes per second */
+  const double *part_time;   /* [n] */
+  const double *cut_bytes;   /* [n-1] */
+  const double *param_bytes; /* [n] */
+  const int32_t *genes;      /* [n] partition -> stage */
+} rn_sim_desc;
+/* stage_s may be NULL ([n_stages]).  Bit-identical to oracle/sim.py step_time.
+ * Errors: RN_ERR_ARG (null pointers, sizes < 1, gene out of range, beta <= 0). */
+rn_status rn_simulate_step(const rn_sim_desc *d, double *step_s, double *pipeline_s, double *allreduce_s,
+                           double *stage_s);
+
+/* rn_contiguous_split — the contiguity option of f2: partitions split into S
+ * contiguous stages in chain order (every stage non-empty) minimising the largest
+ * stage load (dynamic programme; among optimal splits the last stage is the
+ * shortest, recursively).  genes_out[n] in 0..S-1 non-decreasing; max_load_out may
+ * be NULL.  The placement rn_plan_delayed needs.  Identical to oracle/sim.py.
+ * Errors: RN_ERR_ARG (n < S, S < 1, null / negative loads). */
+rn_status rn_contiguous_split(int32_t n, const int64_t *loads, int32_t n_stages, int32_t *genes_out,
+                              int64_t *max_load_out);
+
+/* ------------------------------------------------------------------------- */
 /* Network description, costing and partitioning (§3.1.1).            */
 /* ------------------------------------------------------------------------- */
 

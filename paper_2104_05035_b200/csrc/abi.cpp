@@ -141,6 +141,31 @@ rn_status rn_gabra_place_slack(int32_t n, const int64_t *loads, int32_t m, const
   GUARD_END
 }
 
+rn_status rn_simulate_step(const rn_sim_desc *d, double *step_s, double *pipeline_s, double *allreduce_s,
+                           double *stage_s) {
+  GUARD_BEGIN
+  if (!d || !step_s || !pipeline_s || !allreduce_s || !d->part_time || !d->param_bytes || !d->genes ||
+      (d->n > 1 && !d->cut_bytes) || d->n < 1 || d->n_stages < 1 || d->replicas < 1 || d->micro_batches < 1 ||
+      !(d->beta > 0))
+    return set_error(RN_ERR_ARG, "rn_simulate_step: bad arguments");
+  for (int i = 0; i < d->n; ++i)
+    if (d->genes[i] < 0 || d->genes[i] >= d->n_stages) return set_error(RN_ERR_ARG, "rn_simulate_step: bad gene");
+  simulate_step(*d, step_s, pipeline_s, allreduce_s, stage_s);
+  return RN_OK;
+  GUARD_END
+}
+
+rn_status rn_contiguous_split(int32_t n, const int64_t *loads, int32_t n_stages, int32_t *genes_out,
+                              int64_t *max_load_out) {
+  GUARD_BEGIN
+  if (!loads || !genes_out || n_stages < 1 || n < n_stages) return set_error(RN_ERR_ARG, "rn_contiguous_split: bad arguments");
+  for (int i = 0; i < n; ++i)
+    if (loads[i] < 0) return set_error(RN_ERR_ARG, "rn_contiguous_split: negative load");
+  contiguous_split(n, loads, n_stages, genes_out, max_load_out);
+  return RN_OK;
+  GUARD_END
+}
+
 rn_status rn_net_units(const rn_net_desc *net, int32_t *n_units, int64_t *unit_loads, int32_t *n_parts,
                        int32_t *part_first_unit, int64_t *part_loads) {
   GUARD_BEGIN

@@ -961,9 +961,14 @@ __global__ void __launch_bounds__(NTA) stem_pool_fwd_k(const bf16 *__restrict__ 
   }
 }
 
+inline int bn_grid_mult() {
+  static const int m = getenv("RN_BN_GRID_MULT") ? std::max(1, atoi(getenv("RN_BN_GRID_MULT"))) : 1;
+  return m;
+}
+
 inline unsigned grid_part(int64_t vecs, int G) {
   int64_t b = (vecs + (int64_t)NTA * EU - 1) / ((int64_t)NTA * EU);
-  if (b > 148) b = 148;
+  if (b > 148 * bn_grid_mult()) b = 148 * bn_grid_mult();
   if (b < 1) b = 1;
   return (unsigned)stride_multiple(b, NTA, G);
 }

@@ -63,4 +63,8 @@ NetModel build_net(const rn_net_desc &d);
 void partition_units(const std::vector<int64_t> &costs, double alpha, int64_t max_merge_load,
                      std::vector<int> &first, std::vector<int64_t> &loads);
 
+// f2 step-time model and contiguous split (sim.cpp)
+void simulate_step(const rn_sim_desc &d, double *step, double *pipe, double *ar, double *stage_t);
+void contiguous_split(int n, const int64_t *loads, int S, int32_t *genes, int64_t *max_load);
+
 }  // namespace rn

@@ -1147,7 +1147,11 @@ void Plan::forward_body(const float *x_in, const int32_t *y, int k_only) {
         const Unit &pu = net.units[ui - 1];
         nccl_recv_bytes(pipe_comm, P(units[ui].recv_in[k]), act_bytes(pu.cout, pu.out), unit_stage[ui - 1], stream);
       }
-      unit_fwd(ui, k, x_in, y);
+      {
+        const size_t ue = timing() ? tk_begin(4, 0.0) : 0;  // per-unit time (f2 step-time model)
+        unit_fwd(ui, k, x_in, y);
+        if (timing()) tk_end(ue, ui);
+      }
       if (ui + 1 < nu && !local[ui + 1] && !xfer_external) {
         const Unit &u = net.units[ui];
         nccl_send_bytes(pipe_comm, P(units[ui].out[k]), act_bytes(u.cout, u.out), unit_stage[ui + 1], stream);
@@ -1170,7 +1174,11 @@ void Plan::backward_body(const float *x_in, int k_only) {
         const Unit &u = net.units[ui];
         nccl_recv_bytes(pipe_comm, P(units[ui].dout), act_bytes(u.cout, u.out), unit_stage[ui + 1], stream);
       }
-      unit_bwd(ui, k, x_in);
+      {
+        const size_t ue = timing() ? tk_begin(5, 0.0) : 0;
+        unit_bwd(ui, k, x_in);
+        if (timing()) tk_end(ue, ui);
+      }
       if (ui > 0 && !local[ui - 1] && !xfer_external) {
         const Unit &pu = net.units[ui - 1];
         nccl_send_bytes(pipe_comm, P(units[ui].send_dx), act_bytes(pu.cout, pu.out), unit_stage[ui - 1], stream);
@@ -1539,7 +1547,7 @@ rn_status Plan::query(const std::string &k, double *v) {
     if (k.find("_stem") != std::string::npos) kind = K_STEM;
     double ms = 0, fl = 0, n = 0;
     for (size_t i = 0; i < ev_used; ++i) {
-      if (ev_pool[i].cls == 3) continue;  // elementwise launches
+      if (ev_pool[i].cls >= 3) continue;  // elementwise launches / unit brackets
       if (cls >= 0 && ev_pool[i].cls != cls) continue;
       if (kind >= 0 && ev_pool[i].kind != kind) continue;
       float e = 0.f;
@@ -1552,6 +1560,23 @@ rn_status Plan::query(const std::string &k, double *v) {
     else if (k.rfind("conv_flops", 0) == 0) *v = fl;
     else if (k.rfind("conv_launches", 0) == 0) *v = n;
     else return set_error(RN_ERR_ARG, "unknown statistic " + k);
+    return RN_OK;
+  }
+  if (k.rfind("unit_ms_", 0) == 0) {
+    // unit_ms_fwd_<u> / unit_ms_bwd_<u>: device time of unit u's forward / backward
+    // (all its launches, summed over micro-batches) in the last timed step
+    CUDA_CHECK(cudaStreamSynchronize(stream));
+    const bool fwd = k.rfind("unit_ms_fwd_", 0) == 0;
+    if (!fwd && k.rfind("unit_ms_bwd_", 0) != 0) return set_error(RN_ERR_ARG, "unknown statistic " + k);
+    const int u = atoi(k.c_str() + 12);
+    double ms = 0;
+    for (size_t i = 0; i < ev_used; ++i) {
+      if (ev_pool[i].cls != (fwd ? 4 : 5) || ev_pool[i].kind != u) continue;
+      float e = 0.f;
+      CUDA_CHECK(cudaEventElapsedTime(&e, ev_pool[i].a, ev_pool[i].b));
+      ms += e;
+    }
+    *v = ms;
     return RN_OK;
   }
   if (k.rfind("elt_", 0) == 0) {

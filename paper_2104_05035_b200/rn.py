@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "librn.so")
 RN_F32, RN_BF16 = 0, 1
 STATUS = {0: "RN_OK", 1: "RN_ERR_ARG", 2: "RN_ERR_SCHEMA", 3: "RN_ERR_INFEASIBLE", 4: "RN_ERR_NUMERIC",
           5: "RN_ERR_CUDA", 6: "RN_ERR_NCCL", 7: "RN_ERR_STATE", 8: "RN_ERR_SIZE"}
-EXPORTS = ["rn_ga_default", "rn_gabra_place", "rn_gabra_place_slack", "rn_net_units", "rn_net_param_count", "rn_net_param_info",
+EXPORTS = ["rn_ga_default", "rn_gabra_place", "rn_gabra_place_slack", "rn_simulate_step", "rn_contiguous_split", "rn_net_units", "rn_net_param_count", "rn_net_param_info",
            "rn_nccl_unique_id", "rn_plan", "rn_plan_delayed", "rn_delayed_step", "rn_plan_describe", "rn_plan_bind", "rn_set_params", "rn_get_params", "rn_get_grads",
            "rn_get_bn_running", "rn_get_activation", "rn_get_unit_grad", "rn_get_saved", "rn_forward", "rn_backward", "rn_step", "rn_train_step_host",
            "rn_train_steps_host", "rn_gradcam",
@@ -108,6 +108,37 @@ def gabra_place_slack(loads, m, **kw):
     gp = ga_params(**kw)
     _check(lib().rn_gabra_place_slack(n, L, m, C.byref(gp), genes, C.byref(profit), gl, caps, C.byref(slack)))
     return list(genes), profit.value, list(gl), list(caps), slack.value
+
+
+class SimDesc(C.Structure):
+    _fields_ = [("n", C.c_int32), ("n_stages", C.c_int32), ("replicas", C.c_int32), ("micro_batches", C.c_int32),
+                ("schedule", C.c_int32), ("overlap", C.c_int32), ("alpha", C.c_double), ("beta", C.c_double),
+                ("part_time", C.POINTER(C.c_double)), ("cut_bytes", C.POINTER(C.c_double)),
+                ("param_bytes", C.POINTER(C.c_double)), ("genes", C.POINTER(C.c_int32))]
+
+
+def simulate_step(part_time, cut_bytes, param_bytes, genes, S, R, Mb, alpha, beta, schedule=0, overlap=False):
+    """rn_simulate_step: (step, pipeline, allreduce, per-stage T_s)."""
+    n = len(part_time)
+    pt = (C.c_double * n)(*part_time)
+    cb = (C.c_double * max(n - 1, 1))(*(list(cut_bytes) or [0.0]))
+    pb = (C.c_double * n)(*param_bytes)
+    gn = (C.c_int32 * n)(*genes)
+    d = SimDesc(n, S, R, Mb, schedule, 1 if overlap else 0, alpha, beta, pt, cb, pb, gn)
+    st, pp, ar = C.c_double(), C.c_double(), C.c_double()
+    ts = (C.c_double * S)()
+    _check(lib().rn_simulate_step(C.byref(d), C.byref(st), C.byref(pp), C.byref(ar), ts))
+    return st.value, pp.value, ar.value, list(ts)
+
+
+def contiguous_split(loads, S):
+    """rn_contiguous_split: (genes, max stage load)."""
+    n = len(loads)
+    L = (C.c_int64 * n)(*loads)
+    g = (C.c_int32 * n)()
+    mx = C.c_int64()
+    _check(lib().rn_contiguous_split(n, L, S, g, C.byref(mx)))
+    return list(g), mx.value
 
 
 def net_units(desc: NetDesc):
