@@ -87,7 +87,24 @@ struct __align__(64) TcParams {
   float *part;
   int64_t n_view_vox;
   EpiStats st;  // fused BN statistics of the stored output (needs !use_part, t_nblk == 1)
+  unsigned long long *trace;  // debug (RN_TC_TRACE): per-CTA %globaltimer stamps [grid][8]
+  // TMA-store epilogue (launches whose CTAs own at most one work item): the tile is
+  // staged in the (then idle) smem ring, SW128-swizzled, and written by
+  // cp.async.bulk.tensor -- coalesced, instead of one 16-B store per row per thread.
+  // tma_st 1: bf16 y through y_map (box {64, bw, bh, bd, bn}); 2: fp32 split-K
+  // partials through part_map (box {32, ...}, 5th dim = split * ON + n)
+  int tma_ok;  // host: the maps are valid for this launch (no accumulate / residual, one class)
+  int tma_st;
+  CUtensorMap y_map, part_map;
 };
+
+__device__ __forceinline__ void tc_stamp(const TcParams &p, int k) {
+  if (p.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[blockIdx.x * 8 + k] = t;
+  }
+}
 
 template <int BN, int STAGES>
 struct Smem {
@@ -144,6 +161,7 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
   TapEnt *tab = (TapEnt *)(smem + S::TAB_OFF);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) tc_stamp(p, 0);
   if (warp == 0 && lane < p.n_taps) {
     TapEnt e;
     e.amap = &p.a_map[p.tap_map[lane]];
@@ -177,6 +195,7 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_begin();  // prologue above overlaps the predecessor's tail
+  if (threadIdx.x == 0) tc_stamp(p, 1);
 
   const int64_t n_items = p.cls_item0[p.n_cls];
 
@@ -197,6 +216,7 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
           uint8_t *sa = smem + stage * S::STAGE;
           uint8_t *sb = sa + S::A_BYTES;
           tc::mbar_arrive_expect_tx(&full[stage], S::STAGE);
+          if (kb == it.kb0 && item == blockIdx.x) tc_stamp(p, 2);
           tc::tma_load_5d(sa, e.amap, &full[stage], cb * 64, w0 + e.ow, h0 + e.oh, d0 + e.od, n0);
           tc::tma_load_2d(sb, e.bmap, &full[stage], e.kcoord + cb * 64, nb * BN);
           if (++cb == kpt) { cb = 0; ++t; }
@@ -226,6 +246,7 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
       for (int kb = kb0; kb < kb1; ++kb) {
         tc::mbar_wait(&full[stage], phase);
         tc::tc_fence_after();
+        if (local == 0 && kb == kb0 && lane == 0) tc_stamp(p, 3);
         const uint32_t soff = (uint32_t)(stage * S::STAGE) >> 4;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -240,6 +261,7 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
     }
     // every MMA of this CTA is issued: the dependent grid may start launching
     // (persistent grid: no later wave of this kernel to be displaced)
+    if (lane == 0) tc_stamp(p, 4);
     if (kPdlLate) pdl_trigger();
   } else {
     // ---------------- epilogue (warps 2..5) ----------------
@@ -267,12 +289,21 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
       epi_stats_prefetch(p.st, valid, obase, pf_cur);  // before the accumulator wait
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::tc_fence_after();
+      if (local == 0 && et == 0) tc_stamp(p, 5);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         if (c0 + 32 < BN) epi_stats_prefetch(p.st, valid, obase + c0 + 32, pf_nxt);
         uint32_t v[32];
         tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
         tc::tmem_wait_ld();
+        if (p.tma_st == 2) {  // fp32 partial row -> staging chunk c0/32 (16 KB), SW128
+          uint8_t *ch = smem + (c0 / 32) * 16384 + row * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<uint4 *>(ch + ((j ^ (row & 7)) << 4)) = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                                                                                 v[4 * j + 3]);
+          continue;
+        }
         if (valid && p.use_part) {
           // split-K: raw fp32 partial [class][split][view voxel][Nout]; epilogue in the finish kernel
           const int64_t vidx = ((int64_t)(on * p.OD + od) * p.OH + oh) * p.OW + ow;
@@ -291,6 +322,19 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
 #pragma unroll
             for (int j = 0; j < 32; ++j) f[j] += p.bias[nb * BN + c0 + j];
           }
+        }
+        if (p.tma_st == 1) {  // bf16 row segment -> staging chunk c0/64 (16 KB), SW128
+          uint8_t *ch = smem + (c0 / 64) * 16384 + row * 128;
+          const int q0 = (c0 % 64) / 8;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 u;
+            __nv_bfloat162 *pv = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pv[e] = __floats2bfloat162_rn(f[8 * j + 2 * e], f[8 * j + 2 * e + 1]);
+            *reinterpret_cast<uint4 *>(ch + (((q0 + j) ^ (row & 7)) << 4)) = u;
+          }
+        } else if (valid) {
           bf16 *dst = p.y + obase + c0;
           if (p.accumulate) {
 #pragma unroll
@@ -323,10 +367,30 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+      if (p.tma_st) {
+        // every row of the tile is staged: make the generic-proxy smem writes visible
+        // to the async proxy, then one thread writes the tile with TMA
+        tc::fence_proxy_async();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) {
+          const int w0 = it.tw * p.bw, h0 = it.th * p.bh, d0 = it.td * p.bd, n0 = it.tn * p.bn;
+          if (p.tma_st == 1) {
+            for (int j = 0; j < BN / 64; ++j)
+              tc::tma_store_5d(&p.y_map, smem + j * 16384, nb * BN + j * 64, w0, h0, d0, n0);
+          } else {
+            for (int j = 0; j < BN / 32; ++j)
+              tc::tma_store_5d(&p.part_map, smem + j * 16384, nb * BN + j * 32, w0, h0, d0, split * p.ON + n0);
+          }
+          tc::bulk_commit();
+          tc::bulk_wait0();  // complete before the grid does (the finish / BN kernels read it)
+        }
+      }
     }
     if (p.st.mode) epi_stats_flush(p.st, red, BN, BN, et);
+    if (et == 0) tc_stamp(p, 6);
   }
   __syncthreads();
+  if (threadIdx.x == 0) tc_stamp(p, 7);
   if (warp == 1) {
     tc::tc_fence_after();
     tc::tmem_dealloc<TMEM_COLS>(tmem_base);
@@ -368,6 +432,24 @@ void make_act_map(CUtensorMap *m, const void *base, int C, int W, int H, int D, 
   if (r != CUDA_SUCCESS) throw Error(RN_ERR_CUDA, "cuTensorMapEncodeTiled (activation) failed: " + std::to_string(r));
 }
 
+// 5-D output view of a contiguous NDHWC tensor (bf16 or fp32) for TMA stores:
+// dims {C, W, H, D, N}, box {128 B of channels, bw, bh, bd, bn}, SW128
+static void make_out_map(CUtensorMap *m, const void *base, bool f32, int C, int W, int H, int D, int N, int bw, int bh,
+                         int bd, int bn) {
+  if (g_dry_need) return;
+  load_encode();
+  const int es = f32 ? 4 : 2;
+  cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)D, (cuuint64_t)N};
+  cuuint64_t strides[4] = {(cuuint64_t)C * es, (cuuint64_t)C * es * W, (cuuint64_t)C * es * W * H,
+                           (cuuint64_t)C * es * W * H * D};
+  cuuint32_t box[5] = {(cuuint32_t)(128 / es), (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bd, (cuuint32_t)bn};
+  cuuint32_t ess[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+                        const_cast<void *>(base), dims, strides, box, ess, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(RN_ERR_CUDA, "cuTensorMapEncodeTiled (output) failed: " + std::to_string(r));
+}
+
 void make_w_map(CUtensorMap *m, const void *base, int rows, int64_t ktot, int bn) {
   if (g_dry_need) return;
   load_encode();
@@ -399,8 +481,19 @@ void choose_box(int W, int H, int D, int N, int &bw, int &bh, int &bd, int &bn) 
       }
 }
 
+bool tma_store_off() {
+  static const bool off = getenv("RN_TC_TMA_STORE") && atoi(getenv("RN_TC_TMA_STORE")) == 0;
+  return off;
+}
+
+unsigned long long *g_trace = nullptr;
+int g_trace_n = 0;
+int g_trace_meta[256][8];
+
 template <int BN, int STAGES>
-int launch(const TcParams &p, cudaStream_t st) {
+int launch(const TcParams &p0, cudaStream_t st) {
+  TcParams p = p0;
+  p.trace = nullptr;
   using S = Smem<BN, STAGES>;
   static uint64_t attr_devs = 0;  // kernel attributes are per device
   if (!once_on_device(attr_devs)) {
@@ -428,6 +521,20 @@ int launch(const TcParams &p, cudaStream_t st) {
     per_sm = std::max(1, std::min(per_sm, 512 / (2 * BN)));
   }
   const int grid = (int)std::min<int64_t>(p.cls_item0[p.n_cls], (int64_t)sms * per_sm);
+  // TMA-store epilogue: every CTA owns at most one item (the ring is idle at its
+  // epilogue and doubles as the staging buffer) and the tile fits the ring
+  const int stg_bytes = 128 * BN * (p.use_part ? 4 : 2);
+  p.tma_st = (p.tma_ok && p.n_cls == 1 && p.cls_item0[p.n_cls] <= grid && stg_bytes <= STAGES * S::STAGE &&
+              !tma_store_off())
+                 ? (p.use_part ? 2 : 1)
+                 : 0;
+  if (getenv("RN_TC_TRACE") && g_trace_n < 256) {
+    if (!g_trace) CUDA_CHECK(cudaMalloc(&g_trace, sizeof(unsigned long long) * 256 * 296 * 8));
+    p.trace = g_trace + (size_t)g_trace_n * 296 * 8;
+    int *m = g_trace_meta[g_trace_n++];
+    m[0] = BN; m[1] = STAGES; m[2] = grid; m[3] = (int)p.cls_item0[p.n_cls]; m[4] = p.ksplit; m[5] = p.n_cls;
+    m[6] = p.use_part; m[7] = p.n_taps * p.kblocks_per_tap;
+  }
   if (getenv("RN_DEBUG_GRID"))
     fprintf(stderr, "conv_tc<%d,%d> items %lld per_sm %d grid %d smem %d\n", BN, STAGES,
             (long long)p.cls_item0[p.n_cls], per_sm, grid, S::TOTAL);
@@ -705,6 +812,17 @@ int run(TcParams &p, int BN, float *ws, size_t ws_floats, const EpiStats *est, c
   const bool stats = est && est->mode && p.ksplit == 1 && p.t_nblk == 1;
   const bool fin_stats = est && est->mode && p.ksplit > 1;
   if (stats) p.st = *est;
+  // TMA-store epilogue maps (used when every CTA owns one item; decided at launch):
+  // split-K partials always (the finish kernel applies bias / accumulate / residual),
+  // direct bf16 output without accumulate / residual; aligned views only
+  const bool aligned = ((uintptr_t)p.y % 16 == 0) && ((uintptr_t)ws % 16 == 0);
+  if (aligned && p.ksplit > 1 && p.ON % p.bn == 0) {
+    make_out_map(&p.part_map, ws, true, p.ych, p.OW, p.OH, p.OD, p.ON * p.ksplit, p.bw, p.bh, p.bd, p.bn);
+    p.tma_ok = 1;
+  } else if (aligned && p.ksplit == 1 && !p.accumulate && !p.res) {
+    make_out_map(&p.y_map, p.y, false, p.ych, p.OW, p.OH, p.OD, p.ON, p.bw, p.bh, p.bd, p.bn);
+    p.tma_ok = 1;
+  }
   const int grid = launch_ring(p, BN, st);
   if (p.ksplit > 1) {
     const int64_t n = p.n_view_vox * (p.ych / 8);
@@ -1004,3 +1122,16 @@ size_t tc_conv_ws_floats(const ConvGeom &g, bool dgrad) {
 }
 
 }  // namespace rn
+
+// debug: the traced conv_tc launches (RN_TC_TRACE): host[l][cta][8] %globaltimer stamps,
+// meta[l][8] = {BN, STAGES, grid, items, ksplit, n_cls, use_part, k-blocks}; returns the count
+extern "C" int rn_dbg_tc_trace(unsigned long long *host, int max_launches, int *meta) {
+  using namespace rn;
+  const int n = std::min(g_trace_n, max_launches);
+  if (n > 0 && g_trace) {
+    cudaDeviceSynchronize();
+    cudaMemcpy(host, g_trace, sizeof(unsigned long long) * (size_t)n * 296 * 8, cudaMemcpyDeviceToHost);
+    memcpy(meta, g_trace_meta, sizeof(int) * 8 * n);
+  }
+  return n;
+}
