@@ -93,10 +93,19 @@ struct __align__(64) TcParams {
   // cp.async.bulk.tensor -- coalesced, instead of one 16-B store per row per thread.
   // tma_st 1: bf16 y through y_map (box {64, bw, bh, bd, bn}); 2: fp32 split-K
   // partials through part_map (box {32, ...}, 5th dim = split * ON + n)
-  int tma_ok;  // host: the maps are valid for this launch (no accumulate / residual, one class)
+  int tma_ok;  // host: the maps are valid for this launch (one class, aligned views)
   int tma_st;
   CUtensorMap y_map, part_map;
+  // direct path inputs loaded by TMA into the ring at the epilogue: residual and its
+  // mask (identity-skip dgrad), the consumer BN's h / ReLU mask (backward statistics)
+  CUtensorMap res_map, resm_map, h_map, m_map;
 };
+
+// smem bytes of the TMA epilogue (direct path): output tile + every input tile
+__host__ __device__ inline int tma_epi_bytes(int BN, bool res, int stmode) {
+  const int t = 128 * BN * 2;
+  return t * (1 + (res ? 2 : 0) + (stmode == 2 ? 2 : stmode == 3 ? 1 : 0));
+}
 
 __device__ __forceinline__ void tc_stamp(const TcParams &p, int k) {
   if (p.trace) {
@@ -157,7 +166,7 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
   uint64_t *empty = full + STAGES;
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
-  uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+  uint32_t *tmem_slot = (uint32_t *)(tempty + 3);  // tempty[2] = the TMA epilogue's input barrier
   TapEnt *tab = (TapEnt *)(smem + S::TAB_OFF);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -182,6 +191,7 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
       tc::mbar_init(&tfull[i], 1);
       tc::mbar_init(&tempty[i], 4);
     }
+    tc::mbar_init(&tempty[2], 1);
     tc::fence_barrier_init();
     for (int i = 0; i < p.n_taps; ++i)
       if (i == 0 || p.tap_map[i] != p.tap_map[i - 1]) tc::tma_prefetch(&p.a_map[p.tap_map[i]]);
@@ -275,6 +285,112 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
     }
     const int wx = row % p.bw, hy = (row / p.bw) % p.bh, dz = (row / (p.bw * p.bh)) % p.bd,
               nz = row / (p.bw * p.bh * p.bd);
+    if (p.tma_st == 1 && (int64_t)blockIdx.x < n_items) {
+      // ---- direct TMA epilogue: this CTA's single work item ----
+      const Item it = decode_item(p, blockIdx.x);
+      const int nb = it.nb;
+      const int w0 = it.tw * p.bw, h0 = it.th * p.bh, d0 = it.td * p.bd, n0 = it.tn * p.bn;
+      constexpr int NCH = BN / 64, TB = 128 * BN * 2;
+      uint8_t *s_out = smem;  // output (and the accumulate input)
+      int off = TB;
+      uint8_t *s_res = nullptr, *s_rm = nullptr, *s_h = nullptr, *s_m = nullptr;
+      if (p.res) { s_res = smem + off; off += TB; s_rm = smem + off; off += TB; }
+      if (p.st.mode >= 2) { s_h = smem + off; off += TB; }
+      if (p.st.mode == 2) { s_m = smem + off; off += TB; }
+      uint64_t *ebar = tempty + 2;  // epilogue input barrier (after tempty[2], before tmem_slot)
+      tc::mbar_wait(&tfull[0], 0);
+      tc::tc_fence_after();
+      const bool need_in = p.accumulate || p.res || p.st.mode >= 2;
+      if (need_in) {
+        if (et == 0) {
+          const uint32_t bytes = (uint32_t)(off - (p.accumulate ? 0 : TB));
+          tc::mbar_arrive_expect_tx(ebar, bytes);
+          for (int j = 0; j < NCH; ++j) {
+            const int cc = nb * BN + j * 64;
+            if (p.accumulate) tc::tma_load_5d(s_out + j * 16384, &p.y_map, ebar, cc, w0, h0, d0, n0);
+            if (p.res) {
+              tc::tma_load_5d(s_res + j * 16384, &p.res_map, ebar, cc, w0, h0, d0, n0);
+              tc::tma_load_5d(s_rm + j * 16384, &p.resm_map, ebar, cc, w0, h0, d0, n0);
+            }
+            if (s_h) tc::tma_load_5d(s_h + j * 16384, &p.h_map, ebar, cc, w0, h0, d0, n0);
+            if (s_m) tc::tma_load_5d(s_m + j * 16384, &p.m_map, ebar, cc, w0, h0, d0, n0);
+          }
+        }
+        tc::mbar_wait(ebar, 0);
+      }
+      if (et == 0) tc_stamp(p, 5);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + c0, v);
+        tc::tmem_wait_ld();
+        const int chk = (c0 / 64) * 16384 + row * 128, q0 = (c0 % 64) / 8;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int po = chk + (((q0 + j) ^ (row & 7)) << 4);
+          float f[8], o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * j + e]);
+          if (p.bias)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] += p.bias[nb * BN + c0 + 8 * j + e];
+          if (p.accumulate) {
+            unpack_bf16x8(*reinterpret_cast<const uint4 *>(s_out + po), o);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] += o[e];
+          }
+          if (p.res) {
+            float rv[8], mv[8];
+            unpack_bf16x8(*reinterpret_cast<const uint4 *>(s_res + po), rv);
+            unpack_bf16x8(*reinterpret_cast<const uint4 *>(s_rm + po), mv);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] += mv[e] > 0.f ? rv[e] : 0.f;
+          }
+          uint4 u;
+          __nv_bfloat162 *pv = reinterpret_cast<__nv_bfloat162 *>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) pv[e] = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+          *reinterpret_cast<uint4 *>(s_out + po) = u;
+        }
+      }
+      tc::tc_fence_before();
+      tc::fence_proxy_async();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (et == 0) {
+        for (int j = 0; j < NCH; ++j) tc::tma_store_5d(&p.y_map, s_out + j * 16384, nb * BN + j * 64, w0, h0, d0, n0);
+        tc::bulk_commit();
+      }
+      if (p.st.mode) {
+        // BN statistics of the stored tile by columns from smem (no shuffles): the
+        // bf16 values the store writes; out-of-volume rows are zero (TMA zero fill)
+        for (int c = et; c < BN; c += 128) {
+          const int cb = (c / 64) * 16384 + (c % 8) * 2, pq = (c % 64) / 8;
+          const float mu = p.st.mode >= 2 ? p.st.mean[nb * BN + c] : 0.f;
+          const float ms = p.st.mode == 3 ? p.st.mscale[nb * BN + c] : 0.f;
+          const float mh = p.st.mode == 3 ? p.st.mshift[nb * BN + c] : 0.f;
+          float s1 = 0.f, s2 = 0.f;
+#pragma unroll 4
+          for (int r = 0; r < 128; ++r) {
+            const int a = cb + r * 128 + ((pq ^ (r & 7)) << 4);
+            const float o = __bfloat162float(*reinterpret_cast<const bf16 *>(s_out + a));
+            if (p.st.mode == 1) {
+              s1 += o;
+              s2 = fmaf(o, o, s2);
+            } else {
+              const float h = __bfloat162float(*reinterpret_cast<const bf16 *>(s_h + a));
+              const float m = p.st.mode == 2 ? __bfloat162float(*reinterpret_cast<const bf16 *>(s_m + a))
+                                             : fmaf(h, ms, mh);
+              const float d = m > 0.f ? o : 0.f;
+              s1 += d;
+              s2 = fmaf(d, h - mu, s2);
+            }
+          }
+          red[c] += s1;
+          red[BN + c] += s2;
+        }
+      }
+      if (et == 0) tc::bulk_wait0();
+    } else {
     int local = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
       const Item it = decode_item(p, item);
@@ -367,25 +483,21 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
-      if (p.tma_st) {
+      if (p.tma_st == 2) {
         // every row of the tile is staged: make the generic-proxy smem writes visible
         // to the async proxy, then one thread writes the tile with TMA
         tc::fence_proxy_async();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (et == 0) {
           const int w0 = it.tw * p.bw, h0 = it.th * p.bh, d0 = it.td * p.bd, n0 = it.tn * p.bn;
-          if (p.tma_st == 1) {
-            for (int j = 0; j < BN / 64; ++j)
-              tc::tma_store_5d(&p.y_map, smem + j * 16384, nb * BN + j * 64, w0, h0, d0, n0);
-          } else {
-            for (int j = 0; j < BN / 32; ++j)
-              tc::tma_store_5d(&p.part_map, smem + j * 16384, nb * BN + j * 32, w0, h0, d0, split * p.ON + n0);
-          }
+          for (int j = 0; j < BN / 32; ++j)
+            tc::tma_store_5d(&p.part_map, smem + j * 16384, nb * BN + j * 32, w0, h0, d0, split * p.ON + n0);
           tc::bulk_commit();
           tc::bulk_wait0();  // complete before the grid does (the finish / BN kernels read it)
         }
       }
     }
+    }  // generic epilogue
     if (p.st.mode) epi_stats_flush(p.st, red, BN, BN, et);
     if (et == 0) tc_stamp(p, 6);
   }
@@ -523,7 +635,7 @@ int launch(const TcParams &p0, cudaStream_t st) {
   const int grid = (int)std::min<int64_t>(p.cls_item0[p.n_cls], (int64_t)sms * per_sm);
   // TMA-store epilogue: every CTA owns at most one item (the ring is idle at its
   // epilogue and doubles as the staging buffer) and the tile fits the ring
-  const int stg_bytes = 128 * BN * (p.use_part ? 4 : 2);
+  const int stg_bytes = p.use_part ? 128 * BN * 4 : tma_epi_bytes(BN, p.res != nullptr, p.st.mode);
   p.tma_st = (p.tma_ok && p.n_cls == 1 && p.cls_item0[p.n_cls] <= grid && stg_bytes <= STAGES * S::STAGE &&
               !tma_store_off())
                  ? (p.use_part ? 2 : 1)
@@ -819,8 +931,15 @@ int run(TcParams &p, int BN, float *ws, size_t ws_floats, const EpiStats *est, c
   if (aligned && p.ksplit > 1 && p.ON % p.bn == 0) {
     make_out_map(&p.part_map, ws, true, p.ych, p.OW, p.OH, p.OD, p.ON * p.ksplit, p.bw, p.bh, p.bd, p.bn);
     p.tma_ok = 1;
-  } else if (aligned && p.ksplit == 1 && !p.accumulate && !p.res) {
+  } else if (aligned && p.ksplit == 1 && (!p.res || ((uintptr_t)p.res % 16 == 0 && (uintptr_t)p.res_mask % 16 == 0))) {
     make_out_map(&p.y_map, p.y, false, p.ych, p.OW, p.OH, p.OD, p.ON, p.bw, p.bh, p.bd, p.bn);
+    if (p.res) {
+      make_out_map(&p.res_map, p.res, false, p.ych, p.OW, p.OH, p.OD, p.ON, p.bw, p.bh, p.bd, p.bn);
+      make_out_map(&p.resm_map, p.res_mask, false, p.ych, p.OW, p.OH, p.OD, p.ON, p.bw, p.bh, p.bd, p.bn);
+    }
+    if (p.st.mode >= 2) make_out_map(&p.h_map, p.st.h, false, p.ych, p.OW, p.OH, p.OD, p.ON, p.bw, p.bh, p.bd, p.bn);
+    if (p.st.mode == 2)
+      make_out_map(&p.m_map, p.st.mask, false, p.ych, p.OW, p.OH, p.OD, p.ON, p.bw, p.bh, p.bd, p.bn);
     p.tma_ok = 1;
   }
   const int grid = launch_ring(p, BN, st);
