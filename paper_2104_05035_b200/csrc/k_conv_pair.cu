@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "bnstats.cuh"
@@ -67,6 +68,7 @@ struct __align__(64) PairParams {
   int accumulate;
   const bf16 *res, *res_mask;
   EpiStats st;
+  int res_pf;  // prefetch the residual operands (RN_PAIR_RES_PF=0 turns it off for A/B)
 };
 
 struct Item {
@@ -206,7 +208,23 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
         return it.n * p.s_n + (it.td * 2 + sl) * p.s_d + oh * p.s_h + ow * p.s_w;
       };
       StatsPf pf_cur, pf_nxt;
-      epi_stats_prefetch(p.st, chunk_valid(0), chunk_base(0), pf_cur);
+      // identity-skip residual (dgrad without fused statistics): its residual and mask
+      // rows travel in the statistics prefetch registers, one 32-channel chunk ahead --
+      // the first chunk's before the accumulator wait (latency behind the mainloop)
+      const bool res_pf = p.res && p.st.mode < 2 && p.res_pf;
+      auto prefetch = [&](bool valid, int64_t eo, StatsPf &pf) {
+        if (res_pf) {
+          if (!valid) return;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            pf.m[i] = __ldg(reinterpret_cast<const uint4 *>(p.res_mask + eo) + i);
+            pf.h[i] = __ldg(reinterpret_cast<const uint4 *>(p.res + eo) + i);
+          }
+        } else {
+          epi_stats_prefetch(p.st, valid, eo, pf);
+        }
+      };
+      prefetch(chunk_valid(0), chunk_base(0), pf_cur);
       tc::mbar_wait(&t_full[acc], (local >> 1) & 1);
       tc::tc_fence_after();
 #pragma unroll 1
@@ -215,8 +233,8 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
         const int64_t obase = chunk_base(sl);
 #pragma unroll 1
         for (int c0 = 0; c0 < 64; c0 += 32) {
-          if (c0 == 0) epi_stats_prefetch(p.st, valid, obase + 32, pf_nxt);
-          else if (sl == 0) epi_stats_prefetch(p.st, chunk_valid(1), chunk_base(1), pf_nxt);
+          if (c0 == 0) prefetch(valid, obase + 32, pf_nxt);
+          else if (sl == 0) prefetch(chunk_valid(1), chunk_base(1), pf_nxt);
           uint32_t v[32];
           tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * 128 + sl * 64 + c0, v);
           tc::tmem_wait_ld();
@@ -238,7 +256,16 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
                 for (int e = 0; e < 8; ++e) f[j + e] += o[e];
               }
             }
-            if (p.res) {
+            if (res_pf) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                float rv[8], mv[8];
+                unpack_bf16x8(pf_cur.h[j], rv);
+                unpack_bf16x8(pf_cur.m[j], mv);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) f[8 * j + e] += mv[e] > 0.f ? rv[e] : 0.f;
+              }
+            } else if (p.res) {
 #pragma unroll
               for (int j = 0; j < 32; j += 8) {
                 float rv[8], mv[8];
@@ -251,10 +278,9 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
 #pragma unroll
             for (int j = 0; j < 32; j += 8) store_vec(dst + j, f + j);
           }
-          if (p.st.mode) {
-            epi_stats_add(p.st, f, valid, pf_cur, c0, lane, red + (q * 2) * 64 + c0, red + (q * 2 + 1) * 64 + c0);
-            pf_cur = pf_nxt;
-          }
+          if (p.st.mode) epi_stats_add(p.st, f, valid, pf_cur, c0, lane, red + (q * 2) * 64 + c0,
+                                       red + (q * 2 + 1) * 64 + c0);
+          if (p.st.mode || res_pf) pf_cur = pf_nxt;
         }
       }
       tc::tc_fence_before();
@@ -298,6 +324,7 @@ int conv_pair(const ConvGeom &g, bool dgrad, const bf16 *src, const bf16 *w, con
   p.bias = bias;
   p.accumulate = accumulate;
   p.res = res;
+  p.res_pf = !(getenv("RN_PAIR_RES_PF") && atoi(getenv("RN_PAIR_RES_PF")) == 0);
   p.res_mask = res_mask;
   if (est && est->mode) p.st = *est;
   static uint64_t attr_devs = 0;  // kernel attributes are per device
