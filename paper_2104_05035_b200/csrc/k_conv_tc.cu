@@ -45,6 +45,15 @@ namespace rn {
 namespace {
 
 constexpr int TC_THREADS = 192;
+// one-CTA-per-SM variants (deep ring) run 8 warps: in the direct TMA epilogue of
+// their single work item the producer and MMA warps join the four epilogue warps
+// once their loops are done (two warps per TMEM lane quarter, columns split; the
+// 4-warp epilogue was latency-bound, one warp per scheduler).  8 warps keep the
+// 255-register budget (10 would cap it at 168: 3 warps on one 16 K-register SMSP)
+template <int BN, int STAGES>
+constexpr int tc_threads() {
+  return (STAGES * (128 * 128 + BN * 128) > 110 * 1024) ? 256 : TC_THREADS;
+}
 constexpr bool kPdlLate = true;  // explicit late PDL trigger (after the last MMA issue)
 
 constexpr int MAX_TAPS = 28;  // 27 taps + the appended projection tap (stride-2 dgrad)
@@ -157,7 +166,7 @@ __device__ __forceinline__ Item decode_item(const TcParams &p, int64_t item) {
 
 // deep-ring variants (one CTA per SM by smem) get the whole register file: no spills
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE > 110 * 1024) ? 1 : 2)
+__global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, STAGES>::STAGE > 110 * 1024) ? 1 : 2)
     conv_tc_kernel(const __grid_constant__ TcParams p) {
   using S = Smem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
@@ -273,20 +282,28 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
     // (persistent grid: no later wave of this kernel to be displaced)
     if (lane == 0) tc_stamp(p, 4);
     if (kPdlLate) pdl_trigger();
-  } else {
-    // ---------------- epilogue (warps 2..5) ----------------
+  }
+  const bool direct = p.tma_st == 1 && (int64_t)blockIdx.x < n_items;
+  constexpr bool ALLW = tc_threads<BN, STAGES>() == 256;
+  if ((direct && ALLW) || (warp >= 2 && warp < 6)) {
+    // ---------------- epilogue (warps 2..5; every warp in the 8-warp direct epilogue) ----------------
+    __syncwarp();
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
-    const int et = threadIdx.x - 64;  // 0..127
+    const int et = (direct && ALLW) ? (int)threadIdx.x : (int)threadIdx.x - 64;
+    const int NEPI = (direct && ALLW) ? 256 : 128;  // epilogue threads
     float *red = (float *)(smem + S::RED_OFF);
     if (p.st.mode) {
-      for (int i = et; i < 8 * BN; i += 128) red[i] = 0.f;
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int i = et; i < 8 * BN; i += NEPI) red[i] = 0.f;
+      asm volatile("bar.sync 1, %0;" ::"r"(NEPI) : "memory");
     }
     const int wx = row % p.bw, hy = (row / p.bw) % p.bh, dz = (row / (p.bw * p.bh)) % p.bd,
               nz = row / (p.bw * p.bh * p.bd);
-    if (p.tma_st == 1 && (int64_t)blockIdx.x < n_items) {
+    if (direct) {
       // ---- direct TMA epilogue: this CTA's single work item ----
+      const int NH = NEPI / 128;                        // warps per TMEM lane quarter
+      const int half = ALLW ? warp / 4 : 0;             // this warp's column slice
+      const int cbeg = half * (BN / NH), cend = cbeg + BN / NH;
       const Item it = decode_item(p, blockIdx.x);
       const int nb = it.nb;
       const int w0 = it.tw * p.bw, h0 = it.th * p.bh, d0 = it.td * p.bd, n0 = it.tn * p.bn;
@@ -320,7 +337,7 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
       }
       if (et == 0) tc_stamp(p, 5);
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = cbeg; c0 < cend; c0 += 32) {
         uint32_t v[32];
         tc::tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + c0, v);
         tc::tmem_wait_ld();
@@ -355,22 +372,25 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
       }
       tc::tc_fence_before();
       tc::fence_proxy_async();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(NEPI) : "memory");
       if (et == 0) {
         for (int j = 0; j < NCH; ++j) tc::tma_store_5d(&p.y_map, s_out + j * 16384, nb * BN + j * 64, w0, h0, d0, n0);
         tc::bulk_commit();
       }
       if (p.st.mode) {
         // BN statistics of the stored tile by columns from smem (no shuffles): the
-        // bf16 values the store writes; out-of-volume rows are zero (TMA zero fill)
-        for (int c = et; c < BN; c += 128) {
+        // bf16 values the store writes; out-of-volume rows are zero (TMA zero fill).
+        // NEPI threads: column c = et % BN over row slice et / BN of NRS slices
+        const int NRS = NEPI >= BN ? NEPI / BN : 1, RPS = 128 / NRS;
+        const int rs = et / BN;
+        for (int c = et % BN; c < BN && rs < NRS; c += NEPI) {
           const int cb = (c / 64) * 16384 + (c % 8) * 2, pq = (c % 64) / 8;
           const float mu = p.st.mode >= 2 ? p.st.mean[nb * BN + c] : 0.f;
           const float ms = p.st.mode == 3 ? p.st.mscale[nb * BN + c] : 0.f;
           const float mh = p.st.mode == 3 ? p.st.mshift[nb * BN + c] : 0.f;
           float s1 = 0.f, s2 = 0.f;
 #pragma unroll 4
-          for (int r = 0; r < 128; ++r) {
+          for (int r = rs * RPS; r < (rs + 1) * RPS; ++r) {
             const int a = cb + r * 128 + ((pq ^ (r & 7)) << 4);
             const float o = __bfloat162float(*reinterpret_cast<const bf16 *>(s_out + a));
             if (p.st.mode == 1) {
@@ -385,8 +405,20 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
               s2 = fmaf(d, h - mu, s2);
             }
           }
-          red[c] += s1;
-          red[BN + c] += s2;
+          red[(rs * 2) * BN + c] += s1;      // slice rs in the warp-rs accumulator slot
+          red[(rs * 2 + 1) * BN + c] += s2;
+        }
+        // every slot written: sum the (<= 4) row slices in order and write the partial
+        asm volatile("bar.sync 1, %0;" ::"r"(NEPI) : "memory");
+        for (int c = et; c < BN; c += NEPI) {
+          float a = 0.f, b2 = 0.f;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            a += red[(w * 2 + 0) * BN + c];
+            b2 += red[(w * 2 + 1) * BN + c];
+          }
+          p.st.part[(int64_t)blockIdx.x * 2 * BN + c] = a;
+          p.st.part[(int64_t)blockIdx.x * 2 * BN + BN + c] = b2;
         }
       }
       if (et == 0) tc::bulk_wait0();
@@ -497,8 +529,8 @@ __global__ void __launch_bounds__(TC_THREADS, (STAGES * Smem<BN, STAGES>::STAGE 
         }
       }
     }
-    }  // generic epilogue
-    if (p.st.mode) epi_stats_flush(p.st, red, BN, BN, et);
+      if (p.st.mode) epi_stats_flush(p.st, red, BN, BN, et);
+    }  // generic epilogue (warps 2..5)
     if (et == 0) tc_stamp(p, 6);
   }
   __syncthreads();
@@ -622,7 +654,8 @@ int launch(const TcParams &p0, cudaStream_t st) {
   // resident CTAs per SM: smem and TMEM (2*BN columns each, 512 per SM) permitting
   static int per_sm = 0;
   if (!per_sm) {
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_tc_kernel<BN, STAGES>, TC_THREADS,
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_tc_kernel<BN, STAGES>,
+                                                             tc_threads<BN, STAGES>(),
                                                              S::TOTAL));
     // the 96 KB-ring variants are compiled for 2 CTAs per SM (launch bounds) and two
     // fit in smem (2 x 101 KB of 228 KB); the occupancy query reports 1 for them
@@ -650,7 +683,7 @@ int launch(const TcParams &p0, cudaStream_t st) {
   if (getenv("RN_DEBUG_GRID"))
     fprintf(stderr, "conv_tc<%d,%d> items %lld per_sm %d grid %d smem %d\n", BN, STAGES,
             (long long)p.cls_item0[p.n_cls], per_sm, grid, S::TOTAL);
-  launch_k(conv_tc_kernel<BN, STAGES>, grid, TC_THREADS, S::TOTAL, st, p);
+  launch_k(conv_tc_kernel<BN, STAGES>, grid, tc_threads<BN, STAGES>(), S::TOTAL, st, p);
   LAUNCH_CHECK();
   return grid;
 }
