@@ -378,6 +378,10 @@ int64_t rn_kernel_launches(rn_plan_t plan);
  *                    bucket's units are done (default 1 when replicas > 1; rn_get_grads
  *                    after rn_backward then returns the replica average G of Eq. 11);
  *                    0: one all-reduce per range inside rn_step
+ *  "async_allreduce": 1 ASGD with ring all-reduce (reading F4): step t's
+ *                    gradient is reduced on a comm stream during step t+1 and applied by
+ *                    step t+1's rn_step (w <- w - lr G^{t-1}; the first rn_step applies
+ *                    nothing); double-buffered gradient arrays, CUDA graphs off (default 0)
  * Unknown keys: RN_ERR_ARG.  Every switch changes kernels only, not the result beyond fp32 rounding. */
 rn_status rn_set_option(rn_plan_t plan, const char *key, int64_t value);
 

@@ -661,6 +661,30 @@ def delayed_pipeline_train(net, arrays, batches, lr, unit_stage):
         Q = QW = _identity
 
 
+def async_allreduce_train(net, arrays, batches, lr, m):
+    """ASGD with ring all-reduce ("ASGD ... no need of
+    waiting for the slowest GPU in every iteration"; reading F4 in DESIGN.md):
+    the all-reduce of iteration t's gradients runs while iteration t+1 computes, so
+    the update of iteration t uses the replica-averaged gradient of iteration t-1:
+        G^t = (1/m) sum_r grad of replica r's mean loss on its shard at w^t (Eq. 11)
+        w^{t+1} = w^t - lr G^{t-1},   G^{-1} = 0
+    Every replica applies the same G^{t-1}, so the replicas stay identical.
+    batches[t] = (x, y) of the global batch of iteration t (replica r owns its r-th
+    equal shard).  Returns dict(losses [t][r], params (flat float64))."""
+    cur = [np.asarray(a, dtype=np.float64).copy() for a in arrays]
+    sizes = [int(np.prod(s)) for _, s, _ in net.tensors]
+    offs = np.cumsum([0] + sizes)
+    g_prev = np.zeros(net.n_params)
+    losses = []
+    for x, y in batches:
+        res = net.train_step(cur, x, y, 0.0, m=m)          # G^t at w^t (no update)
+        losses.append(res["losses"])
+        flat = np.concatenate([c.ravel() for c in cur]) - lr * g_prev
+        cur = [flat[offs[i]:offs[i + 1]].reshape(s) for i, (_, s, _) in enumerate(net.tensors)]
+        g_prev = res["grad"]
+    return dict(losses=losses, params=np.concatenate([c.ravel() for c in cur]))
+
+
 def unit_costs(units) -> list:
     """Per-sample MAC cost of each top-level unit (a1; P:366 conv complexity
     O(Co*Ci*T*H*W*Kt*Kh*Kw); light-layer constants BN 2, ReLU/pool/add/mul/

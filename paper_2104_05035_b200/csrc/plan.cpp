@@ -164,6 +164,7 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
   }
   off_master = alloc(sizeof(float) * net.n_params);
   off_grad = alloc(sizeof(float) * net.n_params);
+  off_grad2 = alloc(sizeof(float) * net.n_params);  // the in-flight gradient of ASGD (f4)
   off_run_mean = alloc(sizeof(float) * net.n_bn_channels);
   off_run_var = alloc(sizeof(float) * net.n_bn_channels);
   shadow_f.assign(np, 0);
@@ -309,8 +310,13 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
 
 bool Plan::overlap_ar() const {
   auto it = opts.find("overlap_allreduce");
-  return replicas > 1 && (it == opts.end() || it->second != 0) && stream != nullptr && stream != cudaStreamLegacy &&
-         stream != cudaStreamPerThread;
+  return replicas > 1 && !async_ar() && (it == opts.end() || it->second != 0) && stream != nullptr &&
+         stream != cudaStreamLegacy && stream != cudaStreamPerThread;
+}
+
+bool Plan::async_ar() const {
+  auto it = opts.find("async_allreduce");
+  return it != opts.end() && it->second != 0 && !delayed;
 }
 
 // enqueue bucket bi's all-reduce on the comm stream after everything that writes
@@ -338,6 +344,8 @@ Plan::~Plan() {
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (side) cudaStreamDestroy(side);
   if (comm_st) cudaStreamDestroy(comm_st);
+  for (auto e : ev_async)
+    if (e) cudaEventDestroy(e);
   for (auto e : ar_ev) cudaEventDestroy(e);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
@@ -1061,7 +1069,7 @@ bool Plan::graphs_on() const {
   const bool on = it == opts.end() ? true : it->second != 0;
   // the in-process transport's host rendezvous cannot be captured into a graph
   return on && stream != nullptr && stream != cudaStreamLegacy && stream != cudaStreamPerThread && !timing() &&
-         !nccl_is_local(world_comm) && !delayed;
+         !nccl_is_local(world_comm) && !delayed && !async_ar();  // ASGD swaps gradient arrays per step
 }
 
 void Plan::drop_graphs() {
@@ -1197,6 +1205,24 @@ void Plan::backward_body(const float *x_in, int k_only) {
     CUDA_CHECK(cudaEventRecord(ar_ev.back(), comm_st));
     CUDA_CHECK(cudaStreamWaitEvent(stream, ar_ev.back(), 0));
   }
+  if (async_ar()) {
+    // ASGD: this step's gradient is reduced in the background (not joined here);
+    // the next step's update waits for it
+    if (!comm_st) CUDA_CHECK(cudaStreamCreateWithFlags(&comm_st, cudaStreamNonBlocking));
+    for (auto &e : ev_async)
+      if (!e) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (ar_ev.empty()) {
+      cudaEvent_t e;
+      CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ar_ev.push_back(e);
+    }
+    CUDA_CHECK(cudaEventRecord(ar_ev[0], stream));
+    CUDA_CHECK(cudaStreamWaitEvent(comm_st, ar_ev[0], 0));
+    if (replicas > 1)
+      for (auto &rg : local_ranges())
+        nccl_allreduce_sum_f32(dp_comm, (float *)P(off_grad) + rg.first, (size_t)(rg.second - rg.first), comm_st);
+    CUDA_CHECK(cudaEventRecord(ev_async[async_cur], comm_st));
+  }
 }
 
 // The rank's schedule (host logic only; shared by Plan and rn_plan_describe).
@@ -1270,21 +1296,39 @@ std::vector<std::pair<int64_t, int64_t>> local_param_ranges(const NetModel &net,
 // (bf16 path) updated and repacked into its two bf16 copies in one more launch.
 void Plan::step_body(float lr) {
   auto ranges = local_ranges();
-  if (replicas > 1 && !overlap_ar())  // else reduced during the backward (launch_bucket)
+  const float *gsrc = (const float *)P(off_grad);
+  bool apply = true;
+  const bool as = async_ar();
+  if (as) {
+    // ASGD (reading F4): this update applies the PREVIOUS step's replica-averaged
+    // gradient (off_grad2; its all-reduce ran on comm_st during this step), G^{-1} = 0
+    apply = async_have_prev;
+    if (apply) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_async[async_cur ^ 1], 0));
+    gsrc = (const float *)P(off_grad2);
+  } else if (replicas > 1 && !overlap_ar()) {  // else reduced during the backward (launch_bucket)
     for (auto &rg : ranges)
       nccl_allreduce_sum_f32(dp_comm, (float *)P(off_grad) + rg.first, (size_t)(rg.second - rg.first), stream);
-  int64_t conv_params = 0, all_params = 0;
-  for (const auto &t : net.params)
-    if (local[t.unit]) {
-      all_params += t.numel;
-      if (t.kind == P_CONV) conv_params += t.numel;
-    }
-  // w, g read + w written (fp32), + the bf16 forward and flipped dgrad copies of every conv weight
-  EltTimer tm(this, F_SGD, 12.0 * all_params + (dt == DT_BF16 ? 4.0 * conv_params : 0.0));
-  sgd_ranges((const int64_t *)P(off_sgdrg), n_sgdrg, (float *)P(off_master), (const float *)P(off_grad), lr, stream);
-  if (dt == DT_BF16)
-    sgd_repack_all((const ConvPack *)P(off_pack), n_pack, pack_tiles, (float *)P(off_master),
-                   (const float *)P(off_grad), lr, stream);
+  }
+  if (apply) {
+    int64_t conv_params = 0, all_params = 0;
+    for (const auto &t : net.params)
+      if (local[t.unit]) {
+        all_params += t.numel;
+        if (t.kind == P_CONV) conv_params += t.numel;
+      }
+    // w, g read + w written (fp32), + the bf16 forward and flipped dgrad copies of every conv weight
+    EltTimer tm(this, F_SGD, 12.0 * all_params + (dt == DT_BF16 ? 4.0 * conv_params : 0.0));
+    sgd_ranges((const int64_t *)P(off_sgdrg), n_sgdrg, (float *)P(off_master), gsrc, lr, stream);
+    if (dt == DT_BF16)
+      sgd_repack_all((const ConvPack *)P(off_pack), n_pack, pack_tiles, (float *)P(off_master), gsrc, lr, stream);
+  }
+  if (as) {
+    // the gradient just computed (still reducing on comm_st) becomes the previous one;
+    // the next backward writes the array this update consumed (stream order)
+    std::swap(off_grad, off_grad2);
+    async_cur ^= 1;
+    async_have_prev = true;
+  }
 }
 
 // One iteration t of the delayed-gradient pipeline (reading F1; Eqs.
@@ -1457,6 +1501,7 @@ void Plan::set_params(const float *host) {
 }
 
 void Plan::get_flat(size_t off, float *host) {
+  if (comm_st) CUDA_CHECK(cudaStreamSynchronize(comm_st));  // an ASGD all-reduce may be in flight
   std::vector<float> tmp(net.n_params);
   CUDA_CHECK(cudaStreamSynchronize(stream));
   CUDA_CHECK(cudaMemcpy(tmp.data(), P(off), sizeof(float) * net.n_params, cudaMemcpyDeviceToHost));
@@ -1525,10 +1570,12 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 rn_status Plan::set_option(const std::string &k, int64_t v) {
   if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv" && k != "fused_stats" &&
       k != "pair_conv" && k != "wgrad_stream" && k != "merge_proj" && k != "stem_bwd_fused" &&
-      k != "recompute_mask" && k != "up_bwd_sep" && k != "pair_bwd_stats" && k != "overlap_allreduce")
+      k != "recompute_mask" && k != "up_bwd_sep" && k != "pair_bwd_stats" && k != "overlap_allreduce" &&
+      k != "async_allreduce")
     return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;
+  if (k == "async_allreduce") async_have_prev = false;
   drop_graphs();
   return RN_OK;
 }

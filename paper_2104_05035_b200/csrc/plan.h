@@ -227,6 +227,14 @@ struct Plan {
   std::vector<cudaEvent_t> ar_ev;
   bool overlap_ar() const;
   void launch_bucket(size_t bi);
+  // ASGD with ring all-reduce (reading F4; option async_allreduce): the
+  // all-reduce of step t's gradient runs on comm_st during step t+1, whose update
+  // applies it (double-buffered gradient arrays, swapped every step)
+  size_t off_grad2 = 0;              // the previous step's gradient (reduced on comm_st)
+  bool async_ar() const;
+  bool async_have_prev = false;
+  int async_cur = 0;                  // ev_async[async_cur]: this step's all-reduce
+  cudaEvent_t ev_async[2] = {nullptr, nullptr};
   bool side_on() const;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   float *loss_pinned = nullptr;

@@ -217,3 +217,46 @@ def test_overlapped_bucketed_allreduce_matches_after_backward_allreduce():
                                                              {"overlap_allreduce": ov})))
         for r in range(world):
             assert np.array_equal(outs[0][r]["w"], outs[1][r]["w"])
+
+
+def test_asgd_async_allreduce_vs_oracle():
+    """ASGD with ring all-reduce (reading F4): data parallel,
+    2 replicas, fp32, option async_allreduce -- step t's gradient is reduced on the
+    comm stream during step t+1 and applied there.  Three steps against the oracle's
+    async_allreduce_train at 1e-4 (losses per replica and step, final weights); the
+    replicas' weights stay bit-identical."""
+    dims = (16, 16, 16)
+    desc = rn.net_desc(0, 8, dims)
+    net = O.Net(0, 8, dims)
+    arrays = synthetic.perturb_params(net.tensors, synthetic.init_params(net.tensors, seed=0))
+    flat = np.concatenate([a.ravel() for a in arrays]).astype(np.float32)
+    bs = [synthetic.make_batch(4, *dims, seed=30 + t) for t in range(3)]
+    lr = 1e-2
+    nid = rn.local_transport_id()
+
+    def rank(r):
+        st = torch.cuda.Stream()
+        plan = rn.Plan(desc, 2, rn.RN_F32, rank=r, world=2, n_stages=1, nccl_id=nid, stream=st)
+        plan.set_option("async_allreduce", 1)
+        plan.set_params(flat)
+        losses = []
+        with torch.cuda.stream(st):
+            for x, y in bs:
+                xd = torch.from_numpy(np.ascontiguousarray(x[2 * r:2 * r + 2])).cuda()
+                yd = torch.from_numpy(np.ascontiguousarray(y[2 * r:2 * r + 2])).cuda()
+                losses.append(plan.forward(xd, yd))
+                plan.backward()
+                plan.step(lr)
+            st.synchronize()
+        return dict(losses=losses, w=plan.get_params())
+
+    res = run_ranks(2, rank)
+    ref = O.async_allreduce_train(net, arrays, bs, lr, 2)
+    assert np.array_equal(res[0]["w"], res[1]["w"])
+    for r in range(2):
+        np.testing.assert_allclose(res[r]["losses"], [ls[r] for ls in ref["losses"]], rtol=1e-4)
+    # two applied updates at lr 1e-2: the second gradient is taken at the GPU's own
+    # updated weights, so the fp32 differences of the first step compound -> 1e-3
+    delta = ref["params"] - flat.astype(np.float64)
+    err = np.linalg.norm(res[0]["w"].astype(np.float64) - ref["params"]) / np.linalg.norm(delta)
+    assert update_ok(res[0]["w"], flat, delta, tol=1e-3), err

@@ -114,3 +114,36 @@ def test_two_stages_vs_torch_emulation():
     # the delay matters: plain SGD (S = 1) ends elsewhere
     sgd = O.delayed_pipeline_train(net, arrays, bs, lr, [0] * 4)
     assert np.linalg.norm(sgd["params"] - res["params"]) > 1e-6 * np.linalg.norm(res["params"])
+
+
+def test_async_allreduce_oracle():
+    """f4 (reading F4): lr = 0 keeps the weights; the first iteration applies no
+    update (G^{-1} = 0); against an independent torch emulation (autograd per
+    replica shard, the averaged gradient applied one iteration late)."""
+    net, arrays = setup()
+    bs = [synthetic.make_batch(4, *DIMS, seed=20 + t) for t in range(3)]
+    res0 = O.async_allreduce_train(net, arrays, bs, 0.0, 2)
+    assert np.array_equal(res0["params"], np.concatenate([a.astype(np.float64).ravel() for a in arrays]))
+    res = O.async_allreduce_train(net, arrays, bs[:1], 1e-2, 2)
+    assert np.array_equal(res["params"], res0["params"])            # one iteration: nothing applied yet
+    lr = 1e-2
+    res = O.async_allreduce_train(net, arrays, bs, lr, 2)
+    unit = _torch_units(net)
+    names = [n for n, _, _ in net.tensors]
+    cur = {n: torch.tensor(a, dtype=torch.float64) for n, a in zip(names, arrays)}
+    g_prev = None
+    for x, y in bs:
+        grads = {n: torch.zeros_like(v) for n, v in cur.items()}
+        for r in range(2):
+            P = {n: v.clone().requires_grad_(True) for n, v in cur.items()}
+            h = torch.tensor(x[2 * r:2 * r + 2], dtype=torch.float64)[:, None]
+            for ui in range(len(net.units)):
+                h = unit(ui, h, P)
+            F.cross_entropy(h, torch.tensor(y[2 * r:2 * r + 2], dtype=torch.long)).backward()
+            for n in names:
+                grads[n] += P[n].grad / 2
+        if g_prev is not None:
+            cur = {n: cur[n] - lr * g_prev[n] for n in names}
+        g_prev = grads
+    ref = np.concatenate([cur[n].numpy().ravel() for n in names])
+    np.testing.assert_allclose(res["params"], ref, rtol=1e-9, atol=1e-12)
