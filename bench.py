@@ -188,10 +188,8 @@ def main():
     yd = torch.from_numpy(np.ascontiguousarray(ys)).to(dev)
     lr = 1e-4
 
-    def step():
-        plan.forward(xd, yd, want_loss=False)
-        plan.backward()
-        plan.step(lr)
+    def step():  # rn_train_step: forward + backward + SGD (per-unit early SGD when it applies)
+        plan.train_step(xd, yd, lr)
 
     with torch.cuda.stream(stream):
         for _ in range(a.warmup):

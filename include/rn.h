@@ -348,6 +348,18 @@ rn_status rn_step(rn_plan_t plan, float lr);
 rn_status rn_train_step_host(rn_plan_t plan, const float *x_host, const int32_t *y_host, float lr,
                              float *loss_host);
 
+/* rn_train_step — one training step from DEVICE inputs (x_dev, y_dev as in
+ * rn_forward): forward, backward and SGD with the update rule of rn_step
+ * (w <- w - lr*G).  The result equals rn_forward + rn_backward + rn_step
+ * bit for bit; the call differs only in scheduling: when the plan has one stage,
+ * one micro-batch and no replicas (and option "early_sgd" is not 0), each unit's
+ * update is issued on the weight-gradient stream as soon as that unit's backward
+ * is done and overlaps the backward of the units before it (the update of unit u
+ * reads only u's gradient; no later part of the backward reads u's weights).
+ * Gradients stay readable afterwards (rn_get_grads).  loss_host: optional, as in
+ * rn_forward (a read-back = a synchronisation).  Errors as rn_forward / rn_step. */
+rn_status rn_train_step(rn_plan_t plan, const void *x_dev, const int32_t *y_dev, float lr, float *loss_host);
+
 /* rn_train_steps_host — n_steps training steps from host inputs (x_host[i],
  * y_host[i]: step i's batch, same layout as rn_forward's; pinned memory lets
  * the copies run asynchronously).  The host->device copy of step i+1 runs on a

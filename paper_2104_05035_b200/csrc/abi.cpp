@@ -490,9 +490,19 @@ rn_status rn_train_step_host(rn_plan_t plan, const float *x_host, const int32_t 
   Plan *p = plan->p;
   if (!p->params_set) return set_error(RN_ERR_STATE, "rn_set_params must precede a step");
   p->stage_inputs(x_host, y_host, true);
-  p->forward((const float *)p->P(p->off_x), (const int32_t *)p->P(p->off_y));
-  p->backward((const float *)p->P(p->off_x));
-  p->step(lr);
+  p->train_step((const float *)p->P(p->off_x), (const int32_t *)p->P(p->off_y), lr);
+  return finish_loss(p, loss_host);
+  GUARD_END
+}
+
+rn_status rn_train_step(rn_plan_t plan, const void *x_dev, const int32_t *y_dev, float lr, float *loss_host) {
+  GUARD_BEGIN
+  NEED_BOUND(plan);
+  Plan *p = plan->p;
+  if (!p->params_set) return set_error(RN_ERR_STATE, "rn_set_params must precede a step");
+  p->stage_inputs((const float *)x_dev, y_dev, false);
+  p->train_step((const float *)p->P(p->off_x), (const int32_t *)p->P(p->off_y), lr);
+  p->fwd_done = false;
   return finish_loss(p, loss_host);
   GUARD_END
 }

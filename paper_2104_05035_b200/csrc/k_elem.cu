@@ -2011,8 +2011,9 @@ void repack_conv(DType dt, const float *w, int Co, int taps, int Ci, void *wf, v
 
 constexpr int SGD_MAX_TENSORS = 512;
 
-__global__ void __launch_bounds__(256) sgd_repack_all_k(const ConvPack *__restrict__ tab, int n, int64_t total_tiles,
-                                                        float *master, const float *__restrict__ grad, float lr) {
+__global__ void __launch_bounds__(256) sgd_repack_all_k(const ConvPack *__restrict__ tab, int n, int64_t tile_begin,
+                                                        int64_t total_tiles, float *master,
+                                                        const float *__restrict__ grad, float lr) {
   pdl_begin();
   __shared__ float tile[64][65];
   __shared__ int64_t t0s[SGD_MAX_TENSORS];  // tile0 of every tensor, searched in smem (not L2)
@@ -2022,7 +2023,7 @@ __global__ void __launch_bounds__(256) sgd_repack_all_k(const ConvPack *__restri
   // persistent: blocks stride over the 64x64 (co, ci) tiles of every tap of every conv tensor;
   // a thread owns two consecutive ci of 8 rows: 128-B rows for the fp32 loads and
   // for both bf16 copies (the transposed one through smem)
-  for (int64_t b = blockIdx.x; b < total_tiles; b += gridDim.x) {
+  for (int64_t b = tile_begin + blockIdx.x; b < total_tiles; b += gridDim.x) {
     int lo = 0, hi = n - 1;  // tensor of this tile: binary search on tile0 (uniform across the block)
     while (lo < hi) {
       const int mid = (lo + hi + 1) / 2;
@@ -2132,7 +2133,16 @@ void sgd_repack_all(const ConvPack *table_dev, int n, int64_t total_tiles, float
   if (n <= 0 || total_tiles <= 0) return;
   if (n > SGD_MAX_TENSORS) throw Error(RN_ERR_STATE, "sgd_repack_all: too many conv tensors");
   const unsigned grid = (unsigned)std::min<int64_t>(total_tiles, 148 * 8);
-  launch_k(sgd_repack_all_k, grid, dim3(32, 8), 0, st, table_dev, n, total_tiles, master, grad, lr);
+  launch_k(sgd_repack_all_k, grid, dim3(32, 8), 0, st, table_dev, n, (int64_t)0, total_tiles, master, grad, lr);
+  LAUNCH_CHECK();
+}
+
+void sgd_repack_range(const ConvPack *table_dev, int n, int64_t tile_begin, int64_t tile_end, float *master,
+                      const float *grad, float lr, cudaStream_t st) {
+  if (n <= 0 || tile_end <= tile_begin) return;
+  if (n > SGD_MAX_TENSORS) throw Error(RN_ERR_STATE, "sgd_repack_range: too many conv tensors");
+  const unsigned grid = (unsigned)std::min<int64_t>(tile_end - tile_begin, 148 * 8);
+  launch_k(sgd_repack_all_k, grid, dim3(32, 8), 0, st, table_dev, n, tile_begin, tile_end, master, grad, lr);
   LAUNCH_CHECK();
 }
 

@@ -158,6 +158,10 @@ struct ConvPack {
 };
 void sgd_repack_all(const ConvPack *table_dev, int n, int64_t total_tiles, float *master, const float *grad, float lr,
                     cudaStream_t st);
+// the same over a slice of the table: tiles [tile_begin, tile_end) (absolute tile0
+// numbering) of the n tensors at table_dev
+void sgd_repack_range(const ConvPack *table_dev, int n, int64_t tile_begin, int64_t tile_end, float *master,
+                      const float *grad, float lr, cudaStream_t st);
 // SGD over a device list of (offset, count) ranges, one block per range
 void sgd_ranges(const int64_t *ranges_dev, int n, float *master, const float *grad, float lr, cudaStream_t st);
 void check_finite(const float *v, int n, int *flag, cudaStream_t st);

@@ -348,6 +348,7 @@ Plan::~Plan() {
     if (e) cudaEventDestroy(e);
   for (auto e : ar_ev) cudaEventDestroy(e);
   if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_sgd) cudaEventDestroy(ev_sgd);
   if (ev_join) cudaEventDestroy(ev_join);
   for (int i = 0; i < 2; ++i) {
     if (ev_copied[i]) cudaEventDestroy(ev_copied[i]);
@@ -1073,7 +1074,7 @@ bool Plan::graphs_on() const {
 }
 
 void Plan::drop_graphs() {
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 4; ++i) {
     if (gexec[i]) cudaGraphExecDestroy(gexec[i]);
     gexec[i] = nullptr;
     warm[i] = false;
@@ -1144,6 +1145,59 @@ void Plan::step(float lr) {
   run_phase(2, [&] { step_body(lr); });
 }
 
+// Early SGD (option "early_sgd", default on): the update of unit u depends only on
+// u's own gradient, which is final once u's backward and its weight
+// gradients are done; the next units' backward never reads u's weights.  So in a
+// fused training step each unit's SGD + bf16 repack is issued on the weight-gradient
+// stream right after the unit's backward (ordered after its dgrads by an event and
+// after its wgrads by stream order) and overlaps the backward of the units below it,
+// instead of one launch after the whole backward.  Same kernels, same per-element
+// arithmetic: bitwise the weights of forward / backward / step.  Single stage, one
+// micro-batch, no replica all-reduce (the update must wait for the reduced gradient
+// there), synchronous schedule.
+bool Plan::early_sgd_ok() const {
+  auto it = opts.find("early_sgd");
+  const bool on = it == opts.end() || it->second != 0;
+  return on && unit_tables_ok && side_on() && Mb == 1 && S == 1 && replicas == 1 && !delayed && !async_ar();
+}
+
+void Plan::unit_sgd(int ui, float lr) {
+  if (!side) {
+    CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
+  if (!ev_sgd) CUDA_CHECK(cudaEventCreateWithFlags(&ev_sgd, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventRecord(ev_sgd, stream));  // the unit's dgrads and BN / head gradients are done
+  CUDA_CHECK(cudaStreamWaitEvent(side, ev_sgd, 0));
+  side_used = true;
+  const float *g = (const float *)P(off_grad);
+  if (u_rg1[ui] > u_rg0[ui])
+    sgd_ranges((const int64_t *)P(off_sgdrg) + 2 * u_rg0[ui], u_rg1[ui] - u_rg0[ui], (float *)P(off_master), g, lr,
+               side);
+  if (dt == DT_BF16 && u_pk1[ui] > u_pk0[ui])
+    sgd_repack_range((const ConvPack *)P(off_pack) + u_pk0[ui], u_pk1[ui] - u_pk0[ui], u_t0[ui], u_t1[ui],
+                     (float *)P(off_master), g, lr, side);
+}
+
+void Plan::train_step(const float *x_in, const int32_t *y, float lr) {
+  if (!early_sgd_ok()) {
+    forward(x_in, y);
+    backward(x_in);
+    step(lr);
+    return;
+  }
+  forward(x_in, y);
+  if (lr != graph_lr3) {  // the learning rate is a kernel argument of the captured phase
+    if (gexec[3]) cudaGraphExecDestroy(gexec[3]);
+    gexec[3] = nullptr;
+    warm[3] = false;
+    graph_lr3 = lr;
+  }
+  run_phase(3, [&] { backward_body(x_in, -1, lr); });
+  bwd_ever = true;
+}
+
 void Plan::forward_body(const float *x_in, const int32_t *y, int k_only) {
   if (timing()) ev_used = 0;  // a step's conv events: this forward + its backward (eager launches)
   CUDA_CHECK(cudaMemsetAsync(P(off_loss), 0, sizeof(float), stream));
@@ -1169,7 +1223,7 @@ void Plan::forward_body(const float *x_in, const int32_t *y, int k_only) {
   if (S > 1 && !xfer_external) nccl_bcast_f32(pipe_comm, (float *)P(off_loss), 1, unit_stage[nu - 1], stream);
 }
 
-void Plan::backward_body(const float *x_in, int k_only) {
+void Plan::backward_body(const float *x_in, int k_only, float early_lr) {
   CUDA_CHECK(cudaMemsetAsync(P(off_grad), 0, sizeof(float) * net.n_params, stream));
   const int nu = (int)net.units.size();
   const bool ov = overlap_ar();
@@ -1191,6 +1245,7 @@ void Plan::backward_body(const float *x_in, int k_only) {
         const Unit &pu = net.units[ui - 1];
         nccl_send_bytes(pipe_comm, P(units[ui].send_dx), act_bytes(pu.cout, pu.out), unit_stage[ui - 1], stream);
       }
+      if (early_lr >= 0.f && k == k1 - 1) unit_sgd(ui, early_lr);
       // last micro-batch: a bucket whose units are all done is reduced while the
       // backward of the earlier units continues (P:284 ring all-reduce, Eq. 11)
       if (ov && k == k1 - 1 && bi < buckets.size() && ui == buckets[bi].ulo) launch_bucket(bi++);
@@ -1429,9 +1484,23 @@ void Plan::bind(void *dev, size_t bytes) {
   std::vector<ConvPack> packs;
   std::vector<int64_t> rg;
   int64_t tiles = 0;
+  const int nu = (int)net.units.size();
+  u_pk0.assign(nu, 0); u_pk1.assign(nu, 0); u_rg0.assign(nu, 0); u_rg1.assign(nu, 0);
+  u_t0.assign(nu, 0); u_t1.assign(nu, 0);
+  std::vector<int> seen(nu, 0);
+  unit_tables_ok = true;
+  int last_unit = -1;
   for (int i = 0; i < (int)net.params.size(); ++i) {
     const ParamTensor &t = net.params[i];
     if (!local[t.unit]) continue;
+    if (t.unit != last_unit) {  // a unit's tensors must be contiguous for its table slices
+      if (seen[t.unit]) unit_tables_ok = false;
+      seen[t.unit] = 1;
+      u_pk0[t.unit] = u_pk1[t.unit] = (int)packs.size();
+      u_t0[t.unit] = u_t1[t.unit] = tiles;
+      u_rg0[t.unit] = u_rg1[t.unit] = (int)rg.size() / 2;
+      last_unit = t.unit;
+    }
     if (t.kind == P_CONV && dt == DT_BF16) {
       ConvPack c;
       c.off = t.canon_off;
@@ -1445,12 +1514,16 @@ void Plan::bind(void *dev, size_t bytes) {
       tiles += (int64_t)c.taps * ((c.Co + 63) / 64) * ((c.Ci + 63) / 64);  // 64x64 tiles (sgd_repack_all_k)
       packs.push_back(c);
     } else {
-      if (!rg.empty() && rg.back() == t.canon_off) rg.back() = t.canon_off + t.numel;
+      // adjacent tensors of one unit share a range (not across units: per-unit slices)
+      if ((int)rg.size() / 2 > u_rg0[t.unit] && rg.back() == t.canon_off) rg.back() = t.canon_off + t.numel;
       else {
         rg.push_back(t.canon_off);
         rg.push_back(t.canon_off + t.numel);
       }
     }
+    u_pk1[t.unit] = (int)packs.size();
+    u_t1[t.unit] = tiles;
+    u_rg1[t.unit] = (int)rg.size() / 2;
   }
   n_pack = (int)packs.size();
   pack_tiles = tiles;
@@ -1550,9 +1623,7 @@ void Plan::train_steps_host(const float *const *x_host, const int32_t *const *y_
     if (hy) CUDA_CHECK(cudaMemcpyAsync(P(off_y), slot + yoff, sizeof(int32_t) * (size_t)b, cudaMemcpyDeviceToDevice,
                                        stream));
     CUDA_CHECK(cudaEventRecord(ev_free[i % 2], stream));
-    forward((const float *)P(off_x), (const int32_t *)P(off_y));
-    backward((const float *)P(off_x));
-    step(lr);
+    train_step((const float *)P(off_x), (const int32_t *)P(off_y), lr);
     CUDA_CHECK(cudaMemcpyAsync(loss_pinned + i, P(off_loss), sizeof(float), cudaMemcpyDeviceToHost, stream));
   }
   CUDA_CHECK(cudaStreamSynchronize(stream));

@@ -244,13 +244,24 @@ struct Plan {
   void backward(const float *x_in);
   void step(float lr);
   void forward_body(const float *x_in, const int32_t *y, int k_only = -1);
-  void backward_body(const float *x_in, int k_only = -1);
+  void backward_body(const float *x_in, int k_only = -1, float early_lr = -1.f);
   void step_body(float lr);
-  // CUDA graphs per phase (0 forward, 1 backward, 2 step)
-  cudaGraphExec_t gexec[3] = {nullptr, nullptr, nullptr};
-  bool warm[3] = {false, false, false};
-  int graph_kernels[3] = {0, 0, 0};
-  float graph_lr = -1.f;
+  // fused training step (rn_train_step): with early SGD each unit's update runs on
+  // the weight-gradient stream as soon as its backward is done (early_sgd_ok())
+  void train_step(const float *x_in, const int32_t *y, float lr);
+  bool early_sgd_ok() const;
+  void unit_sgd(int ui, float lr);
+  // per-unit slices of the optimizer tables (bind): conv packs [pk0, pk1) with tiles
+  // [t0, t1), plain SGD ranges [rg0, rg1)
+  std::vector<int> u_pk0, u_pk1, u_rg0, u_rg1;
+  std::vector<int64_t> u_t0, u_t1;
+  bool unit_tables_ok = false;
+  cudaEvent_t ev_sgd = nullptr;
+  // CUDA graphs per phase (0 forward, 1 backward, 2 step, 3 backward + early SGD)
+  cudaGraphExec_t gexec[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool warm[4] = {false, false, false, false};
+  int graph_kernels[4] = {0, 0, 0, 0};
+  float graph_lr = -1.f, graph_lr3 = -1.f;
   bool graphs_on() const;
   void drop_graphs();
   void run_phase(int ph, const std::function<void()> &body);

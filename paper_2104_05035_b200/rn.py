@@ -17,7 +17,7 @@ STATUS = {0: "RN_OK", 1: "RN_ERR_ARG", 2: "RN_ERR_SCHEMA", 3: "RN_ERR_INFEASIBLE
           5: "RN_ERR_CUDA", 6: "RN_ERR_NCCL", 7: "RN_ERR_STATE", 8: "RN_ERR_SIZE"}
 EXPORTS = ["rn_ga_default", "rn_gabra_place", "rn_gabra_place_slack", "rn_simulate_step", "rn_contiguous_split", "rn_net_units", "rn_net_param_count", "rn_net_param_info",
            "rn_nccl_unique_id", "rn_plan", "rn_plan_delayed", "rn_delayed_step", "rn_plan_describe", "rn_plan_bind", "rn_set_params", "rn_get_params", "rn_get_grads",
-           "rn_get_bn_running", "rn_get_activation", "rn_get_unit_grad", "rn_get_saved", "rn_forward", "rn_backward", "rn_step", "rn_train_step_host",
+           "rn_get_bn_running", "rn_get_activation", "rn_get_unit_grad", "rn_get_saved", "rn_forward", "rn_backward", "rn_step", "rn_train_step", "rn_train_step_host",
            "rn_train_steps_host", "rn_gradcam",
            "rn_kernel_launches", "rn_set_option", "rn_query", "rn_op_conv3d", "rn_plan_destroy", "rn_last_error"]
 
@@ -286,6 +286,13 @@ class Plan:
 
     def step(self, lr: float):
         _check(lib().rn_step(self.h, C.c_float(lr)))
+
+    def train_step(self, x_dev, y_dev, lr: float, want_loss=False):
+        """rn_train_step: forward + backward + SGD from device inputs (early per-unit SGD)."""
+        loss = C.c_float()
+        _check(lib().rn_train_step(self.h, C.c_void_p(x_dev.data_ptr()), C.c_void_p(y_dev.data_ptr()),
+                                   C.c_float(lr), C.byref(loss) if want_loss else None))
+        return loss.value if want_loss else None
 
     def train_step_host(self, x_host: np.ndarray, y_host: np.ndarray, lr: float) -> float:
         loss = C.c_float()
