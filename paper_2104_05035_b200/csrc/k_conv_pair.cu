@@ -69,7 +69,19 @@ struct __align__(64) PairParams {
   const bf16 *res, *res_mask;
   EpiStats st;
   int res_pf;  // prefetch the residual operands (RN_PAIR_RES_PF=0 turns it off for A/B)
+  unsigned long long *trace;  // debug (RN_PAIR_TRACE): [cta][32] %globaltimer stamps
 };
+
+// trace slots: 0 entry, 1 after setup + dependency wait, 2 weights resident (MMA
+// warp), 4+2i / 5+2i first / last MMA issue of item i, 16+2i / 17+2i epilogue of
+// item i (accumulator acquired / done), 31 exit
+__device__ __forceinline__ void pair_stamp(const PairParams &p, int k) {
+  if (p.trace && k < 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[blockIdx.x * 32 + k] = t;
+  }
+}
 
 struct Item {
   int n, td, th, tw;
@@ -101,6 +113,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = tc::cluster_ctarank();
   const int pair = blockIdx.x / 2, n_pairs = gridDim.x / 2;
+  if (threadIdx.x == 0) pair_stamp(p, 0);
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 4; ++i) {
@@ -122,6 +135,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_begin();
+  if (threadIdx.x == 0) pair_stamp(p, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -150,11 +164,13 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
       const uint64_t dB0 = tc::smem_desc(tc::smem_u32(sB), 16, 1024, 2);
       tc::mbar_wait_cluster(b_full, 0);
       tc::tc_fence_after();
+      if (lane == 0) pair_stamp(p, 2);
       int local = 0;
       for (int pk = pair; pk < p.n_pair_items; pk += n_pairs, ++local) {
         const int acc = local & 1;
         tc::mbar_wait_cluster(&t_empty[acc], ((local >> 1) & 1) ^ 1);
         tc::tc_fence_after();
+        bool first = true;
         for (int sl = 0; sl < 2; ++sl) {
           for (int kd = 0; kd < 3; ++kd) {
             const int pl = sl + kd;
@@ -162,6 +178,8 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
               tc::mbar_wait_cluster(&a_full[pl], local & 1);
               tc::tc_fence_after();
             }
+            if (first && lane == 0 && local < 6) pair_stamp(p, 4 + 2 * local);
+            first = false;
             const uint64_t dAp = dA0 + (uint32_t)(pl * PLANE_SLOT >> 4);
             const uint32_t dtm = tmem_base + acc * 128 + sl * 64;
 #pragma unroll
@@ -182,6 +200,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
           }
         }
         tc::mma_commit_pair(&t_full[acc], 3);
+        if (lane == 0 && local < 6) pair_stamp(p, 5 + 2 * local);
         __syncwarp();
       }
     }
@@ -227,6 +246,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
       prefetch(chunk_valid(0), chunk_base(0), pf_cur);
       tc::mbar_wait(&t_full[acc], (local >> 1) & 1);
       tc::tc_fence_after();
+      if (et == 0 && local < 6) pair_stamp(p, 16 + 2 * local);
 #pragma unroll 1
       for (int sl = 0; sl < 2; ++sl) {
         const bool valid = chunk_valid(sl);
@@ -286,11 +306,13 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_cluster(acc ? te1 : te0);  // the leader's accumulator-free barrier
+      if (et == 0 && local < 6) pair_stamp(p, 17 + 2 * local);
     }
     if (p.st.mode) epi_stats_flush(p.st, red, 64, 64, et);
   }
   tc::tc_fence_before();
   tc::cluster_sync();  // no CTA leaves while its pair may still read its smem / TMEM
+  if (threadIdx.x == 0) pair_stamp(p, 31);
   if (warp == 1) {
     tc::tc_fence_after();
     tc::tmem_dealloc_pair<256>(tmem_base);
@@ -298,6 +320,10 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
 }
 
 }  // namespace
+
+unsigned long long *g_pair_trace = nullptr;
+int g_pair_trace_n = 0;
+int g_pair_meta[64][4];
 
 bool pair_conv_supported(const ConvGeom &g, bool dgrad) { return halo_conv_supported(g, dgrad); }
 
@@ -327,6 +353,16 @@ int conv_pair(const ConvGeom &g, bool dgrad, const bf16 *src, const bf16 *w, con
   p.res_pf = !(getenv("RN_PAIR_RES_PF") && atoi(getenv("RN_PAIR_RES_PF")) == 0);
   p.res_mask = res_mask;
   if (est && est->mode) p.st = *est;
+  if (getenv("RN_PAIR_TRACE") && g_pair_trace_n < 64) {
+    if (!g_pair_trace) CUDA_CHECK(cudaMalloc(&g_pair_trace, sizeof(unsigned long long) * 64 * 148 * 32));
+    CUDA_CHECK(cudaMemsetAsync(g_pair_trace + (size_t)g_pair_trace_n * 148 * 32, 0, sizeof(unsigned long long) * 148 * 32, st));
+    p.trace = g_pair_trace + (size_t)g_pair_trace_n * 148 * 32;
+    g_pair_meta[g_pair_trace_n][0] = dgrad;
+    g_pair_meta[g_pair_trace_n][1] = res != nullptr;
+    g_pair_meta[g_pair_trace_n][2] = p.st.mode;
+    g_pair_meta[g_pair_trace_n][3] = p.n_pair_items;
+    ++g_pair_trace_n;
+  }
   static uint64_t attr_devs = 0;  // kernel attributes are per device
   if (!once_on_device(attr_devs)) {
     CUDA_CHECK(cudaFuncSetAttribute(conv_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -355,3 +391,15 @@ int conv_pair(const ConvGeom &g, bool dgrad, const bf16 *src, const bf16 *w, con
 }
 
 }  // namespace rn
+
+// debug: copy the RN_PAIR_TRACE stamps of the first launches (148 CTAs x 32 slots each)
+extern "C" int rn_dbg_pair_trace(unsigned long long *host, int max_launches, int *meta) {
+  using namespace rn;
+  const int n = std::min(g_pair_trace_n, max_launches);
+  if (n > 0 && g_pair_trace) {
+    cudaDeviceSynchronize();
+    cudaMemcpy(host, g_pair_trace, sizeof(unsigned long long) * (size_t)n * 148 * 32, cudaMemcpyDeviceToHost);
+    memcpy(meta, g_pair_meta, sizeof(int) * 4 * n);
+  }
+  return n;
+}
