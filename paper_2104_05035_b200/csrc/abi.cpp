@@ -544,7 +544,7 @@ rn_status rn_query(rn_plan_t plan, const char *key, double *value) {
 rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const void *a_dev, const void *b_dev,
                        void *out_dev, int32_t impl, void *stream) {
   GUARD_BEGIN
-  if (!geom || !a_dev || !b_dev || !out_dev || op < 0 || op > 2 || impl < 0 || impl > 4 ||
+  if (!geom || !a_dev || !b_dev || !out_dev || op < 0 || op > 2 || impl < 0 || impl > 5 ||
       (dtype != RN_F32 && dtype != RN_BF16))
     return set_error(RN_ERR_ARG, "rn_op_conv3d: bad arguments");
   ConvGeom g;
@@ -556,7 +556,12 @@ rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const voi
   cudaStream_t st = (cudaStream_t)stream;
   const DType dt = dtype == RN_BF16 ? DT_BF16 : DT_F32;
   const bool tc_ok = dt == DT_BF16 && (op == 2 ? tc_wgrad_supported(g) : tc_conv_supported(g, op == 1));
-  if (impl == 2 && !tc_ok) return set_error(RN_ERR_ARG, "rn_op_conv3d: tcgen05 kernel does not take this conv");
+  if ((impl == 2 || impl == 5) && !tc_ok) return set_error(RN_ERR_ARG, "rn_op_conv3d: tcgen05 kernel does not take this conv");
+  if (impl == 5 && op == 2) return set_error(RN_ERR_ARG, "rn_op_conv3d: impl 5 is fprop / dgrad only");
+  struct PairForce {  // impl 2: single-CTA persistent kernel; 5: on CTA pairs where it applies
+    explicit PairForce(int m) { tc_pair_force(m); }
+    ~PairForce() { tc_pair_force(-1); }
+  } pair_force(impl == 2 ? 0 : impl == 5 ? 1 : -1);
   const bool tc = tc_ok && impl != 1;
   const bool halo_ok = dt == DT_BF16 && op != 2 && halo_conv_supported(g, op == 1);
   if (impl == 3 && !halo_ok) return set_error(RN_ERR_ARG, "rn_op_conv3d: haloed kernel does not take this conv");

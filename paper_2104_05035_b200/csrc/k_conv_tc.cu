@@ -50,9 +50,9 @@ constexpr int TC_THREADS = 192;
 // once their loops are done (two warps per TMEM lane quarter, columns split; the
 // 4-warp epilogue was latency-bound, one warp per scheduler).  8 warps keep the
 // 255-register budget (10 would cap it at 168: 3 warps on one 16 K-register SMSP)
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool PAIR = false>
 constexpr int tc_threads() {
-  return (STAGES * (128 * 128 + BN * 128) > 110 * 1024) ? 256 : TC_THREADS;
+  return (!PAIR && STAGES * (128 * 128 + BN * 128) > 110 * 1024) ? 256 : TC_THREADS;
 }
 constexpr bool kPdlLate = true;  // explicit late PDL trigger (after the last MMA issue)
 
@@ -97,6 +97,16 @@ struct __align__(64) TcParams {
   int64_t n_view_vox;
   EpiStats st;  // fused BN statistics of the stored output (needs !use_part, t_nblk == 1)
   unsigned long long *trace;  // debug (RN_TC_TRACE): per-CTA %globaltimer stamps [grid][8]
+  // CTA pairs (cta_group::2, one-class launches): a cluster of 2 CTAs runs M-tiles
+  // 2j and 2j+1 of the same (N-block, split) as ONE M=256 MMA; each CTA streams its
+  // own A tile and HALF of the B tile (BN/2 output channels), so the per-SM smem
+  // traffic per FLOP drops (operand reads + TMA fills: the stage-2/3 bound).
+  // Work items count pairs; n_mt = M-tiles (an odd last pair has an empty half).
+  int pair;
+  int64_t n_mt;
+  const bf16 *w_base;  // host: weights behind b_map (re-encoded with a BN/2 box for pairs)
+  int w_rows;
+  int64_t w_ktot;
   // TMA-store epilogue (launches whose CTAs own at most one work item): the tile is
   // staged in the (then idle) smem ring, SW128-swizzled, and written by
   // cp.async.bulk.tensor -- coalesced, instead of one 16-B store per row per thread.
@@ -124,10 +134,10 @@ __device__ __forceinline__ void tc_stamp(const TcParams &p, int k) {
   }
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool PAIR = false>
 struct Smem {
-  static constexpr int A_BYTES = 128 * 128;      // 128 rows x 64 bf16
-  static constexpr int B_BYTES = BN * 128;       // BN rows x 64 bf16
+  static constexpr int A_BYTES = 128 * 128;                  // 128 rows x 64 bf16
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * 128;  // BN (pair: BN/2) rows x 64 bf16
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int RED_OFF = STAGES * STAGE;   // [4 warps][2][BN] fp32 BN-statistics accumulators
   static constexpr int BAR_OFF = RED_OFF + 4 * 2 * BN * 4;
@@ -145,7 +155,7 @@ struct __align__(16) TapEnt {
   int16_t od, oh, ow, pad;
   int kcoord;
 };
-__device__ __forceinline__ Item decode_item(const TcParams &p, int64_t item) {
+__device__ __forceinline__ Item decode_item(const TcParams &p, int64_t item, int rank = 0) {
   Item it;
   int c = 0;
   while (c + 1 < p.n_cls && item >= p.cls_item0[c + 1]) ++c;
@@ -154,6 +164,7 @@ __device__ __forceinline__ Item decode_item(const TcParams &p, int64_t item) {
   const int ks = p.cls_ks[c];
   it.split = (int)(r % ks); r /= ks;
   it.nb = (int)(r % p.t_nblk); r /= p.t_nblk;
+  if (p.pair) r = 2 * r + rank;  // this CTA's M-tile of the pair (>= n_mt: empty half, tn out of range)
   it.tw = (int)(r % p.tw); r /= p.tw;
   it.th = (int)(r % p.th); r /= p.th;
   it.td = (int)(r % p.td); r /= p.td;
@@ -165,10 +176,11 @@ __device__ __forceinline__ Item decode_item(const TcParams &p, int64_t item) {
 }
 
 // deep-ring variants (one CTA per SM by smem) get the whole register file: no spills
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, STAGES>::STAGE > 110 * 1024) ? 1 : 2)
+template <int BN, int STAGES, bool PAIR = false>
+__global__ void __launch_bounds__(tc_threads<BN, STAGES, PAIR>(),
+                                  (STAGES * Smem<BN, STAGES, PAIR>::STAGE > 110 * 1024) ? 1 : 2)
     conv_tc_kernel(const __grid_constant__ TcParams p) {
-  using S = Smem<BN, STAGES>;
+  using S = Smem<BN, STAGES, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t *full = (uint64_t *)(smem + S::BAR_OFF);
@@ -179,6 +191,10 @@ __global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, S
   TapEnt *tab = (TapEnt *)(smem + S::TAB_OFF);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // pairs: rank in the cluster (0 = leader: issues the pair MMAs, owns the full /
+  // tempty barriers both CTAs count on); the pair's item stream is blockIdx / 2
+  const int rank = PAIR ? (int)tc::cluster_ctarank() : 0;
+  const int64_t wid = PAIR ? blockIdx.x / 2 : blockIdx.x, wstride = PAIR ? gridDim.x / 2 : gridDim.x;
   if (threadIdx.x == 0) tc_stamp(p, 0);
   if (warp == 0 && lane < p.n_taps) {
     TapEnt e;
@@ -198,7 +214,7 @@ __global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, S
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&tfull[i], 1);
-      tc::mbar_init(&tempty[i], 4);
+      tc::mbar_init(&tempty[i], PAIR ? 8 : 4);  // epilogue warps (of both CTAs of a pair)
     }
     tc::mbar_init(&tempty[2], 1);
     tc::fence_barrier_init();
@@ -208,9 +224,13 @@ __global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, S
     for (int i = 0; i < p.n_taps; ++i)
       if (p.tap_bsel[i]) { tc::tma_prefetch(&p.b_map2); break; }
   }
-  if (warp == 1) tc::tmem_alloc<TMEM_COLS>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (PAIR) tc::tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+    else tc::tmem_alloc<TMEM_COLS>(tmem_slot);
+  }
   tc::tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) tc::cluster_sync();  // both CTAs' barriers initialised, TMEM allocated
+  else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_begin();  // prologue above overlaps the predecessor's tail
@@ -223,8 +243,8 @@ __global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, S
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const Item it = decode_item(p, item);
+      for (int64_t item = wid; item < n_items; item += wstride) {
+        const Item it = decode_item(p, item, rank);
         const int w0 = it.tw * p.bw, h0 = it.th * p.bh, d0 = it.td * p.bd, n0 = it.tn * p.bn;
         const int nb = it.nb;
         const int tap0 = p.cls_tap0[it.c], kpt = p.kblocks_per_tap;
@@ -234,10 +254,18 @@ __global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, S
           tc::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * S::STAGE;
           uint8_t *sb = sa + S::A_BYTES;
-          tc::mbar_arrive_expect_tx(&full[stage], S::STAGE);
-          if (kb == it.kb0 && item == blockIdx.x) tc_stamp(p, 2);
-          tc::tma_load_5d(sa, e.amap, &full[stage], cb * 64, w0 + e.ow, h0 + e.oh, d0 + e.od, n0);
-          tc::tma_load_2d(sb, e.bmap, &full[stage], e.kcoord + cb * 64, nb * BN);
+          if (kb == it.kb0 && item == wid) tc_stamp(p, 2);
+          if constexpr (PAIR) {
+            // both CTAs' bytes land on the leader's full barrier
+            const uint32_t fb = tc::mapa(tc::smem_u32(&full[stage]), 0);
+            if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE);
+            tc::tma_load_5d_pair(sa, e.amap, fb, cb * 64, w0 + e.ow, h0 + e.oh, d0 + e.od, n0);
+            tc::tma_load_2d_pair(sb, e.bmap, fb, e.kcoord + cb * 64, nb * BN + rank * (BN / 2));
+          } else {
+            tc::mbar_arrive_expect_tx(&full[stage], S::STAGE);
+            tc::tma_load_5d(sa, e.amap, &full[stage], cb * 64, w0 + e.ow, h0 + e.oh, d0 + e.od, n0);
+            tc::tma_load_2d(sb, e.bmap, &full[stage], e.kcoord + cb * 64, nb * BN);
+          }
           if (++cb == kpt) { cb = 0; ++t; }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -247,44 +275,53 @@ __global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, S
     // ---------------- MMA issuer ----------------
     // descriptors precomputed: stage s, k-step k = base + (s * STAGE + 32 k) >> 4
     // (the issue loop must sustain one MMA per 32-64 tensor cycles)
-    constexpr uint32_t IDESC = tc::idesc_bf16(128, BN);
+    constexpr uint32_t IDESC = tc::idesc_bf16(PAIR ? 256 : 128, BN);
     const uint64_t dA0 = tc::smem_desc(tc::smem_u32(smem), 16, 1024, 2);
     const uint64_t dB0 = tc::smem_desc(tc::smem_u32(smem) + S::A_BYTES, 16, 1024, 2);
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
-      const Item it = decode_item(p, item);
-      const int kb0 = it.kb0, kb1 = it.kb1;
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc::tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      uint32_t accum = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        tc::mbar_wait(&full[stage], phase);
+    if (!PAIR || rank == 0)  // pairs: the leader issues for both CTAs
+      for (int64_t item = wid; item < n_items; item += wstride, ++local) {
+        const Item it = decode_item(p, item, rank);
+        const int kb0 = it.kb0, kb1 = it.kb1;
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        if constexpr (PAIR) tc::mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+        else tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc::tc_fence_after();
-        if (local == 0 && kb == kb0 && lane == 0) tc_stamp(p, 3);
-        const uint32_t soff = (uint32_t)(stage * S::STAGE) >> 4;
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        uint32_t accum = 0;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          if constexpr (PAIR) tc::mbar_wait_cluster(&full[stage], phase);
+          else tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          if (local == 0 && kb == kb0 && lane == 0) tc_stamp(p, 3);
+          const uint32_t soff = (uint32_t)(stage * S::STAGE) >> 4;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          tc::mma_bf16_warp(d_tmem, dA0 + soff + 2 * k, dB0 + soff + 2 * k, IDESC, accum);
-          accum = 1;
+          for (int k = 0; k < 4; ++k) {
+            if constexpr (PAIR) tc::mma_bf16_pair(d_tmem, dA0 + soff + 2 * k, dB0 + soff + 2 * k, IDESC, accum);
+            else tc::mma_bf16_warp(d_tmem, dA0 + soff + 2 * k, dB0 + soff + 2 * k, IDESC, accum);
+            accum = 1;
+          }
+          if constexpr (PAIR) {
+            tc::mma_commit_pair(&empty[stage], 3);  // both producers' stage is free
+            if (kb == kb1 - 1) tc::mma_commit_pair(&tfull[acc], 3);
+          } else {
+            tc::mma_commit_warp(&empty[stage]);
+            if (kb == kb1 - 1) tc::mma_commit_warp(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc::mma_commit_warp(&empty[stage]);
-        if (kb == kb1 - 1) tc::mma_commit_warp(&tfull[acc]);
-        __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-    }
     // every MMA of this CTA is issued: the dependent grid may start launching
     // (persistent grid: no later wave of this kernel to be displaced)
     if (lane == 0) tc_stamp(p, 4);
     if (kPdlLate) pdl_trigger();
   }
-  const bool direct = p.tma_st == 1 && (int64_t)blockIdx.x < n_items;
-  constexpr bool ALLW = tc_threads<BN, STAGES>() == 256;
+  const bool direct = p.tma_st == 1 && wid < n_items;
+  constexpr bool ALLW = tc_threads<BN, STAGES, PAIR>() == 256;
   if ((direct && ALLW) || (warp >= 2 && warp < 6)) {
     // ---------------- epilogue (warps 2..5; every warp in the 8-warp direct epilogue) ----------------
     __syncwarp();
@@ -304,7 +341,7 @@ __global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, S
       const int NH = NEPI / 128;                        // warps per TMEM lane quarter
       const int half = ALLW ? warp / 4 : 0;             // this warp's column slice
       const int cbeg = half * (BN / NH), cend = cbeg + BN / NH;
-      const Item it = decode_item(p, blockIdx.x);
+      const Item it = decode_item(p, wid, rank);
       const int nb = it.nb;
       const int w0 = it.tw * p.bw, h0 = it.th * p.bh, d0 = it.td * p.bd, n0 = it.tn * p.bn;
       constexpr int NCH = BN / 64, TB = 128 * BN * 2;
@@ -373,7 +410,7 @@ __global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, S
       tc::tc_fence_before();
       tc::fence_proxy_async();
       asm volatile("bar.sync 1, %0;" ::"r"(NEPI) : "memory");
-      if (et == 0) {
+      if (et == 0 && n0 < p.ON) {  // (the empty half of an odd last pair stores nothing)
         for (int j = 0; j < NCH; ++j) tc::tma_store_5d(&p.y_map, s_out + j * 16384, nb * BN + j * 64, w0, h0, d0, n0);
         tc::bulk_commit();
       }
@@ -424,8 +461,8 @@ __global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, S
       if (et == 0) tc::bulk_wait0();
     } else {
     int local = 0;
-    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x, ++local) {
-      const Item it = decode_item(p, item);
+    for (int64_t item = wid; item < n_items; item += wstride, ++local) {
+      const Item it = decode_item(p, item, rank);
       const int split = it.split, nb = it.nb, c = it.c;
       const int ow = it.tw * p.bw + wx, oh = it.th * p.bh + hy, od = it.td * p.bd + dz, on = it.tn * p.bn + nz;
       const bool valid = ow < p.cls_OW[c] && oh < p.cls_OH[c] && od < p.cls_OD[c] && on < p.ON;
@@ -514,14 +551,18 @@ __global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, S
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR) tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(&tempty[acc]), 0));  // the leader's
+        else tc::mbar_arrive(&tempty[acc]);
+      }
       if (p.tma_st == 2) {
         // every row of the tile is staged: make the generic-proxy smem writes visible
         // to the async proxy, then one thread writes the tile with TMA
         tc::fence_proxy_async();
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (et == 0) {
-          const int w0 = it.tw * p.bw, h0 = it.th * p.bh, d0 = it.td * p.bd, n0 = it.tn * p.bn;
+        const int n0 = it.tn * p.bn;
+        if (et == 0 && n0 < p.ON) {  // (an empty pair half must not write into the next split's rows)
+          const int w0 = it.tw * p.bw, h0 = it.th * p.bh, d0 = it.td * p.bd;
           for (int j = 0; j < BN / 32; ++j)
             tc::tma_store_5d(&p.part_map, smem + j * 16384, nb * BN + j * 32, w0, h0, d0, split * p.ON + n0);
           tc::bulk_commit();
@@ -533,11 +574,14 @@ __global__ void __launch_bounds__(tc_threads<BN, STAGES>(), (STAGES * Smem<BN, S
     }  // generic epilogue (warps 2..5)
     if (et == 0) tc_stamp(p, 6);
   }
-  __syncthreads();
+  tc::tc_fence_before();
+  if constexpr (PAIR) tc::cluster_sync();  // no CTA leaves while the pair's MMAs may read its smem / TMEM
+  else __syncthreads();
   if (threadIdx.x == 0) tc_stamp(p, 7);
   if (warp == 1) {
     tc::tc_fence_after();
-    tc::tmem_dealloc<TMEM_COLS>(tmem_base);
+    if constexpr (PAIR) tc::tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+    else tc::tmem_dealloc<TMEM_COLS>(tmem_base);
   }
 }
 
@@ -625,6 +669,12 @@ void choose_box(int W, int H, int D, int N, int &bw, int &bh, int &bd, int &bn) 
       }
 }
 
+thread_local int g_pair_force = -1;  // rn_op_conv3d impl 2 / 5 (kernel tests)
+int tc_pair_mode() {  // RN_TC_PAIR: 0 off, 1 every eligible launch, 2 (default) launches without split-K
+  static const int m = getenv("RN_TC_PAIR") ? atoi(getenv("RN_TC_PAIR")) : 2;
+  return g_pair_force >= 0 ? g_pair_force : m;
+}
+
 bool tma_store_off() {
   static const bool off = getenv("RN_TC_TMA_STORE") && atoi(getenv("RN_TC_TMA_STORE")) == 0;
   return off;
@@ -684,6 +734,56 @@ int launch(const TcParams &p0, cudaStream_t st) {
     fprintf(stderr, "conv_tc<%d,%d> items %lld per_sm %d grid %d smem %d\n", BN, STAGES,
             (long long)p.cls_item0[p.n_cls], per_sm, grid, S::TOTAL);
   launch_k(conv_tc_kernel<BN, STAGES>, grid, tc_threads<BN, STAGES>(), S::TOTAL, st, p);
+  LAUNCH_CHECK();
+  return grid;
+}
+
+// CTA-pair launch (cluster of 2, cta_group::2): one pair per 2 SMs, persistent over
+// the pair items; a pair's two CTAs own M-tiles 2j, 2j+1 of the same (N-block, split)
+template <int BN, int STAGES>
+int launch_pair(const TcParams &p0, cudaStream_t st) {
+  TcParams p = p0;
+  p.trace = nullptr;
+  using S = Smem<BN, STAGES, true>;
+  static uint64_t attr_devs = 0;
+  if (!once_on_device(attr_devs)) {
+    CUDA_CHECK(cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    S::TOTAL));
+    CUDA_CHECK(cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES, true>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t items = p.cls_item0[1];
+  const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(items, sms / 2));
+  const int grid = 2 * pairs;
+  const int stg_bytes = p.use_part ? 128 * BN * 4 : tma_epi_bytes(BN, p.res != nullptr, p.st.mode);
+  p.tma_st = (p.tma_ok && items <= pairs && stg_bytes <= STAGES * S::STAGE && !tma_store_off())
+                 ? (p.use_part ? 2 : 1)
+                 : 0;
+  if (getenv("RN_TC_TRACE") && g_trace_n < 256) {
+    if (!g_trace) CUDA_CHECK(cudaMalloc(&g_trace, sizeof(unsigned long long) * 256 * 296 * 8));
+    p.trace = g_trace + (size_t)g_trace_n * 296 * 8;
+    int *m = g_trace_meta[g_trace_n++];
+    m[0] = BN; m[1] = -STAGES; m[2] = grid; m[3] = (int)items; m[4] = p.ksplit; m[5] = p.n_cls;
+    m[6] = p.use_part; m[7] = p.n_taps * p.kblocks_per_tap;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(tc_threads<BN, STAGES, true>());
+  cfg.dynamicSmemBytes = S::TOTAL;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, conv_tc_kernel<BN, STAGES, true>, p));
   LAUNCH_CHECK();
   return grid;
 }
@@ -975,7 +1075,20 @@ int run(TcParams &p, int BN, float *ws, size_t ws_floats, const EpiStats *est, c
       make_out_map(&p.m_map, p.st.mask, false, p.ych, p.OW, p.OH, p.OD, p.ON, p.bw, p.bh, p.bd, p.bn);
     p.tma_ok = 1;
   }
-  const int grid = launch_ring(p, BN, st);
+  int grid;
+  // CTA pairs for the one-class launches with N tiles of 128 / 256 (stage 2-4 3x3x3
+  // and stride-2 convs): M=256 MMAs, half of B per CTA (RN_TC_PAIR=0 turns them off)
+  const int64_t n_mt = p.n_tiles / p.t_nblk;
+  if (tc_pair_mode() && (tc_pair_mode() == 1 || p.ksplit == 1) && p.n_cls == 1 && (BN == 128 || BN == 256) &&
+      n_mt >= 2 && p.w_base) {
+    p.pair = 1;
+    p.n_mt = n_mt;
+    p.cls_item0[1] = (n_mt + 1) / 2 * p.t_nblk * p.ksplit;
+    make_w_map(&p.b_map, p.w_base, p.w_rows, p.w_ktot, BN / 2);
+    grid = BN == 256 ? launch_pair<256, 6>(p, st) : launch_pair<128, 8>(p, st);
+  } else {
+    grid = launch_ring(p, BN, st);
+  }
   if (p.ksplit > 1) {
     const int64_t n = p.n_view_vox * (p.ych / 8);
     // with statistics: <= 148 blocks (the partial count), stride a multiple of ych/8
@@ -1019,6 +1132,8 @@ void fill_tiles(TcParams &p, int OW, int OH, int OD, int ON, int nout, int BN) {
 }
 
 }  // namespace
+
+void tc_pair_force(int mode) { g_pair_force = mode; }
 
 bool tc_conv_supported(const ConvGeom &g, bool dgrad) {
   const int kc = dgrad ? g.Co : g.Ci;     // A channels
@@ -1075,6 +1190,7 @@ int conv_fprop_tc(const ConvGeom &g, const bf16 *x, const bf16 *w, const float *
     p.tap_kcoord[t] = t * g.Ci;
   }
   make_w_map(&p.b_map, w, g.Co, (int64_t)taps * g.Ci, BN);
+  p.w_base = w; p.w_rows = g.Co; p.w_ktot = (int64_t)taps * g.Ci;
   p.y = y;
   p.ych = g.Co;
   p.s_w = g.Co;
@@ -1108,6 +1224,7 @@ int conv_dgrad_tc(const ConvGeom &g, const bf16 *dy, const bf16 *wd, bf16 *dx, b
       p.tap_kcoord[t] = t * g.Co;  // wd row layout [ci][t'][co] indexed by t' = t here
     }
     make_w_map(&p.b_map, wd, g.Ci, (int64_t)taps * g.Co, BN);
+    p.w_base = wd; p.w_rows = g.Ci; p.w_ktot = (int64_t)taps * g.Co;
     p.y = dx;
     p.ych = g.Ci;
     p.s_w = g.Ci;

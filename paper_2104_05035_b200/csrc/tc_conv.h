@@ -11,6 +11,9 @@ namespace rn {
 // true if the tcgen05 kernels take this convolution (bf16, channels % 64 == 0,
 // k in {1, 3}, stride in {1, 2} with the 'same' ceil(in/2) lattice)
 bool tc_conv_supported(const ConvGeom &g, bool dgrad);
+// CTA-pair dispatch of the persistent tcgen05 kernel for the calling thread:
+// -1 = default (RN_TC_PAIR), 0 = never, 1 = every launch it takes (kernel tests)
+void tc_pair_force(int mode);
 // ws: fp32 split-K workspace of >= tc_conv_ws_floats(g, dgrad) floats (layers with few tiles)
 size_t tc_conv_ws_floats(const ConvGeom &g, bool dgrad);
 // est (optional): fused BN statistics of the stored output (bnstats.cuh); the

@@ -2,7 +2,10 @@
 class of the r18 step at the full 91x109x91 sizes (batch 2), tcgen05 and SIMT,
 against the oracle's float64 convolution on the same bf16-valued inputs.
 Tolerance: fp32 accumulation + one bf16 rounding of the output ->
-per-tensor relative L2 error <= 4e-3."""
+per-tensor relative L2 error <= 4e-3 AND element-wise |err| <= 2^-7 |ref| +
+2^-9 max|ref| (bf16 outputs; fp32 weight gradients: 1e-4 rel-L2 and 1e-3 |ref|
++ 1e-5 max|ref|).  impl 5 runs the persistent kernel
+on CTA pairs (cta_group::2) for every launch it takes, split-K included."""
 import numpy as np
 import pytest
 import torch
@@ -36,7 +39,16 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-@pytest.mark.parametrize("impl", [4, 3, 2, 1])
+def elem_ok(a, b, r=2.0 ** -7, t=2.0 ** -9):
+    """Element-wise: |a - b| <= r |b| + t max|b| at every element (bf16 outputs: one
+    rounding is <= 2^-9 |b|; fp32 accumulation adds far less) -- a single wrong voxel
+    row or channel fails it, which the norm-wise check would not see."""
+    err = np.abs(a - b)
+    bound = r * np.abs(b) + t * np.abs(b).max()
+    return bool((err <= bound).all()), float((err / bound).max())
+
+
+@pytest.mark.parametrize("impl", [5, 4, 3, 2, 1])
 @pytest.mark.parametrize("cv", CONVS, ids=[c[0] for c in CONVS])
 def test_conv_fprop_dgrad(cv, impl):
     name, Di, Hi, Wi, Ci, Co, k, s, p = cv
@@ -61,8 +73,11 @@ def test_conv_fprop_dgrad(cv, impl):
     dyn = dy.float().numpy().astype(np.float64)
     y_ref = O.conv3d(xn, wc, s, p)
     dx_ref, _ = O.conv3d_backward(xn, wc, dyn, s, p)
-    assert rel(y.float().cpu().numpy(), y_ref) < 4e-3
-    assert rel(dx.float().cpu().numpy(), dx_ref) < 4e-3
+    yg, dxg = y.float().cpu().numpy(), dx.float().cpu().numpy()
+    assert rel(yg, y_ref) < 4e-3
+    assert rel(dxg, dx_ref) < 4e-3
+    assert elem_ok(yg, y_ref)[0], elem_ok(yg, y_ref)
+    assert elem_ok(dxg, dx_ref)[0], elem_ok(dxg, dx_ref)
 
 
 @pytest.mark.parametrize("impl", [0, 1])
@@ -83,6 +98,7 @@ def test_conv_wgrad(cv, impl):
     _, dw_ref = O.conv3d_backward(xn, np.zeros((Co, Ci, k, k, k)), dyn, s, p, need_dx=False)
     got = dw.cpu().numpy().reshape(Co, k, k, k, Ci).transpose(0, 4, 1, 2, 3)
     assert rel(got, dw_ref) < 1e-4
+    assert elem_ok(got, dw_ref, 1e-3, 1e-5)[0], elem_ok(got, dw_ref, 1e-3, 1e-5)
 
 
 @pytest.mark.parametrize("cv", CONVS, ids=[c[0] for c in CONVS])
@@ -112,7 +128,11 @@ def test_conv_bench_batch(cv):
     dyn = dy.float().numpy().astype(np.float64)
     y_ref = O.conv3d(xn, wc, s, p)
     dx_ref, dw_ref = O.conv3d_backward(xn, wc, dyn, s, p)
-    assert rel(y.float().cpu().numpy(), y_ref) < 4e-3
-    assert rel(dx.float().cpu().numpy(), dx_ref) < 4e-3
+    yg, dxg = y.float().cpu().numpy(), dx.float().cpu().numpy()
+    assert rel(yg, y_ref) < 4e-3
+    assert rel(dxg, dx_ref) < 4e-3
+    assert elem_ok(yg, y_ref)[0], elem_ok(yg, y_ref)
+    assert elem_ok(dxg, dx_ref)[0], elem_ok(dxg, dx_ref)
     got = dw.cpu().numpy().reshape(Co, k, k, k, Ci).transpose(0, 4, 1, 2, 3)
     assert rel(got, dw_ref) < 1e-4
+    assert elem_ok(got, dw_ref, 1e-3, 1e-5)[0], elem_ok(got, dw_ref, 1e-3, 1e-5)

@@ -50,7 +50,10 @@ for i in range(n):
     t0 = t[:, 0].min()
     span = (t[:, 7].max() - t0) / 1000
     tot += span
-    med = np.median((t - t0) / 1000.0, axis=0)
+    rel = (t - t0) / 1000.0
+    med = np.median(rel, axis=0)
+    if meta[i][1] < 0:  # CTA pairs: the MMA stamps come from the leaders (even CTAs)
+        med[3:5] = np.median(rel[0::2, 3:5], axis=0)
     print(f"{i:>3} {meta[i][0]:>3} {meta[i][1]:>2} {g:>4} {meta[i][3]:>5} {meta[i][4]:>3} {meta[i][7]:>4}  {span:6.1f} " +
           " ".join(f"{v:6.1f}" for v in med[1:]))
 print(f"sum of launch spans {tot:.1f} us")
