@@ -224,15 +224,6 @@ __global__ void __launch_bounds__(NT) wgrad_simt_kernel(ConvGeom g, const TX *__
   }
 }
 
-__global__ void split_reduce_add(const float *__restrict__ part, int splits, int64_t n, float *__restrict__ out) {
-  pdl_begin();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * n + i];
-    out[i] += s;
-  }
-}
-
 void wgrad_split(const ConvGeom &g, int &splits, int64_t &chunks_per_split) {
   const int taps = g.k * g.k * g.k;
   const int64_t tiles = (int64_t)((g.Co + BM - 1) / BM) * ((taps * g.Ci + BN - 1) / BN);
@@ -330,8 +321,7 @@ void conv_wgrad_simt(DType dt, bool x_is_f32, const ConvGeom &g, const void *x, 
     launch_k(wgrad_simt_kernel<bf16, bf16>, grid, NT, 0, st, g, (const bf16 *)x, (const bf16 *)dy, ws, cps);
   LAUNCH_CHECK();
   int64_t n = (int64_t)g.Co * g.taps() * g.Ci;
-  launch_k(split_reduce_add, (unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st, ws, splits, n, dw);
-  LAUNCH_CHECK();
+  split_reduce_add(ws, splits, n, dw, st);
 }
 
 void stem_conv_fprop(DType dt, const ConvGeom &g, const float *x, const float *w, void *y, cudaStream_t st) {

@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256) stem_wgrad_warp_k(ConvGeom g, const float
 // XOR-swizzled by row for conflict-free ldmatrix.trans) and the 27-tap input
 // patches [256][36] fp32 in smem; warp w takes k-steps w and w+8 (16 voxels
 // each): 4 m-tiles x 4 n-tiles x (hi, lo) = 32 MMAs.  Per-block partials are
-// reduced in a fixed order (stem_reduce_k).
+// reduced in a fixed order (split_reduce_add).
 constexpr int SW_CH = 256;     // voxels per chunk
 constexpr int SW_PS = 36;      // patch row stride (floats): conflict-free fragment reads
 constexpr int SW_SMEM = SW_CH * 128 + SW_CH * SW_PS * 4;
@@ -801,15 +801,6 @@ __global__ void __launch_bounds__(256, 2) stem_wgrad_mma_k(ConvGeom g, const flo
   }
 }
 
-__global__ void stem_reduce_k(const float *__restrict__ part, int nblk, int n, float *__restrict__ dw) {
-  pdl_begin();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * n + i];
-    dw[i] += s;
-  }
-}
-
 template <typename T, int CO>
 int stem_fprop_launch(const ConvGeom &g, const float *x, const float *w, void *y, float *part, cudaStream_t st) {
   const int64_t total = g.out_vox();
@@ -839,7 +830,7 @@ template <typename T, int CO>
 void stem_wgrad_launch(const ConvGeom &g, const float *x, const void *dh, float *dw, float *ws, cudaStream_t st,
                        const void *hx = nullptr, const float *coef = nullptr) {
   if (std::is_same<T, bf16>::value && CO == 64 && !getenv("RN_STEM_SIMT") && g.out_vox() < (1LL << 31)) {
-    // tensor-core path (bf16 dh): 3 blocks per SM, partials reduced by stem_reduce_k
+    // tensor-core path (bf16 dh): 3 blocks per SM, partials reduced by split_reduce_add
     static uint64_t attr_devs = 0;  // kernel attributes are per device
     if (!once_on_device(attr_devs)) {
       CUDA_CHECK(cudaFuncSetAttribute(stem_wgrad_mma_k, cudaFuncAttributeMaxDynamicSharedMemorySize, SW_SMEM));
@@ -847,7 +838,7 @@ void stem_wgrad_launch(const ConvGeom &g, const float *x, const void *dh, float 
     const int nb = std::min(stem_wgrad_blocks(g), 2 * 148);
     launch_k(stem_wgrad_mma_k, nb, 256, SW_SMEM, st, g, x, (const bf16 *)dh, ws, (const bf16 *)hx, coef);
     LAUNCH_CHECK();
-    launch_k(stem_reduce_k, (CO * 27 + 255) / 256, 256, 0, st, ws, nb, CO * 27, dw);
+    split_reduce_add(ws, nb, CO * 27, dw, st);
     return;
   }
   if (coef) throw Error(RN_ERR_ARG, "stem_wgrad: the fused BN apply needs the bf16 64-channel tensor-core path");
@@ -857,7 +848,7 @@ void stem_wgrad_launch(const ConvGeom &g, const float *x, const void *dh, float 
   const int64_t vpb = (g.out_vox() + nb - 1) / nb;
   launch_k(stem_wgrad_k<T, CO>, nb, 256, 0, st, g, x, (const T *)dh, ws, vpb);
   LAUNCH_CHECK();
-  launch_k(stem_reduce_k, (CO * 27 + 255) / 256, 256, 0, st, ws, nb, CO * 27, dw);
+  split_reduce_add(ws, nb, CO * 27, dw, st);
 }
 
 }  // namespace
@@ -893,8 +884,7 @@ void stem_wgrad_fused_apply(const ConvGeom &g, const float *x, const void *dprim
     const int nb = std::min(stem_wgrad_blocks(g), 148);  // one CTA per SM (196 KB)
     launch_k(stem_wgrad_pipe_k, nb, 256, SWP_SMEM, st, g, x, (const bf16 *)dprime, (const bf16 *)h, coef, ws);
     LAUNCH_CHECK();
-    launch_k(stem_reduce_k, (64 * 27 + 255) / 256, 256, 0, st, ws, nb, 64 * 27, dw);
-    LAUNCH_CHECK();
+    split_reduce_add(ws, nb, 64 * 27, dw, st);
     return;
   }
   stem_wgrad_launch<bf16, 64>(g, x, dprime, dw, ws, st, h, coef);

@@ -279,12 +279,47 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
   }
 }
 
-__global__ void wg_reduce_add(const float *__restrict__ part, int splits, int64_t n, float *__restrict__ out) {
+// out[i] += sum over z < splits of part[z * n + i] (split-K weight-gradient
+// partials).  Deterministic and parallel over the splits: group g of a block
+// sums z = g, g + G, ... in ascending order (four loads in flight), then the G
+// group sums are added in g order.  The former one-thread-per-element loop was
+// latency-bound for the 1x1x1 and stem weights (n = 4096 / 1728 elements,
+// 138-444 splits: 16 / 7 blocks, ~18 us each).
+template <int G>
+__global__ void __launch_bounds__(256) split_reduce_add_k(const float *__restrict__ part, int splits, int64_t n,
+                                                          float *__restrict__ out) {
+  constexpr int E = 256 / G;
+  __shared__ float red[G][E];
   pdl_begin();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  const int e = threadIdx.x % E, g = threadIdx.x / E;
+  for (int64_t base = (int64_t)blockIdx.x * E; base < n; base += (int64_t)gridDim.x * E) {
+    const int64_t i = base + e;
     float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * n + i];
-    out[i] += s;
+    if (i < n) {
+      int z = g;
+      for (; z + 3 * G < splits; z += 4 * G) {
+        const float a = part[(int64_t)z * n + i], b = part[(int64_t)(z + G) * n + i];
+        const float c = part[(int64_t)(z + 2 * G) * n + i], d = part[(int64_t)(z + 3 * G) * n + i];
+        s += a;
+        s += b;
+        s += c;
+        s += d;
+      }
+      for (; z < splits; z += G) s += part[(int64_t)z * n + i];
+    }
+    if (G > 1) {
+      red[g][e] = s;
+      __syncthreads();
+      if (g == 0 && i < n) {
+        float t = red[0][e];
+#pragma unroll
+        for (int q = 1; q < G; ++q) t += red[q][e];
+        out[i] += t;
+      }
+      __syncthreads();
+    } else if (i < n) {
+      out[i] += s;
+    }
   }
 }
 
@@ -369,6 +404,20 @@ WgShape wg_shape(const ConvGeom &g) {
 }
 
 }  // namespace
+
+void split_reduce_add(const float *part, int splits, int64_t n, float *out, cudaStream_t st) {
+  auto go = [&](auto kern, int G) {
+    const int64_t per = 256 / G;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + per - 1) / per, 148 * 8));
+    launch_k(kern, grid, 256, 0, st, part, splits, n, out);
+  };
+  // enough blocks to cover the SMs: the more splits per element, the more groups
+  if (splits >= 64 && n <= 148 * 64) go(split_reduce_add_k<8>, 8);
+  else if (splits >= 16 && n <= 148 * 256) go(split_reduce_add_k<4>, 4);
+  else if (splits >= 4 && n <= 148 * 512) go(split_reduce_add_k<2>, 2);
+  else go(split_reduce_add_k<1>, 1);
+  LAUNCH_CHECK();
+}
 
 void make_act_map(CUtensorMap *m, const void *base, int C, int W, int H, int D, int N, int64_t sw, int64_t sh,
                   int64_t sd, int64_t sn, int bw, int bh, int bd, int bn);
@@ -473,8 +522,7 @@ void conv_wgrad_tc(const ConvGeom &g, const bf16 *x, const bf16 *dy, float *dw, 
   }
   if (p.accum) return;
   const int64_t n = (int64_t)g.Co * g.taps() * g.Ci;
-  launch_k(wg_reduce_add, (unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st, ws, s.splits, n, dw);
-  LAUNCH_CHECK();
+  split_reduce_add(ws, s.splits, n, dw, st);
 }
 
 }  // namespace rn

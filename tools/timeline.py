@@ -103,3 +103,21 @@ for a, b, s, n in step:
 print("kernel family: total us, launches (overlap: max single-partner overlap, indicative)", file=out)
 for key, (t, o, c) in sorted(fam.items(), key=lambda kv: -kv[1][0])[:30]:
     print(f"  {t:8.1f} {c:4d}  ov {o:7.1f}  {key}", file=out)
+# critical-path increments on the main stream: with PDL a kernel starts early and waits,
+# so its CUPTI duration overstates; end_i - end_{i-1} is what it adds to the stream's span
+inc = collections.defaultdict(lambda: [0.0, 0])
+prev_end = None
+rows = []
+for a, b, s, n in m:
+    key = n.split("(")[0].replace("void ", "").replace("rn::", "").replace("(anonymous namespace)::", "")[:48]
+    d = b - (prev_end if prev_end is not None else a)
+    prev_end = b if prev_end is None else max(prev_end, b)
+    inc[key][0] += d
+    inc[key][1] += 1
+    rows.append((d, key))
+print(f"main-stream end-to-end increments (sum {sum(v[0] for v in inc.values()):.1f} us):", file=out)
+for key, (t, c) in sorted(inc.items(), key=lambda kv: -kv[1][0])[:30]:
+    print(f"  {t:8.1f} {c:4d}  {key}", file=out)
+print("main-stream sequence (increment us, kernel):", file=out)
+for d, key in rows:
+    print(f"  {d:7.1f}  {key}", file=out)
