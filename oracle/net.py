@@ -200,6 +200,29 @@ def bn_backward(dy, cache, gamma):
     return dx, dgamma, dbeta
 
 
+def bn_backward_coefs(dy, cache, gamma, h=None):
+    """bn_backward's dx written as A*dy + B*h + Cc per channel (h = the BN input:
+    x-hat = (h - mu) * invstd), with dgamma / dbeta:
+    dx = gamma*invstd*(dy - mean(dy) - xhat*mean(dy*xhat)) = A dy + B h + Cc.
+    h (optional): the values x-hat is formed from (default: the forward's x-hat)."""
+    axes = (0, 1, 2, 3)
+    xhat, invstd, mu = cache["xhat"], cache["invstd"], cache["mu"]
+    if h is not None:
+        xhat = (h - mu) * invstd
+    dgamma = (dy * xhat).sum(axis=axes)
+    dbeta = dy.sum(axis=axes)
+    mdy = dy.mean(axis=axes)
+    mdyx = (dy * xhat).mean(axis=axes)
+    A = gamma * invstd
+    B = -A * invstd * mdyx
+    Cc = -A * mdy + A * invstd * mu * mdyx
+    return A, B, Cc, dgamma, dbeta
+
+
+# stem widths whose pooled bf16 backward runs at the pooled resolution (reading X23c)
+STEM_POOLED_BWD_WIDTHS = (8, 16, 32, 64)
+
+
 def relu(x):
     return np.maximum(x, 0.0)
 
@@ -374,7 +397,8 @@ def unit_forward(P, ui, u, x, bns):
     c = {}
     if u.kind == "stem":
         c["x"] = x
-        h = Q(conv3d(x, P[pre + ".conv"], u.stride, 1))      # stem reads fp32 master weights
+        c["h_raw"] = conv3d(x, P[pre + ".conv"], u.stride, 1)  # stem reads fp32 master weights
+        h = Q(c["h_raw"])
         y, c["bn"] = bn_forward(h, P[pre + ".bn.gamma"], P[pre + ".bn.beta"])
         bns.append((pre + ".bn", c["bn"]))
         a = relu(y)
@@ -417,10 +441,22 @@ def unit_forward(P, ui, u, x, bns):
 def unit_backward(P, ui, u, dout, c, G):
     pre = f"u{ui}"
     if u.kind == "stem":
-        da = Q(maxpool3_backward(dout, c["am"], c["a"].shape)) if u.extra["pool"] else dout
-        dy = da * (c["a"] > 0)
-        dh, G[pre + ".bn.gamma"], G[pre + ".bn.beta"] = bn_backward(dy, c["bn"], P[pre + ".bn.gamma"])
-        dh = Q(dh)
+        if u.extra["pool"] and (Q is _identity or u.cout in STEM_POOLED_BWD_WIDTHS):
+            # reading X23c: the pooled stem's backward neither reads the stored h nor
+            # stores anything at the conv resolution — the pool adjoint da and dh are
+            # not rounded, and the backward takes the conv's unrounded output h_raw
+            # (x-hat of the BN sums and the h-term of dh; mu / invstd stay those of the
+            # forward).  With store="f64" this IS bn_backward.
+            da = maxpool3_backward(dout, c["am"], c["a"].shape)
+            dy = da * (c["a"] > 0)
+            A, B, Cc, G[pre + ".bn.gamma"], G[pre + ".bn.beta"] = bn_backward_coefs(
+                dy, c["bn"], P[pre + ".bn.gamma"], h=c["h_raw"])
+            dh = A * dy + B * c["h_raw"] + Cc
+        else:
+            da = Q(maxpool3_backward(dout, c["am"], c["a"].shape)) if u.extra["pool"] else dout
+            dy = da * (c["a"] > 0)
+            dh, G[pre + ".bn.gamma"], G[pre + ".bn.beta"] = bn_backward(dy, c["bn"], P[pre + ".bn.gamma"])
+            dh = Q(dh)
         _, G[pre + ".conv"] = conv3d_backward(c["x"], P[pre + ".conv"], dh, u.stride, 1, need_dx=False)
         return None
     if u.kind == "block":

@@ -873,8 +873,7 @@ __global__ void __launch_bounds__(NTA) bn_bwd_apply_part_k(const T *__restrict__
 // for s > 0, -h for s < 0 (sign flip of the bf16 bit pattern) — except when the
 // window maximum is not positive (ReLU makes every tap 0: the first valid tap
 // wins) or s == 0.  Packed bf16x2 compares: 4 instructions per 2 channels and
-// tap.  (A backward that gathered the pool adjoint twice instead of writing it
-// once measured slower: 376 vs 277 us on the r18 stem.)
+// tap.  The backward runs at the pooled resolution (k_stem_bwd.cu).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t sel32(uint32_t m, uint32_t a, uint32_t b) { return (a & m) | (b & ~m); }
 
@@ -905,17 +904,25 @@ __global__ void __launch_bounds__(NTA) stem_pool_fwd_k(const bf16 *__restrict__ 
 #pragma unroll
     for (int q = 0; q < 4; ++q) fm[q] = (s_[2 * q] < 0.f ? 0x8000u : 0u) | (s_[2 * q + 1] < 0.f ? 0x80000000u : 0u);
     uint32_t best[4] = {0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u}, arg[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-    for (int kd = 0; kd < 3; ++kd) {
+    // the 9 taps of plane kd + 1 are requested before plane kd is compared: about
+    // one memory round trip per output instead of three
+    uint4 vb[2][9];
+    bool okb[2][9];
+    auto load_plane = [&](int kd, uint4 (&v)[9], bool (&ok)[9]) {
       const int id = 2 * od + kd - 1;
-      uint4 v[9];
-      bool ok[9];
 #pragma unroll
       for (int tp = 0; tp < 9; ++tp) {
         const int ih = 2 * oh + tp / 3 - 1, iw = 2 * ow + tp % 3 - 1;
         ok[tp] = id >= 0 && id < D && ih >= 0 && ih < H && iw >= 0 && iw < W;
-        if (ok[tp]) v[tp] = ld16(h + ((int64_t)((nn * D + id) * H + ih) * W + iw) * C + c0);
+        v[tp] = ok[tp] ? ld16(h + ((int64_t)((nn * D + id) * H + ih) * W + iw) * C + c0) : make_uint4(0, 0, 0, 0);
       }
+    };
+    load_plane(0, vb[0], okb[0]);
+#pragma unroll
+    for (int kd = 0; kd < 3; ++kd) {
+      if (kd < 2) load_plane(kd + 1, vb[(kd + 1) & 1], okb[(kd + 1) & 1]);
+      const uint4 (&v)[9] = vb[kd & 1];
+      const bool (&ok)[9] = okb[kd & 1];
 #pragma unroll
       for (int tp = 0; tp < 9; ++tp) {
         if (!ok[tp]) continue;
@@ -1186,222 +1193,6 @@ __global__ void __launch_bounds__(256) maxpool_bwd_stage_k(const bf16 *__restric
     }
     store_vec(dx + o, acc);
   }
-}
-
-// Stem backward, part 1 (bf16 path, pooled stem; PAPER.md:366 Conv block =
-// conv + BN + ReLU, reading X4 stem max-pool, X10 tie rule): one persistent
-// pass that computes, per stem voxel and channel,
-//   g  = pool adjoint (gathered from smem-staged pooled rows, as maxpool_bwd_stage_k), rounded to bf16
-//   d' = g * (h*scale + shift > 0)   (ReLU mask recomputed from the BN forward coefficients)
-// stores d' (bf16) and accumulates the BN-backward sums S1 = sum d', S2 = sum d' xhat
-// (xhat = (h - mean) invstd, the BwdOp convention) in registers (each thread keeps
-// one 8-channel group: blockDim is a multiple of C/8); per-block partials are
-// reduced in block order by the last block, which finalizes (BwdFin: dgamma,
-// dbeta, and the apply coefficients consumed by the stem weight gradient).
-// Replaces maxpool_bwd_stage_k + chan_reduce_fin_k<BwdOp> (one fewer 119 MB read).
-// Pool-adjoint gather for one stem voxel x 8 channels, specialised on the voxel's
-// parity (PD, PH, PW): a coordinate i is covered by window o = i >> 1 (tap 1) when
-// even, by o = i >> 1 (tap 2) and o + 1 (tap 0) when odd.  Slots / taps are
-// compile-time; out-of-range pooled rows were staged with code 255 (never
-// matches), only the w-neighbour needs a bound check.  Candidates are visited
-// in (d, h, w) order (the summation order of maxpool_bwd_stage_k).
-template <int C, int PD, int PH, int PW>
-__device__ __forceinline__ void pool_gather(const bf16 *sdy, const uint8_t *sam, int rowel, int ow0, int Wo, int cg,
-                                            float (&acc)[8]) {
-#pragma unroll
-  for (int a = 0; a <= PD; ++a)
-#pragma unroll
-    for (int b = 0; b <= PH; ++b)
-#pragma unroll
-      for (int c = 0; c <= PW; ++c) {
-        const int kd = PD ? (a ? 0 : 2) : 1, kh = PH ? (b ? 0 : 2) : 1, kw = PW ? (c ? 0 : 2) : 1;
-        const uint32_t tap4 = (uint32_t)((kd * 3 + kh) * 3 + kw) * 0x01010101u;
-        const int ow = ow0 + c;
-        if (c == 1 && ow >= Wo) continue;
-        const int e0 = (a * 2 + b) * rowel + ow * C + cg;
-        const uint4 v = *reinterpret_cast<const uint4 *>(sdy + e0);
-        const uint2 code = *reinterpret_cast<const uint2 *>(sam + e0);
-        const uint32_t m0 = __vcmpeq4(code.x, tap4), m1 = __vcmpeq4(code.y, tap4);
-        const uint32_t w4[4] = {v.x & __byte_perm(m0, 0, 0x1100), v.y & __byte_perm(m0, 0, 0x3322),
-                                v.z & __byte_perm(m1, 0, 0x1100), v.w & __byte_perm(m1, 0, 0x3322)};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          acc[2 * k] += __uint_as_float(w4[k] << 16);
-          acc[2 * k + 1] += __uint_as_float(w4[k] & 0xFFFF0000u);
-        }
-      }
-}
-
-constexpr int SPB_PF = 3;  // staged 16-B vectors per thread (4 pooled rows x Wo x C / 8 <= 768)
-template <int C>  // channels (compile-time: the index math is shifts)
-__global__ void __launch_bounds__(256, 2) stem_pool_bwd_k(const bf16 *__restrict__ dy, const uint8_t *__restrict__ am,
-                                                       const bf16 *__restrict__ h, int N, int D, int H, int W, int,
-                                                       int Do, int Ho, int Wo, const float *__restrict__ scale,
-                                                       const float *__restrict__ shift, const float *__restrict__ mean,
-                                                       const float *__restrict__ invstd, bf16 *__restrict__ dprime,
-                                                       float *__restrict__ partial, unsigned *counter, BwdFin fin) {
-  extern __shared__ __align__(16) uint8_t smp[];
-  pdl_begin();
-  const int rowel = Wo * C;
-  bf16 *sdy = reinterpret_cast<bf16 *>(smp);  // [4][Wo][C]
-  uint8_t *sam = smp + 4 * rowel * 2;         // [4][Wo][C]
-  const int Hj = (H + 1) / 2;
-  constexpr int G = C / 8;
-  const int vecs = rowel / 8;
-  const int cg = (threadIdx.x % G) * 8;  // this thread's channel group (items advance by blockDim)
-  __shared__ float coefs[4][C];             // scale, shift, mean, invstd per channel
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    coefs[0][c] = scale[c];
-    coefs[1][c] = shift[c];
-    coefs[2][c] = mean[c];
-    coefs[3][c] = invstd[c];
-  }
-  float a1[8], a2[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) a1[e] = a2[e] = 0.f;
-  const int units = N * D * Hj;
-  // the pooled rows of unit u are loaded into registers while unit u - gridDim.x
-  // is gathered (software pipeline: one global round trip per unit is hidden)
-  uint4 pv[SPB_PF];
-  uint2 pa[SPB_PF];
-  auto stage_load = [&](int u) {
-    const int j = u % Hj, id = (u / Hj) % D, nn = u / (Hj * D);
-    const int od0 = id >> 1, od1 = (id & 1) && ((id + 1) >> 1) < Do ? (id + 1) >> 1 : -1;
-#pragma unroll
-    for (int q = 0; q < SPB_PF; ++q) {
-      const int i = threadIdx.x + q * 256;
-      pv[q] = make_uint4(0, 0, 0, 0);
-      pa[q] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);  // no code matches 255
-      if (i < 4 * vecs) {
-        const int slot = i / vecs, e = (i - slot * vecs) * 8;
-        const int od = (slot >> 1) ? od1 : od0, oh = j + (slot & 1);
-        if (od >= 0 && oh < Ho) {
-          const int64_t o = ((int64_t)(nn * Do + od) * Ho + oh) * rowel + e;
-          pv[q] = ld16(dy + o);
-          pa[q] = *reinterpret_cast<const uint2 *>(am + o);
-        }
-      }
-    }
-  };
-  if (blockIdx.x < units) stage_load(blockIdx.x);
-  for (int u = blockIdx.x; u < units; u += gridDim.x) {
-    const int j = u % Hj, id = (u / Hj) % D, nn = u / (Hj * D);
-    __syncthreads();  // the previous unit's readers are done with the staged rows
-#pragma unroll
-    for (int q = 0; q < SPB_PF; ++q) {
-      const int i = threadIdx.x + q * 256;
-      if (i < 4 * vecs) {
-        const int slot = i / vecs, e = (i - slot * vecs) * 8;
-        *reinterpret_cast<uint4 *>(sdy + slot * rowel + e) = pv[q];
-        *reinterpret_cast<uint2 *>(sam + slot * rowel + e) = pa[q];
-      }
-    }
-    __syncthreads();
-    if (u + (int)gridDim.x < units) stage_load(u + gridDim.x);
-    const int items = 2 * W * G;
-    // item -> (ih parity r, iw): voxels v < We have even iw = 2v, the rest odd iw, so
-    // that a warp's 4 voxels share their parity class (specialised gather below)
-    const int We = (W + 1) / 2;
-    auto item_iw = [&](int it, int &r) {
-      const int v = it / G;
-      r = v >= W;
-      const int vv = v - (r ? W : 0);
-      return vv < We ? 2 * vv : 2 * (vv - We) + 1;
-    };
-    // h of all this thread's items of the unit, loaded up front (one exposed
-    // round trip per unit instead of one per item)
-    uint4 hq[SPB_PF];
-#pragma unroll
-    for (int q = 0; q < SPB_PF; ++q) {
-      const int it = threadIdx.x + q * 256;
-      int r;
-      const int iw = item_iw(it, r);
-      const int ih = 2 * j + r;
-      if (it < items && ih < H) hq[q] = ld16(h + (((int64_t)(nn * D + id) * H + ih) * W + iw) * C + cg);
-    }
-#pragma unroll
-    for (int q = 0; q < SPB_PF; ++q) {
-      const int it = threadIdx.x + q * 256;
-      if (it >= items) break;
-      int r;
-      const int iw = item_iw(it, r);
-      const int ih = 2 * j + r;
-      if (ih >= H) continue;
-      const int64_t o = (((int64_t)(nn * D + id) * H + ih) * W + iw) * C + cg;
-      float hv[8];
-      unpack16(hq[q], hv, h);
-      float acc[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-      const int ow0 = iw >> 1;
-      switch (((id & 1) << 2) | (r << 1) | (iw & 1)) {
-        case 0: pool_gather<C, 0, 0, 0>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
-        case 1: pool_gather<C, 0, 0, 1>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
-        case 2: pool_gather<C, 0, 1, 0>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
-        case 3: pool_gather<C, 0, 1, 1>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
-        case 4: pool_gather<C, 1, 0, 0>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
-        case 5: pool_gather<C, 1, 0, 1>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
-        case 6: pool_gather<C, 1, 1, 0>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
-        default: pool_gather<C, 1, 1, 1>(sdy, sam, rowel, ow0, Wo, cg, acc); break;
-      }
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float g = __bfloat162float(__float2bfloat16_rn(acc[e]));  // the stored pool adjoint
-        const float d = fmaf(hv[e], coefs[0][cg + e], coefs[1][cg + e]) > 0.f ? g : 0.f;
-        acc[e] = d;
-        a1[e] += d;
-        a2[e] = fmaf(d, (hv[e] - coefs[2][cg + e]) * coefs[3][cg + e], a2[e]);
-      }
-      store_vec(dprime + o, acc);
-    }
-  }
-  // per-block partials: channel c = cg + e summed over the threads of group cg, in thread order
-  __syncthreads();
-  float *red = reinterpret_cast<float *>(smp);  // [2][blockDim][8] (<= the staging area)
-  const int nt = blockDim.x;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    red[threadIdx.x * 8 + e] = a1[e];
-    red[(nt + threadIdx.x) * 8 + e] = a2[e];
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < C; c += nt) {
-    float x1 = 0.f, x2 = 0.f;
-    for (int tt = c >> 3; tt < nt; tt += G) {
-      x1 += red[tt * 8 + (c & 7)];
-      x2 += red[(nt + tt) * 8 + (c & 7)];
-    }
-    partial[(int64_t)blockIdx.x * 2 * C + c] = x1;
-    partial[(int64_t)blockIdx.x * 2 * C + C + c] = x2;
-  }
-  __shared__ bool is_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  // last block: fixed-order fp64 reduction over the blocks, P threads per channel
-  double *dsm = reinterpret_cast<double *>(smp);
-  const int P = nt / C;  // C <= nt, nt % C == 0 (checked by the launcher)
-  const int c = threadIdx.x % C, s = threadIdx.x / C;
-  double A = 0.0, B = 0.0;
-  for (int k = s; k < (int)gridDim.x; k += P) {
-    A += (double)partial[(int64_t)k * 2 * C + c];
-    B += (double)partial[(int64_t)k * 2 * C + C + c];
-  }
-  dsm[s * C + c] = A;
-  dsm[nt + s * C + c] = B;
-  __syncthreads();
-  if (s == 0) {
-    double SA = 0.0, SB = 0.0;
-    for (int q = 0; q < P; ++q) {
-      SA += dsm[q * C + c];
-      SB += dsm[nt + q * C + c];
-    }
-    fin(c, SA, SB);
-  }
-  if (threadIdx.x == 0) *counter = 0u;
 }
 
 template <typename T>
@@ -1804,23 +1595,6 @@ void maxpool_bwd(DType dt, const void *dy, const uint8_t *argmax, int N, int D, 
   LAUNCH_CHECK();
 }
 
-int stem_pool_bwd_blocks() { return 148 * 2; }
-
-void stem_pool_bwd(const void *dy, const uint8_t *argmax, const void *h, int N, int D, int H, int W, int C, int Do,
-                   int Ho, int Wo, const float *scale, const float *shift, const float *mean, const float *invstd,
-                   const float *gamma, float *dgamma, float *dbeta, float *coef, void *dprime, float *partial,
-                   unsigned *counter, cudaStream_t st) {
-  const size_t smem = std::max((size_t)4 * Wo * C * 3, (size_t)2 * 256 * 8 * sizeof(float));
-  if (C % 8 != 0 || 256 % C != 0 || smem > 48 * 1024 || 4 * Wo * C / 8 > SPB_PF * 256 || 2 * W * C / 8 > SPB_PF * 256)
-    throw Error(RN_ERR_ARG, "stem_pool_bwd: unsupported C / row");
-  const int units = N * D * ((H + 1) / 2);
-  const unsigned nb = (unsigned)std::min(units, stem_pool_bwd_blocks());
-  BwdFin fin{(int64_t)N * D * H * W, C, gamma, mean, invstd, dgamma, dbeta, coef};
-  if (C != 64) throw Error(RN_ERR_ARG, "stem_pool_bwd: instantiated for 64 channels");
-  launch_k(stem_pool_bwd_k<64>, nb, 256, smem, st, (const bf16 *)dy, argmax, (const bf16 *)h, N, D, H, W, C, Do, Ho, Wo,
-           scale, shift, mean, invstd, (bf16 *)dprime, partial, counter, fin);
-  LAUNCH_CHECK();
-}
 
 // Grad-CAM at the last conv layer (oracle gradcam_last):
 // alpha_k = W[c, k] / V (the GAP + FC head's gradient, averaged over voxels),

@@ -487,170 +487,6 @@ __global__ void __launch_bounds__(SF_WARPS * 32) stem_fprop_mma_k(ConvGeom g, co
   }
 }
 
-// Fused-apply stem weight gradient, software-pipelined: the raw d' and h rows of
-// chunk k+1 stream into a second smem buffer with cp.async (no registers held)
-// and chunk k+1's 27-tap input patches load into registers while chunk k is
-// converted (dh = bf16(A d' + B h + C)) and multiplied; one CTA per SM.
-// (The two-phase kernel below exposed one global round trip per chunk: 115 us.)
-constexpr int SWP_RAW = SW_CH * 128 * 2;                        // d' + h rows of one chunk
-constexpr int SWP_SMEM = 2 * SWP_RAW + SW_CH * 128 + SW_CH * SW_PS * 4;
-__global__ void __launch_bounds__(256, 1) stem_wgrad_pipe_k(ConvGeom g, const float *__restrict__ x,
-                                                          const bf16 *__restrict__ dp, const bf16 *__restrict__ hx,
-                                                          const float *__restrict__ coef, float *__restrict__ part) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  pdl_begin();
-  uint8_t *raw0 = sm;                              // [2][2][256][128 B]: buffer, tensor (d', h), row
-  uint8_t *sdh = sm + 2 * SWP_RAW;                 // [256][128 B] swizzled
-  float *sp = reinterpret_cast<float *>(sdh + SW_CH * 128);  // [256][36]
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31, gq = lane >> 2, tq = lane & 3;
-  const int total = (int)g.out_vox();  // < 2^31 (checked by the launcher)
-  float acc[4][4][4];
-#pragma unroll
-  for (int m = 0; m < 4; ++m)
-#pragma unroll
-    for (int n = 0; n < 4; ++n)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) acc[m][n][r] = 0.f;
-  float cA[8], cB[8], cC[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int c = (t & 7) * 8 + e;
-    cA[e] = coef[c];
-    cB[e] = coef[64 + c];
-    cC[e] = coef[128 + c];
-  }
-  const uint32_t raw_s = (uint32_t)__cvta_generic_to_shared(raw0);
-  auto issue_raw = [&](int v0, int buf) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int i = t + 256 * j, row = i >> 3, c = i & 7;
-      if (v0 + row < total) {
-        const uint32_t dst = raw_s + (uint32_t)(buf * SWP_RAW + row * 128 + c * 16);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
-                     "l"(reinterpret_cast<const uint4 *>(dp + (int64_t)(v0 + row) * 64) + c)
-                     : "memory");
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + SW_CH * 128),
-                     "l"(reinterpret_cast<const uint4 *>(hx + (int64_t)(v0 + row) * 64) + c)
-                     : "memory");
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  float px[27];
-  auto load_patch = [&](int v0) {
-    const int vo = v0 + t;
-    if (vo < total) {
-      int r = vo;
-      const int ow = r % g.Wo; r /= g.Wo;
-      const int oh = r % g.Ho; r /= g.Ho;
-      const int od = r % g.Do;
-      const int n = r / g.Do;
-      const float *xn = x + (int64_t)n * g.Di * g.Hi * g.Wi;
-#pragma unroll
-      for (int tap = 0; tap < 27; ++tap) {
-        const int id = od * g.s + tap / 9 - g.p, ih = oh * g.s + (tap / 3) % 3 - g.p, iw = ow * g.s + tap % 3 - g.p;
-        const bool ok = id >= 0 && id < g.Di && ih >= 0 && ih < g.Hi && iw >= 0 && iw < g.Wi;
-        px[tap] = ok ? __ldg(xn + ((int64_t)id * g.Hi + ih) * g.Wi + iw) : 0.f;
-      }
-    } else {
-#pragma unroll
-      for (int tap = 0; tap < 27; ++tap) px[tap] = 0.f;
-    }
-  };
-  const int stride = gridDim.x * SW_CH;
-  int v0 = blockIdx.x * SW_CH;
-  if (v0 < total) {
-    issue_raw(v0, 0);
-    load_patch(v0);
-  }
-  for (int k = 0; v0 < total; v0 += stride, ++k) {
-    const int buf = k & 1;
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();  // chunk k's rows landed; the previous chunk's MMAs are done with sdh / sp
-    const int vn = v0 + stride;
-    if (vn < total) issue_raw(vn, buf ^ 1);
-    // convert chunk k: dh = bf16(A d' + B h + C), rows past the end are zero
-    const uint8_t *rd = raw0 + buf * SWP_RAW, *rh = rd + SW_CH * 128;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int i = t + 256 * j, row = i >> 3, c = i & 7;
-      const uint4 dv = *reinterpret_cast<const uint4 *>(rd + row * 128 + c * 16);
-      const uint4 hv = *reinterpret_cast<const uint4 *>(rh + row * 128 + c * 16);
-      const __nv_bfloat162 *pd = reinterpret_cast<const __nv_bfloat162 *>(&dv);
-      const __nv_bfloat162 *ph = reinterpret_cast<const __nv_bfloat162 *>(&hv);
-      float o[8];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 a = __bfloat1622float2(pd[q]), b = __bfloat1622float2(ph[q]);
-        o[2 * q] = fmaf(cA[2 * q], a.x, fmaf(cB[2 * q], b.x, cC[2 * q]));
-        o[2 * q + 1] = fmaf(cA[2 * q + 1], a.y, fmaf(cB[2 * q + 1], b.y, cC[2 * q + 1]));
-      }
-      const bool live = v0 + row < total;
-      uint4 v;
-      __nv_bfloat162 *pv = reinterpret_cast<__nv_bfloat162 *>(&v);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) pv[q] = __floats2bfloat162_rn(live ? o[2 * q] : 0.f, live ? o[2 * q + 1] : 0.f);
-      *reinterpret_cast<uint4 *>(sdh + row * 128 + ((c ^ (row & 7)) << 4)) = v;
-    }
-    {
-      float *prow = sp + t * SW_PS;
-#pragma unroll
-      for (int tap = 0; tap < 27; ++tap) prow[tap] = px[tap];
-#pragma unroll
-      for (int tap = 27; tap < 32; ++tap) prow[tap] = 0.f;
-    }
-    if (vn < total) load_patch(vn);  // consumed next iteration
-    __syncthreads();
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const int vb = (warp + 8 * ks) * 16;
-      uint32_t a[4][4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int q = lane >> 3, row = vb + (lane & 7) + ((q >> 1) << 3), c = m * 2 + (q & 1);
-        const uint32_t addr = (uint32_t)__cvta_generic_to_shared(sdh + row * 128 + ((c ^ (row & 7)) << 4));
-        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(a[m][0]), "=r"(a[m][1]), "=r"(a[m][2]), "=r"(a[m][3])
-                     : "r"(addr));
-      }
-#pragma unroll
-      for (int n = 0; n < 4; ++n) {
-        const int col = n * 8 + gq;
-        const float p0 = sp[(vb + 2 * tq) * SW_PS + col], p1 = sp[(vb + 2 * tq + 1) * SW_PS + col];
-        const float p8 = sp[(vb + 2 * tq + 8) * SW_PS + col], p9 = sp[(vb + 2 * tq + 9) * SW_PS + col];
-        const float h0 = __bfloat162float(__float2bfloat16_rn(p0)), h1 = __bfloat162float(__float2bfloat16_rn(p1));
-        const float h8 = __bfloat162float(__float2bfloat16_rn(p8)), h9 = __bfloat162float(__float2bfloat16_rn(p9));
-        const uint32_t bh0 = pack_bf16x2(h0, h1), bh1 = pack_bf16x2(h8, h9);
-        const uint32_t bl0 = pack_bf16x2(p0 - h0, p1 - h1), bl1 = pack_bf16x2(p8 - h8, p9 - h9);
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          mma_bf16_16816(acc[m][n], a[m], bh0, bh1);
-          mma_bf16_16816(acc[m][n], a[m], bl0, bl1);
-        }
-      }
-    }
-  }
-  // fixed-order reduction of the 8 warps' 64 x 32 accumulators through smem
-  __syncthreads();
-  float *red = reinterpret_cast<float *>(sm);  // [8 warps][64][32]
-#pragma unroll
-  for (int m = 0; m < 4; ++m)
-#pragma unroll
-    for (int n = 0; n < 4; ++n)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int co = m * 16 + gq + ((r >> 1) << 3), tap = n * 8 + 2 * tq + (r & 1);
-        red[(warp * 64 + co) * 32 + tap] = acc[m][n][r];
-      }
-  __syncthreads();
-  for (int i = t; i < 64 * 27; i += 256) {
-    const int co = i / 27, tap = i % 27;
-    float sum = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) sum += red[(w * 64 + co) * 32 + tap];
-    part[(int64_t)blockIdx.x * 64 * 27 + co * 27 + tap] = sum;
-  }
-}
 
 // hx/coef (optional): the BN-backward apply fused into the staging, dh = bf16(A d' + B h + Cc)
 // with dh holding d' (bn_bwd_apply_k's arithmetic, coef = [A | B | Cc] per channel)
@@ -873,23 +709,6 @@ int stem_fprop_fast(DType dt, const ConvGeom &g, const float *x, const float *w,
   return P;
 }
 
-void stem_wgrad_fused_apply(const ConvGeom &g, const float *x, const void *dprime, const void *h, const float *coef,
-                            float *dw, float *ws, cudaStream_t st) {
-  if (g.Co != 64 || getenv("RN_STEM_SIMT")) throw Error(RN_ERR_ARG, "stem_wgrad_fused_apply: needs Co = 64");
-  if (!getenv("RN_STEM_WG_2PHASE") && g.out_vox() < (1LL << 31)) {
-    static uint64_t attr_devs = 0;  // kernel attributes are per device
-    if (!once_on_device(attr_devs)) {
-      CUDA_CHECK(cudaFuncSetAttribute(stem_wgrad_pipe_k, cudaFuncAttributeMaxDynamicSharedMemorySize, SWP_SMEM));
-          }
-    const int nb = std::min(stem_wgrad_blocks(g), 148);  // one CTA per SM (196 KB)
-    launch_k(stem_wgrad_pipe_k, nb, 256, SWP_SMEM, st, g, x, (const bf16 *)dprime, (const bf16 *)h, coef, ws);
-    LAUNCH_CHECK();
-    split_reduce_add(ws, nb, 64 * 27, dw, st);
-    return;
-  }
-  stem_wgrad_launch<bf16, 64>(g, x, dprime, dw, ws, st, h, coef);
-  LAUNCH_CHECK();
-}
 
 void stem_wgrad_fast(DType dt, const ConvGeom &g, const float *x, const void *dh, float *dw, float *ws,
                      cudaStream_t st) {

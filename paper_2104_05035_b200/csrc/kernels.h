@@ -44,9 +44,18 @@ size_t stem_wgrad_ws_floats(const ConvGeom &g);
 // part (optional): fused BN statistics partials [P][2][Co] of the stored output; returns P
 int stem_fprop_fast(DType dt, const ConvGeom &g, const float *x, const float *w, void *y, cudaStream_t st,
                     float *part = nullptr);
-// bf16, Co = 64: dW += sum dh x with dh = bf16(A d' + B h + Cc) formed in the staging (coef = [A|B|Cc])
-void stem_wgrad_fused_apply(const ConvGeom &g, const float *x, const void *dprime, const void *h, const float *coef,
-                            float *dw, float *ws, cudaStream_t st);
+// pooled stem backward (bf16, k3 s2 p1 conv, Ci = 1, Co in {8,16,32,64}; reading X23c):
+// dgamma / dbeta / dW (+=) from the pooled output y, its argmax am and gradient dy,
+// the input x and the stem weights, without any conv-resolution tensor
+// Gd [32][32] fp64: G = sum_v X_v X_v^T of the im2col rows, column 27 = sum_v X_v
+// (depends only on x: may run on another stream ahead of the backward)
+bool stem_bwd_sparse_supported(const ConvGeom &g);
+size_t stem_gram_ws_floats();
+size_t stem_bwd_sparse_ws_floats();
+void stem_gram(const ConvGeom &g, const float *x, float *ws, double *Gd, cudaStream_t st);
+void stem_bwd_sparse(const ConvGeom &g, int D2, int H2, int W2, const float *x, const float *w, const void *y,
+                     const void *dy, const uint8_t *am, const float *gamma, const float *mean, const float *invstd,
+                     const double *Gd, float *dgamma, float *dbeta, float *dw, float *ws, cudaStream_t st);
 void stem_wgrad_fast(DType dt, const ConvGeom &g, const float *x, const void *dh, float *dw, float *ws,
                      cudaStream_t st);
 
@@ -107,14 +116,6 @@ void att_bwd_finalize(DType dt, const void *dout, const void *m, const void *T_,
 // y = maxpool3(act(x*scale+shift)) (scale == nullptr: identity, no act); argmax uint8 (0..26)
 void maxpool_fwd(DType dt, const void *x, int N, int D, int H, int W, int C, const float *scale, const float *shift,
                  bool relu, void *y, uint8_t *argmax, int Do, int Ho, int Wo, cudaStream_t st);
-// bf16 pooled stem backward, part 1: d' = bf16(pool adjoint) * ReLU mask (recomputed
-// from h), BN-backward sums, last-block finalize (dgamma, dbeta, coef as bn_bwd_reduce_finalize)
-// partial: >= stem_pool_bwd_blocks() * 2 * C floats
-int stem_pool_bwd_blocks();
-void stem_pool_bwd(const void *dy, const uint8_t *argmax, const void *h, int N, int D, int H, int W, int C, int Do,
-                   int Ho, int Wo, const float *scale, const float *shift, const float *mean, const float *invstd,
-                   const float *gamma, float *dgamma, float *dbeta, float *coef, void *dprime, float *partial,
-                   unsigned *counter, cudaStream_t st);
 void maxpool_bwd(DType dt, const void *dy, const uint8_t *argmax, int N, int D, int H, int W, int C, int Do, int Ho,
                  int Wo, void *dx, bool accumulate, cudaStream_t st);
 struct UpTables {  // device pointers

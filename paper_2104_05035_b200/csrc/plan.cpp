@@ -216,8 +216,15 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
       L.stem_h = per_mb(act_bytes(u.cout, u.conv));
       L.out = per_mb(act_bytes(u.cout, u.out));
       if (u.pool) L.am = per_mb((size_t)mb * u.out.vol() * u.cout);
-      L.tmp0 = alloc(act_bytes(u.cout, u.conv));
-      L.tmp1 = alloc(act_bytes(u.cout, u.conv));
+      if (stem_sparse_bwd(u, L)) {
+        L.sws = alloc(sizeof(float) * stem_bwd_sparse_ws_floats());
+        L.gws = alloc(sizeof(float) * stem_gram_ws_floats());
+        L.gd = per_mb(sizeof(double) * 1024);
+        L.gd_fwd.assign(L.gd.size(), 0);
+      } else {
+        L.tmp0 = alloc(act_bytes(u.cout, u.conv));
+        L.tmp1 = alloc(act_bytes(u.cout, u.conv));
+      }
     } else if (u.kind == U_BLOCK) {
       make_block(L.blk, p0, u.cin, u.cout, u.stride, u.in);
       L.out = L.blk.out_;
@@ -350,6 +357,8 @@ Plan::~Plan() {
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_sgd) cudaEventDestroy(ev_sgd);
   if (ev_join) cudaEventDestroy(ev_join);
+  if (ev_gfork) cudaEventDestroy(ev_gfork);
+  if (ev_gjoin) cudaEventDestroy(ev_gjoin);
   for (int i = 0; i < 2; ++i) {
     if (ev_copied[i]) cudaEventDestroy(ev_copied[i]);
     if (ev_free[i]) cudaEventDestroy(ev_free[i]);
@@ -623,8 +632,12 @@ bool Plan::side_on() const {
   return on && !timing() && stream != nullptr && stream != cudaStreamLegacy && stream != cudaStreamPerThread;
 }
 
-void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32, const void *h_fused,
-                           const float *coef_fused) {
+// the bf16 pooled stem runs its backward at the pooled resolution (k_stem_bwd.cu)
+bool Plan::stem_sparse_bwd(const Unit &u, const UnitL &L) const {
+  return dt == DT_BF16 && u.pool && stem_bwd_sparse_supported(L.stem_conv.g);
+}
+
+void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32) {
   const bool t = timing();
   size_t e = t ? tk_begin(2, conv_flops(c.g)) : 0;
   cudaStream_t ws = stream;
@@ -640,11 +653,7 @@ void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x
     side_used = true;
   }
   int kind = K_SIMT;
-  if (coef_fused) {
-    kind = K_STEM;
-    stem_wgrad_fused_apply(c.g, (const float *)x, dy, h_fused, coef_fused, grad(c.w_idx), (float *)P(off_wgrad_ws),
-                           ws);
-  } else if (x_f32 && stem_fast_supported(c.g)) {
+  if (x_f32 && stem_fast_supported(c.g)) {
     kind = K_STEM;
     stem_wgrad_fast(dt, c.g, (const float *)x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), ws);
   } else if (!x_f32 && use_tc(c.g, false) && tc_wgrad_supported(c.g)) {
@@ -810,6 +819,26 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
   UnitL &L = units[ui];
   const void *x = unit_input(ui, k, x_in);
   if (u.kind == U_STEM) {
+    if (stem_sparse_bwd(u, L)) {
+      // the input Gram matrix of the pooled stem backward depends only on x: on the
+      // weight-gradient stream (idle in the forward), joined at the end of the forward
+      L.gd_fwd[k] = side_on();
+      if (L.gd_fwd[k]) {
+        if (!side) {
+          CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+          CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+          CUDA_CHECK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        }
+        if (!ev_gfork) {
+          CUDA_CHECK(cudaEventCreateWithFlags(&ev_gfork, cudaEventDisableTiming));
+          CUDA_CHECK(cudaEventCreateWithFlags(&ev_gjoin, cudaEventDisableTiming));
+        }
+        CUDA_CHECK(cudaEventRecord(ev_gfork, stream));
+        CUDA_CHECK(cudaStreamWaitEvent(side, ev_gfork, 0));
+        stem_gram(L.stem_conv.g, (const float *)x, (float *)P(L.gws), (double *)P(L.gd[k]), side);
+        gram_pending = true;
+      }
+    }
     {
       const bool t = timing();
       size_t e = t ? tk_begin(0, conv_flops(L.stem_conv.g)) : 0;
@@ -898,22 +927,18 @@ void Plan::unit_bwd(int ui, int k, const float *x_in) {
     const void *dy;
     int mode;
     const void *mt = nullptr;
-    auto it = opts.find("stem_bwd_fused");
-    const bool fuse = (it == opts.end() || it->second != 0) && u.pool && dt == DT_BF16 && u.cout == 64 &&
-                      stem_fast_supported(L.stem_conv.g) && !getenv("RN_STEM_SIMT");
-    if (fuse) {
-      // pool adjoint + ReLU mask + BN-backward sums/finalize in one pass (d' -> tmp0), the
-      // BN-backward apply inside the stem weight gradient (no dh tensor)
+    if (stem_sparse_bwd(u, L)) {
+      // pooled-resolution backward (reading X23c): sparse over the argmax voxels,
+      // dW through the input Gram matrix; no conv-resolution tensor is read or formed
       const BNL &b = L.stem_bn;
-      float *coef = (float *)P(off_coef);
-      {
-        EltTimer tm(this, F_STEM_POOL_BWD, (double)mb * u.cout * (3.0 * u.out.vol() + 4.0 * u.conv.vol()));
-        stem_pool_bwd(P(L.dout), (const uint8_t *)P(L.am[k]), P(L.stem_h[k]), mb, u.conv.d, u.conv.h, u.conv.w,
-                      u.cout, u.out.d, u.out.h, u.out.w, bn_stat(b, k, 2), bn_stat(b, k, 3), bn_stat(b, k, 0),
-                      bn_stat(b, k, 1), master(b.gamma_idx), grad(b.gamma_idx), grad(b.gamma_idx + 1), coef,
-                      P(L.tmp0), (float *)P(off_partial), counter(), stream);
-      }
-      conv_bwd_weight(L.stem_conv, x, P(L.tmp0), true, P(L.stem_h[k]), coef);
+      EltTimer tm(this, F_STEM_POOL_BWD,
+                  (double)mb * (u.cout * u.out.vol() * (2.0 * dt_size(dt) + 1.0) + 4.0 * u.in.vol()));
+      if (!L.gd_fwd[k])  // the forward did not compute the input Gram matrix on the side stream
+        stem_gram(L.stem_conv.g, (const float *)x, (float *)P(L.gws), (double *)P(L.gd[k]), stream);
+      stem_bwd_sparse(L.stem_conv.g, u.out.d, u.out.h, u.out.w, (const float *)x, master(L.stem_conv.w_idx),
+                      P(L.out[k]), P(L.dout), (const uint8_t *)P(L.am[k]), master(b.gamma_idx), bn_stat(b, k, 0),
+                      bn_stat(b, k, 1), (const double *)P(L.gd[k]), grad(b.gamma_idx), grad(b.gamma_idx + 1),
+                      grad(L.stem_conv.w_idx), (float *)P(L.sws), stream);
       return;
     }
     if (u.pool) {
@@ -1014,7 +1039,7 @@ bool Plan::saved(int ui, int k, const std::string &name, SavedRef &r) {
   if (u.kind == U_STEM) {
     if (name == "h") return act(L.stem_h[k], u.cout, u.conv);
     if (name == "bn.stats") return stats(L.stem_bn);
-    if (name == "d1") return act(L.tmp0, u.cout, u.conv);
+    if (name == "d1" && L.tmp0) return act(L.tmp0, u.cout, u.conv);
     if (name == "am" && u.pool) {
       r.ptr = P(L.am[k]);
       r.n = (int64_t)mb * u.out.vol() * u.cout;
@@ -1219,6 +1244,11 @@ void Plan::forward_body(const float *x_in, const int32_t *y, int k_only) {
         nccl_send_bytes(pipe_comm, P(units[ui].out[k]), act_bytes(u.cout, u.out), unit_stage[ui + 1], stream);
       }
     }
+  }
+  if (gram_pending) {  // join the stem's input Gram matrix (weight-gradient stream)
+    CUDA_CHECK(cudaEventRecord(ev_gjoin, side));
+    CUDA_CHECK(cudaStreamWaitEvent(stream, ev_gjoin, 0));
+    gram_pending = false;
   }
   if (S > 1 && !xfer_external) nccl_bcast_f32(pipe_comm, (float *)P(off_loss), 1, unit_stage[nu - 1], stream);
 }

@@ -67,6 +67,10 @@ struct UnitL {
   BNL stem_bn;
   std::vector<size_t> stem_h, am;
   size_t tmp0 = 0, tmp1 = 0;
+  size_t sws = 0;  // stem backward at pooled resolution (k_stem_bwd.cu): partial sums scratch
+  size_t gws = 0;  // its input Gram matrix: per-block partials scratch
+  std::vector<size_t> gd;     // per micro-batch: the fp64 Gram matrix [32][32]
+  std::vector<char> gd_fwd;   // per micro-batch: computed by the forward (weight-gradient stream)
   // block
   BlockL blk;
   // attention
@@ -183,8 +187,8 @@ struct Plan {
   StatsTarget dout_consumer(int ui, int k);
   // h_fused / coef_fused: stem only (bf16, 64 channels): dy holds d' and the BN-backward apply
   // dh = A d' + B h + Cc is formed inside the weight-gradient kernel
-  void conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32, const void *h_fused = nullptr,
-                       const float *coef_fused = nullptr);
+  void conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x_f32);
+  bool stem_sparse_bwd(const Unit &u, const UnitL &L) const;
   void bn_forward_stats(const BNL &b, int k, const void *h);
   void bn_fwd(const BNL &b, int k, const void *h, const void *res, const float *rscale, const float *rshift, bool relu,
               void *y);
@@ -213,6 +217,8 @@ struct Plan {
   // overlap the dgrad / BN chain and fill its tails (option "wgrad_stream")
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_gfork = nullptr, ev_gjoin = nullptr;  // the stem's input Gram matrix on the side stream
+  bool gram_pending = false;
   bool side_used = false;
   // data-parallel gradient all-reduce bucketed and overlapped with the backward
   // (option overlap_allreduce, default on when replicas > 1): bucket = a run of

@@ -188,17 +188,28 @@ def op_parity(depth, w, dims, N):
                 T.chk(ui, "out", acts[ui], Qb(pooled))
                 am_gpu = plan.get_saved(ui, "am", acts[ui].shape)
                 T.chk(ui, "am", am_gpu, am, "exact")
-                d1 = plan.get_saved(ui, "d1", (N,) + cd + (C,)).astype(np.float64)
-                T.chk(ui, "d1 (pool adjoint*mask)", d1,
-                      Qb(O.maxpool3_backward(douts[ui], am_gpu.astype(np.int64), a.shape)) * (a > 0))
-                dy = d1
             else:
                 T.chk(ui, "out", acts[ui], Qb(a))
-                dy = douts[ui] * (acts[ui] > 0)
-            dh, dgb, dbb = O.bn_backward(dy, cb, P[pre + ".bn.gamma"])
+            if u.extra["pool"] and C in O.STEM_POOLED_BWD_WIDTHS:
+                # reading X23c: pooled-resolution backward, nothing rounded at the conv
+                # resolution, the h-term of dh with the conv's unrounded output
+                dy = O.maxpool3_backward(douts[ui], am_gpu.astype(np.int64), a.shape) * (a > 0)
+                h_raw = O.conv3d(xin, P[pre + ".conv"], u.stride, 1)
+                A, B, Cc, dgb, dbb = O.bn_backward_coefs(dy, cb, P[pre + ".bn.gamma"], h=h_raw)
+                dh = A * dy + B * h_raw + Cc
+            else:
+                if u.extra["pool"]:
+                    d1 = plan.get_saved(ui, "d1", (N,) + cd + (C,)).astype(np.float64)
+                    T.chk(ui, "d1 (pool adjoint*mask)", d1,
+                          Qb(O.maxpool3_backward(douts[ui], am_gpu.astype(np.int64), a.shape)) * (a > 0))
+                    dy = d1
+                else:
+                    dy = douts[ui] * (acts[ui] > 0)
+                dh, dgb, dbb = O.bn_backward(dy, cb, P[pre + ".bn.gamma"])
+                dh = Qb(dh)
             T.chk(ui, pre + ".bn.gamma", G(pre + ".bn.gamma"), dgb, "f32")
             T.chk(ui, pre + ".bn.beta", G(pre + ".bn.beta"), dbb, "f32")
-            _, dW = O.conv3d_backward(xin, P[pre + ".conv"], Qb(dh), u.stride, 1, need_dx=False)
+            _, dW = O.conv3d_backward(xin, P[pre + ".conv"], dh, u.stride, 1, need_dx=False)
             T.chk(ui, pre + ".conv", G(pre + ".conv"), dW, "f32")
         elif u.kind == "block":
             ref_dx = check_block(T, plan, P, ui, pre, "", xin, douts[ui].astype(np.float64), G, 0, u.stride)

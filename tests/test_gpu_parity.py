@@ -261,35 +261,6 @@ def test_fused_bn_statistics_match_separate_pass():
     assert rel(g1[idx["u12.fc.weight"]], g0[idx["u12.fc.weight"]]) <= 2e-2
 
 
-def test_fused_stem_backward_matches_separate_kernels():
-    """The fused stem backward (pool adjoint + ReLU mask + BN-backward sums and
-    finalize in one pass, the BN-backward apply inside the stem weight-gradient
-    kernel) computes what maxpool_bwd + the BN reduce/finalize + bn_bwd_apply +
-    the stem weight gradient compute: same d' values, same bf16 dh rounding, the
-    sums differ only in summation order.  Everything upstream of the stem is the
-    same deterministic kernels, so the stem gradients agree to fp32 rounding."""
-    dims = (91, 109, 91)
-    grads = []
-    for fused in (1, 0):
-        plan = rn.Plan(rn.net_desc(18, 64, dims), 2, rn.RN_BF16)
-        plan.set_option("stem_bwd_fused", fused)
-        arrays = synthetic.perturb_params(plan.tensors, synthetic.init_params(plan.tensors, seed=0))
-        plan.set_params(np.concatenate([a.ravel() for a in arrays]).astype(np.float32))
-        x, y = synthetic.make_batch(2, *dims, seed=1)
-        plan.forward(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
-        plan.backward()
-        grads.append(plan.get_grads())
-    off, idx = 0, {}
-    for name, shape, kind in plan.tensors:
-        n = int(np.prod(shape))
-        idx[name] = slice(off, off + n)
-        off += n
-    g1, g0 = grads
-    assert np.array_equal(g1[idx["u1.conv1"]], g0[idx["u1.conv1"]])  # upstream of the stem: bitwise
-    for name in ("u0.conv", "u0.bn.gamma", "u0.bn.beta"):
-        assert rel(g1[idx[name]], g0[idx[name]]) <= 1e-4, name
-
-
 def test_recomputed_relu_mask_matches_mask_tensor():
     """Backward BN sums fused into the dgrad epilogues with the consumer's ReLU
     mask recomputed from h (h*scale + shift > 0, the forward apply's own fp32
