@@ -866,6 +866,245 @@ __global__ void __launch_bounds__(NTA) bn_bwd_apply_part_k(const T *__restrict__
 }
 
 // ---------------------------------------------------------------------------
+// Channel-sliced BN apply (default; RN_BN_APPLY_CS=0 falls back to the kernels
+// above).  Block = (slice of CS = 16 channels, chunk of voxel rows): it finalizes
+// only its 16 channels — 16 splits x 16 channels of threads, partials
+// k = s, s+16, ... of channel j summed in batches of 8 in fp32, fp64 across
+// batches and splits in fixed order (so every block of a slice computes the same
+// coefficients) — instead of every block reducing all P x 2C partials (the
+// prologue that dominated the apply: 4-8 us per launch, most of a stage-3/4
+// apply).  Rows are read 32 B (bf16) / 64 B (fp32) per slice: full sectors.
+// The chunk-0 block of a slice publishes its statistics / dgamma, dbeta.
+// ---------------------------------------------------------------------------
+constexpr int CS = 16, NTS = 256, CS_SPLIT = NTS / CS;
+
+// fp64 per-channel sums (a, b) of the slice's 16 channels over P partials [P][2][C]
+__device__ __forceinline__ void cs_sums(const float *part, int P, int C, int c0, double (*red)[NTS], double *sa,
+                                        double *sb) {
+  const int j = threadIdx.x % CS, sp = threadIdx.x / CS;
+  const int c = c0 + j;
+  double a = 0.0, b = 0.0;
+  for (int k0 = sp; k0 < P; k0 += 8 * CS_SPLIT) {
+    float va[8], vb[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int k = k0 + i * CS_SPLIT;
+      va[i] = k < P ? __ldcg(part + (int64_t)k * 2 * C + c) : 0.f;
+      vb[i] = k < P ? __ldcg(part + (int64_t)k * 2 * C + C + c) : 0.f;
+    }
+    float fa = 0.f, fb = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      fa += va[i];
+      fb += vb[i];
+    }
+    a += (double)fa;
+    b += (double)fb;
+  }
+  red[0][threadIdx.x] = a;
+  red[1][threadIdx.x] = b;
+  __syncthreads();
+  if (threadIdx.x < CS) {
+    double A = 0.0, B = 0.0;
+#pragma unroll
+    for (int q = 0; q < CS_SPLIT; ++q) {
+      A += red[0][q * CS + threadIdx.x];
+      B += red[1][q * CS + threadIdx.x];
+    }
+    sa[threadIdx.x] = A;
+    sb[threadIdx.x] = B;
+  }
+}
+
+// scale / shift of the slice's channels (smem), published by the chunk-0 block
+__device__ __forceinline__ void cs_coefs_fwd(const BnPart &q, int C, int c0, bool publish, double (*red)[NTS],
+                                             double *sa, double *sb, float *sc, float *sh) {
+  if (q.P >= 0) {
+    cs_sums(q.part, q.P, C, c0, red, sa, sb);
+    if (threadIdx.x < CS) {
+      const int c = c0 + threadIdx.x;
+      const double mu = sa[threadIdx.x] / (double)q.V;
+      double var = sb[threadIdx.x] / (double)q.V - mu * mu;
+      if (var < 0) var = 0;
+      const double is = 1.0 / sqrt(var + (double)q.eps);
+      const double scd = (double)q.gamma[c] * is;
+      const float s_ = (float)scd, h_ = (float)((double)q.beta[c] - mu * scd);
+      sc[threadIdx.x] = s_;
+      sh[threadIdx.x] = h_;
+      if (publish) {
+        q.mean[c] = (float)mu;
+        q.invstd[c] = (float)is;
+        q.scale[c] = s_;
+        q.shift[c] = h_;
+        if (q.run_mean) {
+          const double unb = q.V > 1 ? var * (double)q.V / (double)(q.V - 1) : var;
+          q.run_mean[c] = (float)((1.0 - q.momentum) * q.run_mean[c] + q.momentum * mu);
+          q.run_var[c] = (float)((1.0 - q.momentum) * q.run_var[c] + q.momentum * unb);
+        }
+      }
+    }
+  } else if (threadIdx.x < CS) {
+    sc[threadIdx.x] = q.scale[c0 + threadIdx.x];
+    sh[threadIdx.x] = q.shift[c0 + threadIdx.x];
+  }
+  __syncthreads();
+}
+
+// y = act(x*scale + shift + R) over the slice's channels, R = 0 | res | BN_r(res)
+template <typename T>
+__global__ void __launch_bounds__(NTS) bn_apply_cs_k(const T *__restrict__ x, int64_t V, int C, BnPart b, BnPart rb,
+                                                     const T *__restrict__ res, int relu, T *__restrict__ y,
+                                                     int nslice, int64_t rows_per_chunk) {
+  __shared__ double red[2][NTS];
+  __shared__ double sa[CS], sb[CS];
+  __shared__ float sc[CS], sh[CS], rsc[CS], rsh[CS];
+  constexpr int VEC = Vec<T>::N, VPR = CS / VEC, RPI = NTS / VPR;
+  const int slice = blockIdx.x % nslice, chunk = blockIdx.x / nslice;
+  const int c0 = slice * CS;
+  const int64_t r0 = (int64_t)chunk * rows_per_chunk, r1 = min(V, r0 + rows_per_chunk);
+  const int vi = threadIdx.x % VPR, rr = threadIdx.x / VPR;
+  const int cv = c0 + vi * VEC;
+  pdl_begin();
+  // the first batch of rows is in flight while the coefficients are finalized
+  uint4 xv[EU], rv[EU];
+#pragma unroll
+  for (int q = 0; q < EU; ++q) {
+    const int64_t r = r0 + rr + (int64_t)q * RPI;
+    if (r < r1) {
+      xv[q] = ld16(x + r * C + cv);
+      if (res) rv[q] = ld16(res + r * C + cv);
+    }
+  }
+  cs_coefs_fwd(b, C, c0, chunk == 0, red, sa, sb, sc, sh);
+  const bool rbn = rb.part != nullptr;
+  if (rbn) cs_coefs_fwd(rb, C, c0, chunk == 0, red, sa, sb, rsc, rsh);
+  float a[VEC], bb[VEC], ra[VEC], rbv[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    a[e] = sc[vi * VEC + e];
+    bb[e] = sh[vi * VEC + e];
+    ra[e] = rbn ? rsc[vi * VEC + e] : 1.f;
+    rbv[e] = rbn ? rsh[vi * VEC + e] : 0.f;
+  }
+  for (int64_t rb0 = r0 + rr; rb0 < r1; rb0 += (int64_t)EU * RPI) {
+    if (rb0 != r0 + rr) {
+#pragma unroll
+      for (int q = 0; q < EU; ++q) {
+        const int64_t r = rb0 + (int64_t)q * RPI;
+        if (r < r1) {
+          xv[q] = ld16(x + r * C + cv);
+          if (res) rv[q] = ld16(res + r * C + cv);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < EU; ++q) {
+      const int64_t r = rb0 + (int64_t)q * RPI;
+      if (r >= r1) break;
+      float v[VEC];
+      unpack16(xv[q], v, x);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) v[e] = fmaf(v[e], a[e], bb[e]);
+      if (res) {
+        float rf[VEC];
+        unpack16(rv[q], rf, x);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) v[e] += fmaf(rf[e], ra[e], rbv[e]);
+      }
+      if (relu) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) v[e] = fmaxf(v[e], 0.f);
+      }
+      store_vec(y + r * C + cv, v);
+    }
+  }
+}
+
+// dx = A dy' + B h + Cc over the slice's channels, dy' = dy * (mask > 0)
+template <typename T>
+__global__ void __launch_bounds__(NTS) bn_bwd_apply_cs_k(const T *__restrict__ dy, const T *__restrict__ h,
+                                                         const T *__restrict__ mask_t, int64_t V, int C, BnBwdPart b,
+                                                         T *__restrict__ dx, int nslice, int64_t rows_per_chunk) {
+  __shared__ double red[2][NTS];
+  __shared__ double sa[CS], sb[CS];
+  __shared__ float cA[CS], cB[CS], cC[CS];
+  constexpr int VEC = Vec<T>::N, VPR = CS / VEC, RPI = NTS / VPR;
+  const int slice = blockIdx.x % nslice, chunk = blockIdx.x / nslice;
+  const int c0 = slice * CS;
+  const int64_t r0 = (int64_t)chunk * rows_per_chunk, r1 = min(V, r0 + rows_per_chunk);
+  const int vi = threadIdx.x % VPR, rr = threadIdx.x / VPR;
+  const int cv = c0 + vi * VEC;
+  pdl_begin();
+  uint4 dv[EU], xv[EU], mv[EU];
+#pragma unroll
+  for (int q = 0; q < EU; ++q) {
+    const int64_t r = r0 + rr + (int64_t)q * RPI;
+    if (r < r1) {
+      dv[q] = ld16(dy + r * C + cv);
+      xv[q] = ld16(h + r * C + cv);
+      mv[q] = ld16(mask_t + r * C + cv);
+    }
+  }
+  if (b.P >= 0) {
+    cs_sums(b.part, b.P, C, c0, red, sa, sb);
+    if (threadIdx.x < CS) {
+      const int c = c0 + threadIdx.x;
+      const double S1 = sa[threadIdx.x], is = b.invstd[c], mu = b.mean[c];
+      const double S2 = is * sb[threadIdx.x];  // sum dy' * xhat
+      const double m1 = S1 / (double)b.V, m2 = S2 / (double)b.V;
+      const double A = (double)b.gamma[c] * is;
+      cA[threadIdx.x] = (float)A;
+      cB[threadIdx.x] = (float)(-A * is * m2);
+      cC[threadIdx.x] = (float)(-A * m1 + A * is * mu * m2);
+      if (chunk == 0) {
+        b.dgamma[c] += (float)S2;
+        b.dbeta[c] += (float)S1;
+      }
+    }
+  } else if (threadIdx.x < CS) {
+    cA[threadIdx.x] = b.coef[c0 + threadIdx.x];
+    cB[threadIdx.x] = b.coef[C + c0 + threadIdx.x];
+    cC[threadIdx.x] = b.coef[2 * C + c0 + threadIdx.x];
+  }
+  __syncthreads();
+  float A[VEC], B[VEC], Cc[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    A[e] = cA[vi * VEC + e];
+    B[e] = cB[vi * VEC + e];
+    Cc[e] = cC[vi * VEC + e];
+  }
+  for (int64_t rb0 = r0 + rr; rb0 < r1; rb0 += (int64_t)EU * RPI) {
+    if (rb0 != r0 + rr) {
+#pragma unroll
+      for (int q = 0; q < EU; ++q) {
+        const int64_t r = rb0 + (int64_t)q * RPI;
+        if (r < r1) {
+          dv[q] = ld16(dy + r * C + cv);
+          xv[q] = ld16(h + r * C + cv);
+          mv[q] = ld16(mask_t + r * C + cv);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < EU; ++q) {
+      const int64_t r = rb0 + (int64_t)q * RPI;
+      if (r >= r1) break;
+      float d[VEC], xf[VEC], m[VEC], o[VEC];
+      unpack16(dv[q], d, dy);
+      unpack16(xv[q], xf, h);
+      unpack16(mv[q], m, h);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const float dd = m[e] > 0.f ? d[e] : 0.f;
+        o[e] = fmaf(A[e], dd, fmaf(B[e], xf[e], Cc[e]));
+      }
+      store_vec(dx + r * C + cv, o);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Stem Conv block tail (reading X4: BN + ReLU + max-pool k3 s2 p1), bf16.
 // Forward: the stem conv wrote its BN statistics partials; every block
 // finalizes them, and the pool compares RAW h values: max and first argmax of
@@ -1520,6 +1759,21 @@ int bn_bwd_partials(DType dt, const void *dy, const void *h, const void *mask_t,
   return nblk;
 }
 
+// channel-sliced for the small tensors of stages 2-4, where the partials reduce
+// dominated; the full-row kernels stay faster for stage 1 (7.6 M elements:
+// 11-15 us sliced vs 10-12 us per launch measured)
+static bool bn_apply_cs(int64_t V, int C) {
+  static const bool v = !getenv("RN_BN_APPLY_CS") || atoi(getenv("RN_BN_APPLY_CS")) != 0;
+  return v && C % CS == 0 && V * C <= ((int64_t)4 << 20);
+}
+// slices x chunks: about two blocks of 256 threads per SM, chunks of whole rows
+static void cs_grid(int64_t V, int C, int &nslice, int &nchunk, int64_t &rpc) {
+  nslice = C / CS;
+  nchunk = (int)std::max<int64_t>(1, std::min<int64_t>((2 * 148 + nslice - 1) / nslice, (V + 63) / 64));
+  rpc = (V + nchunk - 1) / nchunk;
+  nchunk = (int)((V + rpc - 1) / rpc);
+}
+
 void bn_apply_fused(DType dt, const void *x, int64_t V, int C, const BnFinal &f, const BnFinal *rf, const void *res,
                     bool relu, void *y, cudaStream_t st) {
   auto mk = [&](const BnFinal &q) {
@@ -1539,6 +1793,15 @@ void bn_apply_fused(DType dt, const void *x, int64_t V, int C, const BnFinal &f,
       r.P = -1;
     }
   }
+  if (bn_apply_cs(V, C)) {
+    int nslice, nchunk;
+    int64_t rpc;
+    cs_grid(V, C, nslice, nchunk, rpc);
+    DISPATCH(dt, launch_k(bn_apply_cs_k<T>, (unsigned)(nslice * nchunk), NTS, 0, st, (const T *)x, V, C, b, r,
+                          (const T *)res, relu ? 1 : 0, (T *)y, nslice, rpc));
+    LAUNCH_CHECK();
+    return;
+  }
   const size_t smem = (2 * (size_t)C + 2 * NTA) * sizeof(double) + 4 * (size_t)C * sizeof(float);
   DISPATCH(dt, launch_k(bn_apply_part_k<T>, grid_part(V * C / Vec<T>::N, C / Vec<T>::N), NTA, smem, st, (const T *)x, V, C, b, r,
                         (const T *)res, relu ? 1 : 0, (T *)y));
@@ -1553,6 +1816,15 @@ void bn_bwd_apply_fused(DType dt, const void *dy, const void *h, const void *mas
     launch_k(bn_fin_bwd_k, (unsigned)((C + 31) / 32), 256, 0, st, b, C);
     LAUNCH_CHECK();
     b.P = -1;
+  }
+  if (bn_apply_cs(V, C)) {
+    int nslice, nchunk;
+    int64_t rpc;
+    cs_grid(V, C, nslice, nchunk, rpc);
+    DISPATCH(dt, launch_k(bn_bwd_apply_cs_k<T>, (unsigned)(nslice * nchunk), NTS, 0, st, (const T *)dy,
+                          (const T *)h, (const T *)mask_t, V, C, b, (T *)dx, nslice, rpc));
+    LAUNCH_CHECK();
+    return;
   }
   const size_t smem = (2 * (size_t)C + 2 * NTA) * sizeof(double) + 3 * (size_t)C * sizeof(float);
   DISPATCH(dt, launch_k(bn_bwd_apply_part_k<T>, grid_part(V * C / Vec<T>::N, C / Vec<T>::N), NTA, smem, st, (const T *)dy,
