@@ -417,9 +417,11 @@ rn_status rn_query(rn_plan_t plan, const char *key, double *value);
  *  single-CTA tcgen05 kernel, 4 = CTA-pair (cta_group::2) kernel with resident
  *  weights, 5 = the generic implicit GEMM on CTA pairs (M = 256 MMAs, half of B
  *  per CTA) for every launch with 128- / 256-wide N tiles, split-K included (the
- *  plan uses pairs for the launches without split-K) — 3 and 4 only for
- *  64 -> 64 stride-1 3x3x3 ops 0/1, 5 for ops 0/1 (RN_ERR_ARG when an explicitly
- *  requested kernel does not take the conv).  Device pointers,
+ *  plan uses pairs for the launches without split-K), 6 = the streaming
+ *  warp-tensor-core kernel for 64 -> 64 1x1x1 stride-1 convs over >= 16384
+ *  voxels (k_conv1x1.cu) — 3 and 4 only for 64 -> 64 stride-1 3x3x3 ops 0/1,
+ *  5 and 6 for ops 0/1 (RN_ERR_ARG when an explicitly requested kernel does not
+ *  take the conv).  Device pointers,
  *  stream-ordered on `stream`; scratch is allocated internally.
  * Errors: RN_ERR_ARG, RN_ERR_CUDA. */
 rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const void *a_dev, const void *b_dev,

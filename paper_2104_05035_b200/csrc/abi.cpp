@@ -544,7 +544,7 @@ rn_status rn_query(rn_plan_t plan, const char *key, double *value) {
 rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const void *a_dev, const void *b_dev,
                        void *out_dev, int32_t impl, void *stream) {
   GUARD_BEGIN
-  if (!geom || !a_dev || !b_dev || !out_dev || op < 0 || op > 2 || impl < 0 || impl > 5 ||
+  if (!geom || !a_dev || !b_dev || !out_dev || op < 0 || op > 2 || impl < 0 || impl > 6 ||
       (dtype != RN_F32 && dtype != RN_BF16))
     return set_error(RN_ERR_ARG, "rn_op_conv3d: bad arguments");
   ConvGeom g;
@@ -567,6 +567,20 @@ rn_status rn_op_conv3d(int32_t dtype, int32_t op, const int32_t *geom, const voi
   if (impl == 3 && !halo_ok) return set_error(RN_ERR_ARG, "rn_op_conv3d: haloed kernel does not take this conv");
   const bool pair_ok = dt == DT_BF16 && op != 2 && pair_conv_supported(g, op == 1);
   if (impl == 4 && !pair_ok) return set_error(RN_ERR_ARG, "rn_op_conv3d: CTA-pair kernel does not take this conv");
+  const bool c1_ok = dt == DT_BF16 && op != 2 && conv1x1_supported(g);
+  if (impl == 6 && !c1_ok) return set_error(RN_ERR_ARG, "rn_op_conv3d: 1x1x1 streaming kernel does not take this conv");
+  if ((impl == 6 || impl == 0) && c1_ok) {
+    if (op == 0) {
+      conv1x1(g, (const bf16 *)a_dev, (const bf16 *)b_dev, nullptr, (bf16 *)out_dev, st);
+    } else {
+      void *wd = nullptr;
+      CUDA_CHECK(cudaMallocAsync(&wd, (size_t)g.Co * g.Ci * 2, st));
+      flip_weights(dt, b_dev, g.Co, g.taps(), g.Ci, wd, st);
+      conv1x1(g, (const bf16 *)a_dev, (const bf16 *)wd, nullptr, (bf16 *)out_dev, st);
+      CUDA_CHECK(cudaFreeAsync(wd, st));
+    }
+    return RN_OK;
+  }
   if ((impl == 4 || impl == 0) && pair_ok) {
     if (op == 0) {
       conv_pair(g, false, (const bf16 *)a_dev, (const bf16 *)b_dev, nullptr, (bf16 *)out_dev, false, nullptr, nullptr,

@@ -500,6 +500,11 @@ bool Plan::use_pair() const {
   auto it = opts.find("pair_conv");
   return it == opts.end() || it->second != 0;
 }
+// the streaming warp-tensor-core kernel for the 64 -> 64 1x1x1 convs (option c1x1, default on)
+bool Plan::use_c1x1() const {
+  auto it = opts.find("c1x1");
+  return it == opts.end() || it->second != 0;
+}
 
 bool Plan::use_tc(const ConvGeom &g, bool dgrad) const {
   if (dt != DT_BF16) return false;
@@ -525,7 +530,10 @@ void Plan::conv_fwd(const ConvL &c, const void *x, void *y, const float *bias, B
     es.mode = 1;
   }
   int parts = 0, kind = K_SIMT;
-  if (use_tc(c.g, false) && use_pair() && pair_conv_supported(c.g, false) && ((kind = K_PAIR) != 0))
+  if (use_tc(c.g, false) && use_c1x1() && conv1x1_supported(c.g) && ((kind = K_TC) != 0))
+    parts = conv1x1(c.g, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, stream,
+                    want ? &es : nullptr);
+  else if (use_tc(c.g, false) && use_pair() && pair_conv_supported(c.g, false) && ((kind = K_PAIR) != 0))
     parts = conv_pair(c.g, false, (const bf16 *)x, (const bf16 *)P(shadow_f[c.w_idx]), bias, (bf16 *)y, false,
                       nullptr, nullptr, stream, want ? &es : nullptr);
   else if (use_tc(c.g, false) && use_halo() && halo_conv_supported(c.g, false) && ((kind = K_HALO) != 0))
@@ -560,7 +568,11 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
   // (~8 us), so by default they are left to bn_backward (option pair_bwd_stats)
   auto itp = opts.find("pair_bwd_stats");
   const bool pair_stats = itp != opts.end() && itp->second != 0;
-  if (use_tc(c.g, true) && use_pair() && pair_conv_supported(c.g, true) && ((kind = K_PAIR) != 0))
+  if (use_tc(c.g, true) && use_c1x1() && conv1x1_supported(c.g) && !accumulate && !res && (!want || es.mode == 3) &&
+      ((kind = K_TC) != 0))
+    parts = conv1x1(c.g, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx, stream,
+                    want ? &es : nullptr);
+  else if (use_tc(c.g, true) && use_pair() && pair_conv_supported(c.g, true) && ((kind = K_PAIR) != 0))
     parts = conv_pair(c.g, true, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx,
                       accumulate, (const bf16 *)res, (const bf16 *)res_mask, stream,
                       want && pair_stats ? &es : nullptr);

@@ -175,6 +175,7 @@ struct Plan {
   bool use_tc(const ConvGeom &g, bool dgrad) const;
   bool use_halo() const;
   bool use_pair() const;
+  bool use_c1x1() const;
   bool recompute_mask() const;
   void conv_fwd(const ConvL &c, const void *x, void *y, const float *bias = nullptr, BNL *stats = nullptr);
   void conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumulate, const void *res,

@@ -5,7 +5,8 @@ Tolerance: fp32 accumulation + one bf16 rounding of the output ->
 per-tensor relative L2 error <= 4e-3 AND element-wise |err| <= 2^-7 |ref| +
 2^-9 max|ref| (bf16 outputs; fp32 weight gradients: 1e-4 rel-L2 and 1e-3 |ref|
 + 1e-5 max|ref|).  impl 5 runs the persistent kernel
-on CTA pairs (cta_group::2) for every launch it takes, split-K included."""
+on CTA pairs (cta_group::2) for every launch it takes, split-K included; impl 6
+the streaming mma.sync kernel of the 64 -> 64 1x1x1 convs (k_conv1x1.cu)."""
 import numpy as np
 import pytest
 import torch
@@ -48,12 +49,14 @@ def elem_ok(a, b, r=2.0 ** -7, t=2.0 ** -9):
     return bool((err <= bound).all()), float((err / bound).max())
 
 
-@pytest.mark.parametrize("impl", [5, 4, 3, 2, 1])
+@pytest.mark.parametrize("impl", [6, 5, 4, 3, 2, 1])
 @pytest.mark.parametrize("cv", CONVS, ids=[c[0] for c in CONVS])
 def test_conv_fprop_dgrad(cv, impl):
     name, Di, Hi, Wi, Ci, Co, k, s, p = cv
     if impl in (3, 4) and not (Ci == 64 and Co == 64 and k == 3 and s == 1):
         pytest.skip("haloed / CTA-pair kernels: 64->64 stride-1 3x3x3 only")
+    if impl == 6 and not (Ci == 64 and Co == 64 and k == 1 and s == 1):
+        pytest.skip("streaming 1x1x1 kernel: 64->64 stride-1 1x1x1 only")
     N = 2
     Do, Ho, Wo = (O.conv_out(v, k, s, p) for v in (Di, Hi, Wi))
     rng = np.random.default_rng(0)
