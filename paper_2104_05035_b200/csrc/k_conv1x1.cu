@@ -7,7 +7,7 @@
 // (mma.sync m16n8k16, bf16 -> fp32) rather than a tcgen05 one: the weights stay
 // in smem (ldmatrix per tile), x tiles (128 voxels) stream through a cp.async double buffer,
 // the output leaves through a swizzled smem tile as full-line stores, and the
-// BatchNorm statistics (bnstats.cuh modes 1 and 3) accumulate per thread in
+// BatchNorm statistics (bnstats.cuh modes 1, 2, 3) accumulate per thread in
 // registers across tiles — one [2][64] partial per block, no per-row warp
 // transposes (what made the persistent tcgen05 kernel epilogue-bound here:
 // 20-40 us per launch for a 5 us roofline).
@@ -66,12 +66,12 @@ __device__ __forceinline__ void c1_stage(const C1Args &a, int64_t t, uint32_t xs
     const bool ok = r0 + r < a.V;
     const int64_t g = ok ? (r0 + r) * 64 + j * 8 : 0;
     cp16(xs + swz(r, j), a.x + g, ok);
-    if (MODE == 3) cp16(hs + swz(r, j), a.st.h + g, ok);
+    if (MODE >= 2) cp16(hs + swz(r, j), a.st.h + g, ok);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-template <int MODE>  // 0 no statistics, 1 forward (sum y, sum y^2), 3 backward (recomputed ReLU mask)
+template <int MODE>  // 0 no statistics, 1 forward (sum y, sum y^2), 2 / 3 backward (mask tensor / recomputed)
 __global__ void __launch_bounds__(C1_THREADS, 2) conv1x1_k(const C1Args a) {
   extern __shared__ __align__(128) uint8_t sm[];
   uint8_t *sW = sm, *sX = sm + 8192, *sH = sX + 2 * 16384, *sO = sH + 2 * 16384;
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(C1_THREADS, 2) conv1x1_k(const C1Args a) {
   if (threadIdx.x < 64) {
     const int n = threadIdx.x;
     sb[n] = a.bias ? a.bias[n] : 0.f;
-    smu[n] = MODE == 3 ? a.st.mean[n] : 0.f;
+    smu[n] = MODE >= 2 ? a.st.mean[n] : 0.f;
     sms[n] = MODE == 3 ? a.st.mscale[n] : 0.f;
     smh[n] = MODE == 3 ? a.st.mshift[n] : 0.f;
   }
@@ -156,10 +156,18 @@ __global__ void __launch_bounds__(C1_THREADS, 2) conv1x1_k(const C1Args a) {
             s2[2 * nt + 1] = fmaf(of.y, of.y, s2[2 * nt + 1]);
           } else {
             const float2 hv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(hb + off));
-            const float2 msv = *reinterpret_cast<const float2 *>(sms + n), mhv = *reinterpret_cast<const float2 *>(smh + n);
             const float2 muv = *reinterpret_cast<const float2 *>(smu + n);
-            const float d0 = fmaf(hv.x, msv.x, mhv.x) > 0.f ? of.x : 0.f;
-            const float d1 = fmaf(hv.y, msv.y, mhv.y) > 0.f ? of.y : 0.f;
+            float2 mv;
+            if (MODE == 3) {  // the consumer's ReLU mask recomputed from h
+              const float2 msv = *reinterpret_cast<const float2 *>(sms + n);
+              const float2 mhv = *reinterpret_cast<const float2 *>(smh + n);
+              mv = make_float2(fmaf(hv.x, msv.x, mhv.x), fmaf(hv.y, msv.y, mhv.y));
+            } else {  // mode 2: the stored mask tensor (non-default path; read in place)
+              mv = __bfloat1622float2(
+                  __ldg(reinterpret_cast<const __nv_bfloat162 *>(a.st.mask + (row0 + r) * 64 + n)));
+            }
+            const float d0 = mv.x > 0.f ? of.x : 0.f;
+            const float d1 = mv.y > 0.f ? of.y : 0.f;
             s1[2 * nt] += d0;
             s2[2 * nt] = fmaf(d0, hv.x - muv.x, s2[2 * nt]);
             s1[2 * nt + 1] += d1;
@@ -217,7 +225,7 @@ bool conv1x1_supported(const ConvGeom &g) {
 int conv1x1(const ConvGeom &g, const bf16 *x, const bf16 *w, const float *bias, bf16 *y, cudaStream_t st,
             const EpiStats *stats) {
   const int mode = stats ? stats->mode : 0;
-  if (!conv1x1_supported(g) || (mode != 0 && mode != 1 && mode != 3))
+  if (!conv1x1_supported(g) || mode < 0 || mode > 3)
     throw Error(RN_ERR_ARG, "conv1x1: unsupported geometry / statistics mode");
   C1Args a{x, w, bias, y, g.out_vox(), stats ? *stats : EpiStats()};
   int dev = 0, nsm = 148;
@@ -229,10 +237,12 @@ int conv1x1(const ConvGeom &g, const bf16 *x, const bf16 *w, const float *bias, 
   if (!once_on_device(attr_devs)) {
     CUDA_CHECK(cudaFuncSetAttribute(conv1x1_k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, C1_SMEM));
     CUDA_CHECK(cudaFuncSetAttribute(conv1x1_k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, C1_SMEM));
+    CUDA_CHECK(cudaFuncSetAttribute(conv1x1_k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, C1_SMEM));
     CUDA_CHECK(cudaFuncSetAttribute(conv1x1_k<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, C1_SMEM));
   }
   if (mode == 0) launch_k(conv1x1_k<0>, grid, C1_THREADS, C1_SMEM, st, a);
   else if (mode == 1) launch_k(conv1x1_k<1>, grid, C1_THREADS, C1_SMEM, st, a);
+  else if (mode == 2) launch_k(conv1x1_k<2>, grid, C1_THREADS, C1_SMEM, st, a);
   else launch_k(conv1x1_k<3>, grid, C1_THREADS, C1_SMEM, st, a);
   LAUNCH_CHECK();
   return mode ? (int)grid : 0;

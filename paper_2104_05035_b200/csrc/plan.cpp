@@ -568,7 +568,7 @@ void Plan::conv_bwd_data(const ConvL &c, const void *dy, void *dx, bool accumula
   // (~8 us), so by default they are left to bn_backward (option pair_bwd_stats)
   auto itp = opts.find("pair_bwd_stats");
   const bool pair_stats = itp != opts.end() && itp->second != 0;
-  if (use_tc(c.g, true) && use_c1x1() && conv1x1_supported(c.g) && !accumulate && !res && (!want || es.mode == 3) &&
+  if (use_tc(c.g, true) && use_c1x1() && conv1x1_supported(c.g) && !accumulate && !res &&
       ((kind = K_TC) != 0))
     parts = conv1x1(c.g, (const bf16 *)dy, (const bf16 *)P(shadow_d[c.w_idx]), nullptr, (bf16 *)dx, stream,
                     want ? &es : nullptr);

@@ -44,7 +44,7 @@ int conv_pair(const ConvGeom &g, bool dgrad, const __nv_bfloat16 *src, const __n
 
 // 64 -> 64 channel 1x1x1 stride-1 convs over >= 16 K voxels (k_conv1x1.cu, warp tensor
 // cores, streaming): y = x w^T (+ bias) with w [n][k] (forward copy, or the dgrad copy for
-// the data gradient); est modes 0 / 1 / 3; returns the BN-statistics partial count
+// the data gradient); est modes 0-3; returns the BN-statistics partial count
 bool conv1x1_supported(const ConvGeom &g);
 int conv1x1(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, const float *bias, __nv_bfloat16 *y,
             cudaStream_t st, const EpiStats *est = nullptr);
