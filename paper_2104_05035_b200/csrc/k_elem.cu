@@ -1673,6 +1673,17 @@ int chan_fin_blocks(int64_t V, int C) {
   return (int)b;
 }
 
+// partials-only passes (their consumer, a BN apply, reduces the partials of the
+// channels it needs: the channel-sliced applies 16 at a time): one block per ~8K
+// elements, at most one per SM — small stage-3/4 tensors get 4x the blocks of the
+// last-block-finalize passes above (a 16-block pass was a 10 us latency chain)
+int chan_part_blocks(int64_t V, int C) {
+  int64_t b = (V * C + 8191) / 8192;
+  if (b > 148) b = 148;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
 void bn_stats_finalize(DType dt, const void *x, int64_t V, int C, float *partial, unsigned *counter,
                        const float *gamma, const float *beta, float *mean, float *invstd, float *scale, float *shift,
                        float *run_mean, float *run_var, float momentum, float eps, cudaStream_t st) {
@@ -1733,7 +1744,7 @@ void bn_bwd_apply(DType dt, const void *dy, const void *x, int64_t V, int C, int
 }
 
 int bn_stats_partials(DType dt, const void *x, int64_t V, int C, float *part, cudaStream_t st) {
-  const int nblk = chan_fin_blocks(V, C);
+  const int nblk = chan_part_blocks(V, C);
   DISPATCH(dt, {
     int64_t rpb;
     size_t smem;
@@ -1747,7 +1758,7 @@ int bn_stats_partials(DType dt, const void *x, int64_t V, int C, float *part, cu
 
 int bn_bwd_partials(DType dt, const void *dy, const void *h, const void *mask_t, const float *mean, int64_t V, int C,
                     float *part, cudaStream_t st) {
-  const int nblk = chan_fin_blocks(V, C);
+  const int nblk = chan_part_blocks(V, C);
   DISPATCH(dt, {
     int64_t rpb;
     size_t smem;
