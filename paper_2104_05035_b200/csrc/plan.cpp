@@ -281,6 +281,7 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
   off_counter = alloc(256);  // last-block tickets of the fused reduce+finalize kernels (zeroed at bind)
   off_wgrad_ws = alloc(sizeof(float) * (wgrad_ws_floats ? wgrad_ws_floats : 1));
   off_conv_ws = alloc(sizeof(float) * (conv_ws_floats ? conv_ws_floats : 1));
+  off_conv_ws2 = alloc(sizeof(float) * (conv_ws_floats ? conv_ws_floats : 1));
   size_t up_floats = 1;
   for (int ui = 0; ui < (int)net.units.size(); ++ui) {
     const Unit &u = net.units[ui];
@@ -358,6 +359,9 @@ Plan::~Plan() {
   if (ev_sgd) cudaEventDestroy(ev_sgd);
   if (ev_join) cudaEventDestroy(ev_join);
   if (ev_gfork) cudaEventDestroy(ev_gfork);
+  if (ev_bfork) cudaEventDestroy(ev_bfork);
+  if (ev_bjoin) cudaEventDestroy(ev_bjoin);
+  if (bstream) cudaStreamDestroy(bstream);
   if (ev_gjoin) cudaEventDestroy(ev_gjoin);
   for (int i = 0; i < 2; ++i) {
     if (ev_copied[i]) cudaEventDestroy(ev_copied[i]);
@@ -500,6 +504,16 @@ bool Plan::use_pair() const {
   auto it = opts.find("pair_conv");
   return it == opts.end() || it->second != 0;
 }
+// attention mask branch concurrent with the trunk (option att_branch, default on; eager
+// per-kernel timing and the default / legacy stream run it in order)
+bool Plan::att_branch_on() const {
+  auto it = opts.find("att_branch");
+  static const bool env_off = getenv("RN_ATT_BRANCH") && atoi(getenv("RN_ATT_BRANCH")) == 0;  // A/B
+  const bool on = (it == opts.end() || it->second != 0) && !env_off;
+  // the fp32 / unfused BN paths share reduction scratch (off_partial, counter) across units
+  return on && dt == DT_BF16 && fused_stats() && !timing() && stream != nullptr && stream != cudaStreamLegacy && stream != cudaStreamPerThread;
+}
+
 // the streaming warp-tensor-core kernel for the 64 -> 64 1x1x1 convs (option c1x1, default on)
 bool Plan::use_c1x1() const {
   auto it = opts.find("c1x1");
@@ -883,21 +897,49 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
   } else if (u.kind == U_ATT) {
     const int C = u.cout;
     const int64_t V = (int64_t)mb * u.in.vol();
+    // the soft-mask branch depends only on x: on its own stream, concurrent with the
+    // trunk (P:364 out = (1 + sigmoid(mask)) * trunk; the branches meet in att_fwd)
+    const bool br = att_branch_on();
+    if (br) {
+      if (!bstream) {
+        CUDA_CHECK(cudaStreamCreateWithFlags(&bstream, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaEventCreateWithFlags(&ev_bfork, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventCreateWithFlags(&ev_bjoin, cudaEventDisableTiming));
+      }
+      CUDA_CHECK(cudaEventRecord(ev_bfork, stream));
+      CUDA_CHECK(cudaStreamWaitEvent(bstream, ev_bfork, 0));
+      std::swap(stream, bstream);
+      std::swap(off_conv_ws, off_conv_ws2);
+    }
+    try {
+      {
+      EltTimer tm(this, F_MAXPOOL_FWD, (double)mb * C * (u.in.vol() * dt_size(dt) + u.mask.vol() * (dt_size(dt) + 1.0)));
+      maxpool_fwd(dt, x, mb, u.in.d, u.in.h, u.in.w, C, nullptr, nullptr, false, P(L.u0[k]), (uint8_t *)P(L.am[k]),
+                  u.mask.d, u.mask.h, u.mask.w, stream);
+      }
+      block_fwd(L.mask, k, P(L.u0[k]));
+      {
+      EltTimer tm(this, F_UP_FWD, (double)mb * C * (u.in.vol() + u.mask.vol()) * dt_size(dt));
+      upsample_fwd(dt, P(L.mask.out_[k]), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.up[k]), u.in.d, u.in.h, u.in.w,
+                   L.tab, stream);
+      }
+      conv_fwd(L.mc1, P(L.up[k]), P(L.mh[k]), nullptr, &L.mbn);
+      bn_fwd(L.mbn, k, P(L.mh[k]), nullptr, nullptr, nullptr, true, P(L.r[k]));
+      conv_fwd(L.mc2, P(L.r[k]), P(L.m[k]), master(L.bias_idx));
+    } catch (...) {
+      if (br) {
+        std::swap(stream, bstream);
+        std::swap(off_conv_ws, off_conv_ws2);
+      }
+      throw;
+    }
+    if (br) {
+      CUDA_CHECK(cudaEventRecord(ev_bjoin, stream));
+      std::swap(stream, bstream);
+      std::swap(off_conv_ws, off_conv_ws2);
+    }
     block_fwd(L.trunk, k, x);
-    {
-    EltTimer tm(this, F_MAXPOOL_FWD, (double)mb * C * (u.in.vol() * dt_size(dt) + u.mask.vol() * (dt_size(dt) + 1.0)));
-    maxpool_fwd(dt, x, mb, u.in.d, u.in.h, u.in.w, C, nullptr, nullptr, false, P(L.u0[k]), (uint8_t *)P(L.am[k]),
-                u.mask.d, u.mask.h, u.mask.w, stream);
-    }
-    block_fwd(L.mask, k, P(L.u0[k]));
-    {
-    EltTimer tm(this, F_UP_FWD, (double)mb * C * (u.in.vol() + u.mask.vol()) * dt_size(dt));
-    upsample_fwd(dt, P(L.mask.out_[k]), mb, u.mask.d, u.mask.h, u.mask.w, C, P(L.up[k]), u.in.d, u.in.h, u.in.w,
-                 L.tab, stream);
-    }
-    conv_fwd(L.mc1, P(L.up[k]), P(L.mh[k]), nullptr, &L.mbn);
-    bn_fwd(L.mbn, k, P(L.mh[k]), nullptr, nullptr, nullptr, true, P(L.r[k]));
-    conv_fwd(L.mc2, P(L.r[k]), P(L.m[k]), master(L.bias_idx));
+    if (br) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_bjoin, 0));
     EltTimer tm(this, F_ATT_FWD, 3.0 * V * C * dt_size(dt));
     att_fwd(dt, P(L.m[k]), P(L.trunk.out_[k]), V, C, P(L.out[k]), stream);
   } else {

@@ -217,6 +217,12 @@ struct Plan {
   // at the end of the backward): they are leaves of the backward graph, so they
   // overlap the dgrad / BN chain and fill its tails (option "wgrad_stream")
   cudaStream_t side = nullptr;
+  // attention module: the soft-mask branch runs on its own stream, concurrent with
+  // the trunk (forward); own split-K workspace (off_conv_ws2)
+  cudaStream_t bstream = nullptr;
+  cudaEvent_t ev_bfork = nullptr, ev_bjoin = nullptr;
+  size_t off_conv_ws2 = 0;
+  bool att_branch_on() const;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_gfork = nullptr, ev_gjoin = nullptr;  // the stem's input Gram matrix on the side stream
   bool gram_pending = false;
