@@ -12,6 +12,8 @@
 // data-parallel group and applies SGD.
 #include "plan.h"
 
+#include <functional>
+
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -504,6 +506,30 @@ bool Plan::use_pair() const {
   auto it = opts.find("pair_conv");
   return it == opts.end() || it->second != 0;
 }
+// run f on the branch stream (forked from the plan stream now; own split-K workspace);
+// ev_bjoin is recorded at its end — the caller makes the plan stream wait on it
+void Plan::on_branch(const std::function<void()> &f) {
+  if (!bstream) {
+    CUDA_CHECK(cudaStreamCreateWithFlags(&bstream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&ev_bfork, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&ev_bjoin, cudaEventDisableTiming));
+  }
+  CUDA_CHECK(cudaEventRecord(ev_bfork, stream));
+  CUDA_CHECK(cudaStreamWaitEvent(bstream, ev_bfork, 0));
+  std::swap(stream, bstream);
+  std::swap(off_conv_ws, off_conv_ws2);
+  try {
+    f();
+  } catch (...) {
+    std::swap(stream, bstream);
+    std::swap(off_conv_ws, off_conv_ws2);
+    throw;
+  }
+  CUDA_CHECK(cudaEventRecord(ev_bjoin, stream));
+  std::swap(stream, bstream);
+  std::swap(off_conv_ws, off_conv_ws2);
+}
+
 // attention mask branch concurrent with the trunk (option att_branch, default on; eager
 // per-kernel timing and the default / legacy stream run it in order)
 bool Plan::att_branch_on() const {
@@ -776,6 +802,8 @@ void Plan::block_fwd(BlockL &B, int k, const void *x) {
   bn_fwd(B.b1, k, P(B.h1[k]), nullptr, nullptr, nullptr, true, P(B.a1[k]));
   conv_fwd(B.c2, P(B.a1[k]), P(B.h2[k]), nullptr, &B.b2);
   if (B.proj) {
+    // (on the branch stream, concurrent with conv1 -> BN1 -> conv2, this measured
+    // slower: 3.169 vs 3.123 ms — it competes with conv1 for every SM)
     conv_fwd(B.cp, x, P(B.hp[k]), nullptr, &B.bp);
     if (fused_stats()) {
       // out = ReLU(BN2(h2) + BNp(hp)): both statistics finalized in the apply kernel
@@ -900,18 +928,7 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
     // the soft-mask branch depends only on x: on its own stream, concurrent with the
     // trunk (P:364 out = (1 + sigmoid(mask)) * trunk; the branches meet in att_fwd)
     const bool br = att_branch_on();
-    if (br) {
-      if (!bstream) {
-        CUDA_CHECK(cudaStreamCreateWithFlags(&bstream, cudaStreamNonBlocking));
-        CUDA_CHECK(cudaEventCreateWithFlags(&ev_bfork, cudaEventDisableTiming));
-        CUDA_CHECK(cudaEventCreateWithFlags(&ev_bjoin, cudaEventDisableTiming));
-      }
-      CUDA_CHECK(cudaEventRecord(ev_bfork, stream));
-      CUDA_CHECK(cudaStreamWaitEvent(bstream, ev_bfork, 0));
-      std::swap(stream, bstream);
-      std::swap(off_conv_ws, off_conv_ws2);
-    }
-    try {
+    auto mask_branch = [&]() {
       {
       EltTimer tm(this, F_MAXPOOL_FWD, (double)mb * C * (u.in.vol() * dt_size(dt) + u.mask.vol() * (dt_size(dt) + 1.0)));
       maxpool_fwd(dt, x, mb, u.in.d, u.in.h, u.in.w, C, nullptr, nullptr, false, P(L.u0[k]), (uint8_t *)P(L.am[k]),
@@ -926,18 +943,9 @@ void Plan::unit_fwd(int ui, int k, const float *x_in, const int32_t *y) {
       conv_fwd(L.mc1, P(L.up[k]), P(L.mh[k]), nullptr, &L.mbn);
       bn_fwd(L.mbn, k, P(L.mh[k]), nullptr, nullptr, nullptr, true, P(L.r[k]));
       conv_fwd(L.mc2, P(L.r[k]), P(L.m[k]), master(L.bias_idx));
-    } catch (...) {
-      if (br) {
-        std::swap(stream, bstream);
-        std::swap(off_conv_ws, off_conv_ws2);
-      }
-      throw;
-    }
-    if (br) {
-      CUDA_CHECK(cudaEventRecord(ev_bjoin, stream));
-      std::swap(stream, bstream);
-      std::swap(off_conv_ws, off_conv_ws2);
-    }
+    };
+    if (br) on_branch(mask_branch);
+    else mask_branch();
     block_fwd(L.trunk, k, x);
     if (br) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_bjoin, 0));
     EltTimer tm(this, F_ATT_FWD, 3.0 * V * C * dt_size(dt));

@@ -223,6 +223,7 @@ struct Plan {
   cudaEvent_t ev_bfork = nullptr, ev_bjoin = nullptr;
   size_t off_conv_ws2 = 0;
   bool att_branch_on() const;
+  void on_branch(const std::function<void()> &f);
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_gfork = nullptr, ev_gjoin = nullptr;  // the stem's input Gram matrix on the side stream
   bool gram_pending = false;
