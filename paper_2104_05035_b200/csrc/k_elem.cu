@@ -668,6 +668,7 @@ __global__ void __launch_bounds__(NTA) bn_apply_part_k(const T *__restrict__ x, 
                                                        BnPart rb, const T *__restrict__ res, int relu,
                                                        T *__restrict__ y) {
   extern __shared__ double dsm[];
+  constexpr int EUA = 8;  // rows in flight per thread (stage-1 tensors: one 512-thread block per SM)
   pdl_begin();
   double *sums = dsm, *scr = dsm + 2 * C;  // 2C + 2*NTA doubles
   float *fs = (float *)(scr + 2 * NTA);     // sc, sh, rsc, rsh: 4C floats
@@ -679,9 +680,9 @@ __global__ void __launch_bounds__(NTA) bn_apply_part_k(const T *__restrict__ x, 
   const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int c0 = (int)(i0 % G) * VEC;
   // the first batch of the stream is in flight while the statistics are finalized
-  uint4 xv[EU], rv[EU];
+  uint4 xv[EUA], rv[EUA];
 #pragma unroll
-  for (int q = 0; q < EU; ++q) {
+  for (int q = 0; q < EUA; ++q) {
     const int64_t k = i0 + q * stride;
     if (k < n) {
       xv[q] = ld16(x + k * VEC);
@@ -699,10 +700,10 @@ __global__ void __launch_bounds__(NTA) bn_apply_part_k(const T *__restrict__ x, 
     ra[j] = rbn ? rsc[c0 + j] : 1.f;
     rbv[j] = rbn ? rsh[c0 + j] : 0.f;
   }
-  for (int64_t i = i0; i < n; i += EU * stride) {
+  for (int64_t i = i0; i < n; i += EUA * stride) {
     if (i != i0) {
 #pragma unroll
-      for (int q = 0; q < EU; ++q) {
+      for (int q = 0; q < EUA; ++q) {
         const int64_t k = i + q * stride;
         if (k < n) {
           xv[q] = ld16(x + k * VEC);
@@ -711,7 +712,7 @@ __global__ void __launch_bounds__(NTA) bn_apply_part_k(const T *__restrict__ x, 
       }
     }
 #pragma unroll
-    for (int q = 0; q < EU; ++q) {
+    for (int q = 0; q < EUA; ++q) {
       const int64_t k = i + q * stride;
       if (k >= n) break;
       float v[VEC];
