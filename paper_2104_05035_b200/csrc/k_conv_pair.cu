@@ -231,6 +231,9 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
       // rows travel in the statistics prefetch registers, one 32-channel chunk ahead --
       // the first chunk's before the accumulator wait (latency behind the mainloop)
       const bool res_pf = p.res && p.st.mode < 2 && p.res_pf;
+      // accumulate without residual / backward statistics: the existing output rows
+      // travel in the same prefetch registers, one chunk ahead
+      const bool acc_pf = p.accumulate && !p.res && p.st.mode < 2 && p.res_pf;
       auto prefetch = [&](bool valid, int64_t eo, StatsPf &pf) {
         if (res_pf) {
           if (!valid) return;
@@ -239,6 +242,10 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
             pf.m[i] = __ldg(reinterpret_cast<const uint4 *>(p.res_mask + eo) + i);
             pf.h[i] = __ldg(reinterpret_cast<const uint4 *>(p.res + eo) + i);
           }
+        } else if (acc_pf) {
+          if (!valid) return;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) pf.h[i] = *(reinterpret_cast<const uint4 *>(p.y + eo) + i);
         } else {
           epi_stats_prefetch(p.st, valid, eo, pf);
         }
@@ -267,7 +274,15 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
               for (int j = 0; j < 32; ++j) f[j] += p.bias[c0 + j];
             }
             bf16 *dst = p.y + obase + c0;
-            if (p.accumulate) {
+            if (acc_pf) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                float o[8];
+                unpack_bf16x8(pf_cur.h[j], o);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) f[8 * j + e] += o[e];
+              }
+            } else if (p.accumulate) {
 #pragma unroll
               for (int j = 0; j < 32; j += 8) {
                 float o[8];
@@ -300,7 +315,7 @@ __global__ void __launch_bounds__(THREADS, 1) conv_pair_kernel(const __grid_cons
           }
           if (p.st.mode) epi_stats_add(p.st, f, valid, pf_cur, c0, lane, red + (q * 2) * 64 + c0,
                                        red + (q * 2 + 1) * 64 + c0);
-          if (p.st.mode || res_pf) pf_cur = pf_nxt;
+          if (p.st.mode || res_pf || acc_pf) pf_cur = pf_nxt;
         }
       }
       tc::tc_fence_before();

@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(256) bn_fin_bwd_k(BnBwdPart b, int C) {
 template <typename T>
 __global__ void __launch_bounds__(NTA) bn_bwd_apply_part_k(const T *__restrict__ dy, const T *__restrict__ h,
                                                            const T *__restrict__ mask_t, int64_t V, int C,
-                                                           BnBwdPart b, T *__restrict__ dx) {
+                                                           BnBwdPart b, T *__restrict__ dx, T *__restrict__ dp) {
   extern __shared__ double dsm[];
   pdl_begin();
   double *sums = dsm, *scr = dsm + 2 * C;
@@ -856,12 +856,14 @@ __global__ void __launch_bounds__(NTA) bn_bwd_apply_part_k(const T *__restrict__
       unpack16(dv[q], d, dy);
       unpack16(xv[q], xf, h);
       unpack16(mv[q], m, h);
+      float dd[VEC];
 #pragma unroll
       for (int j = 0; j < VEC; ++j) {
-        const float dd = m[j] > 0.f ? d[j] : 0.f;
-        o[j] = fmaf(A[j], dd, fmaf(B[j], xf[j], Cc[j]));
+        dd[j] = m[j] > 0.f ? d[j] : 0.f;
+        o[j] = fmaf(A[j], dd[j], fmaf(B[j], xf[j], Cc[j]));
       }
       store_vec(dx + k * VEC, o);
+      if (dp) store_vec(dp + k * VEC, dd);  // dy' (exact: dy or 0) for a later accumulate
     }
   }
 }
@@ -1025,7 +1027,8 @@ __global__ void __launch_bounds__(NTS) bn_apply_cs_k(const T *__restrict__ x, in
 template <typename T>
 __global__ void __launch_bounds__(NTS) bn_bwd_apply_cs_k(const T *__restrict__ dy, const T *__restrict__ h,
                                                          const T *__restrict__ mask_t, int64_t V, int C, BnBwdPart b,
-                                                         T *__restrict__ dx, int nslice, int64_t rows_per_chunk) {
+                                                         T *__restrict__ dx, int nslice, int64_t rows_per_chunk,
+                                                         T *__restrict__ dp) {
   __shared__ double red[2][NTS];
   __shared__ double sa[CS], sb[CS];
   __shared__ float cA[CS], cB[CS], cC[CS];
@@ -1095,12 +1098,14 @@ __global__ void __launch_bounds__(NTS) bn_bwd_apply_cs_k(const T *__restrict__ d
       unpack16(dv[q], d, dy);
       unpack16(xv[q], xf, h);
       unpack16(mv[q], m, h);
+      float dd[VEC];
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
-        const float dd = m[e] > 0.f ? d[e] : 0.f;
-        o[e] = fmaf(A[e], dd, fmaf(B[e], xf[e], Cc[e]));
+        dd[e] = m[e] > 0.f ? d[e] : 0.f;
+        o[e] = fmaf(A[e], dd[e], fmaf(B[e], xf[e], Cc[e]));
       }
       store_vec(dx + r * C + cv, o);
+      if (dp) store_vec(dp + r * C + cv, dd);  // dy' (exact: dy or 0) for a later accumulate
     }
   }
 }
@@ -1822,7 +1827,7 @@ void bn_apply_fused(DType dt, const void *x, int64_t V, int C, const BnFinal &f,
 
 void bn_bwd_apply_fused(DType dt, const void *dy, const void *h, const void *mask_t, int64_t V, int C,
                         const float *part, int P, const float *gamma, const float *mean, const float *invstd,
-                        float *dgamma, float *dbeta, void *dx, cudaStream_t st, float *coef) {
+                        float *dgamma, float *dbeta, void *dx, cudaStream_t st, float *coef, void *dprime) {
   BnBwdPart b{part, P, V, gamma, mean, invstd, dgamma, dbeta, coef};
   if (bn_fin_separate() && coef) {
     launch_k(bn_fin_bwd_k, (unsigned)((C + 31) / 32), 256, 0, st, b, C);
@@ -1834,13 +1839,13 @@ void bn_bwd_apply_fused(DType dt, const void *dy, const void *h, const void *mas
     int64_t rpc;
     cs_grid(V, C, nslice, nchunk, rpc);
     DISPATCH(dt, launch_k(bn_bwd_apply_cs_k<T>, (unsigned)(nslice * nchunk), NTS, 0, st, (const T *)dy,
-                          (const T *)h, (const T *)mask_t, V, C, b, (T *)dx, nslice, rpc));
+                          (const T *)h, (const T *)mask_t, V, C, b, (T *)dx, nslice, rpc, (T *)dprime));
     LAUNCH_CHECK();
     return;
   }
   const size_t smem = (2 * (size_t)C + 2 * NTA) * sizeof(double) + 3 * (size_t)C * sizeof(float);
   DISPATCH(dt, launch_k(bn_bwd_apply_part_k<T>, grid_part(V * C / Vec<T>::N, C / Vec<T>::N), NTA, smem, st, (const T *)dy,
-                        (const T *)h, (const T *)mask_t, V, C, b, (T *)dx));
+                        (const T *)h, (const T *)mask_t, V, C, b, (T *)dx, (T *)dprime));
   LAUNCH_CHECK();
 }
 

@@ -104,7 +104,8 @@ int bn_bwd_partials(DType dt, const void *dy, const void *h, const void *mask_t,
 // dgamma += sum dy' xhat, dbeta += sum dy', dx = BN-backward(dy')
 void bn_bwd_apply_fused(DType dt, const void *dy, const void *h, const void *mask_t, int64_t V, int C,
                         const float *part, int P, const float *gamma, const float *mean, const float *invstd,
-                        float *dgamma, float *dbeta, void *dx, cudaStream_t st, float *coef = nullptr);
+                        float *dgamma, float *dbeta, void *dx, cudaStream_t st, float *coef = nullptr,
+                        void *dprime = nullptr);  // dprime (optional): dy' = dy * (mask > 0) as well
 // stem tail, bf16 (reading X4): y = maxpool(ReLU(BN(h))) with the BN statistics
 // finalized from the stem conv's partials (f.part, f.P) and published; argmax uint8
 void stem_pool_fwd(const void *h, int N, int D, int H, int W, int C, const BnFinal &f, int64_t V, void *y,

@@ -769,8 +769,8 @@ void Plan::bn_fwd(const BNL &b, int k, const void *h, const void *res, const flo
 // dx = BN-backward of dy' = dy * mask ; coef scratch slot `slot`.  bf16 path:
 // the sums come from the producer of dy (b.bP > 0) or one standalone pass,
 // and the apply kernel finalizes them.
-void Plan::bn_backward(const BNL &b, int k, const void *dy, const void *h, int mask_mode, const void *mask_t,
-                       void *dx, int slot) {
+bool Plan::bn_backward(const BNL &b, int k, const void *dy, const void *h, int mask_mode, const void *mask_t,
+                       void *dx, int slot, void *dprime) {
   if (fused_stats() && mask_mode == MASK_TENSOR) {
     BNL &m = const_cast<BNL &>(b);
     const double vc = (double)b.V * b.C * dt_size(dt);
@@ -781,9 +781,9 @@ void Plan::bn_backward(const BNL &b, int k, const void *dy, const void *h, int m
     EltTimer tm(this, F_BN_BWD_APPLY, vc * 4);
     bn_bwd_apply_fused(dt, dy, h, mask_t, b.V, b.C, (const float *)P(b.bpart), b.bP, master(b.gamma_idx),
                        bn_stat(b, k, 0), bn_stat(b, k, 1), grad(b.gamma_idx), grad(b.gamma_idx + 1), dx, stream,
-                       (float *)P(off_coef) + slot * 3 * 512);
+                       (float *)P(off_coef) + slot * 3 * 512, dprime);
     m.bP = 0;  // consumed: the next producer decides again
-    return;
+    return true;
   }
   float *part = (float *)P(off_partial);
   float *coef = (float *)P(off_coef) + slot * 3 * 512;
@@ -792,6 +792,7 @@ void Plan::bn_backward(const BNL &b, int k, const void *dy, const void *h, int m
                          bn_stat(b, k, 0), bn_stat(b, k, 1), master(b.gamma_idx), part, counter(),
                          grad(b.gamma_idx), grad(b.gamma_idx + 1), coef, stream);
   bn_bwd_apply(dt, dy, h, b.V, b.C, mask_mode, mask_t, bn_stat(b, k, 2), bn_stat(b, k, 3), coef, dx, stream);
+  return dprime == nullptr;  // this path does not produce dy'
 }
 
 // ---------------------------------------------------------------------------
@@ -834,7 +835,13 @@ void Plan::block_fwd(BlockL &B, int k, const void *x) {
 void Plan::block_bwd(BlockL &B, int k, const void *x, const void *dout, void *dx, bool accumulate,
                      const StatsTarget &dx_stats) {
   const void *out = P(B.out_[k]);
-  bn_backward(B.b2, k, dout, P(B.h2[k]), MASK_TENSOR, out, P(B.dh2), 0);
+  // identity skip, dx written (not accumulated): b2's backward apply, which forms
+  // dy' = dout * (out > 0) anyway, stores it into dx, and conv1's dgrad accumulates
+  // onto it — its epilogue prefetches one operand (dx) instead of two (dout, out)
+  auto itr = opts.find("res_prestore");
+  const bool pre = !B.proj && dx && !accumulate && (itr == opts.end() || itr->second != 0) &&
+                   !(getenv("RN_RES_PRESTORE") && atoi(getenv("RN_RES_PRESTORE")) == 0);
+  const bool pre_ok = bn_backward(B.b2, k, dout, P(B.h2[k]), MASK_TENSOR, out, P(B.dh2), 0, pre ? dx : nullptr) && pre;
   if (B.proj) bn_backward(B.bp, k, dout, P(B.hp[k]), MASK_TENSOR, out, P(B.dhp), 1);
   conv_bwd_weight(B.c2, P(B.a1[k]), P(B.dh2), false);
   StatsTarget t1;
@@ -853,7 +860,8 @@ void Plan::block_bwd(BlockL &B, int k, const void *x, const void *dout, void *dx
       conv_bwd_data_proj(B.c1, P(B.dh1), B.cp, P(B.dhp), dx, accumulate, dx_stats);
     } else {
       // identity skip: dx (+)= dgrad(dh1) + dout * (out > 0)
-      conv_bwd_data(B.c1, P(B.dh1), dx, accumulate, dout, out, dx_stats);
+      if (pre_ok) conv_bwd_data(B.c1, P(B.dh1), dx, true, nullptr, nullptr, dx_stats);
+      else conv_bwd_data(B.c1, P(B.dh1), dx, accumulate, dout, out, dx_stats);
     }
   }
   if (B.proj) conv_bwd_weight(B.cp, x, P(B.dhp), false);

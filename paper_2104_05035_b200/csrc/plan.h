@@ -193,8 +193,9 @@ struct Plan {
   void bn_forward_stats(const BNL &b, int k, const void *h);
   void bn_fwd(const BNL &b, int k, const void *h, const void *res, const float *rscale, const float *rshift, bool relu,
               void *y);
-  void bn_backward(const BNL &b, int k, const void *dy, const void *h, int mask_mode, const void *mask_t, void *dx,
-                   int slot);
+  // dprime (optional): also store dy' = dy * (mask > 0); returns false if this path cannot
+  bool bn_backward(const BNL &b, int k, const void *dy, const void *h, int mask_mode, const void *mask_t, void *dx,
+                   int slot, void *dprime = nullptr);
   void block_fwd(BlockL &B, int k, const void *x);
   void block_bwd(BlockL &B, int k, const void *x, const void *dout, void *dx, bool accumulate,
                  const StatsTarget &dx_stats = StatsTarget());
