@@ -299,7 +299,8 @@ rn_status rn_get_unit_grad(rn_plan_t plan, int32_t unit, float *host, int64_t co
  * (bf16 / uint8 values converted exactly).  Test/diagnostic access for op-level
  * parity; names (NDHWC activation layouts [mb][D][H][W][C] unless stated):
  *   stem : "h" conv output (pre-BN, conv dims), "am" max-pool argmax 0..26 (pooled
- *          dims), "d1" pool adjoint x ReLU mask (fused bf16 stem backward), "bn.stats"
+ *          dims), "d1" pool adjoint x ReLU mask (dense stem backward only: the bf16 pooled
+ *          stem runs at the pooled resolution, reading X23c, and has no d1), "bn.stats"
  *   block: "h1" "a1" "h2" ["hp"] "out" (forward), "dh2" "da1" "dh1" ["dhp"]
  *          (backward), "bn1.stats" "bn2.stats" ["projbn.stats"]
  *   att  : "trunk.<block name>", "mask.<block name>", "u0" "am" (mask-branch
@@ -381,7 +382,12 @@ int64_t rn_kernel_launches(rn_plan_t plan);
  *  "time_kernels"  : 1 record CUDA events around the dominant conv launches
  *  "halo_conv", "pair_conv", "fused_stats", "wgrad_stream" : kernel-variant switches (default 1)
  *  "merge_proj"    : 1 stage-entry projection dgrad merged into the stride-2 dgrad launch (default 1)
- *  "stem_bwd_fused": 1 fused stem backward (pool adjoint + mask + BN sums; BN apply in the wgrad) (default 1)
+ *  "c1x1"          : 1 streaming warp-tensor-core kernel for 64->64 1x1x1 convs (default 1)
+ *  "att_branch"    : 1 attention soft-mask branch on its own stream, concurrent with the trunk (default 1)
+ *  "res_prestore"  : 1 identity-skip blocks: dy' pre-stored in dx, conv1's dgrad accumulates (default 1)
+ *  "wgrad_overwrite": 1 tensor-core weight gradients store (not add) on a backward's first
+ *                    micro-batch; the backward zeroes only the other gradient ranges (default 1)
+ *  "early_sgd"     : 1 rn_train_step issues each unit's SGD right after its backward (default 1)
  *  "recompute_mask": 1 dgrad-epilogue BN sums recompute the consumer's ReLU mask from h (default 1)
  *  "pair_bwd_stats": 1 fuse the backward BN sums into the CTA-pair dgrad epilogue (default 0: standalone pass)
  *  "up_bwd_sep"    : 1 separable trilinear adjoint (default 1)

@@ -2209,6 +2209,19 @@ void sgd_repack_range(const ConvPack *table_dev, int n, int64_t tile_begin, int6
   LAUNCH_CHECK();
 }
 
+__global__ void zero_ranges_k(const int64_t *__restrict__ rg, float *g) {
+  pdl_begin();
+  const int64_t a = rg[2 * blockIdx.y], e = rg[2 * blockIdx.y + 1];
+  for (int64_t i = a + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x)
+    g[i] = 0.f;
+}
+
+void zero_ranges(const int64_t *ranges_dev, int n, float *g, cudaStream_t st) {
+  if (n <= 0) return;
+  launch_k(zero_ranges_k, dim3((unsigned)std::max(1, 148 * 4 / n), (unsigned)n), 256, 0, st, ranges_dev, g);
+  LAUNCH_CHECK();
+}
+
 void sgd_ranges(const int64_t *ranges_dev, int n, float *master, const float *grad, float lr, cudaStream_t st) {
   if (n <= 0) return;
   launch_k(sgd_ranges_k, dim3((unsigned)std::max(1, 148 * 4 / n), (unsigned)n), 256, 0, st, ranges_dev, master, grad,

@@ -51,6 +51,7 @@ struct __align__(64) WgParams {
   int n_cob;      // co blocks of BN
   int splits;
   int accum;  // splits == 1: part is dW itself and the epilogue accumulates
+  int overwrite;  // with accum: store dW instead of adding (first contribution of a backward)
   // atoms of the whole problem: atom a = (tap, ci block); M-tile i = atoms 2i, 2i+1
   int n_mtiles;
   int8_t atom_map[2 * MAX_ATOMS];  // x map index (per-tap mode)
@@ -256,7 +257,10 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
           if (ok) {
             float *dst = P + ((int64_t)(cob * BN + c0) * p.taps + tap) * p.Ci + ci;
             const int64_t cs = (int64_t)p.taps * p.Ci;  // stride between co
-            if (p.accum) {  // single split: straight into dW (all 32 loads issued before the stores)
+            if (p.accum && p.overwrite) {  // single split, first contribution: plain stores
+#pragma unroll
+              for (int j = 0; j < 32; ++j) dst[j * cs] = __uint_as_float(v[j]);
+            } else if (p.accum) {  // single split: straight into dW (all 32 loads issued before the stores)
               float old[32];
 #pragma unroll
               for (int j = 0; j < 32; ++j) old[j] = dst[j * cs];
@@ -287,7 +291,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) wgrad_tc_kernel(const __grid_co
 // 138-444 splits: 16 / 7 blocks, ~18 us each).
 template <int G>
 __global__ void __launch_bounds__(256) split_reduce_add_k(const float *__restrict__ part, int splits, int64_t n,
-                                                          float *__restrict__ out) {
+                                                          float *__restrict__ out, int overwrite) {
   constexpr int E = 256 / G;
   __shared__ float red[G][E];
   pdl_begin();
@@ -314,11 +318,11 @@ __global__ void __launch_bounds__(256) split_reduce_add_k(const float *__restric
         float t = red[0][e];
 #pragma unroll
         for (int q = 1; q < G; ++q) t += red[q][e];
-        out[i] += t;
+        out[i] = overwrite ? t : out[i] + t;
       }
       __syncthreads();
     } else if (i < n) {
-      out[i] += s;
+      out[i] = overwrite ? s : out[i] + s;
     }
   }
 }
@@ -405,11 +409,11 @@ WgShape wg_shape(const ConvGeom &g) {
 
 }  // namespace
 
-void split_reduce_add(const float *part, int splits, int64_t n, float *out, cudaStream_t st) {
+void split_reduce_add(const float *part, int splits, int64_t n, float *out, cudaStream_t st, bool overwrite) {
   auto go = [&](auto kern, int G) {
     const int64_t per = 256 / G;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + per - 1) / per, 148 * 8));
-    launch_k(kern, grid, 256, 0, st, part, splits, n, out);
+    launch_k(kern, grid, 256, 0, st, part, splits, n, out, overwrite ? 1 : 0);
   };
   // enough blocks to cover the SMs: the more splits per element, the more groups
   if (splits >= 64 && n <= 148 * 64) go(split_reduce_add_k<8>, 8);
@@ -436,7 +440,8 @@ size_t tc_wgrad_ws_floats(const ConvGeom &g) {
   return s.splits > 1 ? (size_t)s.splits * g.Co * g.taps() * g.Ci : 0;
 }
 
-void conv_wgrad_tc(const ConvGeom &g, const bf16 *x, const bf16 *dy, float *dw, float *ws, cudaStream_t st) {
+void conv_wgrad_tc(const ConvGeom &g, const bf16 *x, const bf16 *dy, float *dw, float *ws, cudaStream_t st,
+                   bool overwrite) {
   WgShape s = wg_shape(g);
   WgParams p;
   memset(&p, 0, sizeof p);
@@ -452,6 +457,7 @@ void conv_wgrad_tc(const ConvGeom &g, const bf16 *x, const bf16 *dy, float *dw, 
   p.n_vtiles = s.n_vtiles;
   p.vt_per_split = s.vt_per_split;
   p.accum = s.splits == 1;
+  p.overwrite = overwrite ? 1 : 0;
   p.part = p.accum ? dw : ws;
   p.Co = g.Co; p.Ci = g.Ci; p.taps = g.taps();
   // dy map: NDHWC [N][Do][Ho][Wo][Co]
@@ -522,7 +528,7 @@ void conv_wgrad_tc(const ConvGeom &g, const bf16 *x, const bf16 *dy, float *dw, 
   }
   if (p.accum) return;
   const int64_t n = (int64_t)g.Co * g.taps() * g.Ci;
-  split_reduce_add(ws, s.splits, n, dw, st);
+  split_reduce_add(ws, s.splits, n, dw, st, overwrite);
 }
 
 }  // namespace rn

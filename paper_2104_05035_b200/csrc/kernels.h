@@ -35,7 +35,9 @@ size_t conv_wgrad_ws_floats(const ConvGeom &g);
 void conv_wgrad_simt(DType dt, bool x_is_f32, const ConvGeom &g, const void *x, const void *dy, float *dw,
                      float *ws, cudaStream_t st);
 // out[i] += sum_z part[z*n + i] over z < splits, fixed order (split-K weight-gradient partials)
-void split_reduce_add(const float *part, int splits, int64_t n, float *out, cudaStream_t st);
+void split_reduce_add(const float *part, int splits, int64_t n, float *out, cudaStream_t st, bool overwrite = false);
+// g[a, e) = 0 over n ranges [2][n] (device table)
+void zero_ranges(const int64_t *ranges_dev, int n, float *g, cudaStream_t st);
 // stem: Ci = 1, x fp32 [N][D][H][W], w fp32 [Co][27]
 void stem_conv_fprop(DType dt, const ConvGeom &g, const float *x, const float *w, void *y, cudaStream_t st);
 // k_stem.cu: Co in {8,16,32,64}

@@ -12,6 +12,8 @@
 // data-parallel group and applies SGD.
 #include "plan.h"
 
+#include <algorithm>
+
 #include <functional>
 
 #include <cmath>
@@ -50,6 +52,7 @@ void Plan::make_bn(BNL &b, int gamma_idx, int C, int64_t V) {
 }
 
 void Plan::make_conv(ConvL &c, int w_idx, int Ci, int Co, int k, int s, int p, Dims in, Dims out) {
+  conv_reg.push_back(&c);
   c.w_idx = w_idx;
   c.g.N = mb;
   c.g.Di = in.d; c.g.Hi = in.h; c.g.Wi = in.w; c.g.Ci = Ci;
@@ -281,6 +284,7 @@ Plan::Plan(const rn_net_desc &nd, const rn_dist_desc &dd, int local_batch, int d
   off_partial = alloc(sizeof(float) * nblk_max * 2 * 512);
   off_coef = alloc(sizeof(float) * 3 * 512 * 2);
   off_counter = alloc(256);  // last-block tickets of the fused reduce+finalize kernels (zeroed at bind)
+  off_zrg = alloc(2 * sizeof(int64_t) * (conv_reg.size() + 2));  // after every make_conv
   off_wgrad_ws = alloc(sizeof(float) * (wgrad_ws_floats ? wgrad_ws_floats : 1));
   off_conv_ws = alloc(sizeof(float) * (conv_ws_floats ? conv_ws_floats : 1));
   off_conv_ws2 = alloc(sizeof(float) * (conv_ws_floats ? conv_ws_floats : 1));
@@ -710,7 +714,8 @@ void Plan::conv_bwd_weight(const ConvL &c, const void *x, const void *dy, bool x
     stem_wgrad_fast(dt, c.g, (const float *)x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), ws);
   } else if (!x_f32 && use_tc(c.g, false) && tc_wgrad_supported(c.g)) {
     kind = K_WGRAD;
-    conv_wgrad_tc(c.g, (const bf16 *)x, (const bf16 *)dy, grad(c.w_idx), (float *)P(off_wgrad_ws), ws);
+    conv_wgrad_tc(c.g, (const bf16 *)x, (const bf16 *)dy, grad(c.w_idx), (float *)P(off_wgrad_ws), ws,
+                  wg_overwrite && wg_first);
   } else {
     conv_wgrad_simt(dt, x_f32, c.g, x, dy, grad(c.w_idx), (float *)P(off_wgrad_ws), ws);
   }
@@ -1226,6 +1231,7 @@ void Plan::forward(const float *x_in, const int32_t *y) {
 }
 
 void Plan::backward(const float *x_in) {
+  prepare_grad_clear();
   run_phase(1, [&] { backward_body(x_in); });
   bwd_ever = true;
 }
@@ -1289,6 +1295,7 @@ void Plan::train_step(const float *x_in, const int32_t *y, float lr) {
     warm[3] = false;
     graph_lr3 = lr;
   }
+  prepare_grad_clear();
   run_phase(3, [&] { backward_body(x_in, -1, lr); });
   bwd_ever = true;
 }
@@ -1323,13 +1330,57 @@ void Plan::forward_body(const float *x_in, const int32_t *y, int k_only) {
   if (S > 1 && !xfer_external) nccl_bcast_f32(pipe_comm, (float *)P(off_loss), 1, unit_stage[nu - 1], stream);
 }
 
+// Gradient clearing: the tensor-core weight gradients of a backward's first
+// micro-batch STORE their result (option wgrad_overwrite, bf16 path), so only
+// the rest of the gradient array — BN parameters, biases, the head, the stem and
+// SIMT-path convs, non-local units — is zeroed (a few MB instead of the whole
+// 134 MB array of r18, which cost ~28 us at the start of the backward).  The
+// range table is rebuilt on the host before each backward / fused step (outside
+// graph capture) and uploaded only when it changes.
+void Plan::prepare_grad_clear() {
+  auto it = opts.find("wgrad_overwrite");
+  const bool on = (it == opts.end() || it->second != 0) && dt == DT_BF16;
+  std::vector<std::pair<int64_t, int64_t>> tc;  // [begin, end) of tensor-core weight gradients
+  if (on)
+    for (const ConvL *c : conv_reg) {
+      const bool x_f32 = c->g.Ci == 1;  // the stem reads the fp32 input
+      if (!x_f32 && use_tc(c->g, false) && tc_wgrad_supported(c->g)) {
+        const int64_t b = net.params[c->w_idx].canon_off;
+        tc.emplace_back(b, b + net.params[c->w_idx].numel);
+      }
+    }
+  std::sort(tc.begin(), tc.end());
+  std::vector<int64_t> rg;
+  int64_t cur = 0;
+  for (auto &r : tc) {
+    if (r.first > cur) {
+      rg.push_back(cur);
+      rg.push_back(r.first);
+    }
+    cur = std::max(cur, r.second);
+  }
+  if (cur < net.n_params) {
+    rg.push_back(cur);
+    rg.push_back(net.n_params);
+  }
+  wg_overwrite = on && !tc.empty();
+  if (rg != zrg_host) {
+    zrg_host = rg;
+    if (!rg.empty())
+      CUDA_CHECK(cudaMemcpyAsync(P(off_zrg), zrg_host.data(), zrg_host.size() * sizeof(int64_t),
+                                 cudaMemcpyHostToDevice, stream));  // stream-ordered (outside any capture)
+  }
+}
+
 void Plan::backward_body(const float *x_in, int k_only, float early_lr) {
-  CUDA_CHECK(cudaMemsetAsync(P(off_grad), 0, sizeof(float) * net.n_params, stream));
+  if (wg_overwrite) zero_ranges((const int64_t *)P(off_zrg), (int)(zrg_host.size() / 2), (float *)P(off_grad), stream);
+  else CUDA_CHECK(cudaMemsetAsync(P(off_grad), 0, sizeof(float) * net.n_params, stream));
   const int nu = (int)net.units.size();
   const bool ov = overlap_ar();
   size_t bi = 0;
   const int k0 = k_only < 0 ? 0 : k_only, k1 = k_only < 0 ? Mb : k_only + 1;
   for (int k = k0; k < k1; ++k) {
+    wg_first = k == k0;  // the first contribution to every weight gradient of this backward
     for (int ui = nu - 1; ui >= 0; --ui) {
       if (!local[ui]) continue;
       if (ui + 1 < nu && !local[ui + 1] && !xfer_external) {
@@ -1552,6 +1603,7 @@ void Plan::delayed_step(const float *x_dev, const int32_t *y_dev, float lr) {
     std::swap(off_master, stash_master[bs]);  // the weights of batch bb's forward
     std::swap(shadow_d, stash_shadow_d[bs]);
     try {
+      prepare_grad_clear();
       backward_body((const float *)P(off_x), bs);
     } catch (...) {
       std::swap(off_master, stash_master[bs]);
@@ -1739,11 +1791,13 @@ void Plan::stage_inputs(const float *x, const int32_t *y, bool from_host) {
 }
 
 rn_status Plan::set_option(const std::string &k, int64_t v) {
-  if (k != "graphs" && k != "tc_conv" && k != "time_kernels" && k != "halo_conv" && k != "fused_stats" &&
-      k != "pair_conv" && k != "wgrad_stream" && k != "merge_proj" && k != "stem_bwd_fused" &&
-      k != "recompute_mask" && k != "up_bwd_sep" && k != "pair_bwd_stats" && k != "overlap_allreduce" &&
-      k != "async_allreduce")
-    return set_error(RN_ERR_ARG, "unknown option " + k);
+  static const char *const known[] = {"graphs", "tc_conv", "time_kernels", "halo_conv", "fused_stats", "pair_conv",
+                                      "wgrad_stream", "merge_proj", "recompute_mask", "up_bwd_sep", "pair_bwd_stats",
+                                      "overlap_allreduce", "async_allreduce", "early_sgd", "c1x1", "att_branch",
+                                      "res_prestore", "wgrad_overwrite"};
+  bool ok = false;
+  for (const char *n : known) ok = ok || k == n;
+  if (!ok) return set_error(RN_ERR_ARG, "unknown option " + k);
   opts[k] = v;
   if (k == "time_kernels") ev_used = 0;
   if (k == "async_allreduce") async_have_prev = false;

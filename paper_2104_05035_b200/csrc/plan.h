@@ -119,6 +119,12 @@ struct Plan {
   size_t off_counter = 0;
   unsigned *counter() { return (unsigned *)P(off_counter); }
   size_t off_partial = 0, off_coef = 0, off_wgrad_ws = 0, off_x = 0, off_y = 0;
+  // gradient clearing with overwriting tensor-core weight gradients (prepare_grad_clear)
+  std::vector<const ConvL *> conv_reg;  // every conv of the local units
+  size_t off_zrg = 0;                   // device [2][n] ranges zeroed at the start of a backward
+  std::vector<int64_t> zrg_host;
+  bool wg_overwrite = false, wg_first = false;
+  void prepare_grad_clear();
   size_t wgrad_ws_floats = 0, conv_ws_floats = 0, off_conv_ws = 0, off_up_ws = 0;
   size_t off_pack = 0, off_sgdrg = 0;
   int n_pack = 0, n_sgdrg = 0, max_pack = 0, max_sgdrg = 0;

@@ -52,7 +52,8 @@ int conv1x1(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *w, c
 // weight gradient dw[co][tap][ci] += sum dy x (fp32 partials in ws, fixed-order reduce)
 bool tc_wgrad_supported(const ConvGeom &g);
 size_t tc_wgrad_ws_floats(const ConvGeom &g);
+// overwrite: dW = (not +=) the gradient — the first contribution of a backward pass
 void conv_wgrad_tc(const ConvGeom &g, const __nv_bfloat16 *x, const __nv_bfloat16 *dy, float *dw, float *ws,
-                   cudaStream_t st);
+                   cudaStream_t st, bool overwrite = false);
 
 }  // namespace rn
