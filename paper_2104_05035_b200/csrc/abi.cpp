@@ -500,8 +500,7 @@ rn_status rn_train_step(rn_plan_t plan, const void *x_dev, const int32_t *y_dev,
   NEED_BOUND(plan);
   Plan *p = plan->p;
   if (!p->params_set) return set_error(RN_ERR_STATE, "rn_set_params must precede a step");
-  p->stage_inputs((const float *)x_dev, y_dev, false);
-  p->train_step((const float *)p->P(p->off_x), (const int32_t *)p->P(p->off_y), lr);
+  p->train_step_dev((const float *)x_dev, y_dev, lr);
   p->fwd_done = false;
   return finish_loss(p, loss_host);
   GUARD_END

@@ -1174,7 +1174,7 @@ bool Plan::graphs_on() const {
 }
 
 void Plan::drop_graphs() {
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 5; ++i) {
     if (gexec[i]) cudaGraphExecDestroy(gexec[i]);
     gexec[i] = nullptr;
     warm[i] = false;
@@ -1288,7 +1288,18 @@ void Plan::train_step(const float *x_in, const int32_t *y, float lr) {
     step(lr);
     return;
   }
-  forward(x_in, y);
+  if (x_in != tx_ptr || y != ty_ptr) {  // phases 3 / 4 bake the input pointers in
+    for (int ph : {3, 4}) {
+      if (gexec[ph]) cudaGraphExecDestroy(gexec[ph]);
+      gexec[ph] = nullptr;
+      warm[ph] = false;
+    }
+    tx_ptr = x_in;
+    ty_ptr = y;
+  }
+  run_phase(4, [&] { forward_body(x_in, y); });
+  fwd_done = true;
+  fwd_ever = true;
   if (lr != graph_lr3) {  // the learning rate is a kernel argument of the captured phase
     if (gexec[3]) cudaGraphExecDestroy(gexec[3]);
     gexec[3] = nullptr;
@@ -1298,6 +1309,21 @@ void Plan::train_step(const float *x_in, const int32_t *y, float lr) {
   prepare_grad_clear();
   run_phase(3, [&] { backward_body(x_in, -1, lr); });
   bwd_ever = true;
+}
+
+void Plan::train_step_dev(const float *x_dev, const int32_t *y_dev, float lr) {
+  const bool same = x_dev == dev_x && y_dev == dev_y;
+  same_xy = same ? same_xy + 1 : 0;
+  dev_x = x_dev;
+  dev_y = y_dev;
+  const int nu = (int)net.units.size();
+  const bool direct = same_xy >= 2 && early_sgd_ok() && graphs_on() && local[0] && local[nu - 1];
+  if (direct) {
+    train_step(x_dev, y_dev, lr);
+  } else {
+    stage_inputs(x_dev, y_dev, false);
+    train_step((const float *)P(off_x), (const int32_t *)P(off_y), lr);
+  }
 }
 
 void Plan::forward_body(const float *x_in, const int32_t *y, int k_only) {

@@ -48,3 +48,43 @@ def test_train_step_equals_separate_calls(depth, w, dims, dtype, graphs):
     assert np.array_equal(a["g"], b["g"])
     assert np.array_equal(a["w"], b["w"])
     assert not np.array_equal(a["w"], flat)  # the steps did update
+
+
+def test_train_step_direct_inputs():
+    """rn_train_step called with the SAME device buffers (new batch contents copied
+    in each step): from the third call on the fused step runs straight on them —
+    its graphs re-captured for those pointers, no staging copy — and must still
+    equal the separate calls bit for bit; a different buffer afterwards falls back
+    to the staged path (graphs re-captured again)."""
+    depth, w, dims, dtype = 18, 64, (40, 48, 40), rn.RN_BF16
+    desc = rn.net_desc(depth, w, dims)
+    tensors = rn.net_params(desc)[0]
+    arrays = synthetic.perturb_params(tensors, synthetic.init_params(tensors, seed=0))
+    flat = np.concatenate([a.ravel() for a in arrays]).astype(np.float32)
+    bs = [synthetic.make_batch(2, *dims, seed=40 + t) for t in range(6)]
+    res = []
+    for fused in (False, True):
+        st = torch.cuda.Stream()
+        plan = rn.Plan(desc, 2, dtype, stream=st)
+        plan.set_params(flat)
+        losses = []
+        with torch.cuda.stream(st):
+            xd = torch.empty((2,) + dims, dtype=torch.float32, device="cuda")
+            yd = torch.empty((2,), dtype=torch.int32, device="cuda")
+            for t, (x, y) in enumerate(bs):
+                if t == 5:  # a new buffer: back to the staged path
+                    xd = torch.empty((2,) + dims, dtype=torch.float32, device="cuda")
+                xd.copy_(torch.from_numpy(x))
+                yd.copy_(torch.from_numpy(y))
+                if fused:
+                    losses.append(plan.train_step(xd, yd, 1e-3, want_loss=True))
+                else:
+                    losses.append(plan.forward(xd, yd))
+                    plan.backward()
+                    plan.step(1e-3)
+            st.synchronize()
+        res.append(dict(losses=losses, w=plan.get_params(), g=plan.get_grads()))
+    a, b = res
+    assert a["losses"] == b["losses"]
+    assert np.array_equal(a["g"], b["g"])
+    assert np.array_equal(a["w"], b["w"])
