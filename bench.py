@@ -250,7 +250,7 @@ def main():
             dist.barrier()
         # the public pipelined host-input loop: each step's batch crosses PCIe inside
         # the timed call (step i+1's copy overlaps step i's compute)
-        plan.train_steps_host([xh] * 2, [yh] * 2, lr)  # warm the side stream / staging path
+        plan.train_steps_host([xh] * 4, [yh] * 4, lr)  # warm the side stream / staging slots (graphs per slot)
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         plan.train_steps_host([xh] * a.e2e_steps, [yh] * a.e2e_steps, lr)

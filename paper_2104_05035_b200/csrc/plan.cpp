@@ -1179,6 +1179,9 @@ void Plan::drop_graphs() {
     gexec[i] = nullptr;
     warm[i] = false;
   }
+  if (alt_step.g3) cudaGraphExecDestroy(alt_step.g3);
+  if (alt_step.g4) cudaGraphExecDestroy(alt_step.g4);
+  alt_step = StepGraphs();
 }
 
 void Plan::run_phase(int ph, const std::function<void()> &body) {
@@ -1288,15 +1291,7 @@ void Plan::train_step(const float *x_in, const int32_t *y, float lr) {
     step(lr);
     return;
   }
-  if (x_in != tx_ptr || y != ty_ptr) {  // phases 3 / 4 bake the input pointers in
-    for (int ph : {3, 4}) {
-      if (gexec[ph]) cudaGraphExecDestroy(gexec[ph]);
-      gexec[ph] = nullptr;
-      warm[ph] = false;
-    }
-    tx_ptr = x_in;
-    ty_ptr = y;
-  }
+  if (x_in != tx_ptr || y != ty_ptr) select_step_graphs(x_in, y);  // phases 3 / 4 bake the pointers in
   run_phase(4, [&] { forward_body(x_in, y); });
   fwd_done = true;
   fwd_ever = true;
@@ -1309,6 +1304,40 @@ void Plan::train_step(const float *x_in, const int32_t *y, float lr) {
   prepare_grad_clear();
   run_phase(3, [&] { backward_body(x_in, -1, lr); });
   bwd_ever = true;
+}
+
+// the active phase-3/4 graphs belong to (tx_ptr, ty_ptr); alt_step caches the pair
+// of one other input pointer: swap it in when it matches, else evict it
+void Plan::select_step_graphs(const float *x, const int32_t *y) {
+  StepGraphs cur;
+  cur.x = tx_ptr;
+  cur.y = ty_ptr;
+  cur.g3 = gexec[3];
+  cur.g4 = gexec[4];
+  cur.w3 = warm[3];
+  cur.w4 = warm[4];
+  cur.k3 = graph_kernels[3];
+  cur.k4 = graph_kernels[4];
+  cur.lr3 = graph_lr3;
+  StepGraphs nxt;
+  if (alt_step.x == x && alt_step.y == y) {
+    nxt = alt_step;
+  } else {
+    if (alt_step.g3) cudaGraphExecDestroy(alt_step.g3);
+    if (alt_step.g4) cudaGraphExecDestroy(alt_step.g4);
+    nxt.x = x;
+    nxt.y = y;
+  }
+  alt_step = cur;
+  tx_ptr = nxt.x;
+  ty_ptr = nxt.y;
+  gexec[3] = nxt.g3;
+  gexec[4] = nxt.g4;
+  warm[3] = nxt.w3;
+  warm[4] = nxt.w4;
+  graph_kernels[3] = nxt.k3;
+  graph_kernels[4] = nxt.k4;
+  graph_lr3 = nxt.lr3;
 }
 
 void Plan::train_step_dev(const float *x_dev, const int32_t *y_dev, float lr) {
@@ -1792,16 +1821,25 @@ void Plan::train_steps_host(const float *const *x_host, const int32_t *const *y_
                                        copy_stream));
     CUDA_CHECK(cudaEventRecord(ev_copied[i % 2], copy_stream));
   };
+  // graphs captured per staging slot (the fused step only; the separate-phase path
+  // bakes the workspace input in)
+  const bool direct = early_sgd_ok() && graphs_on();
   h2d(0);
   for (int i = 0; i < n; ++i) {
     if (i + 1 < n) h2d(i + 1);
     const char *slot = (const char *)P(off_stage[i % 2]);
     CUDA_CHECK(cudaStreamWaitEvent(stream, ev_copied[i % 2], 0));
-    if (hx) CUDA_CHECK(cudaMemcpyAsync(P(off_x), slot, xb, cudaMemcpyDeviceToDevice, stream));
-    if (hy) CUDA_CHECK(cudaMemcpyAsync(P(off_y), slot + yoff, sizeof(int32_t) * (size_t)b, cudaMemcpyDeviceToDevice,
-                                       stream));
-    CUDA_CHECK(cudaEventRecord(ev_free[i % 2], stream));
-    train_step((const float *)P(off_x), (const int32_t *)P(off_y), lr);
+    if (direct) {  // the step reads the staging slot itself (its graphs cached per slot)
+      train_step(hx ? (const float *)slot : (const float *)P(off_x),
+                 hy ? (const int32_t *)(slot + yoff) : (const int32_t *)P(off_y), lr);
+      CUDA_CHECK(cudaEventRecord(ev_free[i % 2], stream));  // the slot is read until the stem backward
+    } else {
+      if (hx) CUDA_CHECK(cudaMemcpyAsync(P(off_x), slot, xb, cudaMemcpyDeviceToDevice, stream));
+      if (hy) CUDA_CHECK(cudaMemcpyAsync(P(off_y), slot + yoff, sizeof(int32_t) * (size_t)b,
+                                         cudaMemcpyDeviceToDevice, stream));
+      CUDA_CHECK(cudaEventRecord(ev_free[i % 2], stream));
+      train_step((const float *)P(off_x), (const int32_t *)P(off_y), lr);
+    }
     CUDA_CHECK(cudaMemcpyAsync(loss_pinned + i, P(off_loss), sizeof(float), cudaMemcpyDeviceToHost, stream));
   }
   CUDA_CHECK(cudaStreamSynchronize(stream));

@@ -276,6 +276,17 @@ struct Plan {
   void train_step_dev(const float *x_dev, const int32_t *y_dev, float lr);
   const float *tx_ptr = nullptr;         // the input pointers phases 3 / 4 were captured with
   const int32_t *ty_ptr = nullptr;
+  // a second cached pair of phase-3/4 graphs for another input pointer (the e2e path
+  // alternates two staging slots): swapped in when its pointers come back
+  struct StepGraphs {
+    const float *x = nullptr;
+    const int32_t *y = nullptr;
+    cudaGraphExec_t g3 = nullptr, g4 = nullptr;
+    bool w3 = false, w4 = false;
+    int k3 = 0, k4 = 0;
+    float lr3 = -1.f;
+  } alt_step;
+  void select_step_graphs(const float *x, const int32_t *y);
   const void *dev_x = nullptr, *dev_y = nullptr;   // the previous call's device inputs
   int same_xy = 0;
   bool early_sgd_ok() const;

@@ -281,13 +281,15 @@ def test_recomputed_relu_mask_matches_mask_tensor():
 
 
 def test_pipelined_host_steps_match_single_steps():
-    """rn_train_steps_host (step i+1's H2D overlapped with step i) computes
-    exactly what the same number of rn_train_step_host calls computes."""
+    """rn_train_steps_host (step i+1's H2D overlapped with step i; the fused step
+    runs on the two staging slots directly, one cached graph pair per slot, so five
+    steps replay both) computes exactly what the same number of rn_train_step_host
+    calls computes."""
     dims = (40, 48, 40)
     x, y = synthetic.make_batch(2, *dims, seed=1)
     x2, y2 = synthetic.make_batch(2, *dims, seed=2)
-    xs = [torch.from_numpy(v).pin_memory().numpy() for v in (x, x2, x)]
-    ys = [torch.from_numpy(v).pin_memory().numpy() for v in (y, y2, y)]
+    xs = [torch.from_numpy(v).pin_memory().numpy() for v in (x, x2, x, x2, x)]
+    ys = [torch.from_numpy(v).pin_memory().numpy() for v in (y, y2, y, y2, y)]
     outs = []
     for pipelined in (True, False):
         st = torch.cuda.Stream()
