@@ -1783,10 +1783,13 @@ static bool bn_apply_cs(int64_t V, int C) {
   static const bool v = !getenv("RN_BN_APPLY_CS") || atoi(getenv("RN_BN_APPLY_CS")) != 0;
   return v && C % CS == 0 && V * C <= ((int64_t)4 << 20);
 }
-// slices x chunks: about two blocks of 256 threads per SM, chunks of whole rows
+// slices x chunks of whole rows
 static void cs_grid(int64_t V, int C, int &nslice, int &nchunk, int64_t &rpc) {
+  // about one 256-thread block per SM (A/B, RN_CS_BLOCKS: 148 -> 3.0930 ms, 296 -> 3.0984,
+  // 592 -> 3.1334, 100 -> 3.0995, 74 -> 3.1252), chunks of >= 64 rows
+  static const int target = getenv("RN_CS_BLOCKS") ? std::max(1, atoi(getenv("RN_CS_BLOCKS"))) : 148;
   nslice = C / CS;
-  nchunk = (int)std::max<int64_t>(1, std::min<int64_t>((2 * 148 + nslice - 1) / nslice, (V + 63) / 64));
+  nchunk = (int)std::max<int64_t>(1, std::min<int64_t>((target + nslice - 1) / nslice, (V + 63) / 64));
   rpc = (V + nchunk - 1) / nchunk;
   nchunk = (int)((V + rpc - 1) / rpc);
 }
